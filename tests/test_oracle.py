@@ -1,0 +1,211 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+The oracle (oracle/oracle.cpp) is the plain definition of what the method computes: the stable
+ascending sort of 100-byte records by the unsigned 10-byte key, ties broken by input index (PAPER.md
+§3.1-§3.2 lines 50-106; §4.1; BASELINE.json north_star). Here it is pinned
+to things other than itself: brute force over all orders, an insertion sort written out in Python,
+Python's stable sort on the key alone, closed forms, the paper's §2.2 worked example and the digest
+invariants. Each test names the plausible oracle mistake it would catch.
+"""
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _keys(recs):
+    a = np.asarray(recs, dtype=np.uint8).reshape(-1, 100)
+    return [bytes(a[i, :10]) for i in range(a.shape[0])]
+
+
+def _with_keys(keys, seed=0):
+    """Records whose keys are `keys` (bytes, padded to 10) and whose payload is random."""
+    rng = np.random.default_rng(seed)
+    n = len(keys)
+    recs = rng.integers(0, 256, size=(n, 100), dtype=np.uint8)
+    for i, k in enumerate(keys):
+        kb = (bytes(k) + bytes(10))[:10]
+        recs[i, :10] = np.frombuffer(kb, dtype=np.uint8)
+    return recs.reshape(-1)
+
+
+def _insertion_sort_perm(keys):
+    """Insertion sort on (key, index) — written out; no library sort."""
+    perm = []
+    for i, k in enumerate(keys):
+        j = len(perm)
+        while j > 0 and keys[perm[j - 1]] > k:  # strict '>' keeps equal keys in index order
+            j -= 1
+        perm.insert(j, i)
+    return perm
+
+
+# ---------------------------------------------------------------- brute force (catches anything)
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 6, 7])
+def test_brute_force_all_orders(n):
+    """For n <= 7, enumerate all n! arrangements: exactly one has (key, index) strictly increasing,
+    and it must be the oracle's. Keys over {0x00, 0x01, 0xFF} so ties and high bytes are common."""
+    for seed in range(4 if n > 0 else 1):
+        rng = random.Random(1000 * n + seed)
+        keys = [bytes(rng.choice((0x00, 0x01, 0xFF)) for _ in range(10)) for _ in range(n)]
+        recs = _with_keys(keys, seed)
+        out, perm = oracle.sort(recs)
+        winners = []
+        for p in itertools.permutations(range(n)):
+            if all((keys[p[j]], p[j]) < (keys[p[j + 1]], p[j + 1]) for j in range(n - 1)):
+                winners.append(list(p))
+        assert len(winners) == 1
+        assert list(perm) == winners[0]
+        a = recs.reshape(-1, 100)
+        assert np.array_equal(out.reshape(-1, 100), a[winners[0]] if n else a)
+
+
+# ---------------------------------------------------------------- independent twins
+@pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "three_keys", "ascii"])
+def test_insertion_sort_twin(dist):
+    recs = gen.records(300, seed=7, dist=dist)
+    keys = _keys(recs)
+    out, perm = oracle.sort(recs)
+    assert list(perm) == _insertion_sort_perm(keys)
+    assert np.array_equal(out.reshape(-1, 100), recs.reshape(-1, 100)[perm])
+
+
+@pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "byte9"])
+def test_python_stable_sort_on_key_alone(dist):
+    """Python's sorted() is guaranteed stable, so sorting indices by key ALONE must give the oracle's
+    tie order (catches a dropped or reversed index tie-break)."""
+    recs = gen.records(20000, seed=11, dist=dist)
+    keys = _keys(recs)
+    expect = sorted(range(len(keys)), key=lambda i: keys[i])
+    _, perm = oracle.sort(recs)
+    assert list(perm) == expect
+
+
+# ---------------------------------------------------------------- closed forms
+def test_all_equal_is_identity():
+    recs = gen.records(5000, seed=3, dist="all_equal")
+    out, perm = oracle.sort(recs)
+    assert np.array_equal(perm, np.arange(5000, dtype=np.uint32))
+    assert np.array_equal(out, recs)
+
+
+def test_sorted_is_identity_and_reverse_is_reversal():
+    recs = gen.records(4097, seed=5, dist="sorted")
+    out, perm = oracle.sort(recs)
+    assert np.array_equal(perm, np.arange(4097, dtype=np.uint32))
+    recs = gen.records(4097, seed=5, dist="reverse")
+    out, perm = oracle.sort(recs)
+    assert np.array_equal(perm, np.arange(4096, -1, -1, dtype=np.uint32))
+    assert np.array_equal(out.reshape(-1, 100), recs.reshape(-1, 100)[::-1])
+
+
+@pytest.mark.parametrize("pos", [0, 1, 4, 8, 9])
+def test_single_varying_byte_is_counting_order(pos):
+    """Keys that differ only at byte `pos`: the answer is bucket order by that byte, index order inside
+    each bucket (a counting sort written out). Byte 9 catches a key truncated to 8 or 9 bytes."""
+    rng = np.random.default_rng(pos)
+    n = 3000
+    base = rng.integers(0, 256, size=10, dtype=np.uint8)
+    vals = rng.integers(0, 256, size=n, dtype=np.uint8)
+    keys = []
+    for v in vals:
+        k = base.copy()
+        k[pos] = v
+        keys.append(bytes(k))
+    recs = _with_keys(keys, pos)
+    buckets = [[] for _ in range(256)]
+    for i, v in enumerate(vals):
+        buckets[int(v)].append(i)
+    expect = [i for b in buckets for i in b]
+    _, perm = oracle.sort(recs)
+    assert list(perm) == expect
+
+
+def test_unsigned_byte_order():
+    """0x7F < 0x80 < 0xFF (unsigned); a signed-char compare would invert them."""
+    keys = [b"\xff" + bytes(9), b"\x80" + bytes(9), b"\x7f" + bytes(9), b"\x00" + bytes(9),
+            bytes(9) + b"\x80", bytes(9) + b"\x7f"]
+    recs = _with_keys(keys)
+    _, perm = oracle.sort(recs)
+    assert list(perm) == [3, 5, 4, 2, 1, 0]
+
+
+def test_paper_section_2_2_example():
+    """PAPER.md §2.2 line 33 worked example (tests/golden/paper_s2_2_example.json)."""
+    with open(os.path.join(GOLDEN, "paper_s2_2_example.json")) as f:
+        g = json.load(f)
+    keys = [k.encode() for k in g["input_order"]]
+    recs = _with_keys(keys)
+    out, perm = oracle.sort(recs)
+    got = [bytes(out.reshape(-1, 100)[j, :3]).decode() for j in range(len(keys))]
+    assert got == g["sorted_keys"]
+    # first round: buckets by the first character (the §2.2 bucket counts)
+    first = {}
+    for k in got:
+        first[k[0]] = first.get(k[0], 0) + 1
+    assert first == g["first_round_buckets"]
+
+
+def test_empty_and_single():
+    out, perm = oracle.sort(np.zeros(0, dtype=np.uint8))
+    assert out.size == 0 and perm.size == 0
+    r = gen.records(1, seed=9)
+    out, perm = oracle.sort(r)
+    assert np.array_equal(out, r) and list(perm) == [0]
+
+
+# ---------------------------------------------------------------- digests and certificate
+def test_multiset_hash_permutation_invariant_and_sensitive():
+    recs = gen.records(2000, seed=13).reshape(-1, 100)
+    h = oracle.multiset_hash(recs)
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        assert oracle.multiset_hash(recs[rng.permutation(2000)]) == h
+    rng = random.Random(1)
+    for _ in range(1000):
+        m = recs.copy()
+        i, b = rng.randrange(2000), rng.randrange(100)
+        m[i, b] ^= 1 << rng.randrange(8)
+        assert oracle.multiset_hash(m) != h
+    # sum of parts (mod 2^128) equals the whole
+    assert oracle.mod128(oracle.multiset_hash(recs[:700]) + oracle.multiset_hash(recs[700:])) == h
+
+
+def test_sequence_digest_is_order_dependent_and_additive():
+    recs = gen.records(3000, seed=17).reshape(-1, 100)
+    d = oracle.sequence_digest(recs)
+    assert oracle.mod128(oracle.sequence_digest(recs[:1234]) + oracle.sequence_digest(recs[1234:], j0=1234)) == d
+    sw = recs.copy()
+    sw[[10, 11]] = sw[[11, 10]]
+    assert oracle.sequence_digest(sw) != d
+    out, _ = oracle.sort(recs)
+    assert oracle.sorted_digest(recs) == oracle.sequence_digest(out)
+
+
+def test_certificate():
+    recs = gen.records(4000, seed=19, dist="tiny_alphabet")
+    out, perm = oracle.sort(recs)
+    assert oracle.certify(recs, out, perm) == 0
+    # unstable tie order is rejected
+    o2, p2 = out.reshape(-1, 100).copy(), perm.copy()
+    k = _keys(out)
+    j = next(j for j in range(len(k) - 1) if k[j] == k[j + 1])
+    o2[[j, j + 1]] = o2[[j + 1, j]]
+    p2[[j, j + 1]] = p2[[j + 1, j]]
+    assert oracle.certify(recs, o2, p2) == j + 2
+    # non-permutation rejected
+    p3 = perm.copy()
+    p3[0] = p3[1]
+    assert oracle.certify(recs, out, p3) == 4001
+    # payload mismatch rejected
+    o4 = out.copy()
+    o4[150] ^= 0xFF
+    assert oracle.certify(recs, o4, perm) == 2
