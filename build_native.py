@@ -118,7 +118,7 @@ def build_leyenda(force=False, jobs=8):
         raise RuntimeError("libleyenda build failed")
     nccl_so = os.path.join(nccl_lib, "libnccl.so.2")
     link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out + ".tmp", *objs,
-            "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart", nccl_so,
+            "-L", nccl_lib, "-l:libnccl.so.2",
             "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", f"-rpath,{os.path.join(CUDA_HOME, 'lib64')}"]
     _run(link)
     os.replace(out + ".tmp", out)

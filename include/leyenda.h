@@ -1,0 +1,142 @@
+/* leyenda.h — C ABI of libleyenda.so: a B200-native (sm_100a) stable MSB radix sort of fixed 100-byte
+ * records, the hot path of Leyenda (arXiv 1909.08006).
+ *
+ * Citations: P:n = PAPER.md line n (the paper text), S:n = SPEC.md line n, BJ = BASELINE.json.
+ *   Problem statement: sort records of "a 10-byte key and 90-byte value" under a memory limit
+ *   ("only 30 GB of memory is allowed"), internally or externally ("able to adaptively
+ *   sort divergent workloads that may or may not fit into memory"). Signature: BJ north_star
+ *   "ley_sort(in, out, n_records, record_bytes=100, key_bytes=10, device_budget_bytes, stream)".
+ *
+ * RESULT (all entry points): the unique stable ascending arrangement out[j] = in[pi(j)] where pi orders
+ * record ordinals by (key bytes 0..9 compared as unsigned bytes, most significant first; then ordinal).
+ * Ties keep input order (BJ north_star "stable tie order"). Output is bit-identical
+ * across runs, budgets, thresholds/options and GPU counts.
+ *
+ * THREADING: calls on different devices may run concurrently; calls on the same device are serialised
+ * by a per-device mutex. ley_last_error() is thread-local.
+ *
+ * OWNERSHIP: the caller owns in, out, perm and the stream. The library owns a per-device cached device
+ * arena (allocated on first use, grown on demand, released by ley_release_cache), pinned host staging
+ * for the external path, internal events, and NCCL communicators created by ley_comm_init.
+ *
+ * ERRORS: every entry point returns a ley_status. On any error `out` (and `perm`) are unspecified,
+ * nothing the caller owns is freed, and ley_last_error() holds a stage-tagged message
+ * ("K-c split: an illegal memory access ..."). n_records == 0 returns LEY_OK without touching memory.
+ */
+#ifndef LEYENDA_H_
+#define LEYENDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LEY_OK = 0,
+  LEY_ERR_INVALID_ARGUMENT = 1, /* NULL with n>0; in/out (or perm) overlap; base not 16-byte aligned;
+                                   pointer on another device; unknown option name                      */
+  LEY_ERR_UNSUPPORTED = 2,      /* record_bytes != 100 or key_bytes != 10 (v1); pageable or managed
+                                   memory; in/out of different kinds (one host, one device)           */
+  LEY_ERR_BUDGET = 3,           /* device_budget_bytes below the minimum working set of every path   */
+  LEY_ERR_TOO_LARGE = 4,        /* n_records > 2^32 - 2 (u32 ordinals plus one sentinel) */
+  LEY_ERR_CAPACITY = 5,         /* dist: out_capacity_records < records this rank must hold          */
+  LEY_ERR_CUDA = 6,             /* a CUDA runtime error; text in ley_last_error()                     */
+  LEY_ERR_NCCL = 7              /* an NCCL error; text in ley_last_error()                            */
+} ley_status;
+
+#define LEY_RECORD_BYTES 100u
+#define LEY_KEY_BYTES 10u
+#define LEY_MAX_RECORDS 0xFFFFFFFEull
+
+/* ley_sort — stable ascending sort of n_records fixed-size records by key bytes [0, key_bytes).
+ *   in, out       : both DEVICE pointers on the current device (internal path: K-a .. K-e, §8a rows
+ *                   a1-a6), or both PINNED HOST pointers (cudaHostAlloc / cudaHostRegister). Host
+ *                   pointers take the staged-internal path when the working set fits
+ *                   device_budget_bytes, else the external path (run generation + merge-path K-way
+ *                   merge). Layout: n_records * record_bytes contiguous bytes, record i at
+ *                   byte offset i*record_bytes, key = its first key_bytes bytes. 16-byte aligned bases.
+ *                   Out-of-place only ("from the key to the tmp array"); `in` is never written.
+ *   n_records     : 0 .. 2^32-2.
+ *   record_bytes  : must be 100.   key_bytes: must be 10.
+ *   device_budget_bytes : cap on device memory the LIBRARY allocates for this call (caller buffers
+ *                   excluded); 0 = no cap (P:19's memory limit; BJ configs[4] "4 GB per GPU").
+ *   stream        : a cudaStream_t (0 = legacy default stream). Work is ordered after prior work on
+ *                   `stream`; v1 returns when `out` is complete (host-synchronous). */
+ley_status ley_sort(const void* in, void* out, uint64_t n_records, uint32_t record_bytes,
+                    uint32_t key_bytes, uint64_t device_budget_bytes, void* stream);
+
+/* ley_sort_perm — ley_sort that also writes perm[j] = input ordinal of output record j (u32, n_records
+ * entries, same memory kind as out). Verification hook; not the timed path. */
+ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_records,
+                         uint32_t record_bytes, uint32_t key_bytes, uint64_t device_budget_bytes,
+                         void* stream);
+
+/* Stage-tagged message for the last failing call on this thread ("" if none). Valid until the next
+ * call on this thread. */
+const char* ley_last_error(void);
+
+/* ---------------------------------------------------------------- multi-GPU (one process per GPU)
+ * BJ north_star: "Each GPU histograms the leading key bytes, all GPUs agree on range splitters, and
+ * records move to their owning GPU by an NCCL all-to-all over NVLink; each GPU then sorts its range
+ * locally, and the output is the concatenation of the ranges."
+ * Rank r passes its contiguous input slice (device memory); the global ordinal of local record i is
+ * (sum of n_local over ranks < r) + i. On return rank r holds global sorted positions
+ * [*out_global_offset, *out_global_offset + *n_out_local) with exact splitters:
+ * n_out_local(r) = floor((r+1) n / G) - floor(r n / G). Concatenating ranks 0..G-1 equals ley_sort of
+ * the concatenated input. */
+typedef struct ley_comm ley_comm;
+ley_status ley_comm_get_unique_id(uint8_t id_out[128]);  /* rank 0; broadcast it (e.g. torch PG)  */
+ley_status ley_comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);
+ley_status ley_sort_dist(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local,
+                         uint64_t out_capacity_records, uint64_t* n_out_local,
+                         uint64_t* out_global_offset, uint32_t record_bytes, uint32_t key_bytes,
+                         uint64_t device_budget_bytes, void* stream);
+ley_status ley_comm_destroy(ley_comm* comm);
+
+/* ---------------------------------------------------------------- introspection and tuning */
+
+/* Host-only plan query (no CUDA calls): device bytes the library allocates to sort n_records on one
+ * GPU in-core (internal path), and the path ley_sort would choose for host pointers under `budget`
+ * (0 = staged internal, 1 = external). Lets tests and callers size budgets. */
+typedef struct {
+  uint64_t n_records;
+  uint64_t tile_records;        /* K-a tile (records)                                    */
+  uint64_t tiles;               /* ceil(n / tile)                                        */
+  uint64_t chunk_records;       /* K-c / K-c' chunk (pairs)                              */
+  uint64_t internal_scratch;    /* bytes of library device memory for the internal path  */
+  uint64_t staged_bytes;        /* internal_scratch + in/out staging (host pointers)     */
+  int32_t host_path;            /* 0 = staged internal, 1 = external                    */
+  uint64_t run_records;         /* external: records per sorted run                      */
+  uint64_t runs;                /* external: number of runs                              */
+} ley_plan_info;
+ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_plan_info* info);
+
+/* Integer options (process-wide; they change speed, never output):
+ *   "warp_tier_max"  K-d: buckets up to this size use the one-warp tier       (1..32, default 32)
+ *   "smem_tier_max"  K-d: buckets up to this size are sorted in shared memory; larger ones recurse
+ *                    on the next key byte (Alg. 1 bigBucketThreshold) (0..16384, default 16384)
+ *   "kd_digit_bits"  K-d: max width of the in-CTA counting digit; 0 = pure comparison sort of each
+ *                    bucket (Alg. 1 ComparisonSort)                   (0..12, default 12)
+ *   "kd_insert_max"  K-d: sub-buckets up to this size use per-thread insertion sort, larger ones a
+ *                    warp bitonic network (tinyBucketThreshold)       (1..64, default 16)
+ *   "profile"        1 = record CUDA events around every stage (ley_stage_times)
+ *   "ext_run_records" external path: force the run size (records; 0 = from the budget)
+ * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
+ley_status ley_set_option(const char* name, int64_t value);
+ley_status ley_get_option(const char* name, int64_t* value);
+
+/* Per-stage device times (ms) of the last ley_sort on this thread when "profile" was 1. names[i] points
+ * to static strings. Returns the number of stages written (<= max). Kernel launch count of the last call
+ * is written to *launches. */
+int ley_stage_times(const char** names, float* ms, int max, int* launches);
+
+/* Free the cached arena of `device` (-1 = all devices). */
+ley_status ley_release_cache(int device);
+
+uint32_t ley_version(void); /* (major << 16) | minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEYENDA_H_ */

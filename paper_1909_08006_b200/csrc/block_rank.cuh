@@ -1,0 +1,88 @@
+// block_rank.cuh — stable block-wide ranking of one 8-bit digit per item (warp multi-split).
+//
+// The in-CTA counterpart of PAPER.md §3.1 line 96 ("compute a histogram based on the current radix to
+// decide the size of each bucket and where each key should be placed"): items are ranked in element
+// order e = warp * 32 * ITEMS + j * 32 + lane, so equal digits keep their input order (stability is
+// the whole correctness contract).
+#pragma once
+#include "common.cuh"
+
+namespace ley {
+
+// s_wh: [THREADS/32][256] u32 scratch; s_tmp: [32] u32.
+// Output: pos[j] = position of item j in the block's digit-sorted order; for threads < 256,
+// total_d / excl_d = count of digit d = threadIdx.x in the block and its exclusive offset.
+template <int THREADS, int ITEMS>
+__device__ __forceinline__ void block_rank_digits(const uint32_t (&dig)[ITEMS], uint32_t count, uint32_t (&pos)[ITEMS],
+                                                  uint32_t* s_wh, uint32_t* s_tmp, uint32_t& total_d,
+                                                  uint32_t& excl_d) {
+  constexpr int WARPS = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < WARPS * kRadix; i += THREADS) s_wh[i] = 0;
+  __syncthreads();
+  uint32_t* wh = s_wh + warp * kRadix;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
+    bool valid = e < count;
+    uint32_t d = dig[j];
+    uint32_t key = valid ? d : (0x100u | lane);
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t before = __popc(peers & lt);
+    uint32_t cur = valid ? wh[d] : 0;
+    __syncwarp();
+    if (valid && before == 0) wh[d] = cur + __popc(peers);
+    __syncwarp();
+    pos[j] = cur + before;
+  }
+  __syncthreads();
+  uint32_t total = 0;
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+#pragma unroll 4
+    for (int w = 0; w < WARPS; ++w) {
+      uint32_t v = s_wh[w * kRadix + d];
+      s_wh[w * kRadix + d] = total;
+      total += v;
+    }
+  }
+  uint32_t excl = block_excl_scan<THREADS>(threadIdx.x < kRadix ? total : 0, s_tmp, nullptr);
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+#pragma unroll 4
+    for (int w = 0; w < WARPS; ++w) s_wh[w * kRadix + d] += excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
+    if (e < count) pos[j] += wh[dig[j]];
+  }
+  total_d = total;
+  excl_d = excl;
+}
+
+// Decoupled look-back for digit d of chunk k whose segment starts at chunk k0: publishes the chunk's
+// aggregate, walks back until an inclusive prefix, publishes its own; returns the exclusive prefix.
+__device__ __forceinline__ uint32_t lookback_digit(uint64_t* status, uint64_t k, uint64_t k0, int d, uint32_t agg) {
+  if (k == k0) {
+    st_relaxed_u64(&status[k * kRadix + d], kFlagPrefix | agg);
+    return 0;
+  }
+  st_relaxed_u64(&status[k * kRadix + d], kFlagAggregate | agg);
+  uint32_t excl = 0;
+  uint64_t j = k - 1;
+  while (true) {
+    uint64_t s = ld_relaxed_u64(&status[j * kRadix + d]);
+    uint32_t f = status_flag(s);
+    if (f == 0) continue;
+    excl += (uint32_t)s;
+    if (f == 2) break;
+    --j;
+  }
+  st_relaxed_u64(&status[k * kRadix + d], kFlagPrefix | (uint64_t)(excl + agg));
+  return excl;
+}
+
+}  // namespace ley

@@ -1,0 +1,115 @@
+// common.cuh — shared device helpers and data-structure definitions of the sm_100a sort path.
+// Product code: shares nothing with oracle/ (SURVEY.md §8c).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "config.h"
+
+namespace ley {
+
+// A bucket still to be sorted: [start, start+len) of the pair buffer `parity` (0 = A, 1 = B),
+// key bytes [0, depth) already equal across the bucket (consumed by MSD splits).
+struct Seg {
+  uint32_t start;
+  uint32_t len;
+  uint32_t depth;
+  uint32_t parity;
+};
+
+// Work lists produced by classification (device-built; Alg. 1 smallBucketQueue).
+enum ListId : int {
+  kListWarp = 0,   // len <= warp_tier_max: one warp, register bitonic network
+  kListMed1 = 1,   // len <= 512:   one CTA (128 threads), shared memory
+  kListMed2 = 2,   // len <= 2048   (256 threads)
+  kListMed3 = 3,   // len <= 8192   (512 threads)
+  kListMed4 = 4,   // len <= 16384  (512 threads, 1 CTA/SM)
+  kListPass = 5,   // depth == 10: all key bytes equal -> already in index order
+  kNumKdLists = 6
+};
+constexpr uint32_t kMedCap[4] = {512, 2048, 8192, 16384};
+
+struct ListSet {
+  Seg* items[kNumKdLists];
+  uint32_t* counts;  // [kNumKdLists] device counters
+  uint32_t cap;      // capacity of each list
+};
+
+// Runtime tunables (ley_set_option); copied by value into kernels that need them.
+struct Tunables {
+  uint32_t warp_tier_max = kWarpTierMax;
+  uint32_t smem_tier_max = kSmemTierMax;
+  int kd_digit_bits = kKdMaxBits;
+  int kd_insert_max = 16;
+};
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ldg_nc_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_cs_v4(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Decoupled look-back status word: [33:32] flag, [31:0] value.
+constexpr uint64_t kFlagAggregate = 1ull << 32;
+constexpr uint64_t kFlagPrefix = 2ull << 32;
+__device__ __forceinline__ uint32_t status_flag(uint64_t s) { return (uint32_t)(s >> 32); }
+
+// Block-wide exclusive scan of one u32 per thread (THREADS <= 1024). `tmp` holds >= 32 words.
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {
+  constexpr int WARPS = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < WARPS) tmp[lane] = w;  // inclusive per-warp totals
+  }
+  __syncthreads();
+  uint32_t warp_excl = warp ? tmp[warp - 1] : 0;
+  if (total) *total = tmp[WARPS - 1];
+  uint32_t r = warp_excl + x - v;
+  __syncthreads();  // tmp reusable after return
+  return r;
+}
+
+// Composite (key-tail, ordinal) order: the strict total order of the sort.
+__device__ __forceinline__ bool pair_less(uint64_t ta, uint32_t ia, uint64_t tb, uint32_t ib) {
+  return ta < tb || (ta == tb && ia < ib);
+}
+
+}  // namespace ley

@@ -1,0 +1,35 @@
+// config.h — compile-time geometry shared by the kernels and the host planner (plain C++).
+#pragma once
+#include <stdint.h>
+
+namespace ley {
+
+constexpr uint32_t kRecordBytes = 100;   // P:126 "100-byte records"
+constexpr uint32_t kKeyBytes = 10;       // P:126 "10-byte key"
+constexpr uint32_t kRecordWords = 25;    // 100 / 4
+
+// K-a tile: THREADS x ITEMS records (tile-local stable sort by key byte 0, P:59 ParallelRadixSort).
+constexpr int kTileThreads = 512;
+constexpr int kTileItems = 8;
+constexpr uint32_t kTileRecords = kTileThreads * kTileItems;  // 4096, power of two (< 2^24)
+constexpr uint32_t kTileLog2 = 12;
+static_assert((1u << kTileLog2) == kTileRecords, "tile must be a power of two");
+
+// K-c / K-c' chunk: THREADS x ITEMS (key-tail, index) pairs.
+constexpr int kSplitThreads = 512;
+constexpr int kSplitItems = 8;
+constexpr uint32_t kChunk = kSplitThreads * kSplitItems;  // 4096
+
+constexpr int kRadix = 256;
+
+// K-b block tile
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr uint32_t kScanTile = kScanThreads * kScanItems;
+
+// K-d tiers (Algorithm 1: bigBucketThreshold / tinyBucketThreshold).
+constexpr uint32_t kWarpTierMax = 32;
+constexpr uint32_t kSmemTierMax = 16384;
+constexpr int kKdMaxBits = 12;
+
+}  // namespace ley

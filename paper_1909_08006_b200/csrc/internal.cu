@@ -1,0 +1,188 @@
+// internal.cu — the 1-GPU internal sort driver: Algorithm 1 (§3.1, lines 54-90) on the device.
+//
+//   K-a  tile-local sort by byte 0 + hist16            (ParallelRadixSort, radix 0; P:102 extraction)
+//   K-b  scans: tile runs -> global byte-0 positions; hist16 -> level-1 bucket bases
+//   K-c  split every byte-0 bucket on byte 1           (the next round of ParallelRadixSort)
+//   classify level-1 buckets                           (big -> recurse P:62-63; small -> queue P:65-66)
+//   K-d  sort the queued buckets (warp / CTA tiers)    (SingleThreadRadixSort + ComparisonSort)
+//   loop while big buckets remain: K-c' on byte depth (MSDRadixSort(key, radix+1, k)) + K-d
+//   K-e  gather the records by the sorted ordinals     (record scatter of P:104-106)
+//
+// All work is on the caller's stream. The only host synchronisations are one 4-byte read of the
+// big-bucket count per recursion level (usually exactly one per call) and the final completion wait.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace ley {
+
+namespace {
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                                cudaStream_t s, Profiler& prof) {
+  const InternalLayout L = plan_internal(n);
+  ley_status st = ensure_buffer(ctx.work, L.bytes, "workspace", s);
+  if (st) return st;
+  if (!ctx.host_pinned) LEY_CUDA("setup", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  uint8_t* base = static_cast<uint8_t*>(ctx.work.ptr);
+  uint64_t* At = reinterpret_cast<uint64_t*>(base + L.off_At);
+  uint32_t* Ai = reinterpret_cast<uint32_t*>(base + L.off_Ai);
+  uint64_t* Bt = reinterpret_cast<uint64_t*>(base + L.off_Bt);
+  uint32_t* Bi = reinterpret_cast<uint32_t*>(base + L.off_Bi);
+  uint32_t* perm = reinterpret_cast<uint32_t*>(base + L.off_perm);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(base + L.off_cnt);
+  uint32_t* off = reinterpret_cast<uint32_t*>(base + L.off_off);
+  uint32_t* lo = reinterpret_cast<uint32_t*>(base + L.off_lo);
+  uint32_t* hist16 = reinterpret_cast<uint32_t*>(base + L.off_hist16);
+  uint32_t* B16 = reinterpret_cast<uint32_t*>(base + L.off_B16);
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(base + L.off_cstart);
+  uint64_t* scan_status = reinterpret_cast<uint64_t*>(base + L.off_scan_status);
+  uint64_t* split_status = reinterpret_cast<uint64_t*>(base + L.off_split_status);
+  uint32_t* small = reinterpret_cast<uint32_t*>(base + L.off_small);
+  uint32_t* tickets = small;          // [0..15]
+  uint32_t* kd_counts = small + 16;   // [kNumKdLists]
+  uint32_t* big_count = small + 32;   // [1]
+  uint32_t* host_cnt = static_cast<uint32_t*>(ctx.host_pinned);
+
+  const Options o = options_snapshot();
+  Tunables tu;
+  tu.warp_tier_max = (uint32_t)o.warp_tier_max;
+  tu.smem_tier_max = (uint32_t)o.smem_tier_max;
+  tu.kd_digit_bits = (int)o.kd_digit_bits;
+  tu.kd_insert_max = (int)o.kd_insert_max;
+  const uint32_t tiles = (uint32_t)L.tiles;
+  const int sms = ctx.sms;
+  int& launches = prof.launches;
+
+  // ---------------------------------------------------------------- zero counters / look-back state
+  if ((st = prof.begin("init"))) return st;
+  LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4 * 65536, s));
+  LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * 64, s));
+  LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
+  LEY_CUDA("init", cudaMemsetAsync(split_status, 0, 8 * (size_t)kRadix * L.split_chunks_ub, s));
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- K-a
+  if ((st = prof.begin("K-a tile sort"))) return st;
+  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, s));
+  ++launches;
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- K-b
+  if ((st = prof.begin("K-b scan"))) return st;
+  LEY_CUDA("K-b scan", launch_scan_excl(cnt, off, L.m, scan_status, tickets + 0, off + L.m, s));
+  LEY_CUDA("K-b scan", launch_scan_excl(hist16, B16, 65536, scan_status + L.scan_status_words, tickets + 1,
+                                        B16 + 65536, s));
+  LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
+  launches += 3;
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- K-c (byte 1)
+  if ((st = prof.begin("K-c split"))) return st;
+  LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart, split_status, tickets + 2,
+                                               Bt, Bi, (uint32_t)L.split_chunks_ub, s));
+  ++launches;
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- classify level 1, K-d
+  if ((st = prof.begin("K-d buckets"))) return st;
+  uint64_t tier = std::max<uint64_t>(tu.smem_tier_max, tu.warp_tier_max);
+  uint64_t big_cap = std::min<uint64_t>(65536, n / (tier + 1) + 1);
+  uint32_t kd_cap = 65536;
+  if ((st = ensure_buffer(ctx.lists, (size_t)kNumKdLists * a256((size_t)kd_cap * sizeof(Seg)), "K-d lists", s)))
+    return st;
+  if ((st = ensure_buffer(ctx.big[0], big_cap * sizeof(Seg), "big-bucket list", s))) return st;
+  ListSet kd;
+  auto bind_lists = [&](uint32_t cap) {
+    for (int l = 0; l < kNumKdLists; ++l)
+      kd.items[l] = reinterpret_cast<Seg*>(static_cast<uint8_t*>(ctx.lists.ptr) + l * a256((size_t)cap * sizeof(Seg)));
+    kd.counts = kd_counts;
+    kd.cap = cap;
+  };
+  bind_lists(kd_cap);
+  LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
+  ++launches;
+  LEY_CUDA("K-d buckets", launch_kd_all(kd, At, Ai, Bt, Bi, perm, tu, sms, s, &launches));
+  LEY_CUDA("K-d buckets", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("K-d buckets", cudaStreamSynchronize(s));
+  uint32_t nbig = host_cnt[0];
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- recursion on big buckets
+  if (nbig) {
+    if ((st = prof.begin("K-c' recursion"))) return st;
+  }
+  int cur = 0;
+  while (nbig) {
+    const uint64_t chunks_ub = n / kChunk + nbig + 1;
+    const uint64_t child_cap = std::min<uint64_t>((uint64_t)nbig * kRadix, n + 1);
+    const uint64_t next_big_cap = std::min<uint64_t>(child_cap, n / (tier + 1) + 1);
+    const size_t scan_words = scan_status_words(nbig);
+    // rec layout: nch | cstart2 | seg_hist | seg_excl | noscatter | scan status | split status | tickets
+    size_t r_nch = 0, r_cst = a256(4ull * (nbig + 1)), r_hist = r_cst + a256(4ull * (nbig + 1));
+    size_t r_excl = r_hist + a256(4ull * nbig * kRadix), r_nos = r_excl + a256(4ull * nbig * kRadix);
+    size_t r_scan = r_nos + a256(nbig), r_stat = r_scan + a256(8 * scan_words);
+    size_t r_tick = r_stat + a256(8ull * kRadix * chunks_ub), r_end = r_tick + 256;
+    if ((st = ensure_buffer(ctx.rec, r_end, "recursion arrays", s))) return st;
+    if (child_cap > kd.cap) {
+      if ((st = ensure_buffer(ctx.lists, (size_t)kNumKdLists * a256(child_cap * sizeof(Seg)), "K-d lists", s)))
+        return st;
+      bind_lists((uint32_t)child_cap);
+    }
+    if ((st = ensure_buffer(ctx.big[cur ^ 1], std::max<uint64_t>(next_big_cap, 1) * sizeof(Seg), "big-bucket list",
+                            s)))
+      return st;
+    uint8_t* rb = static_cast<uint8_t*>(ctx.rec.ptr);
+    uint32_t* nch = reinterpret_cast<uint32_t*>(rb + r_nch);
+    uint32_t* cst = reinterpret_cast<uint32_t*>(rb + r_cst);
+    uint32_t* seg_hist = reinterpret_cast<uint32_t*>(rb + r_hist);
+    uint32_t* seg_excl = reinterpret_cast<uint32_t*>(rb + r_excl);
+    uint8_t* noscatter = rb + r_nos;
+    uint64_t* rscan = reinterpret_cast<uint64_t*>(rb + r_scan);
+    uint64_t* rstat = reinterpret_cast<uint64_t*>(rb + r_stat);
+    uint32_t* rtick = reinterpret_cast<uint32_t*>(rb + r_tick);
+    const Seg* segs = static_cast<const Seg*>(ctx.big[cur].ptr);
+    Seg* next_big = static_cast<Seg*>(ctx.big[cur ^ 1].ptr);
+
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(seg_hist, 0, 4ull * nbig * kRadix, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(rscan, 0, 8 * scan_words, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(rstat, 0, 8ull * kRadix * chunks_ub, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(rtick, 0, 256, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(kd_counts, 0, 4 * kNumKdLists, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(big_count, 0, 4, s));
+    LEY_CUDA("K-c' recursion", launch_kr_nchunks(segs, nbig, nch, s));
+    LEY_CUDA("K-c' recursion", launch_scan_excl(nch, cst, nbig, rscan, rtick + 0, cst + nbig, s));
+    uint32_t hist_grid = (uint32_t)std::min<uint64_t>(chunks_ub, (uint64_t)sms * 8);
+    LEY_CUDA("K-c' recursion", launch_kr_hist(segs, nbig, cst, hist_grid, At, Bt, seg_hist, s));
+    LEY_CUDA("K-c' recursion",
+             launch_kr_plan(segs, nbig, seg_hist, seg_excl, noscatter, tu, kd, next_big, big_count, s));
+    LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rstat, rtick + 1,
+                                              (uint32_t)chunks_ub, s));
+    launches += 5;
+    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm, tu, sms, s, &launches));
+    LEY_CUDA("K-c' recursion", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
+    nbig = host_cnt[0];
+    cur ^= 1;
+    if (!nbig) {
+      if ((st = prof.end())) return st;
+    }
+  }
+
+  // ---------------------------------------------------------------- K-e
+  if ((st = prof.begin("K-e gather"))) return st;
+  LEY_CUDA("K-e gather", launch_ke_gather(in, perm, n, out, sms, s, &launches));
+  if ((st = prof.end())) return st;
+  if (perm_out) {
+    cudaPointerAttributes pa{};
+    LEY_CUDA("perm", cudaPointerGetAttributes(&pa, perm_out));
+    cudaMemcpyKind kind = pa.type == cudaMemoryTypeDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    LEY_CUDA("perm", cudaMemcpyAsync(perm_out, perm, 4 * n, kind, s));
+  }
+  return LEY_OK;
+}
+
+}  // namespace ley

@@ -1,0 +1,271 @@
+// k_bucket.cu — K-d: per-bucket sort of (key-tail, index) pairs, plus level-1 classification.
+//
+// PAPER.md §3.1 Algorithm 1 lines 65-85: buckets below bigBucketThreshold go to smallBucketQueue and
+// are finished by one worker each — SingleThreadRadixSort on the next radix, then ComparisonSort for
+// buckets under tinyBucketThreshold ("size is small enough for comparison-based sort to perform
+// more efficient than Radix Sort"). On the GPU a "worker" is a warp (tiny buckets, register bitonic
+// network over the composite (tail, index)) or a CTA (shared-memory counting pass on the next 1..12 key
+// bits, then per-sub-bucket comparison sort). SURVEY.md §8a row a5.
+//
+// Every bucket writes perm[start .. start+len) = input ordinals in sorted order. The comparison order is
+// the composite (tail, index), which is the sort's strict total order, so the result does not depend on
+// the (non-deterministic) atomics used to place elements inside a CTA.
+#include "classify.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ley {
+namespace {
+
+__global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
+                                   Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= 65536) return;
+  Seg s{B16[p], hist16[p], 2u, 1u};
+  classify_bucket(s, tu, kd, big_out, big_count);
+}
+
+// ---------------------------------------------------------------------------- warp tier (len <= 32)
+__global__ void __launch_bounds__(256)
+    kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
+                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
+                 uint32_t* __restrict__ perm) {
+  const uint32_t nitems = *count;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems; it += nwarps) {
+    const Seg sg = list[it];
+    const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
+    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
+    uint64_t t = ~0ull;
+    uint32_t x = ~0u;
+    if ((uint32_t)lane < sg.len) {
+      t = tp[lane];
+      x = ip[lane];
+    }
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        uint64_t ot = __shfl_xor_sync(0xffffffffu, t, j);
+        uint32_t ox = __shfl_xor_sync(0xffffffffu, x, j);
+        bool up = (lane & k) == 0;
+        bool lower = (lane & j) == 0;
+        bool take = (lower == up) ? pair_less(ot, ox, t, x) : pair_less(t, x, ot, ox);
+        if (take) {
+          t = ot;
+          x = ox;
+        }
+      }
+    }
+    if ((uint32_t)lane < sg.len) perm[sg.start + lane] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------- pass-through (depth 10)
+__global__ void kd_passthrough(const Seg* __restrict__ list, const uint32_t* __restrict__ count,
+                               const uint32_t* __restrict__ i0, const uint32_t* __restrict__ i1,
+                               uint32_t* __restrict__ perm) {
+  const uint32_t nitems = *count;
+  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const Seg sg = list[it];
+    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
+    for (uint32_t i = threadIdx.x; i < sg.len; i += blockDim.x) perm[sg.start + i] = ip[i];
+  }
+}
+
+// ---------------------------------------------------------------------------- CTA tier
+// In-smem all-ascending bitonic network over [b, e) by one warp; virtual +inf padding beyond e never
+// moves, so compare-exchanges touching it are skipped.
+__device__ void warp_bitonic_smem(uint64_t* st, uint32_t* si, uint32_t b, uint32_t e) {
+  const uint32_t sz = e - b;
+  uint32_t P = 1;
+  while (P < sz) P <<= 1;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    const uint32_t hk = k >> 1;
+    for (uint32_t q = lane; q < P / 2; q += 32) {  // flip step: (blk*k + r, blk*k + k-1-r)
+      uint32_t blk = q / hk, r = q % hk;
+      uint32_t lo = blk * k + r, hi = blk * k + k - 1 - r;
+      if (hi < sz) {
+        uint64_t ta = st[b + lo], tb = st[b + hi];
+        uint32_t xa = si[b + lo], xb = si[b + hi];
+        if (pair_less(tb, xb, ta, xa)) {
+          st[b + lo] = tb; st[b + hi] = ta;
+          si[b + lo] = xb; si[b + hi] = xa;
+        }
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = hk >> 1; j > 0; j >>= 1) {
+      for (uint32_t q = lane; q < P / 2; q += 32) {
+        uint32_t lo = (q / j) * 2 * j + (q % j), hi = lo + j;
+        if (hi < sz) {
+          uint64_t ta = st[b + lo], tb = st[b + hi];
+          uint32_t xa = si[b + lo], xb = si[b + hi];
+          if (pair_less(tb, xb, ta, xa)) {
+            st[b + lo] = tb; st[b + hi] = ta;
+            si[b + lo] = xb; si[b + hi] = xa;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <uint32_t CAP>
+__host__ __device__ constexpr uint32_t kd_bins() {
+  return CAP >= 4096 ? 4096u : CAP;  // <= 2^12 counting bins
+}
+template <uint32_t CAP>
+__host__ __device__ constexpr size_t kd_smem() {
+  return (size_t)CAP * 12 + (size_t)(2 * kd_bins<CAP>() + 1) * 4 + 64 * 4 + 16;
+}
+
+template <uint32_t CAP, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
+                const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
+                uint32_t* __restrict__ perm, Tunables tu) {
+  constexpr uint32_t BINS = kd_bins<CAP>();
+  constexpr int WARPS = THREADS / 32;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + CAP);
+  uint32_t* s_beg = s_idx + CAP;            // [BINS + 1]
+  uint32_t* s_cur = s_beg + BINS + 1;       // [BINS]
+  uint32_t* s_tmp = s_cur + BINS;           // [32] scan tmp, [32] = #big sub-buckets, [33..] list
+  uint32_t* s_nbig = s_tmp + 32;
+  uint32_t* s_big = s_tmp + 33;             // reuses s_cur after placement (see below)
+
+  const uint32_t nitems = *count;
+  const int warp = threadIdx.x >> 5;
+  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const Seg sg = list[it];
+    const uint32_t s = sg.len;
+    const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
+    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
+    const uint32_t avail = 8u * (kKeyBytes - sg.depth);  // unconsumed key bits held in the tail
+    uint32_t bits = s > 1 ? 32u - __clz(s - 1) : 0u;
+    bits = min(bits, (uint32_t)tu.kd_digit_bits);
+    bits = min(bits, avail);
+    bits = min(bits, 31u - __clz(BINS));
+    const uint32_t shift = avail - bits;
+    const uint32_t nb = 1u << bits;
+    const uint32_t mask = nb - 1;
+    auto digit = [&](uint64_t t) -> uint32_t { return bits ? (uint32_t)(t >> shift) & mask : 0u; };
+
+    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_cur[g] = 0;
+    if (threadIdx.x == 0) *s_nbig = 0;
+    __syncthreads();
+    // pass 1: sub-bucket sizes on the next `bits` key bits
+    for (uint32_t i = threadIdx.x; i < s; i += THREADS) atomicAdd(&s_cur[digit(tp[i])], 1u);
+    __syncthreads();
+    // exclusive scan of the nb counters (contiguous slice per thread)
+    {
+      const uint32_t per = (nb + THREADS - 1) / THREADS;
+      const uint32_t g0 = threadIdx.x * per;
+      uint32_t sum = 0;
+      for (uint32_t g = g0; g < min(nb, g0 + per); ++g) sum += s_cur[g];
+      uint32_t run = block_excl_scan<THREADS>(sum, s_tmp, nullptr);
+      for (uint32_t g = g0; g < min(nb, g0 + per); ++g) {
+        uint32_t c = s_cur[g];
+        s_beg[g] = run;
+        s_cur[g] = run;
+        run += c;
+      }
+      if (threadIdx.x == 0) s_beg[nb] = s;
+    }
+    __syncthreads();
+    // pass 2: place (tail, idx) into its sub-bucket (order inside fixed later by the composite sort)
+    for (uint32_t i = threadIdx.x; i < s; i += THREADS) {
+      uint64_t t = tp[i];
+      uint32_t x = ip[i];
+      uint32_t p = atomicAdd(&s_cur[digit(t)], 1u);
+      s_tail[p] = t;
+      s_idx[p] = x;
+    }
+    __syncthreads();
+    // comparison sort of every sub-bucket: insertion (tiny) or warp bitonic (larger)
+    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) {
+      uint32_t b = s_beg[g], e = s_beg[g + 1];
+      uint32_t sz = e - b;
+      if (sz <= 1) continue;
+      if (sz <= (uint32_t)tu.kd_insert_max) {
+        for (uint32_t i = b + 1; i < e; ++i) {
+          uint64_t t = s_tail[i];
+          uint32_t x = s_idx[i];
+          uint32_t j = i;
+          while (j > b && pair_less(t, x, s_tail[j - 1], s_idx[j - 1])) {
+            s_tail[j] = s_tail[j - 1];
+            s_idx[j] = s_idx[j - 1];
+            --j;
+          }
+          s_tail[j] = t;
+          s_idx[j] = x;
+        }
+      } else {
+        uint32_t q = atomicAdd(s_nbig, 1u);
+        s_cur[q] = g;  // s_cur is dead after placement: reuse as the big-sub-bucket list
+      }
+    }
+    __syncthreads();
+    const uint32_t nbig = *s_nbig;
+    for (uint32_t q = warp; q < nbig; q += WARPS) {
+      uint32_t g = s_cur[q];
+      warp_bitonic_smem(s_tail, s_idx, s_beg[g], s_beg[g + 1]);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_idx[i];
+    __syncthreads();
+  }
+  (void)s_big;
+}
+
+template <uint32_t CAP, int THREADS>
+cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
+                            const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
+                            cudaStream_t s) {
+  auto kern = kd_cta_sort<CAP, THREADS>;
+  const size_t smem = kd_smem<CAP>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
+                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s) {
+  kd_classify_level1<<<256, 256, 0, s>>>(hist16, B16, tu, kd, big_out, big_count);
+  return cudaGetLastError();
+}
+
+// All K-d tiers for the lists of one level (counts are read on the device; no host sync).
+cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
+                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, cudaStream_t s,
+                          int* launches) {
+  cudaError_t e;
+  kd_warp_sort<<<sms * 8, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, s)))
+    return e;
+  if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, s)))
+    return e;
+  if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, s)))
+    return e;
+  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms, s)))
+    return e;
+  kd_passthrough<<<sms * 4, 256, 0, s>>>(kd.items[kListPass], kd.counts + kListPass, i0, i1, perm);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (launches) *launches += 6;
+  return cudaSuccess;
+}
+
+}  // namespace ley

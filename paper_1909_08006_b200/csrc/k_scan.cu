@@ -1,0 +1,102 @@
+// k_scan.cu — K-b: single-pass decoupled-lookback device-wide exclusive scan,
+// plus the small planning kernels that turn scanned histograms into work decompositions.
+//
+// PAPER.md §3.1 line 96: "we first compute a histogram based on the current radix to decide the size of
+// each bucket and where each key should be placed" — the "where" is an exclusive prefix sum over the
+// histogram. Over the bucket-major count matrix cnt[b * tiles + t] written by K-a it yields, for every
+// (byte-0 value b, tile t), the global position of tile t's run of b in the byte-0-ordered sequence.
+// Over hist16 it yields the level-1 bucket bases B16[p] (p = key bytes 0..1).
+//
+// Block tiles are claimed with an atomic ticket, so every block a block waits on is already resident
+// (forward progress). Status words pack [flag | value] in 64 bits and are read/written with relaxed
+// gpu-scope 64-bit accesses (single-copy atomic), so no torn reads.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ley {
+namespace {
+
+__global__ void __launch_bounds__(kScanThreads)
+    kb_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t m,
+                 uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, uint32_t* __restrict__ total_out) {
+  __shared__ uint32_t s_tmp[32];
+  __shared__ uint32_t s_blk;
+  __shared__ uint32_t s_prefix;
+  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const uint64_t base = (uint64_t)blk * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+
+  uint32_t v[kScanItems];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < m) ? in[base + i] : 0u;
+    sum += v[i];
+  }
+  uint32_t agg;
+  uint32_t texcl = block_excl_scan<kScanThreads>(sum, s_tmp, &agg);
+
+  if (threadIdx.x == 0) {
+    uint32_t excl = 0;
+    if (blk == 0) {
+      st_relaxed_u64(&status[0], kFlagPrefix | agg);
+    } else {
+      st_relaxed_u64(&status[blk], kFlagAggregate | agg);
+      int64_t j = (int64_t)blk - 1;
+      while (true) {
+        uint64_t s = ld_relaxed_u64(&status[j]);
+        uint32_t f = status_flag(s);
+        if (f == 0) continue;
+        excl += (uint32_t)s;
+        if (f == 2) break;
+        --j;
+      }
+      st_relaxed_u64(&status[blk], kFlagPrefix | (uint64_t)(excl + agg));
+    }
+    s_prefix = excl;
+    if (total_out && (uint64_t)(blk + 1) * kScanTile >= m) *total_out = excl + agg;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + texcl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < m) out[base + i] = run;
+    run += v[i];
+  }
+}
+
+// Level-1 decomposition (K-c): byte-0 segment b = [B16[256 b], B16[256 (b+1)]) of the byte-0-ordered
+// sequence; it is cut into ceil(len / chunk) chunks; cstart = exclusive scan of the chunk counts.
+__global__ void kc_plan_chunks(const uint32_t* __restrict__ B16, uint64_t n, uint32_t chunk,
+                               uint32_t* __restrict__ cstart) {
+  __shared__ uint32_t s_tmp[32];
+  const int b = threadIdx.x;  // 256 threads
+  uint64_t beg = B16[b * 256];
+  uint64_t end = (b < 255) ? B16[(b + 1) * 256] : n;
+  uint32_t nch = (uint32_t)((end - beg + chunk - 1) / chunk);
+  uint32_t total;
+  uint32_t ex = block_excl_scan<256>(nch, s_tmp, &total);
+  cstart[b] = ex;
+  if (b == 0) cstart[256] = total;
+}
+
+}  // namespace
+
+cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
+                             uint32_t* total_out, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  uint64_t blocks = (m + kScanTile - 1) / kScanTile;
+  kb_scan_excl<<<(unsigned)blocks, kScanThreads, 0, s>>>(in, out, m, status, ticket, total_out);
+  return cudaGetLastError();
+}
+
+uint64_t scan_status_words(uint64_t m) { return (m + kScanTile - 1) / kScanTile; }
+
+cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
+                                  cudaStream_t s) {
+  kc_plan_chunks<<<1, 256, 0, s>>>(B16, n, chunk, cstart);
+  return cudaGetLastError();
+}
+
+}  // namespace ley

@@ -1,0 +1,371 @@
+// k_split.cu — K-c / K-c': stable segmented scatter of (key-tail, index) pairs into MSB buckets.
+//
+// PAPER.md §3.1 line 96 (cache-aware scattering: "we then scatter the keys to their bucket offsets by
+// copying from the key to the tmp array ... this scattering process takes the most time in radix sort")
+// and Algorithm 1 lines 59-63 (after the first round every bucket is split again on the next radix;
+// "if k > bigBucketThreshold then MSDRadixSort(key, radix + 1, k)"). SURVEY.md §8a rows a3 and a4.
+//
+// K-c (level 1): byte-0 bucket b is the concatenation, in tile order, of the byte-0 runs K-a left in
+// every tile. Each CTA takes one chunk (kChunk consecutive pairs of one bucket, claimed by atomic ticket
+// in global chunk order), gathers it from the runs, ranks it stably by key byte 1 (warp multi-split),
+// finds its per-digit offset inside the bucket by decoupled look-back over the bucket's earlier chunks,
+// stages the pairs in shared memory in digit order and writes them to their 16-bit bucket
+// B16[b:d] + offset. Output pair: tail = key bytes 2..9 big-endian (u64), idx = global ordinal (u32).
+//
+// K-c' (level >= 2): the same on contiguous big buckets, digit = key byte `depth`; the bucket's digit
+// histogram comes from kr_hist and its children are classified by kr_plan before the split.
+#include "block_rank.cuh"
+#include "classify.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ley {
+namespace {
+
+constexpr int kThreads = kSplitThreads;
+constexpr int kItems = kSplitItems;
+constexpr int kWarps = kThreads / 32;
+
+struct SplitSmem {
+  static constexpr size_t kRegionA = (size_t)kChunk * 13 + 16;          // tails u64 + idx u32 + digit u8
+  static constexpr size_t kRuns = (size_t)(kChunk + 1) * 8;              // run_v u32 + run_src u32
+  static constexpr size_t kRegion = kRegionA > kRuns ? kRegionA : kRuns;
+  static constexpr size_t kWh = (size_t)kWarps * kRadix * 4;
+  static constexpr size_t kBytes = kRegion + kWh + 256 * 4 + 64 * 4;
+};
+
+// largest i in [lo, hi) with a[i] <= v (a non-decreasing, a[lo] <= v)
+__device__ __forceinline__ uint32_t search_le(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t v) {
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ uint64_t search_le_g(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t v) {
+  while (hi - lo > 1) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    kc_split_level1(const uint64_t* __restrict__ k1_in, const uint32_t* __restrict__ w_in, uint32_t tiles,
+                    const uint32_t* __restrict__ off /*[256*tiles+1]*/, const uint32_t* __restrict__ lo,
+                    const uint32_t* __restrict__ B16, uint64_t n, const uint32_t* __restrict__ cstart,
+                    uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, uint64_t* __restrict__ tail_out,
+                    uint32_t* __restrict__ idx_out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* region = smem;
+  uint32_t* s_wh = reinterpret_cast<uint32_t*>(smem + SplitSmem::kRegion);
+  uint32_t* s_dst = s_wh + kWarps * kRadix;
+  uint32_t* s_misc = s_dst + 256;  // [0..31] scan tmp, [32..] scalars
+  uint32_t* run_v = reinterpret_cast<uint32_t*>(region);
+  uint32_t* run_src = run_v + (kChunk + 1);
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(region);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
+  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kChunk);
+
+  if (threadIdx.x == 0) {
+    uint32_t k = atomicAdd(ticket, 1u);
+    s_misc[32] = k;
+    if (k < cstart[256]) {
+      // segment (byte-0 value) holding chunk k
+      uint32_t b = 0, hi = 256;
+      while (hi - b > 1) {
+        uint32_t mid = (b + hi) >> 1;
+        if (cstart[mid] <= k) b = mid; else hi = mid;
+      }
+      uint32_t c = k - cstart[b];
+      uint32_t seg_beg = B16[b * 256];
+      uint64_t seg_end = (b < 255) ? B16[(b + 1) * 256] : n;
+      uint32_t v0 = seg_beg + c * kChunk;
+      uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
+      const uint32_t* off_b = off + (uint64_t)b * tiles;
+      uint32_t t0 = (uint32_t)search_le_g(off_b, 0, tiles, v0);
+      uint32_t t1 = (uint32_t)search_le_g(off_b, t0, tiles, v0 + cnt - 1);
+      s_misc[33] = b;
+      s_misc[34] = v0;
+      s_misc[35] = cnt;
+      s_misc[36] = t0;
+      s_misc[37] = t1;
+      s_misc[38] = k - c;  // first chunk of the segment
+    }
+  }
+  __syncthreads();
+  const uint32_t k = s_misc[32];
+  if (k >= cstart[256]) return;
+  const uint32_t b = s_misc[33], v0 = s_misc[34], cnt = s_misc[35], t0 = s_misc[36], t1 = s_misc[37];
+  const uint32_t k0 = s_misc[38];
+  const uint32_t* off_b = off + (uint64_t)b * tiles;
+
+  // ---- compact the non-empty runs of tiles [t0, t1] into (virtual start, source base)
+  uint32_t nruns = 0;
+  for (uint32_t tb = t0; tb <= t1; tb += kThreads) {
+    uint32_t t = tb + threadIdx.x;
+    uint32_t vs = 0, len = 0;
+    if (t <= t1) {
+      uint64_t fi = (uint64_t)b * tiles + t;
+      vs = off[fi];
+      len = off[fi + 1] - vs;
+    }
+    uint32_t flag = len > 0 ? 1u : 0u, tot;
+    uint32_t ex = block_excl_scan<kThreads>(flag, s_misc, &tot);
+    if (flag) {
+      run_v[nruns + ex] = vs;
+      run_src[nruns + ex] = ((uint32_t)t << kTileLog2) + lo[(uint64_t)t * kRadix + b] - vs;
+    }
+    nruns += tot;
+  }
+  __syncthreads();
+  (void)off_b;
+
+  // ---- gather the chunk's pairs (element order = virtual order = stable order)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t src[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+    uint32_t v = v0 + e;
+    src[j] = 0;
+    if (e < cnt) {
+      uint32_t r = search_le(run_v, 0, nruns, v);
+      src[j] = run_src[r] + v;
+    }
+  }
+  uint64_t k1[kItems];
+  uint32_t w[kItems], dig[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+    if (e < cnt) {
+      k1[j] = k1_in[src[j]];
+      w[j] = w_in[src[j]];
+    } else {
+      k1[j] = 0;
+      w[j] = 0;
+    }
+    dig[j] = (uint32_t)(k1[j] >> 56);
+  }
+  __syncthreads();  // run tables dead from here on
+
+  uint32_t pos[kItems], total_d, excl_d;
+  block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+    uint32_t pre = lookback_digit(status, k, k0, d, total_d);
+    s_dst[d] = B16[b * 256 + d] + pre - excl_d;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+    if (e < cnt) {
+      uint32_t p = pos[j];
+      s_tail[p] = (k1[j] << 8) | (w[j] >> 24);
+      s_idx[p] = (src[j] & ~(kTileRecords - 1)) | (w[j] & 0xFFFFFFu);
+      s_dig[p] = (uint8_t)dig[j];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+    uint32_t g = s_dst[s_dig[i]] + i;
+    tail_out[g] = s_tail[i];
+    idx_out[g] = s_idx[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------ level >= 2
+// chunk -> segment of the current big list
+__device__ __forceinline__ uint32_t chunk_segment(const uint32_t* cstart, uint32_t nseg, uint32_t k) {
+  uint32_t s = 0, hi = nseg;
+  while (hi - s > 1) {
+    uint32_t mid = (s + hi) >> 1;
+    if (cstart[mid] <= k) s = mid; else hi = mid;
+  }
+  return s;
+}
+
+__device__ __forceinline__ uint32_t byte_of_tail(uint64_t tail, uint32_t depth) {
+  return (uint32_t)(tail >> (8 * (9 - depth))) & 0xFFu;  // tail = key bytes 2..9
+}
+
+__global__ void kr_nchunks(const Seg* __restrict__ segs, uint32_t nseg, uint32_t* __restrict__ nch) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) nch[s] = (segs[s].len + kChunk - 1) / kChunk;
+}
+
+__global__ void __launch_bounds__(256)
+    kr_hist(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart, uint32_t nchunks_total_ub,
+            const uint64_t* __restrict__ tails0, const uint64_t* __restrict__ tails1, uint32_t* __restrict__ seg_hist) {
+  __shared__ uint32_t h[kRadix];
+  const uint32_t total = cstart[nseg];
+  for (uint32_t k = blockIdx.x; k < total; k += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t s = chunk_segment(cstart, nseg, k);
+    Seg sg = segs[s];
+    uint32_t c = k - cstart[s];
+    uint32_t beg = c * kChunk, end = min(sg.len, beg + kChunk);
+    const uint64_t* t = (sg.parity ? tails1 : tails0) + sg.start;
+    for (uint32_t i = beg + threadIdx.x; i < end; i += 256) atomicAdd(&h[byte_of_tail(t[i], sg.depth)], 1u);
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&seg_hist[(uint64_t)s * kRadix + threadIdx.x], h[threadIdx.x]);
+    __syncthreads();
+  }
+  (void)nchunks_total_ub;
+}
+
+// One CTA (256 threads) per big segment: bucket offsets, children, constant-digit skip.
+__global__ void __launch_bounds__(256)
+    kr_plan(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ seg_hist,
+            uint32_t* __restrict__ seg_excl, uint8_t* __restrict__ noscatter, Tunables tu, ListSet kd,
+            Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
+  __shared__ uint32_t s_tmp[32];
+  __shared__ uint32_t s_single;
+  const uint32_t s = blockIdx.x;
+  const Seg sg = segs[s];
+  const int d = threadIdx.x;
+  uint32_t h = seg_hist[(uint64_t)s * kRadix + d];
+  if (d == 0) s_single = 0;
+  __syncthreads();
+  if (h == sg.len) s_single = 1;  // one digit holds the whole bucket: nothing to move
+  uint32_t ex = block_excl_scan<256>(h, s_tmp, nullptr);
+  seg_excl[(uint64_t)s * kRadix + d] = ex;
+  if (s_single) {
+    if (d == 0) {
+      noscatter[s] = 1;
+      Seg ch{sg.start, sg.len, sg.depth + 1, sg.parity};
+      classify_bucket(ch, tu, kd, big_out, big_count);
+    }
+  } else {
+    if (d == 0) noscatter[s] = 0;
+    if (h) {
+      Seg ch{sg.start + ex, h, sg.depth + 1, sg.parity ^ 1u};
+      classify_bucket(ch, tu, kd, big_out, big_count);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    kr_split(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart,
+             const uint32_t* __restrict__ seg_excl, const uint8_t* __restrict__ noscatter, uint64_t* tails0,
+             uint32_t* idx0, uint64_t* tails1, uint32_t* idx1, uint64_t* __restrict__ status,
+             uint32_t* __restrict__ ticket) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
+  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kChunk);
+  uint32_t* s_wh = reinterpret_cast<uint32_t*>(smem + SplitSmem::kRegion);
+  uint32_t* s_dst = s_wh + kWarps * kRadix;
+  uint32_t* s_misc = s_dst + 256;
+
+  if (threadIdx.x == 0) {
+    uint32_t k = atomicAdd(ticket, 1u);
+    s_misc[32] = k;
+    if (k < cstart[nseg]) {
+      uint32_t s = chunk_segment(cstart, nseg, k);
+      s_misc[33] = s;
+      s_misc[34] = k - cstart[s];
+    }
+  }
+  __syncthreads();
+  const uint32_t k = s_misc[32];
+  if (k >= cstart[nseg]) return;
+  const uint32_t s = s_misc[33], c = s_misc[34];
+  if (noscatter[s]) return;
+  const Seg sg = segs[s];
+  const uint32_t beg = c * kChunk;
+  const uint32_t cnt = min(kChunk, sg.len - beg);
+  const uint64_t* tin = (sg.parity ? tails1 : tails0) + sg.start + beg;
+  const uint32_t* iin = (sg.parity ? idx1 : idx0) + sg.start + beg;
+  uint64_t* tout = (sg.parity ? tails0 : tails1) + sg.start;
+  uint32_t* iout = (sg.parity ? idx0 : idx1) + sg.start;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t tv[kItems];
+  uint32_t iv[kItems], dig[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+    if (e < cnt) {
+      tv[j] = tin[e];
+      iv[j] = iin[e];
+    } else {
+      tv[j] = 0;
+      iv[j] = 0;
+    }
+    dig[j] = byte_of_tail(tv[j], sg.depth);
+  }
+  uint32_t pos[kItems], total_d, excl_d;
+  block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+    uint32_t pre = lookback_digit(status, k, k - c, d, total_d);
+    s_dst[d] = seg_excl[(uint64_t)s * kRadix + d] + pre - excl_d;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+    if (e < cnt) {
+      uint32_t p = pos[j];
+      s_tail[p] = tv[j];
+      s_idx[p] = iv[j];
+      s_dig[p] = (uint8_t)dig[j];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+    uint32_t g = s_dst[s_dig[i]] + i;
+    tout[g] = s_tail[i];
+    iout[g] = s_idx[i];
+  }
+}
+
+}  // namespace
+
+size_t split_smem_bytes() { return SplitSmem::kBytes; }
+
+cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
+                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
+                                   uint64_t* status, uint32_t* ticket, uint64_t* tail_out, uint32_t* idx_out,
+                                   uint32_t grid_ub, cudaStream_t s) {
+  size_t smem = SplitSmem::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kc_split_level1<<<grid_ub, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, n, cstart, status, ticket,
+                                                   tail_out, idx_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s) {
+  kr_nchunks<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, nch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
+                           const uint64_t* tails0, const uint64_t* tails1, uint32_t* seg_hist, cudaStream_t s) {
+  kr_hist<<<grid, 256, 0, s>>>(segs, nseg, cstart, grid, tails0, tails1, seg_hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kr_plan(const Seg* segs, uint32_t nseg, const uint32_t* seg_hist, uint32_t* seg_excl,
+                           uint8_t* noscatter, const Tunables& tu, const ListSet& kd, Seg* big_out,
+                           uint32_t* big_count, cudaStream_t s) {
+  kr_plan<<<nseg, 256, 0, s>>>(segs, nseg, seg_hist, seg_excl, noscatter, tu, kd, big_out, big_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, const uint32_t* seg_excl,
+                            const uint8_t* noscatter, uint64_t* tails0, uint32_t* idx0, uint64_t* tails1,
+                            uint32_t* idx1, uint64_t* status, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s) {
+  size_t smem = SplitSmem::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(kr_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kr_split<<<grid_ub, kThreads, smem, s>>>(segs, nseg, cstart, seg_excl, noscatter, tails0, idx0, tails1, idx1,
+                                           status, ticket);
+  return cudaGetLastError();
+}
+
+}  // namespace ley

@@ -1,0 +1,145 @@
+// k_tile.cu — K-a: key-prefix extraction + per-CTA byte-0 histogram + tile-local stable sort by byte 0.
+//
+// PAPER.md §3.1 Algorithm 1 line 59 "buckets[256][k] = ParallelRadixSort(key, radix, n)" with
+// radix = 0, and the cache-aware scatter of line 96 ("we first compute a histogram based on the current
+// radix ... aggregate the keys in the thread level CPU cache first, before scattering them"): here the
+// "thread-level cache" is the CTA's shared memory. §3.2: "Leyenda extracts the (key, pointer)
+// tuples from records during the read process" — K-a is that extraction. SURVEY.md §8a row a1.
+//
+// One CTA per tile of kTileRecords records:
+//   1. load key bytes 0..9 of each record (three 4-byte loads; record i sits at byte 100 i, 4-aligned)
+//   2. warp multi-split rank on byte 0 (match.any + popc of lanemask_lt): stable, input order
+//   3. block scan of the 256 x WARPS counts -> tile-local offsets
+//   4. scatter pairs into shared memory in byte-0 order, write them out coalesced:
+//        k1 = key bytes 1..8 big-endian (u64)     w = key byte 9 << 24 | local index (u32)
+//   5. cnt[b * tiles + t] = tile count of byte-0 value b (bucket-major, for K-b's scan)
+//      lo[t * 256 + b]    = tile-local exclusive offset of b
+//   6. hist16[key bytes 0..1] += 1 (warp-aggregated global reductions) — the level-1 bucket sizes
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ley {
+namespace {
+
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles,
+                                                         uint64_t* __restrict__ k1_out, uint32_t* __restrict__ w_out,
+                                                         uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
+                                                         uint32_t* __restrict__ hist16) {
+  constexpr int T = THREADS * ITEMS;
+  constexpr int WARPS = THREADS / 32;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem);                   // [T]
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                // [T]
+  uint32_t* s_wh = s_w + T;                                             // [WARPS][256]
+  uint32_t* s_tmp = s_wh + WARPS * kRadix;                              // [32]
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x;
+  const uint64_t base = (uint64_t)t * T;
+  const uint32_t cnt_t = (uint32_t)(n - base < (uint64_t)T ? n - base : (uint64_t)T);
+
+  for (int i = threadIdx.x; i < WARPS * kRadix; i += THREADS) s_wh[i] = 0;
+
+  // ---- 1. load keys (all loads issued before use)
+  uint32_t a[ITEMS], b[ITEMS], c[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    uint32_t r = warp * (32 * ITEMS) + j * 32 + lane;
+    if (r < cnt_t) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (base + r) * kRecordBytes);
+      a[j] = __ldg(p);
+      b[j] = __ldg(p + 1);
+      c[j] = __ldg(p + 2);
+    } else {
+      a[j] = b[j] = c[j] = 0;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. warp multi-split ranking on byte 0, in record order (stable)
+  uint32_t rank[ITEMS];
+  uint32_t* wh = s_wh + warp * kRadix;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    uint32_t r = warp * (32 * ITEMS) + j * 32 + lane;
+    bool valid = r < cnt_t;
+    uint32_t hi = bswap32(a[j]);            // key bytes 0..3, big-endian
+    uint32_t d = hi >> 24;                  // byte 0
+    uint32_t key = valid ? d : (0x100u | lane);
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t before = __popc(peers & lt);
+    uint32_t cur = valid ? wh[d] : 0;
+    __syncwarp();
+    if (valid && before == 0) wh[d] = cur + __popc(peers);
+    __syncwarp();
+    rank[j] = cur + before;
+    // level-1 bucket sizes: 16-bit prefix (bytes 0..1)
+    uint32_t p16 = hi >> 16;
+    uint32_t key16 = valid ? p16 : (0x10000u | lane);
+    uint32_t peers16 = __match_any_sync(0xffffffffu, key16);
+    if (valid && __popc(peers16 & lt) == 0) atomicAdd(&hist16[p16], (uint32_t)__popc(peers16));
+  }
+  __syncthreads();
+
+  // ---- 3. per-digit totals over warps, tile exclusive offsets
+  uint32_t total = 0;
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+#pragma unroll 4
+    for (int w = 0; w < WARPS; ++w) {
+      uint32_t v = s_wh[w * kRadix + d];
+      s_wh[w * kRadix + d] = total;
+      total += v;
+    }
+  }
+  uint32_t excl = block_excl_scan<THREADS>(threadIdx.x < kRadix ? total : 0, s_tmp, nullptr);
+  if (threadIdx.x < kRadix) {
+    const int d = threadIdx.x;
+#pragma unroll 4
+    for (int w = 0; w < WARPS; ++w) s_wh[w * kRadix + d] += excl;
+    cnt[(uint64_t)d * tiles + t] = total;
+    lo[(uint64_t)t * kRadix + d] = excl;
+  }
+  __syncthreads();
+
+  // ---- 4. scatter into shared memory in byte-0 order
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    uint32_t r = warp * (32 * ITEMS) + j * 32 + lane;
+    if (r < cnt_t) {
+      uint32_t hi = bswap32(a[j]);
+      uint32_t d = hi >> 24;
+      uint32_t pos = wh[d] + rank[j];
+      uint64_t kk = ((uint64_t)hi << 32) | bswap32(b[j]);  // key bytes 0..7 big-endian
+      s_k1[pos] = (kk << 8) | (c[j] & 0xFFu);               // bytes 1..8
+      s_w[pos] = ((c[j] >> 8) & 0xFFu) << 24 | r;           // byte 9 | local index
+    }
+  }
+  __syncthreads();
+
+  // ---- 5. coalesced write-out
+  for (uint32_t i = threadIdx.x; i < cnt_t; i += THREADS) {
+    k1_out[base + i] = s_k1[i];
+    w_out[base + i] = s_w[i];
+  }
+}
+
+}  // namespace
+
+size_t ka_smem_bytes() {
+  return (size_t)kTileRecords * 12 + (size_t)(kTileThreads / 32) * kRadix * 4 + 32 * 4;
+}
+
+cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, cudaStream_t s) {
+  auto kern = ka_tile_sort<kTileThreads, kTileItems>;
+  size_t smem = ka_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16);
+  return cudaGetLastError();
+}
+
+}  // namespace ley

@@ -1,0 +1,50 @@
+// kernels.cuh — launch wrappers of the sm_100a kernels (K-a .. K-e) used by the host drivers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace ley {
+
+// K-a (k_tile.cu)
+size_t ka_smem_bytes();
+cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, cudaStream_t s);
+
+// K-b (k_scan.cu)
+cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
+                             uint32_t* total_out, cudaStream_t s);
+uint64_t scan_status_words(uint64_t m);
+cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
+                                  cudaStream_t s);
+
+// K-c / K-c' (k_split.cu)
+size_t split_smem_bytes();
+cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
+                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
+                                   uint64_t* status, uint32_t* ticket, uint64_t* tail_out, uint32_t* idx_out,
+                                   uint32_t grid_ub, cudaStream_t s);
+cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
+cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
+                           const uint64_t* tails0, const uint64_t* tails1, uint32_t* seg_hist, cudaStream_t s);
+cudaError_t launch_kr_plan(const Seg* segs, uint32_t nseg, const uint32_t* seg_hist, uint32_t* seg_excl,
+                           uint8_t* noscatter, const Tunables& tu, const ListSet& kd, Seg* big_out,
+                           uint32_t* big_count, cudaStream_t s);
+cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, const uint32_t* seg_excl,
+                            const uint8_t* noscatter, uint64_t* tails0, uint32_t* idx0, uint64_t* tails1,
+                            uint32_t* idx1, uint64_t* status, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s);
+
+// K-d (k_bucket.cu)
+cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
+                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
+cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
+                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, cudaStream_t s,
+                          int* launches);
+
+// K-e (k_gather.cu)
+cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t n, uint8_t* out, int sms,
+                             cudaStream_t s, int* launches);
+
+}  // namespace ley

@@ -1,0 +1,273 @@
+// runtime.cpp — errors, options, planning, device arena and profiling for libleyenda (host C++).
+#include "runtime.h"
+
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <memory>
+
+#include "config.h"
+
+namespace ley {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+void clear_error() { g_error.clear(); }
+const char* last_error() { return g_error.c_str(); }
+
+// ------------------------------------------------------------------ options
+namespace {
+std::mutex g_opt_mu;
+Options g_opt;
+
+struct OptDesc {
+  const char* name;
+  int64_t Options::*field;
+  int64_t lo, hi;
+};
+const OptDesc kOpts[] = {
+    {"warp_tier_max", &Options::warp_tier_max, 1, 32},
+    {"smem_tier_max", &Options::smem_tier_max, 0, 16384},
+    {"kd_digit_bits", &Options::kd_digit_bits, 0, 12},
+    {"kd_insert_max", &Options::kd_insert_max, 1, 64},
+    {"profile", &Options::profile, 0, 1},
+    {"ext_run_records", &Options::ext_run_records, 0, (int64_t)0xFFFFFFFEll},
+};
+}  // namespace
+
+Options options_snapshot() {
+  std::lock_guard<std::mutex> g(g_opt_mu);
+  return g_opt;
+}
+
+ley_status option_set(const char* name, int64_t value) {
+  if (!name) {
+    set_error("ley_set_option: NULL name");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  for (const OptDesc& d : kOpts) {
+    if (strcmp(d.name, name) == 0) {
+      if (value < d.lo || value > d.hi) {
+        set_error(std::string("ley_set_option: ") + name + " out of range [" + std::to_string(d.lo) + ", " +
+                  std::to_string(d.hi) + "]");
+        return LEY_ERR_INVALID_ARGUMENT;
+      }
+      std::lock_guard<std::mutex> g(g_opt_mu);
+      g_opt.*(d.field) = value;
+      return LEY_OK;
+    }
+  }
+  set_error(std::string("ley_set_option: unknown option '") + name + "'");
+  return LEY_ERR_INVALID_ARGUMENT;
+}
+
+ley_status option_get(const char* name, int64_t* value) {
+  if (!name || !value) {
+    set_error("ley_get_option: NULL argument");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  for (const OptDesc& d : kOpts) {
+    if (strcmp(d.name, name) == 0) {
+      std::lock_guard<std::mutex> g(g_opt_mu);
+      *value = g_opt.*(d.field);
+      return LEY_OK;
+    }
+  }
+  set_error(std::string("ley_get_option: unknown option '") + name + "'");
+  return LEY_ERR_INVALID_ARGUMENT;
+}
+
+// ------------------------------------------------------------------ plan
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+InternalLayout plan_internal(uint64_t n) {
+  InternalLayout L;
+  L.n = n;
+  L.tiles = (n + kTileRecords - 1) / kTileRecords;
+  L.m = (uint64_t)kRadix * L.tiles;
+  L.split_chunks_ub = n / kChunk + kRadix + 1;
+  L.scan_status_words = (std::max<uint64_t>(L.m, 65536) + kScanTile - 1) / kScanTile;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += align256(bytes);
+    return at;
+  };
+  L.off_At = take(8 * n);
+  L.off_Ai = take(4 * n);
+  L.off_Bt = take(8 * n);
+  L.off_Bi = take(4 * n);
+  L.off_perm = take(4 * n);
+  L.off_cnt = take(4 * L.m);
+  L.off_off = take(4 * (L.m + 1));
+  L.off_lo = take(4 * L.m);
+  L.off_hist16 = take(4 * 65536);
+  L.off_B16 = take(4 * (65536 + 1));
+  L.off_cstart = take(4 * 260);
+  L.off_scan_status = take(8 * 2 * L.scan_status_words);
+  L.off_split_status = take(8 * (size_t)kRadix * L.split_chunks_ub);
+  L.off_small = take(4 * 64);  // tickets + list counters
+  L.bytes = o;
+  return L;
+}
+
+// External path: the largest run (records) whose staged internal sort fits the budget:
+// 100 r (run in) + 100 r (run out) + scratch(r) <= budget.
+uint64_t external_run_records(uint64_t n, uint64_t budget) {
+  Options o = options_snapshot();
+  if (o.ext_run_records > 0) return std::min<uint64_t>(n, (uint64_t)o.ext_run_records);
+  uint64_t lo = 0, hi = std::min<uint64_t>(n, 0xFFFFFFFEull);
+  while (lo < hi) {
+    uint64_t mid = lo + (hi - lo + 1) / 2;
+    uint64_t need = 200 * mid + plan_internal(mid).bytes + (64ull << 20);
+    if (need <= budget) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info) {
+  if (!info) {
+    set_error("ley_plan_query: NULL info");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  if (n > LEY_MAX_RECORDS) {
+    set_error("ley_plan_query: n_records > 2^32-2");
+    return LEY_ERR_TOO_LARGE;
+  }
+  memset(info, 0, sizeof(*info));
+  InternalLayout L = plan_internal(n);
+  info->n_records = n;
+  info->tile_records = kTileRecords;
+  info->tiles = L.tiles;
+  info->chunk_records = kChunk;
+  info->internal_scratch = L.bytes;
+  info->staged_bytes = L.bytes + 2 * align256(100 * n);
+  info->host_path = (budget == 0 || info->staged_bytes <= budget) ? 0 : 1;
+  if (info->host_path == 1) {
+    info->run_records = external_run_records(n, budget);
+    info->runs = info->run_records ? (n + info->run_records - 1) / info->run_records : 0;
+  } else {
+    info->run_records = n;
+    info->runs = n ? 1 : 0;
+  }
+  return LEY_OK;
+}
+
+// ------------------------------------------------------------------ arena
+namespace {
+std::mutex g_ctx_mu;
+std::unique_ptr<DeviceContext> g_ctx[64];
+}  // namespace
+
+DeviceContext& device_context(int device) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  if (!g_ctx[device]) {
+    g_ctx[device].reset(new DeviceContext());
+    g_ctx[device]->device = device;
+  }
+  return *g_ctx[device];
+}
+
+ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s) {
+  if (b.cap >= bytes && b.ptr) return LEY_OK;
+  if (b.ptr) {
+    LEY_CUDA(what, cudaStreamSynchronize(s));
+    LEY_CUDA(what, cudaFree(b.ptr));
+    b.ptr = nullptr;
+    b.cap = 0;
+  }
+  size_t want = std::max<size_t>(bytes, 1 << 20);
+  cudaError_t e = cudaMalloc(&b.ptr, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    b.ptr = nullptr;
+    set_error(std::string(what) + ": cudaMalloc of " + std::to_string(want) + " bytes failed (" +
+              cudaGetErrorString(e) + ")");
+    return LEY_ERR_CUDA;
+  }
+  b.cap = want;
+  return LEY_OK;
+}
+
+void release_device(int device) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  for (int d = 0; d < 64; ++d) {
+    if (device >= 0 && d != device) continue;
+    if (!g_ctx[d]) continue;
+    DeviceContext& c = *g_ctx[d];
+    std::lock_guard<std::mutex> g2(c.mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d);
+    for (DeviceBuffer* b : {&c.work, &c.lists, &c.big[0], &c.big[1], &c.rec, &c.stage, &c.ext}) {
+      if (b->ptr) cudaFree(b->ptr);
+      b->ptr = nullptr;
+      b->cap = 0;
+    }
+    if (c.host_pinned) cudaFreeHost(c.host_pinned);
+    c.host_pinned = nullptr;
+    for (cudaEvent_t e : c.events) cudaEventDestroy(e);
+    c.events.clear();
+    cudaSetDevice(prev);
+  }
+}
+
+// ------------------------------------------------------------------ profiling
+namespace {
+struct StageRecord {
+  std::vector<const char*> names;
+  std::vector<float> ms;
+  int launches = 0;
+};
+thread_local StageRecord g_stages;
+}  // namespace
+
+ley_status Profiler::begin(const char* name) {
+  if (!on) return LEY_OK;
+  int need = next_event + 2;
+  while ((int)ctx->events.size() < need) {
+    cudaEvent_t e;
+    LEY_CUDA("profiler", cudaEventCreate(&e));
+    ctx->events.push_back(e);
+  }
+  names.push_back(name);
+  ev_begin.push_back(next_event);
+  LEY_CUDA("profiler", cudaEventRecord(ctx->events[next_event++], stream));
+  return LEY_OK;
+}
+
+ley_status Profiler::end() {
+  if (!on) return LEY_OK;
+  ev_end.push_back(next_event);
+  LEY_CUDA("profiler", cudaEventRecord(ctx->events[next_event++], stream));
+  return LEY_OK;
+}
+
+void Profiler::finish() {
+  g_stages.names.clear();
+  g_stages.ms.clear();
+  g_stages.launches = launches;
+  if (!on) return;
+  for (size_t i = 0; i < names.size() && i < ev_end.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->events[ev_begin[i]], ctx->events[ev_end[i]]);
+    g_stages.names.push_back(names[i]);
+    g_stages.ms.push_back(ms);
+  }
+}
+
+void record_launches(int launches) { g_stages.launches = launches; }
+
+int stage_times(const char** names, float* ms, int max, int* launches) {
+  int k = 0;
+  for (size_t i = 0; i < g_stages.names.size() && k < max; ++i, ++k) {
+    if (names) names[k] = g_stages.names[i];
+    if (ms) ms[k] = g_stages.ms[i];
+  }
+  if (launches) *launches = g_stages.launches;
+  return k;
+}
+
+}  // namespace ley

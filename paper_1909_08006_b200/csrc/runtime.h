@@ -1,0 +1,110 @@
+// runtime.h — host-side runtime of libleyenda: status/error plumbing, options, plan, device arena,
+// per-call profiling. Plain C++ (no device code) so the plan logic is testable without a GPU.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "leyenda.h"
+
+namespace ley {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+void clear_error();
+const char* last_error();
+
+struct Status {
+  ley_status code = LEY_OK;
+  bool ok() const { return code == LEY_OK; }
+};
+
+// CUDA call wrapper: returns LEY_ERR_CUDA with a stage-tagged message on failure.
+#define LEY_CUDA(stage, expr)                                                                          \
+  do {                                                                                                 \
+    cudaError_t _e = (expr);                                                                           \
+    if (_e != cudaSuccess) {                                                                           \
+      ::ley::set_error(std::string(stage) + ": " + cudaGetErrorName(_e) + " (" + cudaGetErrorString(_e) + \
+                       ") at " #expr);                                                                 \
+      return LEY_ERR_CUDA;                                                                             \
+    }                                                                                                  \
+  } while (0)
+
+// ------------------------------------------------------------------ options
+struct Options {
+  int64_t warp_tier_max = 32;
+  int64_t smem_tier_max = 16384;
+  int64_t kd_digit_bits = 12;
+  int64_t kd_insert_max = 16;
+  int64_t profile = 0;
+  int64_t ext_run_records = 0;
+};
+Options options_snapshot();
+ley_status option_set(const char* name, int64_t value);
+ley_status option_get(const char* name, int64_t* value);
+
+// ------------------------------------------------------------------ plan (host-only arithmetic)
+struct InternalLayout {
+  uint64_t n = 0, tiles = 0, m = 0;  // m = 256 * tiles
+  uint64_t split_chunks_ub = 0;      // level-1 chunk upper bound
+  // byte offsets inside the workspace
+  size_t off_At = 0, off_Ai = 0, off_Bt = 0, off_Bi = 0, off_perm = 0;
+  size_t off_cnt = 0, off_off = 0, off_lo = 0, off_hist16 = 0, off_B16 = 0, off_cstart = 0;
+  size_t off_scan_status = 0, off_split_status = 0, off_small = 0;
+  size_t scan_status_words = 0;
+  size_t bytes = 0;  // total
+};
+InternalLayout plan_internal(uint64_t n);
+ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info);
+uint64_t external_run_records(uint64_t n, uint64_t budget);
+
+// ------------------------------------------------------------------ device arena
+// A growable cached buffer per (device, slot). Growth frees and reallocates (stream synchronised first).
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t cap = 0;
+};
+
+struct DeviceContext {
+  std::mutex mu;
+  int device = -1;
+  int sms = 148;
+  DeviceBuffer work;      // internal workspace (InternalLayout)
+  DeviceBuffer lists;     // K-d work lists (kNumKdLists x cap)
+  DeviceBuffer big[2];    // big-bucket lists, ping-pong across recursion levels
+  DeviceBuffer rec;       // recursion-level arrays (chunk starts, histograms, look-back status)
+  DeviceBuffer stage;     // staged input/output for host pointers
+  DeviceBuffer ext;       // external path device buffers
+  void* host_pinned = nullptr;  // small pinned host scratch (counters)
+  std::vector<cudaEvent_t> events;
+};
+DeviceContext& device_context(int device);
+ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s);
+void release_device(int device);
+
+// ------------------------------------------------------------------ profiling
+struct Profiler {
+  bool on = false;
+  cudaStream_t stream = nullptr;
+  DeviceContext* ctx = nullptr;
+  std::vector<const char*> names;
+  std::vector<int> ev_begin, ev_end;
+  int next_event = 0;
+  int launches = 0;
+  ley_status begin(const char* name);
+  ley_status end();
+  void finish();  // after stream sync: compute times into the thread-local record
+};
+void record_launches(int launches);
+int stage_times(const char** names, float* ms, int max, int* launches);
+
+// ------------------------------------------------------------------ drivers
+// Internal sort of device-resident records (K-a .. K-e). perm_out may be null.
+ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                                cudaStream_t s, Profiler& prof);
+
+}  // namespace ley
