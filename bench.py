@@ -1,0 +1,274 @@
+#!/usr/bin/env python3
+"""bench.py — sorted GB/s of 100-byte records on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+A "step" is one pass of the whole hot path (K-a .. K-e: SURVEY.md §8a rows a1-a6) over one batch of
+synthetic records already resident in HBM: one ley_sort call through the C ABI. Default workload:
+BASELINE.json configs[1] (C2: 1e8 uniform records = 10 GB, seed 1) on 1 GPU. Inputs are 10 GB, far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c1|c2|c3|c4] [--impl ours|reference]
+
+Keys beyond the base contract: `roofline` (dominant kernel, algorithmic bytes / CUDA-event time against
+MEASURED_PEAKS.json hbm_gbs), `step_roofline` (the whole step: 200 B/record / HBM peak),
+`cpu_baseline` (the oracle timed on this host on a bounded sample), `e2e` (same metric through the C
+ABI with pinned host buffers: H2D + sort + D2H inside the timed region), `clocks`, `gpu_launches`.
+Multi-GPU (N > 1, torchrun): every rank sorts its own C2-sized slice ("scaling": "weak"); the dist
+key-range path is reported separately once it lands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(n=1_000_000, seed=0, dist="uniform", name="C1 1e6 x 100 B uniform (BASELINE.json configs[0])"),
+    "c2": dict(n=100_000_000, seed=1, dist="uniform", name="C2 1e8 x 100 B uniform, 10 GB (BASELINE.json configs[1])"),
+    "c3": dict(n=200_000_000, seed=2, dist="skewed",
+               name="C3 2e8 x 100 B Zipf(1.2) byte0, 8-valued byte1, 2% dup keys, 20 GB (BASELINE.json configs[2])"),
+    "c4": dict(n=600_000_000, seed=3, dist="uniform", name="C4 6e8 x 100 B uniform, 60 GB (BASELINE.json configs[3])"),
+}
+METRIC = "sorted GB/s of 100-byte records"
+# algorithmic bytes per record of each stage: what the step must move
+STAGE_ALG_BYTES = {"K-a tile sort": 10 + 12, "K-c split": 12 + 12, "K-d buckets": 12 + 4, "K-e gather": 4 + 100 + 100}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in r.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [s for s in self.samples if s[6] not in ("0", "[N/A]")] or self.samples
+        sm = [float(s[0]) for s in loaded if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in loaded if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in loaded for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def cpu_baseline(cfg, sample_n: int):
+    """The oracle as it stands (oracle/), timed on this host's cores on a bounded sample."""
+    import gen
+    import oracle
+
+    recs = gen.records(sample_n, cfg["seed"], cfg["dist"])
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    _, (te, ts, tg) = oracle.sort_timed(recs, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": round(sample_n * 100 / dt / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {sample_n:,} records of {cfg['name'].split(' (')[0]} (same generator/seed); "
+                      f"extract {te:.2f} s, sort {ts:.2f} s, gather {tg:.2f} s (__gnu_parallel::sort, OpenMP)",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import gen
+    import oracle
+
+    sample_n = args.cpu_sample
+    recs = gen.records(sample_n, cfg["seed"], cfg["dist"])
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.sort_timed(recs[: min(sample_n, 1_000_000) * 100], threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sort_timed(recs, threads=threads)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    v = sample_n * 100 / t / 1e9
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["name"], "n_records": cfg["n"], "sample_records": sample_n},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {sample_n:,} records of the workload per step"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    import paper_1909_08006_b200 as ley
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = cfg["n"]
+    stream = torch.cuda.current_stream()
+    x = torch.empty(n * 100, dtype=torch.uint8, device="cuda")
+    gen.records_cuda(x.data_ptr(), n, cfg["seed"] + 1000 * rank, cfg["dist"], stream=stream.cuda_stream)
+    out = torch.empty_like(x)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        ley.ley_sort(x, out, n, stream=stream)
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region (device events)
+    ley.ley_set_option("profile", 1)
+    stage_ms: dict[str, list[float]] = {}
+    launches = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            ley.ley_sort(x, out, n, stream=stream)
+            st, nl = ley.ley_stage_times()
+            launches += nl
+            for name, ms in st:
+                stage_ms.setdefault(name, []).append(ms)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ley.ley_set_option("profile", 0)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n * 100 / (ms / 1e3) / 1e9
+
+    peak, peak_src = _peaks()
+    avg = {k: statistics.mean(v) for k, v in stage_ms.items()}
+    dominant = max((k for k in avg if k in STAGE_ALG_BYTES), key=lambda k: avg[k])
+    alg = STAGE_ALG_BYTES[dominant] * n
+    achieved = alg / (avg[dominant] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f)
+        ent = tr.get(args.config, {}).get(dominant)
+        if ent:
+            traffic = ent.get("bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dominant,
+                "alg_bytes_per_record": STAGE_ALG_BYTES[dominant], "peak_source": peak_src}
+    step_roof_ms = 200 * n / (peak * 1e9) * 1e3
+    step_roofline = {"alg_bytes_per_record": 200, "t_roof_ms": round(step_roof_ms, 3),
+                     "frac": round(step_roof_ms / ms, 4), "peak": peak, "unit": "GB/s"}
+
+    # ---------------------------------------------------------------- e2e through the C ABI, host buffers
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        hin = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
+        hin.copy_(x)
+        hout = torch.empty_like(hin).pin_memory()
+        ley.ley_sort(hin, hout, n, stream=stream)  # warm (staging arena)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            ley.ley_sort(hin, hout, n, stream=stream)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / args.e2e_steps
+        e2e = {"value": round(n * 100 / (ems / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * 100,
+               "d2h_bytes_per_step": n * 100, "ms_per_step": round(ems, 3), "steps": args.e2e_steps}
+        del hin, hout
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        cpu = cpu_baseline(cfg, args.cpu_sample)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based generator, SURVEY App. A)",
+            "config": {"workload": cfg["name"], "n_records": n, "record_bytes": 100, "key_bytes": 10,
+                       "seed": cfg["seed"], "distribution": cfg["dist"],
+                       "l2": "inputs (10 GB+) larger than the 126 MB L2; no flush needed",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "roofline": roofline, "step_roofline": step_roofline,
+            "stages_ms": {k: round(v, 4) for k, v in avg.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
