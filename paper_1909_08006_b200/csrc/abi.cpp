@@ -151,8 +151,10 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms > 0) ctx.sms = sms;
   }
+  const Options opts = options_snapshot();
+  if (opts.l2_fetch_bytes) LEY_CUDA("setup", cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)opts.l2_fetch_bytes));
   Profiler prof;
-  prof.on = options_snapshot().profile != 0;
+  prof.on = opts.profile != 0;
   prof.stream = s;
   prof.ctx = &ctx;
   const uint8_t* in8 = static_cast<const uint8_t*>(in);

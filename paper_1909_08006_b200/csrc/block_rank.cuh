@@ -9,6 +9,20 @@
 
 namespace ley {
 
+// Lanes of the warp holding the same 8-bit digit (and valid): 8 ballots, one per digit bit (warp
+// multi-split), cheaper than match.any on sm_100a.
+__device__ __forceinline__ uint32_t warp_peers8(uint32_t d, bool valid) {
+  uint32_t peers = __ballot_sync(0xffffffffu, valid);
+  if (!valid) peers = ~peers;
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const bool set = (d >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, set);
+    peers &= set ? bal : ~bal;
+  }
+  return peers;
+}
+
 // s_wh: [THREADS/32][256] u32 scratch; s_tmp: [32] u32.
 // Output: pos[j] = position of item j in the block's digit-sorted order; for threads < 256,
 // total_d / excl_d = count of digit d = threadIdx.x in the block and its exclusive offset.
@@ -27,8 +41,7 @@ __device__ __forceinline__ void block_rank_digits(const uint32_t (&dig)[ITEMS], 
     uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
     bool valid = e < count;
     uint32_t d = dig[j];
-    uint32_t key = valid ? d : (0x100u | lane);
-    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t peers = warp_peers8(d, valid);
     uint32_t before = __popc(peers & lt);
     uint32_t cur = valid ? wh[d] : 0;
     __syncwarp();

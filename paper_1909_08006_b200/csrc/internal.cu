@@ -82,9 +82,11 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
 
   // ---------------------------------------------------------------- K-c (byte 1)
   if ((st = prof.begin("K-c split"))) return st;
-  LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart, split_status, tickets + 2,
-                                               Bt, Bi, (uint32_t)L.split_chunks_ub, s));
-  ++launches;
+  LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
+                                               reinterpret_cast<uint4*>(base + L.off_plan_a),
+                                               reinterpret_cast<uint2*>(base + L.off_plan_b), split_status,
+                                               tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s));
+  launches += 2;
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- classify level 1, K-d

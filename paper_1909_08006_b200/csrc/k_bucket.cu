@@ -10,6 +10,9 @@
 // Every bucket writes perm[start .. start+len) = input ordinals in sorted order. The comparison order is
 // the composite (tail, index), which is the sort's strict total order, so the result does not depend on
 // the (non-deterministic) atomics used to place elements inside a CTA.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "classify.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -123,22 +126,34 @@ __host__ __device__ constexpr size_t kd_smem() {
   return (size_t)CAP * 12 + (size_t)(2 * kd_bins<CAP>() + 1) * 4 + 64 * 4 + 16;
 }
 
+// One CTA per bucket (len <= CAP), persistent over its list:
+//   1. load the bucket's (tail, idx) pairs (coalesced; kept in registers when CAP/THREADS <= 16,
+//      else re-read from L2),
+//   2. counting pass on the next `bits` unconsumed key bits (shared-memory atomics give each item its
+//      rank inside its sub-bucket), block scan of the 2^bits counters, placement into shared memory,
+//   3. comparison sort of every sub-bucket on the composite (tail, idx): insertion sort by one thread
+//      (tiny) or a warp bitonic network (larger) — Alg. 1's ComparisonSort below tinyBucketThreshold,
+//   4. perm[start + i] = idx of the i-th smallest, coalesced.
 template <uint32_t CAP, int THREADS>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THREADS) > 4 ? 4 : 6)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                 uint32_t* __restrict__ perm, Tunables tu) {
   constexpr uint32_t BINS = kd_bins<CAP>();
   constexpr int WARPS = THREADS / 32;
+  constexpr int ITEMS = CAP / THREADS;
+  constexpr bool REGS = ITEMS <= 16;
+  constexpr int RITEMS = REGS ? ITEMS : 1;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + CAP);
-  uint32_t* s_beg = s_idx + CAP;            // [BINS + 1]
-  uint32_t* s_cur = s_beg + BINS + 1;       // [BINS]
-  uint32_t* s_tmp = s_cur + BINS;           // [32] scan tmp, [32] = #big sub-buckets, [33..] list
+  uint32_t* s_cnt = s_idx + CAP;            // [BINS + 1]: counts, then exclusive starts
+  uint32_t* s_bigl = s_cnt + BINS + 1;      // [BINS]: sub-buckets needing the warp network
+  uint32_t* s_tmp = s_bigl + BINS;          // [32] scan tmp, [32] = number of big sub-buckets
   uint32_t* s_nbig = s_tmp + 32;
-  uint32_t* s_big = s_tmp + 33;             // reuses s_cur after placement (see below)
 
+  for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;
+  __syncthreads();
   const uint32_t nitems = *count;
   const int warp = threadIdx.x >> 5;
   for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -156,40 +171,98 @@ __global__ void __launch_bounds__(THREADS)
     const uint32_t mask = nb - 1;
     auto digit = [&](uint64_t t) -> uint32_t { return bits ? (uint32_t)(t >> shift) & mask : 0u; };
 
-    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_cur[g] = 0;
+    uint64_t tr[RITEMS];
+    uint32_t xr[RITEMS], rr[RITEMS];
+    if (REGS) {
+#pragma unroll
+      for (int j = 0; j < RITEMS; ++j) {
+        uint32_t i = j * THREADS + threadIdx.x;
+        if (i < s) {
+          tr[j] = tp[i];
+          xr[j] = ip[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RITEMS; ++j) {
+        uint32_t i = j * THREADS + threadIdx.x;
+        if (i < s) rr[j] = atomicAdd(&s_cnt[digit(tr[j])], 1u);
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < s; i += THREADS) atomicAdd(&s_cnt[digit(tp[i])], 1u);
+    }
     if (threadIdx.x == 0) *s_nbig = 0;
     __syncthreads();
-    // pass 1: sub-bucket sizes on the next `bits` key bits
-    for (uint32_t i = threadIdx.x; i < s; i += THREADS) atomicAdd(&s_cur[digit(tp[i])], 1u);
-    __syncthreads();
-    // exclusive scan of the nb counters (contiguous slice per thread)
+    // exclusive scan of the nb counters in place (contiguous slice per thread)
     {
       const uint32_t per = (nb + THREADS - 1) / THREADS;
       const uint32_t g0 = threadIdx.x * per;
+      const uint32_t g1 = min(nb, g0 + per);
       uint32_t sum = 0;
-      for (uint32_t g = g0; g < min(nb, g0 + per); ++g) sum += s_cur[g];
+      for (uint32_t g = g0; g < g1; ++g) sum += s_cnt[g];
       uint32_t run = block_excl_scan<THREADS>(sum, s_tmp, nullptr);
-      for (uint32_t g = g0; g < min(nb, g0 + per); ++g) {
-        uint32_t c = s_cur[g];
-        s_beg[g] = run;
-        s_cur[g] = run;
+      for (uint32_t g = g0; g < g1; ++g) {
+        uint32_t c = s_cnt[g];
+        s_cnt[g] = run;
         run += c;
       }
-      if (threadIdx.x == 0) s_beg[nb] = s;
+      if (threadIdx.x == 0) s_cnt[nb] = s;
     }
     __syncthreads();
-    // pass 2: place (tail, idx) into its sub-bucket (order inside fixed later by the composite sort)
+    if (REGS) {
+      // place, then every item finds its final rank inside its (tiny) sub-bucket by counting the
+      // smaller composites there, and writes its ordinal straight to perm.
+#pragma unroll
+      for (int j = 0; j < RITEMS; ++j) {
+        uint32_t i = j * THREADS + threadIdx.x;
+        if (i < s) {
+          uint32_t p = s_cnt[digit(tr[j])] + rr[j];
+          s_tail[p] = tr[j];
+          s_idx[p] = xr[j];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < RITEMS; ++j) {
+        uint32_t i = j * THREADS + threadIdx.x;
+        if (i < s) {
+          const uint32_t d = digit(tr[j]);
+          const uint32_t b = s_cnt[d], e = s_cnt[d + 1];
+          if (e - b <= (uint32_t)tu.kd_insert_max) {
+            uint32_t rank = 0;
+            for (uint32_t m = b; m < e; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
+            perm[sg.start + b + rank] = xr[j];
+          } else if (rr[j] == 0) {
+            s_bigl[atomicAdd(s_nbig, 1u)] = d;
+          }
+        }
+      }
+      __syncthreads();
+      const uint32_t nbig = *s_nbig;
+      for (uint32_t q = warp; q < nbig; q += WARPS) {
+        const uint32_t g = s_bigl[q];
+        const uint32_t b = s_cnt[g], e = s_cnt[g + 1];
+        warp_bitonic_smem(s_tail, s_idx, b, e);
+        for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) perm[sg.start + i] = s_idx[i];
+      }
+      __syncthreads();  // every warp is done reading the sub-bucket bounds before they are cleared
+      for (uint32_t g = threadIdx.x; g <= nb; g += THREADS) s_cnt[g] = 0;
+      __syncthreads();
+      continue;
+    }
+    // ---- large-CAP path: elements re-read from L2, placed by a second counter pass
+    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_bigl[g] = 0;
+    __syncthreads();
     for (uint32_t i = threadIdx.x; i < s; i += THREADS) {
       uint64_t t = tp[i];
-      uint32_t x = ip[i];
-      uint32_t p = atomicAdd(&s_cur[digit(t)], 1u);
+      uint32_t d = digit(t);
+      uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
       s_tail[p] = t;
-      s_idx[p] = x;
+      s_idx[p] = ip[i];
     }
     __syncthreads();
-    // comparison sort of every sub-bucket: insertion (tiny) or warp bitonic (larger)
+    // comparison sort of every sub-bucket
     for (uint32_t g = threadIdx.x; g < nb; g += THREADS) {
-      uint32_t b = s_beg[g], e = s_beg[g + 1];
+      uint32_t b = s_cnt[g], e = s_cnt[g + 1];
       uint32_t sz = e - b;
       if (sz <= 1) continue;
       if (sz <= (uint32_t)tu.kd_insert_max) {
@@ -206,21 +279,20 @@ __global__ void __launch_bounds__(THREADS)
           s_idx[j] = x;
         }
       } else {
-        uint32_t q = atomicAdd(s_nbig, 1u);
-        s_cur[q] = g;  // s_cur is dead after placement: reuse as the big-sub-bucket list
+        s_bigl[atomicAdd(s_nbig, 1u)] = g;
       }
     }
     __syncthreads();
     const uint32_t nbig = *s_nbig;
     for (uint32_t q = warp; q < nbig; q += WARPS) {
-      uint32_t g = s_cur[q];
-      warp_bitonic_smem(s_tail, s_idx, s_beg[g], s_beg[g + 1]);
+      uint32_t g = s_bigl[q];
+      warp_bitonic_smem(s_tail, s_idx, s_cnt[g], s_cnt[g + 1]);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_idx[i];
+    for (uint32_t g = threadIdx.x; g <= nb; g += THREADS) s_cnt[g] = 0;
     __syncthreads();
   }
-  (void)s_big;
 }
 
 template <uint32_t CAP, int THREADS>
@@ -236,6 +308,11 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu);
+  if (getenv("LEY_DEBUG_SYNC")) {
+    fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    fprintf(stderr, "[ley]   done: %s\n", cudaGetErrorString(e2));
+  }
   return cudaGetLastError();
 }
 

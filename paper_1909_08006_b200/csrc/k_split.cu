@@ -50,88 +50,109 @@ __device__ __forceinline__ uint64_t search_le_g(const uint32_t* a, uint64_t lo, 
   return lo;
 }
 
+// Per-chunk decomposition of level 1, one thread per chunk: segment b, virtual range [v0, v0+cnt), the
+// tile range [t0, t1] whose byte-0 runs cover it, and the segment's first chunk k0. Parallel binary
+// searches here keep them off the K-c critical path.
+__global__ void kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles, const uint32_t* __restrict__ B16,
+                               uint64_t n, const uint32_t* __restrict__ cstart, uint32_t grid_ub,
+                               uint4* __restrict__ plan_a, uint2* __restrict__ plan_b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cstart[256] || k >= grid_ub) return;
+  uint32_t b = 0, hi = 256;
+  while (hi - b > 1) {
+    uint32_t mid = (b + hi) >> 1;
+    if (cstart[mid] <= k) b = mid; else hi = mid;
+  }
+  const uint32_t c = k - cstart[b];
+  const uint32_t seg_beg = B16[b * 256];
+  const uint64_t seg_end = (b < 255) ? B16[(b + 1) * 256] : n;
+  const uint32_t v0 = seg_beg + c * kChunk;
+  const uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
+  const uint32_t* off_b = off + (uint64_t)b * tiles;
+  const uint32_t t0 = (uint32_t)search_le_g(off_b, 0, tiles, v0);
+  const uint32_t t1 = (uint32_t)search_le_g(off_b, t0, tiles, v0 + cnt - 1);
+  plan_a[k] = make_uint4(b, v0, cnt, k - c);
+  plan_b[k] = make_uint2(t0, t1);
+}
+
+constexpr uint32_t kMaxRuns = (uint32_t)((kChunk * 13 + 16) / 8);  // run table fits the staging region
+
 __global__ void __launch_bounds__(kThreads, 2)
     kc_split_level1(const uint64_t* __restrict__ k1_in, const uint32_t* __restrict__ w_in, uint32_t tiles,
                     const uint32_t* __restrict__ off /*[256*tiles+1]*/, const uint32_t* __restrict__ lo,
-                    const uint32_t* __restrict__ B16, uint64_t n, const uint32_t* __restrict__ cstart,
-                    uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, uint64_t* __restrict__ tail_out,
-                    uint32_t* __restrict__ idx_out) {
+                    const uint32_t* __restrict__ B16, const uint32_t* __restrict__ cstart,
+                    const uint4* __restrict__ plan_a, const uint2* __restrict__ plan_b, uint64_t* __restrict__ status,
+                    uint32_t* __restrict__ ticket, uint64_t* __restrict__ tail_out, uint32_t* __restrict__ idx_out) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* region = smem;
   uint32_t* s_wh = reinterpret_cast<uint32_t*>(smem + SplitSmem::kRegion);
   uint32_t* s_dst = s_wh + kWarps * kRadix;
   uint32_t* s_misc = s_dst + 256;  // [0..31] scan tmp, [32..] scalars
-  uint32_t* run_v = reinterpret_cast<uint32_t*>(region);
-  uint32_t* run_src = run_v + (kChunk + 1);
-  uint64_t* s_tail = reinterpret_cast<uint64_t*>(region);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(region);  // run table (load phase)
+  uint32_t* s_lo = s_off + kMaxRuns;
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(region);  // staging (scatter phase)
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kChunk);
 
   if (threadIdx.x == 0) {
     uint32_t k = atomicAdd(ticket, 1u);
+    uint32_t total = cstart[256];
     s_misc[32] = k;
-    if (k < cstart[256]) {
-      // segment (byte-0 value) holding chunk k
-      uint32_t b = 0, hi = 256;
-      while (hi - b > 1) {
-        uint32_t mid = (b + hi) >> 1;
-        if (cstart[mid] <= k) b = mid; else hi = mid;
-      }
-      uint32_t c = k - cstart[b];
-      uint32_t seg_beg = B16[b * 256];
-      uint64_t seg_end = (b < 255) ? B16[(b + 1) * 256] : n;
-      uint32_t v0 = seg_beg + c * kChunk;
-      uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
-      const uint32_t* off_b = off + (uint64_t)b * tiles;
-      uint32_t t0 = (uint32_t)search_le_g(off_b, 0, tiles, v0);
-      uint32_t t1 = (uint32_t)search_le_g(off_b, t0, tiles, v0 + cnt - 1);
-      s_misc[33] = b;
-      s_misc[34] = v0;
-      s_misc[35] = cnt;
-      s_misc[36] = t0;
-      s_misc[37] = t1;
-      s_misc[38] = k - c;  // first chunk of the segment
+    s_misc[39] = total;
+    if (k < total) {
+      uint4 pa = plan_a[k];
+      uint2 pb = plan_b[k];
+      s_misc[33] = pa.x;
+      s_misc[34] = pa.y;
+      s_misc[35] = pa.z;
+      s_misc[38] = pa.w;
+      s_misc[36] = pb.x;
+      s_misc[37] = pb.y;
     }
   }
   __syncthreads();
   const uint32_t k = s_misc[32];
-  if (k >= cstart[256]) return;
+  if (k >= s_misc[39]) return;
   const uint32_t b = s_misc[33], v0 = s_misc[34], cnt = s_misc[35], t0 = s_misc[36], t1 = s_misc[37];
   const uint32_t k0 = s_misc[38];
+  const uint32_t R = t1 - t0 + 1;
   const uint32_t* off_b = off + (uint64_t)b * tiles;
-
-  // ---- compact the non-empty runs of tiles [t0, t1] into (virtual start, source base)
-  uint32_t nruns = 0;
-  for (uint32_t tb = t0; tb <= t1; tb += kThreads) {
-    uint32_t t = tb + threadIdx.x;
-    uint32_t vs = 0, len = 0;
-    if (t <= t1) {
-      uint64_t fi = (uint64_t)b * tiles + t;
-      vs = off[fi];
-      len = off[fi + 1] - vs;
+  const bool table = R <= kMaxRuns / 2;
+  if (table) {
+    for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
+      s_off[i] = off_b[t0 + i];
+      s_lo[i] = lo[(uint64_t)(t0 + i) * kRadix + b];
     }
-    uint32_t flag = len > 0 ? 1u : 0u, tot;
-    uint32_t ex = block_excl_scan<kThreads>(flag, s_misc, &tot);
-    if (flag) {
-      run_v[nruns + ex] = vs;
-      run_src[nruns + ex] = ((uint32_t)t << kTileLog2) + lo[(uint64_t)t * kRadix + b] - vs;
-    }
-    nruns += tot;
   }
   __syncthreads();
-  (void)off_b;
 
   // ---- gather the chunk's pairs (element order = virtual order = stable order)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t src[kItems];
+  if (table) {
+    uint32_t r = 0;
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-    uint32_t v = v0 + e;
-    src[j] = 0;
-    if (e < cnt) {
-      uint32_t r = search_le(run_v, 0, nruns, v);
-      src[j] = run_src[r] + v;
+    for (int j = 0; j < kItems; ++j) {
+      uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+      uint32_t v = v0 + e;
+      src[j] = 0;
+      if (e < cnt) {
+        if (j == 0) r = search_le(s_off, 0, R, v);
+        else
+          while (r + 1 < R && s_off[r + 1] <= v) ++r;
+        src[j] = ((t0 + r) << kTileLog2) + s_lo[r] + (v - s_off[r]);
+      }
+    }
+  } else {  // very sparse bucket: search the global run table directly
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+      uint32_t v = v0 + e;
+      src[j] = 0;
+      if (e < cnt) {
+        uint32_t t = (uint32_t)search_le_g(off_b, t0, (uint64_t)t1 + 1, v);
+        src[j] = (t << kTileLog2) + lo[(uint64_t)t * kRadix + b] + (v - off_b[t]);
+      }
     }
   }
   uint64_t k1[kItems];
@@ -329,13 +350,16 @@ size_t split_smem_bytes() { return SplitSmem::kBytes; }
 
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
-                                   uint64_t* status, uint32_t* ticket, uint64_t* tail_out, uint32_t* idx_out,
-                                   uint32_t grid_ub, cudaStream_t s) {
-  size_t smem = SplitSmem::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                   uint4* plan_a, uint2* plan_b, uint64_t* status, uint32_t* ticket,
+                                   uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s) {
+  kc_plan_level1<<<(grid_ub + 255) / 256, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  kc_split_level1<<<grid_ub, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, n, cstart, status, ticket,
-                                                   tail_out, idx_out);
+  size_t smem = SplitSmem::kBytes;
+  e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kc_split_level1<<<grid_ub, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, status,
+                                                   ticket, tail_out, idx_out);
   return cudaGetLastError();
 }
 

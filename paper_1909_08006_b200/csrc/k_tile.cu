@@ -15,6 +15,7 @@
 //   5. cnt[b * tiles + t] = tile count of byte-0 value b (bucket-major, for K-b's scan)
 //      lo[t * 256 + b]    = tile-local exclusive offset of b
 //   6. hist16[key bytes 0..1] += 1 (warp-aggregated global reductions) — the level-1 bucket sizes
+#include "block_rank.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -67,8 +68,7 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
     bool valid = r < cnt_t;
     uint32_t hi = bswap32(a[j]);            // key bytes 0..3, big-endian
     uint32_t d = hi >> 24;                  // byte 0
-    uint32_t key = valid ? d : (0x100u | lane);
-    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t peers = warp_peers8(d, valid);
     uint32_t before = __popc(peers & lt);
     uint32_t cur = valid ? wh[d] : 0;
     __syncwarp();
@@ -77,8 +77,7 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
     rank[j] = cur + before;
     // level-1 bucket sizes: 16-bit prefix (bytes 0..1)
     uint32_t p16 = hi >> 16;
-    uint32_t key16 = valid ? p16 : (0x10000u | lane);
-    uint32_t peers16 = __match_any_sync(0xffffffffu, key16);
+    uint32_t peers16 = peers & warp_peers8((hi >> 16) & 0xFFu, valid);
     if (valid && __popc(peers16 & lt) == 0) atomicAdd(&hist16[p16], (uint32_t)__popc(peers16));
   }
   __syncthreads();

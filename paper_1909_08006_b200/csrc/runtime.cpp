@@ -34,6 +34,7 @@ const OptDesc kOpts[] = {
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"profile", &Options::profile, 0, 1},
     {"ext_run_records", &Options::ext_run_records, 0, (int64_t)0xFFFFFFFEll},
+    {"l2_fetch_bytes", &Options::l2_fetch_bytes, 0, 128},
 };
 }  // namespace
 
@@ -109,6 +110,8 @@ InternalLayout plan_internal(uint64_t n) {
   L.off_scan_status = take(8 * 2 * L.scan_status_words);
   L.off_split_status = take(8 * (size_t)kRadix * L.split_chunks_ub);
   L.off_small = take(4 * 64);  // tickets + list counters
+  L.off_plan_a = take(16 * L.split_chunks_ub);
+  L.off_plan_b = take(8 * L.split_chunks_ub);
   L.bytes = o;
   return L;
 }

@@ -42,6 +42,7 @@ struct Options {
   int64_t kd_insert_max = 16;
   int64_t profile = 0;
   int64_t ext_run_records = 0;
+  int64_t l2_fetch_bytes = 0;  // 0 = leave the device default; else cudaLimitMaxL2FetchGranularity
 };
 Options options_snapshot();
 ley_status option_set(const char* name, int64_t value);
@@ -54,7 +55,7 @@ struct InternalLayout {
   // byte offsets inside the workspace
   size_t off_At = 0, off_Ai = 0, off_Bt = 0, off_Bi = 0, off_perm = 0;
   size_t off_cnt = 0, off_off = 0, off_lo = 0, off_hist16 = 0, off_B16 = 0, off_cstart = 0;
-  size_t off_scan_status = 0, off_split_status = 0, off_small = 0;
+  size_t off_scan_status = 0, off_split_status = 0, off_small = 0, off_plan_a = 0, off_plan_b = 0;
   size_t scan_status_words = 0;
   size_t bytes = 0;  // total
 };
