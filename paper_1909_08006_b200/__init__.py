@@ -15,7 +15,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libleyenda.so")
+_LIB_PATH = os.environ.get("LEY_LIBRARY_OVERRIDE") or os.path.join(_HERE, "libleyenda.so")
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(

@@ -76,14 +76,14 @@ __device__ __forceinline__ void block_rank_digits(const uint32_t (&dig)[ITEMS], 
   excl_d = excl;
 }
 
-// Decoupled look-back for digit d of chunk k whose segment starts at chunk k0: publishes the chunk's
-// aggregate, walks back until an inclusive prefix, publishes its own; returns the exclusive prefix.
-__device__ __forceinline__ uint32_t lookback_digit(uint64_t* status, uint64_t k, uint64_t k0, int d, uint32_t agg) {
-  if (k == k0) {
-    st_relaxed_u64(&status[k * kRadix + d], kFlagPrefix | agg);
-    return 0;
-  }
-  st_relaxed_u64(&status[k * kRadix + d], kFlagAggregate | agg);
+// Decoupled look-back for digit d of chunk k whose segment starts at chunk k0, in two halves so the
+// CTA can do useful work between them: publish the chunk's aggregate as soon as it is known, then
+// later walk back to an inclusive prefix and publish it. Returns the exclusive prefix.
+__device__ __forceinline__ void lookback_publish(uint64_t* status, uint64_t k, uint64_t k0, int d, uint32_t agg) {
+  st_relaxed_u64(&status[k * kRadix + d], (k == k0 ? kFlagPrefix : kFlagAggregate) | agg);
+}
+__device__ __forceinline__ uint32_t lookback_wait(uint64_t* status, uint64_t k, uint64_t k0, int d, uint32_t agg) {
+  if (k == k0) return 0;
   uint32_t excl = 0;
   uint64_t j = k - 1;
   while (true) {
@@ -96,6 +96,10 @@ __device__ __forceinline__ uint32_t lookback_digit(uint64_t* status, uint64_t k,
   }
   st_relaxed_u64(&status[k * kRadix + d], kFlagPrefix | (uint64_t)(excl + agg));
   return excl;
+}
+__device__ __forceinline__ uint32_t lookback_digit(uint64_t* status, uint64_t k, uint64_t k0, int d, uint32_t agg) {
+  lookback_publish(status, k, k0, d, agg);
+  return lookback_wait(status, k, k0, d, agg);
 }
 
 }  // namespace ley

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
     auto digit = [&](uint64_t t) -> uint32_t { return bits ? (uint32_t)(t >> shift) & mask : 0u; };
 
     uint64_t tr[RITEMS];
-    uint32_t xr[RITEMS], rr[RITEMS];
+    uint32_t xr[RITEMS], rr[RITEMS], dr[RITEMS];
     if (REGS) {
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
@@ -185,7 +185,10 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) rr[j] = atomicAdd(&s_cnt[digit(tr[j])], 1u);
+        if (i < s) {
+          dr[j] = digit(tr[j]);
+          rr[j] = atomicAdd(&s_cnt[dr[j]], 1u);
+        }
       }
     } else {
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) atomicAdd(&s_cnt[digit(tp[i])], 1u);
@@ -215,9 +218,11 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          uint32_t p = s_cnt[digit(tr[j])] + rr[j];
-          s_tail[p] = tr[j];
-          s_idx[p] = xr[j];
+          const uint32_t b = s_cnt[dr[j]], e = s_cnt[dr[j] + 1];
+          rr[j] |= (e - b) << 16;  // keep the sub-bucket size next to the rank (both < 2^16)
+          dr[j] = b;               // and its start
+          s_tail[b + (rr[j] & 0xFFFFu)] = tr[j];
+          s_idx[b + (rr[j] & 0xFFFFu)] = xr[j];
         }
       }
       __syncthreads();
@@ -225,14 +230,15 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t d = digit(tr[j]);
-          const uint32_t b = s_cnt[d], e = s_cnt[d + 1];
-          if (e - b <= (uint32_t)tu.kd_insert_max) {
+          const uint32_t b = dr[j], sz = rr[j] >> 16;
+          if (sz == 1) {
+            perm[sg.start + b] = xr[j];
+          } else if (sz <= (uint32_t)tu.kd_insert_max) {
             uint32_t rank = 0;
-            for (uint32_t m = b; m < e; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
+            for (uint32_t m = b; m < b + sz; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
             perm[sg.start + b + rank] = xr[j];
-          } else if (rr[j] == 0) {
-            s_bigl[atomicAdd(s_nbig, 1u)] = d;
+          } else if ((rr[j] & 0xFFFFu) == 0) {
+            s_bigl[atomicAdd(s_nbig, 1u)] = digit(tr[j]);
           }
         }
       }

@@ -93,107 +93,111 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(region);  // staging (scatter phase)
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kChunk);
-
-  if (threadIdx.x == 0) {
-    uint32_t k = atomicAdd(ticket, 1u);
-    uint32_t total = cstart[256];
-    s_misc[32] = k;
-    s_misc[39] = total;
-    if (k < total) {
-      uint4 pa = plan_a[k];
-      uint2 pb = plan_b[k];
-      s_misc[33] = pa.x;
-      s_misc[34] = pa.y;
-      s_misc[35] = pa.z;
-      s_misc[38] = pa.w;
-      s_misc[36] = pb.x;
-      s_misc[37] = pb.y;
-    }
-  }
-  __syncthreads();
-  const uint32_t k = s_misc[32];
-  if (k >= s_misc[39]) return;
-  const uint32_t b = s_misc[33], v0 = s_misc[34], cnt = s_misc[35], t0 = s_misc[36], t1 = s_misc[37];
-  const uint32_t k0 = s_misc[38];
-  const uint32_t R = t1 - t0 + 1;
-  const uint32_t* off_b = off + (uint64_t)b * tiles;
-  const bool table = R <= kMaxRuns / 2;
-  if (table) {
-    for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
-      s_off[i] = off_b[t0 + i];
-      s_lo[i] = lo[(uint64_t)(t0 + i) * kRadix + b];
-    }
-  }
-  __syncthreads();
-
-  // ---- gather the chunk's pairs (element order = virtual order = stable order)
+  const uint32_t total = cstart[256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t src[kItems];
-  if (table) {
-    uint32_t r = 0;
+
+  // persistent: thread 0 claims a ticket (= chunk id, handed out in order) whenever the CTA is free, so
+  // every chunk a chunk waits on in its look-back is already owned by a running CTA.
+  while (true) {
+    if (threadIdx.x == 0) {
+      const uint32_t k = atomicAdd(ticket, 1u);
+      s_misc[32] = k;
+      if (k < total) {
+        uint4 pa = plan_a[k];
+        uint2 pb = plan_b[k];
+        s_misc[33] = pa.x;
+        s_misc[34] = pa.y;
+        s_misc[35] = pa.z;
+        s_misc[38] = pa.w;
+        s_misc[36] = pb.x;
+        s_misc[37] = pb.y;
+      }
+    }
+    __syncthreads();
+    const uint32_t k = s_misc[32];
+    if (k >= total) return;
+    const uint32_t b = s_misc[33], v0 = s_misc[34], cnt = s_misc[35], t0 = s_misc[36], t1 = s_misc[37];
+    const uint32_t k0 = s_misc[38];
+    const uint32_t R = t1 - t0 + 1;
+    const uint32_t* off_b = off + (uint64_t)b * tiles;
+    const bool table = R <= kMaxRuns / 2;
+    if (table) {
+      for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
+        s_off[i] = off_b[t0 + i];
+        s_lo[i] = lo[(uint64_t)(t0 + i) * kRadix + b];
+      }
+    }
+    __syncthreads();
+
+    // ---- gather the chunk's pairs (element order = virtual order = stable order)
+    uint32_t src[kItems];
+    if (table) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+        uint32_t v = v0 + e;
+        src[j] = 0;
+        if (e < cnt) {
+          if (j == 0) r = search_le(s_off, 0, R, v);
+          else
+            while (r + 1 < R && s_off[r + 1] <= v) ++r;
+          src[j] = ((t0 + r) << kTileLog2) + s_lo[r] + (v - s_off[r]);
+        }
+      }
+    } else {  // very sparse bucket: search the global run table directly
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+        uint32_t v = v0 + e;
+        src[j] = 0;
+        if (e < cnt) {
+          uint32_t t = (uint32_t)search_le_g(off_b, t0, (uint64_t)t1 + 1, v);
+          src[j] = (t << kTileLog2) + lo[(uint64_t)t * kRadix + b] + (v - off_b[t]);
+        }
+      }
+    }
+    uint64_t k1[kItems];
+    uint32_t w[kItems], dig[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-      uint32_t v = v0 + e;
-      src[j] = 0;
       if (e < cnt) {
-        if (j == 0) r = search_le(s_off, 0, R, v);
-        else
-          while (r + 1 < R && s_off[r + 1] <= v) ++r;
-        src[j] = ((t0 + r) << kTileLog2) + s_lo[r] + (v - s_off[r]);
+        k1[j] = k1_in[src[j]];
+        w[j] = w_in[src[j]];
+      } else {
+        k1[j] = 0;
+        w[j] = 0;
       }
+      dig[j] = (uint32_t)(k1[j] >> 56);
     }
-  } else {  // very sparse bucket: search the global run table directly
+    __syncthreads();  // run tables dead from here on
+
+    uint32_t pos[kItems], total_d, excl_d;
+    block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+    if (threadIdx.x < kRadix) lookback_publish(status, k, k0, threadIdx.x, total_d);
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-      uint32_t v = v0 + e;
-      src[j] = 0;
       if (e < cnt) {
-        uint32_t t = (uint32_t)search_le_g(off_b, t0, (uint64_t)t1 + 1, v);
-        src[j] = (t << kTileLog2) + lo[(uint64_t)t * kRadix + b] + (v - off_b[t]);
+        uint32_t p = pos[j];
+        s_tail[p] = (k1[j] << 8) | (w[j] >> 24);
+        s_idx[p] = (src[j] & ~(kTileRecords - 1)) | (w[j] & 0xFFFFFFu);
+        s_dig[p] = (uint8_t)dig[j];
       }
     }
-  }
-  uint64_t k1[kItems];
-  uint32_t w[kItems], dig[kItems];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-    if (e < cnt) {
-      k1[j] = k1_in[src[j]];
-      w[j] = w_in[src[j]];
-    } else {
-      k1[j] = 0;
-      w[j] = 0;
+    if (threadIdx.x < kRadix) {
+      const int d = threadIdx.x;
+      uint32_t pre = lookback_wait(status, k, k0, d, total_d);
+      s_dst[d] = B16[b * 256 + d] + pre - excl_d;
     }
-    dig[j] = (uint32_t)(k1[j] >> 56);
-  }
-  __syncthreads();  // run tables dead from here on
-
-  uint32_t pos[kItems], total_d, excl_d;
-  block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
-
-  if (threadIdx.x < kRadix) {
-    const int d = threadIdx.x;
-    uint32_t pre = lookback_digit(status, k, k0, d, total_d);
-    s_dst[d] = B16[b * 256 + d] + pre - excl_d;
-  }
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-    if (e < cnt) {
-      uint32_t p = pos[j];
-      s_tail[p] = (k1[j] << 8) | (w[j] >> 24);
-      s_idx[p] = (src[j] & ~(kTileRecords - 1)) | (w[j] & 0xFFFFFFu);
-      s_dig[p] = (uint8_t)dig[j];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      uint32_t g = s_dst[s_dig[i]] + i;
+      tail_out[g] = s_tail[i];
+      idx_out[g] = s_idx[i];
     }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-    uint32_t g = s_dst[s_dig[i]] + i;
-    tail_out[g] = s_tail[i];
-    idx_out[g] = s_idx[i];
+    __syncthreads();  // staging and s_misc reused by the next chunk
   }
 }
 
@@ -358,8 +362,15 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
   size_t smem = SplitSmem::kBytes;
   e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kc_split_level1<<<grid_ub, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, status,
-                                                   ticket, tail_out, idx_out);
+  int per_sm = 2, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc_split_level1, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  uint32_t grid = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
+  if (grid > grid_ub) grid = grid_ub;
+  kc_split_level1<<<grid, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, status,
+                                               ticket, tail_out, idx_out);
   return cudaGetLastError();
 }
 
