@@ -1,11 +1,425 @@
-// external.cu — the external path (pinned host in/out larger than the device budget). Placeholder.
+// external.cu — the external path: pinned-host records larger than the device budget (SURVEY.md §8a
+// rows a10-a12; BASELINE.json configs[4]).
+//
+// PAPER.md §3.2 lines 114-118 (Figure 1, "External Sort-Merge-Write Routine"): "in the sort stage,
+// Leyenda reads and sorts records in small trunks and writes them down ... creating several sorted
+// intermediate files. In the merge stage ... a reader thread pool [reads] one partition at a time ...
+// merged by the merger thread to a globally sorted partition, using a K-way merge algorithm. Then the
+// writer thread will write it to the final output file. The partitioning, in other words - load
+// balancing process, makes it possible for read/merge/write threads to work simultaneously."
+//
+// B200 mapping (device memory capped by device_budget_bytes, P:19's memory limit):
+//   a10 run generation: run r = input records [r C, (r+1) C) -> H2D -> internal sort (K-a..K-e) -> D2H
+//       into pinned host run scratch; every S-th record of each sorted run is kept on the device as a
+//       sample. H2D of run r+1 overlaps D2H of run r (two copy streams, full-duplex PCIe).
+//   a11 partition location: the samples are sorted (the internal sort again: sample order = (key, run,
+//       pos)), every q-th one becomes a splitter, and K-loc binary-searches every sorted run for every
+//       splitter directly in pinned host memory (zero-copy) -> exact slice bounds split[p][r].
+//   a12 merge: partition p's R slices are copied H2D (concatenated in run order), turned into 16-byte
+//       composite keys (key bytes 0..9, position in the concatenation = (run, pos) order), merged by a
+//       ceil(log2 R)-level tree of 2-way merge-path merges (K-m), gathered (K-e style, device-local) and
+//       copied D2H to out at the partition's offset. D2H of p overlaps H2D of p+1.
+// Ties: records with equal keys from different runs come out in run order, within a run in position
+// order — i.e. by global input index, which is the stable order.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
 #include "runtime.h"
 
 namespace ley {
+namespace {
+
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------------------- kernels
+// samples[base + s] = run[s * S] (full 100-byte records, 4-byte words)
+__global__ void ext_take_samples(const uint32_t* __restrict__ run, uint64_t run_len, uint32_t S,
+                                 uint32_t* __restrict__ samples, uint64_t base) {
+  const uint64_t nsamp = (run_len + S - 1) / S;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nsamp * kRecordWords;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = w / kRecordWords, o = w - s * kRecordWords;
+    samples[(base + s) * kRecordWords + o] = run[s * S * kRecordWords + o];
+  }
+}
+
+// perm of a run -> global ordinals (run base added)
+__global__ void ext_add_base(uint32_t* __restrict__ p, uint64_t n, uint32_t base) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] += base;
+}
+
+struct Splitter {
+  uint8_t key[12];   // key bytes 0..9 (+2 pad)
+  uint32_t run;      // run of the splitter record
+  uint64_t pos;      // its position in that run
+};
+
+__device__ __forceinline__ int cmp_key10(const uint8_t* a, const uint8_t* b) {
+  for (int i = 0; i < 10; ++i) {
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  }
+  return 0;
+}
+
+// split[p * R + r] = number of records of run r that precede splitter p in (key, run, pos) order.
+// Binary search over the sorted run, reading keys from pinned host scratch (zero-copy).
+__global__ void ext_locate(const uint8_t* __restrict__ scratch_dev, const uint64_t* __restrict__ run_off,
+                           const uint64_t* __restrict__ run_len, uint32_t R, const Splitter* __restrict__ spl,
+                           uint32_t nspl, uint64_t* __restrict__ split) {
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (uint64_t)nspl * R) return;
+  const uint32_t p = (uint32_t)(id / R), r = (uint32_t)(id % R);
+  const Splitter sp = spl[p];
+  const uint8_t* base = scratch_dev + run_off[r] * kRecordBytes;
+  uint64_t lo = 0, hi = run_len[r];
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    uint8_t k[10];
+    const uint8_t* rec = base + mid * kRecordBytes;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) k[i] = rec[i];
+    const int c = cmp_key10(k, sp.key);
+    const bool before = c < 0 || (c == 0 && (r < sp.run || (r == sp.run && mid < sp.pos)));
+    if (before) lo = mid + 1; else hi = mid;
+  }
+  split[id] = lo;
+}
+
+// composite key of element i of the concatenated slice buffer: (key bytes 0..7 BE, bytes 8..9 << 48 | i)
+__global__ void ext_make_comp(const uint8_t* __restrict__ recs, uint64_t m, uint64_t* __restrict__ hi,
+                              uint64_t* __restrict__ lo) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(recs + i * kRecordBytes);
+    const uint32_t a = w[0], b = w[1], c = w[2];
+    hi[i] = ((uint64_t)bswap32(a) << 32) | bswap32(b);
+    lo[i] = ((uint64_t)(((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) << 48) | i;
+  }
+}
+
+__device__ __forceinline__ bool comp_less(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+
+// One level of the K-m merge tree: adjacent sequence pairs (bnd[2q], bnd[2q+1], bnd[2q+2]) are merged
+// into the same output range. Each thread owns kMergeItems consecutive outputs: one merge-path binary
+// search on its start diagonal, then a sequential merge.
+constexpr int kMergeItems = 16;
+__global__ void ext_merge_level(const uint64_t* __restrict__ ih, const uint64_t* __restrict__ il,
+                                uint64_t* __restrict__ oh, uint64_t* __restrict__ ol, uint64_t m,
+                                const uint64_t* __restrict__ bnd, uint32_t K) {
+  const uint64_t j0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
+  if (j0 >= m) return;
+  const uint64_t j1 = min(m, j0 + kMergeItems);
+  uint64_t j = j0;
+  while (j < j1) {
+    // pair q containing output j: largest q with bnd[2q] <= j
+    uint32_t qlo = 0, qhi = (K + 1) / 2;
+    while (qhi - qlo > 1) {
+      uint32_t mid = (qlo + qhi) >> 1;
+      if (bnd[2 * mid] <= j) qlo = mid; else qhi = mid;
+    }
+    const uint32_t q = qlo;
+    const uint64_t a0 = bnd[2 * q];
+    const uint64_t a1 = (2 * q + 1 <= K) ? bnd[min(2 * q + 1, K)] : a0;
+    const uint64_t b1 = (2 * q + 2 <= K) ? bnd[2 * q + 2] : a1;
+    const uint64_t lenA = a1 - a0, lenB = b1 - a1;
+    const uint64_t diag = j - a0;
+    uint64_t lo = diag > lenB ? diag - lenB : 0, hi = min(diag, lenA);
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      const uint64_t bi = a1 + diag - 1 - mid;
+      if (comp_less(ih[a0 + mid], il[a0 + mid], ih[bi], il[bi])) lo = mid + 1; else hi = mid;
+    }
+    uint64_t ia = a0 + lo, ib = a1 + (diag - lo);
+    const uint64_t jend = min(j1, b1);
+    for (; j < jend; ++j) {
+      bool takeA;
+      if (ia >= a1) takeA = false;
+      else if (ib >= b1) takeA = true;
+      else takeA = comp_less(ih[ia], il[ia], ih[ib], il[ib]);
+      if (takeA) {
+        oh[j] = ih[ia];
+        ol[j] = il[ia];
+        ++ia;
+      } else {
+        oh[j] = ih[ib];
+        ol[j] = il[ib];
+        ++ib;
+      }
+    }
+  }
+}
+
+// out[j] = slice[pos_j], pos_j = low 48 bits of the merged composite (device-local gather, word stream)
+__global__ void ext_gather(const uint32_t* __restrict__ slice, const uint64_t* __restrict__ lo, uint64_t m,
+                           uint32_t* __restrict__ out, const uint32_t* __restrict__ pslice, uint32_t* __restrict__ pout) {
+  const uint64_t words = m * kRecordWords;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = w / kRecordWords, o = w - j * kRecordWords;
+    const uint64_t p = lo[j] & 0xFFFFFFFFFFFFull;
+    out[w] = slice[p * kRecordWords + o];
+    if (pout && o == 0) pout[j] = pslice[p];
+  }
+}
+
+unsigned grid_for(uint64_t work, int sms, int per_sm = 8) {
+  uint64_t b = (work + 255) / 256;
+  uint64_t cap = (uint64_t)sms * per_sm;
+  return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------- driver
 ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                               uint64_t budget, cudaStream_t s, Profiler& prof) {
-  (void)ctx; (void)in; (void)out; (void)perm_out; (void)n; (void)budget; (void)s; (void)prof;
-  set_error("external path: not available in this build");
-  return LEY_ERR_UNSUPPORTED;
+  ley_status st;
+  const uint64_t C = external_run_records(n, budget);
+  if (C < 1024 && C < n) {
+    set_error("external: device_budget_bytes " + std::to_string(budget) +
+              " is below the minimum working set (runs of >= 1024 records)");
+    return LEY_ERR_BUDGET;
+  }
+  const uint32_t R = (uint32_t)((n + C - 1) / C);
+  const int sms = ctx.sms;
+  // ---------------------------------------------------------------- device buffer plan (within budget)
+  // run generation: run in (100 C) + run out (100 C) + internal workspace(C) + samples
+  const InternalLayout LC = plan_internal(C);
+  const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>(4096, C / 16));  // sample stride
+  uint64_t nsamp = 0;
+  std::vector<uint64_t> run_off(R), run_len(R), samp_base(R);
+  for (uint32_t r = 0; r < R; ++r) {
+    run_off[r] = (uint64_t)r * C;
+    run_len[r] = std::min<uint64_t>(C, n - run_off[r]);
+    samp_base[r] = nsamp;
+    nsamp += (run_len[r] + S - 1) / S;
+  }
+  const size_t sz_run = a256(C * kRecordBytes);
+  const size_t sz_samples = a256(nsamp * kRecordBytes);
+  const size_t phase1 = 2 * sz_run + a256(LC.bytes) + 2 * sz_samples + a256(4 * nsamp) + a256(4 * C) +
+                        a256(plan_internal(nsamp).bytes);
+  if ((st = ensure_buffer(ctx.ext, phase1, "external buffers", s))) return st;
+  uint8_t* eb = static_cast<uint8_t*>(ctx.ext.ptr);
+  uint8_t* d_in = eb;
+  uint8_t* d_out = d_in + sz_run;
+  uint8_t* d_work = d_out + sz_run;
+  uint8_t* d_samp = d_work + a256(LC.bytes);
+  uint8_t* d_samp_sorted = d_samp + sz_samples;
+  uint32_t* d_samp_perm = reinterpret_cast<uint32_t*>(d_samp_sorted + sz_samples);
+  uint32_t* d_run_perm = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_samp_perm) + a256(4 * nsamp));
+  uint8_t* d_work2 = reinterpret_cast<uint8_t*>(d_run_perm) + a256(4 * C);
+
+  // pinned host run scratch (records, and global ordinals when perm is requested)
+  const size_t scratch_bytes = (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0);
+  if (ctx.host_scratch_cap < scratch_bytes) {
+    if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
+    ctx.host_scratch = nullptr;
+    ctx.host_scratch_cap = 0;
+    LEY_CUDA("external scratch", cudaHostAlloc(&ctx.host_scratch, scratch_bytes, cudaHostAllocMapped));
+    ctx.host_scratch_cap = scratch_bytes;
+  }
+  uint8_t* h_runs = static_cast<uint8_t*>(ctx.host_scratch);
+  uint32_t* h_perm = perm_out ? reinterpret_cast<uint32_t*>(h_runs + (size_t)n * kRecordBytes) : nullptr;
+  uint8_t* h_runs_dev = nullptr;
+  LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&h_runs_dev, h_runs, 0));
+
+  if (!ctx.copy_stream[0]) {
+    for (int i = 0; i < 2; ++i) LEY_CUDA("external", cudaStreamCreateWithFlags(&ctx.copy_stream[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) LEY_CUDA("external", cudaEventCreateWithFlags(&ctx.ev[i], cudaEventDisableTiming));
+  }
+  cudaStream_t h2d = ctx.copy_stream[0], d2h = ctx.copy_stream[1];
+  cudaEvent_t ev_start = ctx.ev[0], ev_in = ctx.ev[1], ev_sorted = ctx.ev[2], ev_out = ctx.ev[3];
+
+  // ---------------------------------------------------------------- a10: run generation
+  if ((st = prof.begin("ext run generation"))) return st;
+  LEY_CUDA("ext runs", cudaEventRecord(ev_start, s));
+  LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_start, 0));
+  LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_start, 0));
+  Profiler quiet;  // inner sorts are not profiled stage by stage
+  quiet.ctx = &ctx;
+  quiet.stream = s;
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint64_t len = run_len[r];
+    // d_in is free once the previous run's sort finished (ev_sorted on s)
+    if (r > 0) LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_sorted, 0));
+    LEY_CUDA("ext H2D", cudaMemcpyAsync(d_in, in + run_off[r] * kRecordBytes, len * kRecordBytes,
+                                        cudaMemcpyHostToDevice, h2d));
+    LEY_CUDA("ext runs", cudaEventRecord(ev_in, h2d));
+    LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_in, 0));
+    // d_out is free once the previous run's D2H finished
+    if (r > 0) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out, 0));
+    st = sort_internal_device(ctx, d_in, d_out, perm_out ? d_run_perm : nullptr, len, s, quiet, d_work, LC.bytes);
+    if (st) return st;
+    prof.launches += quiet.launches;
+    quiet.launches = 0;
+    ext_take_samples<<<grid_for((len + S - 1) / S * kRecordWords, sms), 256, 0, s>>>(
+        reinterpret_cast<const uint32_t*>(d_out), len, (uint32_t)S, reinterpret_cast<uint32_t*>(d_samp), samp_base[r]);
+    LEY_CUDA("ext samples", cudaGetLastError());
+    prof.launches += 1;
+    if (perm_out) {
+      ext_add_base<<<grid_for(len, sms), 256, 0, s>>>(d_run_perm, len, (uint32_t)run_off[r]);
+      LEY_CUDA("ext perm", cudaGetLastError());
+      prof.launches += 1;
+    }
+    LEY_CUDA("ext runs", cudaEventRecord(ev_sorted, s));
+    LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_sorted, 0));
+    LEY_CUDA("ext D2H", cudaMemcpyAsync(h_runs + run_off[r] * kRecordBytes, d_out, len * kRecordBytes,
+                                        cudaMemcpyDeviceToHost, d2h));
+    if (perm_out)
+      LEY_CUDA("ext D2H", cudaMemcpyAsync(h_perm + run_off[r], d_run_perm, len * 4, cudaMemcpyDeviceToHost, d2h));
+    LEY_CUDA("ext runs", cudaEventRecord(ev_out, d2h));
+  }
+  LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out, 0));
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- a11: splitters and slice bounds
+  if ((st = prof.begin("ext partition"))) return st;
+  // merge-phase device plan: a partition of m records needs slice (100 m) + out (100 m) + 2 x 16 m
+  // composites (+ 8 m perm); keep it inside the same budget as phase 1.
+  const size_t per_rec = 2 * kRecordBytes + 32 + (perm_out ? 8 : 0);
+  const size_t lists = 7ull * 16 * std::min<uint64_t>(65536, C) + (2u << 20);
+  const size_t avail = std::max<size_t>(budget > lists ? budget - lists : 0, per_rec * 1024);
+  uint64_t m_target = std::max<uint64_t>(1024, avail / per_rec);
+  // samples between splitters q: partition size <= (q + R) * S
+  uint64_t q = m_target / S > 2ull * R ? m_target / S - R : std::max<uint64_t>(1, m_target / (2 * S));
+  if (q == 0) q = 1;
+  const uint32_t P = (uint32_t)std::max<uint64_t>(1, (nsamp + q - 1) / q);
+  std::vector<Splitter> spl(P > 1 ? P - 1 : 0);
+  std::vector<uint64_t> split((size_t)(P + 1) * R);
+  for (uint32_t r = 0; r < R; ++r) {
+    split[r] = 0;
+    split[(size_t)P * R + r] = run_len[r];
+  }
+  if (P > 1) {
+    st = sort_internal_device(ctx, d_samp, d_samp_sorted, d_samp_perm, nsamp, s, quiet, d_work2,
+                              plan_internal(nsamp).bytes);
+    if (st) return st;
+    prof.launches += quiet.launches;
+    quiet.launches = 0;
+    std::vector<uint32_t> sp_idx(P - 1);
+    std::vector<uint8_t> sp_key(10);
+    for (uint32_t p = 1; p < P; ++p) {
+      const uint64_t at = (uint64_t)p * q;
+      uint32_t sidx = 0;
+      LEY_CUDA("ext splitters", cudaMemcpyAsync(&sidx, d_samp_perm + at, 4, cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("ext splitters", cudaMemcpyAsync(spl[p - 1].key, d_samp_sorted + at * kRecordBytes, 10,
+                                                cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("ext splitters", cudaStreamSynchronize(s));
+      const uint32_t r = (uint32_t)(std::upper_bound(samp_base.begin(), samp_base.end(), (uint64_t)sidx) -
+                                    samp_base.begin() - 1);
+      spl[p - 1].run = r;
+      spl[p - 1].pos = (sidx - samp_base[r]) * S;
+    }
+    Splitter* d_spl = reinterpret_cast<Splitter*>(d_work);
+    uint64_t* d_runoff = reinterpret_cast<uint64_t*>(d_work + a256(sizeof(Splitter) * spl.size()));
+    uint64_t* d_runlen = d_runoff + R;
+    uint64_t* d_split = d_runlen + R;
+    LEY_CUDA("ext locate", cudaMemcpyAsync(d_spl, spl.data(), sizeof(Splitter) * spl.size(), cudaMemcpyHostToDevice, s));
+    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runoff, run_off.data(), 8 * R, cudaMemcpyHostToDevice, s));
+    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runlen, run_len.data(), 8 * R, cudaMemcpyHostToDevice, s));
+    const uint64_t nthreads = (uint64_t)(P - 1) * R;
+    ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
+                                                                  d_split);
+    LEY_CUDA("ext locate", cudaGetLastError());
+    prof.launches += 1;
+    LEY_CUDA("ext locate", cudaMemcpyAsync(split.data() + R, d_split, 8 * nthreads, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("ext locate", cudaStreamSynchronize(s));
+  }
+  uint64_t m_max = 0;
+  std::vector<uint64_t> part_off(P + 1, 0);
+  for (uint32_t p = 0; p < P; ++p) {
+    uint64_t m = 0;
+    for (uint32_t r = 0; r < R; ++r) m += split[(size_t)(p + 1) * R + r] - split[(size_t)p * R + r];
+    part_off[p + 1] = part_off[p] + m;
+    m_max = std::max(m_max, m);
+  }
+  if ((st = prof.end())) return st;
+
+  // ---------------------------------------------------------------- a12: K-way merge per partition
+  if ((st = prof.begin("ext merge"))) return st;
+  const size_t sz_slice = a256(m_max * kRecordBytes);
+  const size_t sz_comp = a256(m_max * 8);
+  const size_t phase2 = 2 * sz_slice + 4 * sz_comp + (perm_out ? 2 * a256(m_max * 4) : 0) + a256(8 * (R + 1));
+  if (phase2 > ctx.ext.cap) {
+    if ((st = ensure_buffer(ctx.ext, phase2, "external merge buffers", s))) return st;
+  }
+  eb = static_cast<uint8_t*>(ctx.ext.ptr);
+  uint8_t* d_slice = eb;
+  uint8_t* d_mout = d_slice + sz_slice;
+  uint64_t* c_h[2] = {reinterpret_cast<uint64_t*>(d_mout + sz_slice), nullptr};
+  uint64_t* c_l[2] = {reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_h[0]) + sz_comp), nullptr};
+  c_h[1] = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_l[0]) + sz_comp);
+  c_l[1] = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_h[1]) + sz_comp);
+  uint8_t* after = reinterpret_cast<uint8_t*>(c_l[1]) + sz_comp;
+  uint32_t* d_pslice = perm_out ? reinterpret_cast<uint32_t*>(after) : nullptr;
+  uint32_t* d_pout = perm_out ? reinterpret_cast<uint32_t*>(after + a256(m_max * 4)) : nullptr;
+  uint64_t* d_bnd = reinterpret_cast<uint64_t*>(after + (perm_out ? 2 * a256(m_max * 4) : 0));
+  std::vector<uint64_t> bnd(R + 1);
+  bool first = true;
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint64_t m = part_off[p + 1] - part_off[p];
+    if (m == 0) continue;
+    // slices H2D (d_slice free once the previous partition's gather finished)
+    if (!first) LEY_CUDA("ext merge", cudaStreamWaitEvent(h2d, ev_sorted, 0));
+    uint64_t at = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      const uint64_t lo = split[(size_t)p * R + r], hi = split[(size_t)(p + 1) * R + r];
+      bnd[r] = at;
+      if (hi > lo) {
+        LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice + at * kRecordBytes,
+                                                  h_runs + (run_off[r] + lo) * kRecordBytes, (hi - lo) * kRecordBytes,
+                                                  cudaMemcpyHostToDevice, h2d));
+        if (perm_out)
+          LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice + at, h_perm + run_off[r] + lo, (hi - lo) * 4,
+                                                    cudaMemcpyHostToDevice, h2d));
+      }
+      at += hi - lo;
+    }
+    bnd[R] = at;
+    LEY_CUDA("ext merge", cudaEventRecord(ev_in, h2d));
+    LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_in, 0));
+    if (!first) LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out, 0));  // d_mout free
+    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice, m, c_h[0], c_l[0]);
+    LEY_CUDA("K-m merge", cudaGetLastError());
+    prof.launches += 1;
+    // merge tree over the R run slices
+    std::vector<uint64_t> cur(bnd.begin(), bnd.end());
+    int src = 0;
+    while (cur.size() > 2) {
+      const uint32_t K = (uint32_t)cur.size() - 1;
+      LEY_CUDA("K-m merge", cudaMemcpyAsync(d_bnd, cur.data(), 8 * cur.size(), cudaMemcpyHostToDevice, s));
+      const uint64_t threads = (m + kMergeItems - 1) / kMergeItems;
+      ext_merge_level<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(c_h[src], c_l[src], c_h[src ^ 1], c_l[src ^ 1],
+                                                                        m, d_bnd, K);
+      LEY_CUDA("K-m merge", cudaGetLastError());
+      prof.launches += 1;
+      // host copy of the boundaries must outlive the async H2D: wait for it before reusing `cur`
+      LEY_CUDA("K-m merge", cudaStreamSynchronize(s));
+      std::vector<uint64_t> nxt;
+      for (size_t i = 0; i < cur.size(); i += 2) nxt.push_back(cur[i]);
+      if (nxt.back() != cur.back()) nxt.push_back(cur.back());
+      cur.swap(nxt);
+      src ^= 1;
+    }
+    ext_gather<<<grid_for(m * kRecordWords, sms), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(d_slice), c_l[src], m,
+                                                               reinterpret_cast<uint32_t*>(d_mout), d_pslice, d_pout);
+    LEY_CUDA("K-e gather", cudaGetLastError());
+    prof.launches += 1;
+    LEY_CUDA("ext merge", cudaEventRecord(ev_sorted, s));
+    LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ev_sorted, 0));
+    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + part_off[p] * kRecordBytes, d_mout, m * kRecordBytes,
+                                              cudaMemcpyDeviceToHost, d2h));
+    if (perm_out)
+      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + part_off[p], d_pout, m * 4, cudaMemcpyDeviceToHost, d2h));
+    LEY_CUDA("ext merge", cudaEventRecord(ev_out, d2h));
+    first = false;
+  }
+  LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out, 0));
+  if ((st = prof.end())) return st;
+  return LEY_OK;
 }
+
 }  // namespace ley

@@ -22,12 +22,18 @@ inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                                cudaStream_t s, Profiler& prof) {
+                                cudaStream_t s, Profiler& prof, void* work, size_t work_bytes) {
   const InternalLayout L = plan_internal(n);
-  ley_status st = ensure_buffer(ctx.work, L.bytes, "workspace", s);
-  if (st) return st;
+  ley_status st;
+  if (!work) {
+    if ((st = ensure_buffer(ctx.work, L.bytes, "workspace", s))) return st;
+    work = ctx.work.ptr;
+  } else if (work_bytes < L.bytes) {
+    set_error("internal: caller workspace too small");
+    return LEY_ERR_BUDGET;
+  }
   if (!ctx.host_pinned) LEY_CUDA("setup", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
-  uint8_t* base = static_cast<uint8_t*>(ctx.work.ptr);
+  uint8_t* base = static_cast<uint8_t*>(work);
   uint64_t* At = reinterpret_cast<uint64_t*>(base + L.off_At);
   uint32_t* Ai = reinterpret_cast<uint32_t*>(base + L.off_Ai);
   uint64_t* Bt = reinterpret_cast<uint64_t*>(base + L.off_Bt);
@@ -93,7 +99,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   if ((st = prof.begin("K-d buckets"))) return st;
   uint64_t tier = std::max<uint64_t>(tu.smem_tier_max, tu.warp_tier_max);
   uint64_t big_cap = std::min<uint64_t>(65536, n / (tier + 1) + 1);
-  uint32_t kd_cap = 65536;
+  uint32_t kd_cap = (uint32_t)std::min<uint64_t>(65536, n);  // level-1 buckets: at most min(2^16, n) non-empty
   if ((st = ensure_buffer(ctx.lists, (size_t)kNumKdLists * a256((size_t)kd_cap * sizeof(Seg)), "K-d lists", s)))
     return st;
   if ((st = ensure_buffer(ctx.big[0], big_cap * sizeof(Seg), "big-bucket list", s))) return st;

@@ -116,16 +116,26 @@ InternalLayout plan_internal(uint64_t n) {
   return L;
 }
 
-// External path: the largest run (records) whose staged internal sort fits the budget:
-// 100 r (run in) + 100 r (run out) + scratch(r) <= budget.
+// External path: the largest run C (records) whose run-generation working set fits the
+// budget: run in + run out (200 C) + the internal sort's workspace and K-d lists for C records + the run's
+// perm (4 C) + the sample buffers (every S-th record of every run, S = min(4096, C/16)) + 2 MB slack.
+uint64_t external_run_need(uint64_t n, uint64_t C) {
+  if (C == 0) return 0;
+  const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>(4096, C / 16));
+  const uint64_t runs = (n + C - 1) / C;
+  const uint64_t nsamp = runs * ((C + S - 1) / S);
+  const uint64_t lists = 6ull * 16 * std::min<uint64_t>(65536, C) + 16ull * std::min<uint64_t>(65536, C);
+  return 204 * C + plan_internal(C).bytes + lists + 2 * 100 * nsamp + 4 * nsamp + plan_internal(nsamp).bytes +
+         (2ull << 20);
+}
+
 uint64_t external_run_records(uint64_t n, uint64_t budget) {
   Options o = options_snapshot();
   if (o.ext_run_records > 0) return std::min<uint64_t>(n, (uint64_t)o.ext_run_records);
   uint64_t lo = 0, hi = std::min<uint64_t>(n, 0xFFFFFFFEull);
   while (lo < hi) {
     uint64_t mid = lo + (hi - lo + 1) / 2;
-    uint64_t need = 200 * mid + plan_internal(mid).bytes + (64ull << 20);
-    if (need <= budget) lo = mid; else hi = mid - 1;
+    if (external_run_need(n, mid) <= budget) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -211,6 +221,17 @@ void release_device(int device) {
     }
     if (c.host_pinned) cudaFreeHost(c.host_pinned);
     c.host_pinned = nullptr;
+    if (c.host_scratch) cudaFreeHost(c.host_scratch);
+    c.host_scratch = nullptr;
+    c.host_scratch_cap = 0;
+    for (int i = 0; i < 2; ++i) {
+      if (c.copy_stream[i]) cudaStreamDestroy(c.copy_stream[i]);
+      c.copy_stream[i] = nullptr;
+    }
+    for (int i = 0; i < 4; ++i) {
+      if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+      c.ev[i] = nullptr;
+    }
     for (cudaEvent_t e : c.events) cudaEventDestroy(e);
     c.events.clear();
     cudaSetDevice(prev);

@@ -81,6 +81,10 @@ struct DeviceContext {
   DeviceBuffer stage;     // staged input/output for host pointers
   DeviceBuffer ext;       // external path device buffers
   void* host_pinned = nullptr;  // small pinned host scratch (counters)
+  void* host_scratch = nullptr;  // external path: pinned (mapped) host run scratch
+  size_t host_scratch_cap = 0;
+  cudaStream_t copy_stream[2] = {nullptr, nullptr};  // external path: H2D / D2H copy streams
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> events;
 };
 DeviceContext& device_context(int device);
@@ -105,7 +109,8 @@ int stage_times(const char** names, float* ms, int max, int* launches);
 
 // ------------------------------------------------------------------ drivers
 // Internal sort of device-resident records (K-a .. K-e). perm_out may be null.
+// `work` (optional) is a caller-provided workspace of >= plan_internal(n).bytes; else ctx.work is used.
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                                cudaStream_t s, Profiler& prof);
+                                cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0);
 
 }  // namespace ley

@@ -154,3 +154,53 @@ def test_c3_full_size_certificate():
     x = device_records(n, seed=2, dist="skewed")
     h_in, h_out = _certify_on_host(x, n)
     assert oracle.multiset_hash(h_in) == oracle.multiset_hash(h_out)
+
+
+# ------------------------------------------------------------------ external path
+def _pinned(recs):
+    x = torch.from_numpy(recs).pin_memory()
+    return x, torch.empty_like(x).pin_memory()
+
+
+@pytest.mark.parametrize("dist,n,budget", [
+    ("uniform", 1_000_000, 16 << 20),     # ~28 runs, many partitions
+    ("skewed", 600_001, 12 << 20),        # duplicates spanning runs and partitions
+    ("all_equal", 300_000, 8 << 20),      # every tie crosses runs: output == input
+    ("tiny_alphabet", 250_003, 8 << 20),
+    ("sorted", 200_000, 8 << 20),
+    ("reverse", 200_000, 8 << 20),
+])
+def test_external_matches_oracle(dist, n, budget):
+    import paper_1909_08006_b200 as ley
+
+    plan = ley.ley_plan_query(n, budget)
+    assert plan["host_path"] == 1 and plan["runs"] > 1
+    recs = gen.records(n, seed=41, dist=dist)
+    x, out = _pinned(recs)
+    perm = torch.empty(n, dtype=torch.int32).pin_memory()
+    ley.ley_sort_perm(x, out, perm, n, device_budget_bytes=budget)
+    assert_parity(recs, out.numpy(), perm.numpy().view(np.uint32))
+
+
+def test_external_equals_internal_and_single_run():
+    import paper_1909_08006_b200 as ley
+
+    n = 400_000
+    recs = gen.records(n, seed=43, dist="skewed")
+    x, out_ext = _pinned(recs)
+    ley.ley_sort(x, out_ext, n, device_budget_bytes=10 << 20)
+    out_int, _ = gpu_sort(recs, with_perm=False)
+    assert np.array_equal(out_ext.numpy(), out_int)
+    # K = 1 run: the merge stage degenerates to a copy
+    with Options(ext_run_records=n):
+        out1 = torch.empty_like(x).pin_memory()
+        ley.ley_sort(x, out1, n, device_budget_bytes=10 << 20)
+    assert np.array_equal(out1.numpy(), out_int)
+
+
+def test_external_budget_too_small():
+    import paper_1909_08006_b200 as ley
+
+    n = 100_000
+    x, out = _pinned(gen.records(n, seed=1))
+    assert ley.ley_sort(x, out, n, device_budget_bytes=1 << 20, raise_on_error=False) == ley.LEY_ERR_BUDGET
