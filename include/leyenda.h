@@ -94,6 +94,30 @@ ley_status ley_sort_dist(ley_comm* comm, const void* in_local, uint64_t n_local,
                          uint64_t device_budget_bytes, void* stream);
 ley_status ley_comm_destroy(ley_comm* comm);
 
+/* Loopback verification hook: the same G-rank algorithm (kernels K-s0/K-s1/
+ * K-s2/K-p, plans, local sort) with all G ranks' slices on the CURRENT device and device copies standing
+ * in for the NCCL collectives. Arrays have nranks entries; in_local[r]/out_local[r] are device pointers.
+ * Same results as ley_sort_dist on G GPUs. Not a performance path. */
+ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const uint64_t* n_local,
+                                  void* const* out_local, const uint64_t* out_capacity_records,
+                                  uint64_t* n_out_local, uint64_t* out_global_offset, uint32_t record_bytes,
+                                  uint32_t key_bytes, void* stream);
+
+/* Host-only planning steps of the distributed sort (pure functions, no CUDA; exposed so the multi-rank
+ * logic is testable on CPU with any transport):
+ *  ley_dist_plan_splitters: global 65536-bin histogram of key bytes 0..1 (u64) and N -> for k = 1..G-1
+ *    the bin holding global sorted rank floor(k N / G) (bins[k-1]), that rank's offset inside the bin
+ *    (rank_in_bin[k-1]) and the number of records in smaller bins (bin_first[k-1]). 0 on success.
+ *  ley_dist_bin_dest_counts: per-destination record counts of a rank's WHOLE bins (bins that hold no
+ *    splitter); boundary-bin records are counted separately against the exact splitters.
+ *  ley_dist_plan_exchange: G x G send-count matrix [src][dst] -> this rank's receive counts/offsets (in
+ *    source-rank order), send offsets, output size and global output offset. */
+int ley_dist_plan_splitters(const uint64_t* global_hist16, uint64_t n_total, int nranks, uint32_t* bins,
+                            uint64_t* rank_in_bin, uint64_t* bin_first);
+void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins, int nranks, uint64_t* counts);
+void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
+                            uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset);
+
 /* ---------------------------------------------------------------- introspection and tuning */
 
 /* Host-only plan query (no CUDA calls): device bytes the library allocates to sort n_records on one

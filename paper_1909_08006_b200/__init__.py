@@ -40,7 +40,8 @@ MAX_RECORDS = 0xFFFFFFFE
 
 EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get_unique_id", "ley_comm_init",
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
-                    "ley_stage_times", "ley_release_cache", "ley_version")
+                    "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
+                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange")
 
 
 class ley_plan_info(ctypes.Structure):
@@ -79,6 +80,16 @@ _lib.ley_release_cache.argtypes = [_i32]
 _lib.ley_release_cache.restype = _i32
 _lib.ley_version.argtypes = []
 _lib.ley_version.restype = _u32
+_pu64 = ctypes.POINTER(_u64)
+_lib.ley_sort_dist_loopback.argtypes = [_i32, ctypes.POINTER(_vp), _pu64, ctypes.POINTER(_vp), _pu64, _pu64, _pu64,
+                                        _u32, _u32, _vp]
+_lib.ley_sort_dist_loopback.restype = _i32
+_lib.ley_dist_plan_splitters.argtypes = [_pu64, _u64, _i32, ctypes.POINTER(_u32), _pu64, _pu64]
+_lib.ley_dist_plan_splitters.restype = _i32
+_lib.ley_dist_bin_dest_counts.argtypes = [_pu64, ctypes.POINTER(_u32), _i32, _pu64]
+_lib.ley_dist_bin_dest_counts.restype = None
+_lib.ley_dist_plan_exchange.argtypes = [_pu64, _i32, _i32, _pu64, _pu64, _pu64, _pu64, _pu64]
+_lib.ley_dist_plan_exchange.restype = None
 
 
 class LeyendaError(RuntimeError):
@@ -199,6 +210,51 @@ def ley_sort_dist(comm: int, in_local, n_local: int, out_local, out_capacity_rec
 
 def ley_comm_destroy(comm: int) -> None:
     _check(_lib.ley_comm_destroy(comm), "ley_comm_destroy", True)
+
+
+def ley_sort_dist_loopback(ins, n_locals, outs, caps, record_bytes: int = RECORD_BYTES, key_bytes: int = KEY_BYTES,
+                           stream=None):
+    """G logical ranks on the current device (test hook). Returns [(n_out, out_global_offset)] per rank."""
+    G = len(ins)
+    a_in = (_vp * G)(*[_addr(x) for x in ins])
+    a_out = (_vp * G)(*[_addr(x) for x in outs])
+    a_n = (_u64 * G)(*n_locals)
+    a_cap = (_u64 * G)(*caps)
+    n_out = (_u64 * G)()
+    off = (_u64 * G)()
+    st = _lib.ley_sort_dist_loopback(G, a_in, a_n, a_out, a_cap, n_out, off, record_bytes, key_bytes, _stream(stream))
+    _check(st, "ley_sort_dist_loopback", True)
+    return [(n_out[i], off[i]) for i in range(G)]
+
+
+def ley_dist_plan_splitters(global_hist16, n_total: int, nranks: int):
+    """-> (bins, rank_in_bin, bin_first), each a list of nranks-1 ints."""
+    h = (_u64 * 65536)(*[int(x) for x in global_hist16])
+    k = max(nranks - 1, 1)
+    bins, rho, first = (_u32 * k)(), (_u64 * k)(), (_u64 * k)()
+    rc = _lib.ley_dist_plan_splitters(h, n_total, nranks, bins, rho, first)
+    if rc:
+        raise ValueError(f"ley_dist_plan_splitters failed ({rc})")
+    return list(bins)[: nranks - 1], list(rho)[: nranks - 1], list(first)[: nranks - 1]
+
+
+def ley_dist_bin_dest_counts(local_hist16, bins, nranks: int):
+    h = (_u64 * 65536)(*[int(x) for x in local_hist16])
+    b = (_u32 * max(len(bins), 1))(*bins)
+    c = (_u64 * nranks)()
+    _lib.ley_dist_bin_dest_counts(h, b, nranks, c)
+    return list(c)
+
+
+def ley_dist_plan_exchange(send_counts, nranks: int, rank: int):
+    """send_counts: nranks x nranks [src][dst] -> dict(recv_counts, recv_offsets, send_offsets, n_out, out_offset)."""
+    flat = [int(x) for row in send_counts for x in row]
+    m = (_u64 * (nranks * nranks))(*flat)
+    rc, ro, so = (_u64 * nranks)(), (_u64 * nranks)(), (_u64 * nranks)()
+    n_out, off = _u64(), _u64()
+    _lib.ley_dist_plan_exchange(m, nranks, rank, rc, ro, so, ctypes.byref(n_out), ctypes.byref(off))
+    return dict(recv_counts=list(rc), recv_offsets=list(ro), send_offsets=list(so), n_out=n_out.value,
+                out_offset=off.value)
 
 
 def library_path() -> str:

@@ -19,6 +19,12 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
 ley_status comm_get_unique_id(uint8_t id_out[128]);
 ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);
 ley_status comm_destroy(ley_comm* comm);
+ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, cudaStream_t s);
+int dist_plan_splitters(const uint64_t* hist, uint64_t N, int G, uint32_t* bins, uint64_t* rho, uint64_t* first);
+void dist_bin_dest_counts(const uint64_t* local_hist, const uint32_t* bins, int nspl, uint64_t* counts);
+void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* recv_counts, uint64_t* recv_off,
+                        uint64_t* send_off, uint64_t* n_out, uint64_t* out_off);
 }  // namespace ley
 
 using namespace ley;
@@ -231,6 +237,37 @@ ley_status ley_sort_dist(ley_comm* comm, const void* in_local, uint64_t n_local,
 ley_status ley_comm_destroy(ley_comm* comm) {
   clear_error();
   return comm_destroy(comm);
+}
+
+ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const uint64_t* n_local,
+                                  void* const* out_local, const uint64_t* out_capacity_records, uint64_t* n_out_local,
+                                  uint64_t* out_global_offset, uint32_t record_bytes, uint32_t key_bytes, void* stream) {
+  clear_error();
+  if (record_bytes != kRecordBytes || key_bytes != kKeyBytes) {
+    set_error("validate: only record_bytes=100, key_bytes=10 are supported (P:126)");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  if (!in_local || !n_local || !out_local || !out_capacity_records || !n_out_local || !out_global_offset) {
+    set_error("validate: NULL argument array");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  return dist_sort_loopback(nranks, in_local, n_local, out_local, out_capacity_records, n_out_local,
+                            out_global_offset, static_cast<cudaStream_t>(stream));
+}
+
+int ley_dist_plan_splitters(const uint64_t* global_hist16, uint64_t n_total, int nranks, uint32_t* bins,
+                            uint64_t* rank_in_bin, uint64_t* bin_first) {
+  if (!global_hist16 || !bins || !rank_in_bin || !bin_first) return 1;
+  return dist_plan_splitters(global_hist16, n_total, nranks, bins, rank_in_bin, bin_first);
+}
+
+void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins, int nranks, uint64_t* counts) {
+  dist_bin_dest_counts(local_hist16, bins, nranks - 1, counts);
+}
+
+void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
+                            uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset) {
+  dist_plan_exchange(send_counts, nranks, rank, recv_counts, recv_offsets, send_offsets, n_out, out_offset);
 }
 
 }  // extern "C"

@@ -32,4 +32,12 @@ constexpr uint32_t kWarpTierMax = 32;
 constexpr uint32_t kSmemTierMax = 16384;
 constexpr int kKdMaxBits = 12;
 
+// multi-GPU: at most 8 ranks (one 8 x B200 box; BASELINE.json configs)
+constexpr int kMaxRanks = 8;
+
+// Exact range splitter (key bytes 0..3, 4..7, 8..9 big-endian; global ordinal) — SURVEY §8e.
+struct DistSplitter {
+  uint32_t hi, mid, lo16, gidx;
+};
+
 }  // namespace ley

@@ -1,0 +1,600 @@
+// dist.cpp — multi-GPU key-range sort: host orchestration over NCCL, and
+// a loopback transport that runs the same G-rank algorithm on one device.
+//
+// BASELINE.json north_star: "Each GPU histograms the leading key bytes, all GPUs agree on range
+// splitters, and records move to their owning GPU by an NCCL all-to-all over NVLink; each GPU then sorts
+// its range locally, and the output is the concatenation of the ranges."
+//
+// Phases of one rank (collectives between them):
+//   P1  K-s0 local hist16 of key bytes 0..1                       C1 allreduce(hist16), allgather(n_local)
+//   P2  plan: split ranks q_k = floor(k N / G), k = 1..G-1 -> boundary bin b_k and rank rho_k inside it
+//       (ley_dist_plan_splitters); K-s1 compacts this rank's records of the boundary bins (with global
+//       ordinals)                                                 C2 allgather(candidate counts, candidates)
+//   P3  sort all candidates (the internal sort: order = (key, global ordinal)), splitter s_k = candidate
+//       at (first candidate of bin b_k) + rho_k -> exact (key, ordinal) splitters, identical on all ranks
+//   P4  send counts per destination: whole bins from the local hist16 (ley_dist_bin_dest_counts) +
+//       K-s2 over the local candidates                             C3 allgather(send counts G x G)
+//   P5  exchange plan (ley_dist_plan_exchange); K-p stable partition into the send buffer
+//                                                                  C4 all-to-all-v (grouped send/recv)
+//   P6  internal sort of the received records (K-a..K-e); receive order = global ordinal order.
+// With exact splitters rank r ends up with global sorted positions [floor(r N/G), floor((r+1) N/G)).
+#include <nccl.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace ley {
+
+// ------------------------------------------------------------------------------- host planning (pure)
+// For k = 1..G-1: q_k = floor(k N / G); bin b_k = the 16-bit prefix bin holding global sorted rank q_k;
+// rho_k = q_k - (records in bins < b_k). bin_first_k = records in bins < b_k.
+int dist_plan_splitters(const uint64_t* hist, uint64_t N, int G, uint32_t* bins, uint64_t* rho, uint64_t* first) {
+  if (G < 1 || G > kMaxRanks) return 1;
+  uint64_t cum = 0;
+  uint32_t b = 0;
+  for (int k = 1; k < G; ++k) {
+    const uint64_t q = (uint64_t)((unsigned __int128)k * N / (unsigned)G);
+    while (b < 65536 && cum + hist[b] <= q) {
+      cum += hist[b];
+      ++b;
+    }
+    if (b >= 65536) return 2;  // q >= N: impossible for k < G and N > 0
+    bins[k - 1] = b;
+    rho[k - 1] = q - cum;
+    first[k - 1] = cum;
+  }
+  return 0;
+}
+
+// Destination counts of the whole (non-boundary) bins of a local histogram: bin b goes to rank
+// #{k : b_k < b}; the boundary bins themselves are counted from the candidates (K-s2).
+void dist_bin_dest_counts(const uint64_t* local_hist, const uint32_t* bins, int nspl, uint64_t* counts) {
+  for (int d = 0; d <= nspl; ++d) counts[d] = 0;
+  for (uint32_t b = 0; b < 65536; ++b) {
+    if (!local_hist[b]) continue;
+    bool boundary = false;
+    int d = 0;
+    for (int k = 0; k < nspl; ++k) {
+      if (bins[k] == b) boundary = true;
+      if (bins[k] < b) ++d;
+    }
+    if (!boundary) counts[d] += local_hist[b];
+  }
+}
+
+// send_counts[src * G + dst] (records). Receive order = source rank order (= global ordinal order).
+void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* recv_counts, uint64_t* recv_off,
+                        uint64_t* send_off, uint64_t* n_out, uint64_t* out_off) {
+  uint64_t acc = 0;
+  for (int s = 0; s < G; ++s) {
+    recv_counts[s] = send_counts[(size_t)s * G + rank];
+    recv_off[s] = acc;
+    acc += recv_counts[s];
+  }
+  *n_out = acc;
+  uint64_t so = 0;
+  for (int d = 0; d < G; ++d) {
+    send_off[d] = so;
+    so += send_counts[(size_t)rank * G + d];
+  }
+  uint64_t before = 0;
+  for (int r = 0; r < rank; ++r)
+    for (int s = 0; s < G; ++s) before += send_counts[(size_t)s * G + r];
+  *out_off = before;
+}
+
+namespace {
+
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+#define LEY_NCCL(stage, expr)                                                                   \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess) {                                                                    \
+      ::ley::set_error(std::string(stage) + ": " + ncclGetErrorString(_r) + " at " #expr);     \
+      return LEY_ERR_NCCL;                                                                      \
+    }                                                                                           \
+  } while (0)
+
+// Per-rank state of one distributed sort.
+struct RankState {
+  int rank = 0;
+  DeviceContext* ctx = nullptr;
+  cudaStream_t s = nullptr;
+  const uint8_t* in = nullptr;
+  uint64_t n = 0;
+  uint8_t* out = nullptr;
+  uint64_t cap = 0;
+  uint64_t gbase = 0;
+  // device scratch (one buffer)
+  DeviceBuffer buf;
+  uint32_t* d_hist = nullptr;        // [65536]
+  uint64_t* d_status = nullptr;      // look-back status (candidates / partition)
+  uint32_t* d_small = nullptr;       // tickets, counts
+  uint8_t* d_cand = nullptr;         // local candidates (records)
+  uint32_t* d_cand_gidx = nullptr;
+  unsigned long long* d_dcount = nullptr;  // [kMaxRanks]
+  uint64_t* d_sendbase = nullptr;    // [kMaxRanks]
+  DistSplitter* d_spl = nullptr;     // [kMaxRanks]
+  uint32_t* d_bins = nullptr;        // [kMaxRanks]
+  uint8_t* d_send = nullptr;         // n records
+  uint8_t* d_recv = nullptr;         // received records
+  uint64_t recv_cap = 0;
+  // host side
+  std::vector<uint64_t> hist;        // local hist16 (u64)
+  uint32_t ncand = 0;
+  uint64_t send_counts[kMaxRanks] = {0};
+  uint64_t recv_counts[kMaxRanks], recv_off[kMaxRanks], send_off[kMaxRanks];
+  uint64_t n_out = 0, out_off = 0;
+  ~RankState() {
+    if (buf.ptr) cudaFree(buf.ptr);
+  }
+};
+
+// Shared (replicated) plan of the sort.
+struct Plan {
+  int G = 1;
+  uint64_t N = 0;
+  std::vector<uint64_t> n_local, ghist;
+  uint32_t bins[kMaxRanks] = {0};
+  uint64_t rho[kMaxRanks] = {0}, first[kMaxRanks] = {0};
+  DistSplitter spl[kMaxRanks];
+  std::vector<uint64_t> send_matrix;  // G x G
+};
+
+ley_status rank_alloc(RankState& r) {
+  const uint64_t n = std::max<uint64_t>(r.n, 1);
+  const uint64_t cand_cap = n;  // worst case: every record in a boundary bin
+  const uint64_t status_words = std::max<uint64_t>(std::max<uint64_t>(ks_candidate_tiles(n), kp_tiles(n) * kMaxRanks), 128) + 16;
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t at = o; o += a256(b); return at; };
+  const size_t o_hist = take(4 * 65536), o_status = take(8 * status_words), o_small = take(256),
+               o_cand = take(cand_cap * kRecordBytes), o_cgidx = take(4 * cand_cap), o_dcount = take(8 * kMaxRanks),
+               o_sbase = take(8 * kMaxRanks), o_spl = take(sizeof(DistSplitter) * kMaxRanks),
+               o_bins = take(4 * kMaxRanks), o_send = take(n * kRecordBytes);
+  if (r.buf.cap < o) {
+    if (r.buf.ptr) cudaFree(r.buf.ptr);
+    r.buf.ptr = nullptr;
+    r.buf.cap = 0;
+    LEY_CUDA("dist alloc", cudaMalloc(&r.buf.ptr, o));
+    r.buf.cap = o;
+  }
+  uint8_t* b = static_cast<uint8_t*>(r.buf.ptr);
+  r.d_hist = reinterpret_cast<uint32_t*>(b + o_hist);
+  r.d_status = reinterpret_cast<uint64_t*>(b + o_status);
+  r.d_small = reinterpret_cast<uint32_t*>(b + o_small);
+  r.d_cand = b + o_cand;
+  r.d_cand_gidx = reinterpret_cast<uint32_t*>(b + o_cgidx);
+  r.d_dcount = reinterpret_cast<unsigned long long*>(b + o_dcount);
+  r.d_sendbase = reinterpret_cast<uint64_t*>(b + o_sbase);
+  r.d_spl = reinterpret_cast<DistSplitter*>(b + o_spl);
+  r.d_bins = reinterpret_cast<uint32_t*>(b + o_bins);
+  r.d_send = b + o_send;
+  return LEY_OK;
+}
+
+// ---------------------------------------------------------------------------- phases (one rank)
+ley_status phase1_hist(RankState& r) {
+  LEY_CUDA("K-s0 hist", cudaMemsetAsync(r.d_hist, 0, 4 * 65536, r.s));
+  LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.ctx->sms, r.s));
+  return LEY_OK;
+}
+
+ley_status phase2_candidates(RankState& r, const Plan& P) {
+  const int nspl = P.G - 1;
+  LEY_CUDA("K-s1 candidates", cudaMemcpyAsync(r.d_bins, P.bins, 4 * std::max(nspl, 1), cudaMemcpyHostToDevice, r.s));
+  LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_small, 0, 256, r.s));
+  LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_status, 0, 8 * (ks_candidate_tiles(r.n) + 1), r.s));
+  LEY_CUDA("K-s1 candidates", launch_ks_candidates(r.in, r.n, (uint32_t)r.gbase, r.d_bins, nspl, r.d_status,
+                                                   r.d_small + 0, r.d_cand, r.d_cand_gidx, r.d_small + 1, r.s));
+  uint32_t* h = static_cast<uint32_t*>(r.ctx->host_pinned);
+  LEY_CUDA("K-s1 candidates", cudaMemcpyAsync(h, r.d_small + 1, 4, cudaMemcpyDeviceToHost, r.s));
+  LEY_CUDA("K-s1 candidates", cudaStreamSynchronize(r.s));
+  r.ncand = r.n ? h[0] : 0;
+  return LEY_OK;
+}
+
+// Given all candidates concatenated in rank order (device records + ordinals), find the exact splitters.
+ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* all_cand, const uint32_t* all_gidx,
+                            uint64_t total_cand, Plan& P) {
+  const int nspl = P.G - 1;
+  if (nspl == 0) return LEY_OK;
+  DeviceBuffer tmp;
+  const InternalLayout L = plan_internal(total_cand);
+  const size_t bytes = a256(total_cand * kRecordBytes) + a256(4 * total_cand) + a256(L.bytes);
+  LEY_CUDA("K-s splitters", cudaMalloc(&tmp.ptr, bytes));
+  std::unique_ptr<void, decltype(&cudaFree)> guard(tmp.ptr, &cudaFree);
+  uint8_t* sorted = static_cast<uint8_t*>(tmp.ptr);
+  uint32_t* perm = reinterpret_cast<uint32_t*>(sorted + a256(total_cand * kRecordBytes));
+  uint8_t* work = reinterpret_cast<uint8_t*>(perm) + a256(4 * total_cand);
+  Profiler quiet;
+  quiet.ctx = &ctx;
+  quiet.stream = s;
+  ley_status st = sort_internal_device(ctx, all_cand, sorted, perm, total_cand, s, quiet, work, L.bytes);
+  if (st) return st;
+  // first sorted index of each boundary bin = candidates in smaller boundary bins
+  for (int k = 0; k < nspl; ++k) {
+    uint64_t start = 0;
+    std::vector<uint32_t> seen;
+    for (int j = 0; j < nspl; ++j) {
+      if (P.bins[j] < P.bins[k] && std::find(seen.begin(), seen.end(), P.bins[j]) == seen.end()) {
+        start += P.ghist[P.bins[j]];
+        seen.push_back(P.bins[j]);
+      }
+    }
+    const uint64_t at = start + P.rho[k];
+    uint8_t key[12] = {0};
+    uint32_t p = 0, g = 0;
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(key, sorted + at * kRecordBytes, 10, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&p, perm + at, 4, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&g, all_gidx + p, 4, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
+    DistSplitter& d = P.spl[k];
+    d.hi = ((uint32_t)key[0] << 24) | ((uint32_t)key[1] << 16) | ((uint32_t)key[2] << 8) | key[3];
+    d.mid = ((uint32_t)key[4] << 24) | ((uint32_t)key[5] << 16) | ((uint32_t)key[6] << 8) | key[7];
+    d.lo16 = ((uint32_t)key[8] << 8) | key[9];
+    d.gidx = g;
+  }
+  return LEY_OK;
+}
+
+ley_status phase4_counts(RankState& r, const Plan& P) {
+  const int nspl = P.G - 1;
+  dist_bin_dest_counts(r.hist.data(), P.bins, nspl, r.send_counts);
+  if (nspl == 0) return LEY_OK;
+  LEY_CUDA("K-s2 counts", cudaMemcpyAsync(r.d_spl, P.spl, sizeof(DistSplitter) * nspl, cudaMemcpyHostToDevice, r.s));
+  LEY_CUDA("K-s2 counts", cudaMemsetAsync(r.d_dcount, 0, 8 * kMaxRanks, r.s));
+  LEY_CUDA("K-s2 counts", launch_ks_dest_counts(r.d_cand, r.d_cand_gidx, r.ncand, r.d_spl, nspl, r.d_dcount,
+                                                r.ctx->sms, r.s));
+  unsigned long long c[kMaxRanks];
+  LEY_CUDA("K-s2 counts", cudaMemcpyAsync(c, r.d_dcount, 8 * kMaxRanks, cudaMemcpyDeviceToHost, r.s));
+  LEY_CUDA("K-s2 counts", cudaStreamSynchronize(r.s));
+  for (int d = 0; d <= nspl; ++d) r.send_counts[d] += c[d];
+  return LEY_OK;
+}
+
+ley_status phase5_partition(RankState& r, const Plan& P) {
+  const int G = P.G;
+  dist_plan_exchange(P.send_matrix.data(), G, r.rank, r.recv_counts, r.recv_off, r.send_off, &r.n_out, &r.out_off);
+  if (r.n_out > r.cap) {
+    set_error("dist: rank " + std::to_string(r.rank) + " must hold " + std::to_string(r.n_out) +
+              " records but out_capacity_records is " + std::to_string(r.cap));
+    return LEY_ERR_CAPACITY;
+  }
+  if (G == 1) return LEY_OK;
+  LEY_CUDA("K-p partition", cudaMemcpyAsync(r.d_sendbase, r.send_off, 8 * G, cudaMemcpyHostToDevice, r.s));
+  LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_small, 0, 256, r.s));
+  LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_status, 0, 8 * (kp_tiles(r.n) * kMaxRanks + 1), r.s));
+  LEY_CUDA("K-p partition", launch_kp_partition(r.in, r.n, (uint32_t)r.gbase, r.d_spl, G - 1, r.d_sendbase,
+                                                r.d_status, r.d_small + 2, r.d_send, r.s));
+  return LEY_OK;
+}
+
+ley_status phase6_local_sort(RankState& r, const uint8_t* recv) {
+  Profiler quiet;
+  quiet.ctx = r.ctx;
+  quiet.stream = r.s;
+  if (r.n_out == 0) return LEY_OK;
+  return sort_internal_device(*r.ctx, recv, r.out, nullptr, r.n_out, r.s, quiet);
+}
+
+void host_hist(RankState& r) {
+  r.hist.assign(65536, 0);
+  std::vector<uint32_t> h(65536);
+  cudaMemcpy(h.data(), r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost);
+  for (int b = 0; b < 65536; ++b) r.hist[b] = h[b];
+}
+
+}  // namespace
+}  // namespace ley
+
+// ------------------------------------------------------------------------------------ NCCL comm
+struct ley_comm {
+  int nranks = 0, rank = 0, device = 0;
+  ncclComm_t nccl = nullptr;
+  ley::RankState state;
+};
+
+namespace ley {
+
+ley_status comm_get_unique_id(uint8_t id_out[128]) {
+  if (!id_out) {
+    set_error("ley_comm_get_unique_id: NULL");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  ncclUniqueId id;
+  LEY_NCCL("comm", ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id_out, &id, 128);
+  return LEY_OK;
+}
+
+ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device) {
+  if (!comm || !id || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) {
+    set_error("ley_comm_init: invalid arguments (1 <= nranks <= 8, 0 <= rank < nranks)");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  LEY_CUDA("comm", cudaSetDevice(device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  std::unique_ptr<ley_comm> c(new ley_comm());
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  LEY_NCCL("comm", ncclCommInitRank(&c->nccl, nranks, uid, rank));
+  *comm = c.release();
+  return LEY_OK;
+}
+
+ley_status comm_destroy(ley_comm* comm) {
+  if (!comm) return LEY_OK;
+  if (comm->nccl) ncclCommDestroy(comm->nccl);
+  delete comm;
+  return LEY_OK;
+}
+
+ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
+                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, cudaStream_t s) {
+  (void)budget;
+  const int G = comm->nranks;
+  LEY_CUDA("dist", cudaSetDevice(comm->device));
+  DeviceContext& ctx = device_context(comm->device);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
+  if (sms > 0) ctx.sms = sms;
+  if (!ctx.host_pinned) LEY_CUDA("dist", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  if (n_local && (!in_local || !out_local)) {
+    set_error("dist: NULL in/out with n_local > 0");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  RankState& r = comm->state;
+  r.rank = comm->rank;
+  r.ctx = &ctx;
+  r.s = s;
+  r.in = static_cast<const uint8_t*>(in_local);
+  r.n = n_local;
+  r.out = static_cast<uint8_t*>(out_local);
+  r.cap = out_capacity;
+  ley_status st = rank_alloc(r);
+  if (st) return st;
+  Plan P;
+  P.G = G;
+  // C1: allgather n_local, allreduce hist16
+  uint64_t* d_tmp = reinterpret_cast<uint64_t*>(r.d_status);  // status area reused as collective scratch
+  {
+    uint64_t* d_nl = d_tmp;
+    LEY_CUDA("dist", cudaMemcpyAsync(d_nl + G, &n_local, 8, cudaMemcpyHostToDevice, s));
+    LEY_NCCL("dist allgather n", ncclAllGather(d_nl + G, d_nl, 1, ncclUint64, comm->nccl, s));
+    P.n_local.resize(G);
+    LEY_CUDA("dist", cudaMemcpyAsync(P.n_local.data(), d_nl, 8 * G, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("dist", cudaStreamSynchronize(s));
+  }
+  P.N = 0;
+  r.gbase = 0;
+  for (int i = 0; i < G; ++i) {
+    if (i < r.rank) r.gbase += P.n_local[i];
+    P.N += P.n_local[i];
+  }
+  if (P.N > LEY_MAX_RECORDS) {
+    set_error("dist: total records > 2^32-2");
+    return LEY_ERR_TOO_LARGE;
+  }
+  if ((st = phase1_hist(r))) return st;
+  host_hist(r);
+  // global histogram (u32 sums: N < 2^32), in place: the local one is already on the host
+  std::vector<uint32_t> gh(65536);
+  LEY_NCCL("dist allreduce hist16", ncclAllReduce(r.d_hist, r.d_hist, 65536, ncclUint32, ncclSum, comm->nccl, s));
+  LEY_CUDA("dist", cudaMemcpyAsync(gh.data(), r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("dist", cudaStreamSynchronize(s));
+  P.ghist.assign(gh.begin(), gh.end());
+  if (P.N && dist_plan_splitters(P.ghist.data(), P.N, G, P.bins, P.rho, P.first)) {
+    set_error("dist: splitter planning failed");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  // P2 + C2: candidates
+  if (G > 1 && P.N) {
+    if ((st = phase2_candidates(r, P))) return st;
+    std::vector<uint64_t> counts(G);
+    {
+      uint64_t* d_c = d_tmp;
+      uint64_t mine = r.ncand;
+      LEY_CUDA("dist", cudaMemcpyAsync(d_c + G, &mine, 8, cudaMemcpyHostToDevice, s));
+      LEY_NCCL("dist allgather cand", ncclAllGather(d_c + G, d_c, 1, ncclUint64, comm->nccl, s));
+      LEY_CUDA("dist", cudaMemcpyAsync(counts.data(), d_c, 8 * G, cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("dist", cudaStreamSynchronize(s));
+    }
+    uint64_t maxc = 0, total = 0;
+    for (int i = 0; i < G; ++i) {
+      maxc = std::max(maxc, counts[i]);
+      total += counts[i];
+    }
+    // padded allgather of candidate records and ordinals, then compaction into rank order
+    DeviceBuffer cb;
+    const size_t rec_b = a256(maxc * kRecordBytes), gid_b = a256(4 * maxc);
+    const size_t bytes = (size_t)G * (rec_b + gid_b) + rec_b + gid_b + a256(total * kRecordBytes) + a256(4 * total);
+    LEY_CUDA("dist cand", cudaMalloc(&cb.ptr, std::max<size_t>(bytes, 256)));
+    std::unique_ptr<void, decltype(&cudaFree)> g2(cb.ptr, &cudaFree);
+    uint8_t* base = static_cast<uint8_t*>(cb.ptr);
+    uint8_t* all_rec = base;                                   // G x rec_b
+    uint8_t* all_gid = all_rec + (size_t)G * rec_b;            // G x gid_b
+    uint8_t* my_rec = all_gid + (size_t)G * gid_b;
+    uint8_t* my_gid = my_rec + rec_b;
+    uint8_t* cat_rec = my_gid + gid_b;
+    uint32_t* cat_gid = reinterpret_cast<uint32_t*>(cat_rec + a256(total * kRecordBytes));
+    if (r.ncand) {
+      LEY_CUDA("dist cand", cudaMemcpyAsync(my_rec, r.d_cand, r.ncand * kRecordBytes, cudaMemcpyDeviceToDevice, s));
+      LEY_CUDA("dist cand", cudaMemcpyAsync(my_gid, r.d_cand_gidx, 4ull * r.ncand, cudaMemcpyDeviceToDevice, s));
+    }
+    LEY_NCCL("dist allgather cand", ncclAllGather(my_rec, all_rec, rec_b, ncclUint8, comm->nccl, s));
+    LEY_NCCL("dist allgather cand", ncclAllGather(my_gid, all_gid, gid_b, ncclUint8, comm->nccl, s));
+    uint64_t at = 0;
+    for (int i = 0; i < G; ++i) {
+      if (counts[i]) {
+        LEY_CUDA("dist cand", cudaMemcpyAsync(cat_rec + at * kRecordBytes, all_rec + (size_t)i * rec_b,
+                                              counts[i] * kRecordBytes, cudaMemcpyDeviceToDevice, s));
+        LEY_CUDA("dist cand", cudaMemcpyAsync(cat_gid + at, all_gid + (size_t)i * gid_b, 4 * counts[i],
+                                              cudaMemcpyDeviceToDevice, s));
+      }
+      at += counts[i];
+    }
+    if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P))) return st;
+    LEY_CUDA("dist cand", cudaStreamSynchronize(s));
+  }
+  // P4 + C3: send counts
+  if ((st = phase4_counts(r, P))) return st;
+  P.send_matrix.assign((size_t)G * G, 0);
+  {
+    uint64_t* d_m = d_tmp;
+    LEY_CUDA("dist", cudaMemcpyAsync(d_m + (size_t)G * G, r.send_counts, 8 * G, cudaMemcpyHostToDevice, s));
+    LEY_NCCL("dist allgather counts", ncclAllGather(d_m + (size_t)G * G, d_m, G, ncclUint64, comm->nccl, s));
+    LEY_CUDA("dist", cudaMemcpyAsync(P.send_matrix.data(), d_m, 8ull * G * G, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("dist", cudaStreamSynchronize(s));
+  }
+  // P5 + C4: partition and all-to-all-v
+  if ((st = phase5_partition(r, P))) return st;
+  const uint8_t* recv = r.in;
+  DeviceBuffer rb;
+  std::unique_ptr<void, decltype(&cudaFree)> g3(nullptr, &cudaFree);
+  if (G > 1) {
+    LEY_CUDA("dist exchange", cudaMalloc(&rb.ptr, std::max<size_t>(r.n_out * kRecordBytes, 256)));
+    g3.reset(rb.ptr);
+    LEY_NCCL("dist exchange", ncclGroupStart());
+    for (int peer = 0; peer < G; ++peer) {
+      const uint64_t sc = P.send_matrix[(size_t)r.rank * G + peer];
+      if (sc)
+        LEY_NCCL("dist exchange", ncclSend(r.d_send + r.send_off[peer] * kRecordBytes, sc * kRecordBytes, ncclUint8,
+                                           peer, comm->nccl, s));
+      if (r.recv_counts[peer])
+        LEY_NCCL("dist exchange", ncclRecv(static_cast<uint8_t*>(rb.ptr) + r.recv_off[peer] * kRecordBytes,
+                                           r.recv_counts[peer] * kRecordBytes, ncclUint8, peer, comm->nccl, s));
+    }
+    LEY_NCCL("dist exchange", ncclGroupEnd());
+    recv = static_cast<uint8_t*>(rb.ptr);
+  }
+  // P6: local sort of the received range
+  if ((st = phase6_local_sort(r, recv))) return st;
+  LEY_CUDA("dist", cudaStreamSynchronize(s));
+  *n_out_local = r.n_out;
+  *out_global_offset = r.out_off;
+  return LEY_OK;
+}
+
+// ------------------------------------------------------------------------------ loopback transport
+// All G ranks on the current device in one process; collectives are host-side reductions and device
+// copies. Exercises exactly the kernels and plans of dist_sort (test hook).
+ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, cudaStream_t s) {
+  if (G < 1 || G > kMaxRanks) {
+    set_error("loopback: 1 <= G <= 8");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  int dev = 0;
+  LEY_CUDA("loopback", cudaGetDevice(&dev));
+  DeviceContext& ctx = device_context(dev);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms > 0) ctx.sms = sms;
+  if (!ctx.host_pinned) LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  std::vector<std::unique_ptr<RankState>> R(G);
+  Plan P;
+  P.G = G;
+  P.n_local.assign(n_local, n_local + G);
+  ley_status st;
+  for (int i = 0; i < G; ++i) {
+    R[i].reset(new RankState());
+    RankState& r = *R[i];
+    r.rank = i;
+    r.ctx = &ctx;
+    r.s = s;
+    r.in = static_cast<const uint8_t*>(in[i]);
+    r.n = n_local[i];
+    r.out = static_cast<uint8_t*>(out[i]);
+    r.cap = caps[i];
+    r.gbase = P.N;
+    P.N += n_local[i];
+    if ((st = rank_alloc(r))) return st;
+  }
+  if (P.N > LEY_MAX_RECORDS) {
+    set_error("loopback: total records > 2^32-2");
+    return LEY_ERR_TOO_LARGE;
+  }
+  // P1 + C1
+  P.ghist.assign(65536, 0);
+  for (int i = 0; i < G; ++i) {
+    if ((st = phase1_hist(*R[i]))) return st;
+    LEY_CUDA("loopback", cudaStreamSynchronize(s));
+    host_hist(*R[i]);
+    for (int b = 0; b < 65536; ++b) P.ghist[b] += R[i]->hist[b];
+  }
+  if (P.N && dist_plan_splitters(P.ghist.data(), P.N, G, P.bins, P.rho, P.first)) {
+    set_error("loopback: splitter planning failed");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  // P2 + C2 + P3
+  if (G > 1 && P.N) {
+    uint64_t total = 0;
+    for (int i = 0; i < G; ++i) {
+      if ((st = phase2_candidates(*R[i], P))) return st;
+      total += R[i]->ncand;
+    }
+    DeviceBuffer cb;
+    LEY_CUDA("loopback", cudaMalloc(&cb.ptr, a256(total * kRecordBytes) + a256(4 * total) + 256));
+    std::unique_ptr<void, decltype(&cudaFree)> g(cb.ptr, &cudaFree);
+    uint8_t* cat = static_cast<uint8_t*>(cb.ptr);
+    uint32_t* gid = reinterpret_cast<uint32_t*>(cat + a256(total * kRecordBytes));
+    uint64_t at = 0;
+    for (int i = 0; i < G; ++i) {
+      const uint64_t c = R[i]->ncand;
+      if (c) {
+        LEY_CUDA("loopback", cudaMemcpyAsync(cat + at * kRecordBytes, R[i]->d_cand, c * kRecordBytes,
+                                             cudaMemcpyDeviceToDevice, s));
+        LEY_CUDA("loopback", cudaMemcpyAsync(gid + at, R[i]->d_cand_gidx, 4 * c, cudaMemcpyDeviceToDevice, s));
+      }
+      at += c;
+    }
+    if ((st = phase3_splitters(ctx, s, cat, gid, total, P))) return st;
+  }
+  // P4 + C3
+  P.send_matrix.assign((size_t)G * G, 0);
+  for (int i = 0; i < G; ++i) {
+    if ((st = phase4_counts(*R[i], P))) return st;
+    for (int d = 0; d < G; ++d) P.send_matrix[(size_t)i * G + d] = R[i]->send_counts[d];
+  }
+  // P5 + C4
+  for (int i = 0; i < G; ++i)
+    if ((st = phase5_partition(*R[i], P))) return st;
+  std::vector<std::unique_ptr<void, decltype(&cudaFree)>> recvs;
+  for (int i = 0; i < G; ++i) {
+    RankState& r = *R[i];
+    const uint8_t* recv = r.in;
+    if (G > 1) {
+      void* p = nullptr;
+      LEY_CUDA("loopback exchange", cudaMalloc(&p, std::max<size_t>(r.n_out * kRecordBytes, 256)));
+      recvs.emplace_back(p, &cudaFree);
+      for (int src = 0; src < G; ++src) {
+        const uint64_t c = r.recv_counts[src];
+        if (c)
+          LEY_CUDA("loopback exchange",
+                   cudaMemcpyAsync(static_cast<uint8_t*>(p) + r.recv_off[src] * kRecordBytes,
+                                   R[src]->d_send + R[src]->send_off[i] * kRecordBytes, c * kRecordBytes,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+      recv = static_cast<uint8_t*>(p);
+    }
+    if ((st = phase6_local_sort(r, recv))) return st;
+    LEY_CUDA("loopback", cudaStreamSynchronize(s));
+    n_out[i] = r.n_out;
+    out_off[i] = r.out_off;
+  }
+  return LEY_OK;
+}
+
+}  // namespace ley

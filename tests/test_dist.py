@@ -1,0 +1,191 @@
+"""Multi-GPU key-range sort.
+
+* -m gpu: the loopback transport runs the real G-rank algorithm (K-s0/K-s1/K-s2/K-p kernels, plans, local
+  sort) on one B200 with device copies standing in for NCCL; and the NCCL path itself at world size 1.
+  Checks: concatenation of the ranks' outputs == oracle of the concatenated input; closed-form sizes
+  n_out(r) = floor((r+1)N/G) - floor(rN/G) and offsets floor(rN/G) (exact splitters).
+* -m "not gpu": two gloo processes run the host-side planning of the library (ley_dist_plan_splitters,
+  ley_dist_bin_dest_counts, ley_dist_plan_exchange) around a numpy stand-in for the kernels and a real
+  all-to-all, and must reproduce the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+
+def _closed_form(N, G):
+    return [((r + 1) * N // G) - (r * N // G) for r in range(G)], [r * N // G for r in range(G)]
+
+
+# ----------------------------------------------------------------------------------------- GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("dist", ["uniform", "skewed", "all_equal", "tiny_alphabet", "sorted", "reverse"])
+def test_loopback_matches_oracle(cuda_ok, G, dist):
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    rng = np.random.default_rng(G * 7 + len(dist))
+    N = 90_001
+    cuts = np.sort(rng.integers(0, N, size=G - 1))
+    n_local = np.diff(np.concatenate([[0], cuts, [N]])).tolist()
+    if G > 2:
+        n_local[1] += n_local[2]  # one empty rank
+        n_local[2] = 0
+    recs = gen.records(N, seed=51, dist=dist)
+    ins, outs, caps = [], [], []
+    at = 0
+    for r in range(G):
+        part = recs[at * 100:(at + n_local[r]) * 100]
+        at += n_local[r]
+        ins.append(torch.from_numpy(part.copy()).cuda() if n_local[r] else torch.empty(100, dtype=torch.uint8,
+                                                                                       device="cuda"))
+        cap = N // G + 2
+        outs.append(torch.empty(cap * 100, dtype=torch.uint8, device="cuda"))
+        caps.append(cap)
+    res = ley.ley_sort_dist_loopback(ins, n_local, outs, caps)
+    torch.cuda.synchronize()
+    sizes, offs = _closed_form(N, G)
+    assert [x[0] for x in res] == sizes
+    assert [x[1] for x in res] == offs
+    got = np.concatenate([outs[r][: res[r][0] * 100].cpu().numpy() for r in range(G)])
+    exp, _ = oracle.sort(recs)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.gpu
+def test_loopback_tiny_and_capacity(cuda_ok):
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    G, N = 8, 5  # fewer records than ranks
+    recs = gen.records(N, seed=3)
+    n_local = [1, 0, 2, 0, 0, 1, 1, 0]
+    ins, outs, at = [], [], 0
+    for r in range(G):
+        ins.append(torch.from_numpy(recs[at * 100:(at + n_local[r]) * 100].copy()).cuda() if n_local[r]
+                   else torch.empty(100, dtype=torch.uint8, device="cuda"))
+        at += n_local[r]
+        outs.append(torch.empty(200, dtype=torch.uint8, device="cuda"))
+    res = ley.ley_sort_dist_loopback(ins, n_local, outs, [2] * G)
+    sizes, offs = _closed_form(N, G)
+    assert [x[0] for x in res] == sizes and [x[1] for x in res] == offs
+    got = np.concatenate([outs[r][: res[r][0] * 100].cpu().numpy() for r in range(G)])
+    assert np.array_equal(got, oracle.sort(recs)[0])
+    # capacity error path
+    with pytest.raises(ley.LeyendaError) as ei:
+        ley.ley_sort_dist_loopback(ins, n_local, outs, [0] * G)
+    assert ei.value.status == ley.LEY_ERR_CAPACITY
+
+
+@pytest.mark.gpu
+def test_nccl_world_size_one(cuda_ok):
+    """The NCCL path itself (communicator of one rank): equals ley_sort."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    n = 50_003
+    recs = gen.records(n, seed=61, dist="skewed")
+    uid = ley.ley_comm_get_unique_id()
+    comm = ley.ley_comm_init(1, 0, uid, 0)
+    try:
+        x = torch.from_numpy(recs).cuda()
+        out = torch.empty_like(x)
+        n_out, off = ley.ley_sort_dist(comm, x, n, out, n)
+        torch.cuda.synchronize()
+        assert (n_out, off) == (n, 0)
+        assert np.array_equal(out.cpu().numpy(), oracle.sort(recs)[0])
+    finally:
+        ley.ley_comm_destroy(comm)
+
+
+# ----------------------------------------------------------------------------------------- CPU (gloo)
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, N, dist, q):
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1909_08006_b200 as ley
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        recs = gen.records(N, seed=77, dist=dist).reshape(N, 100)
+        bounds = [0, N // 3, N] if world == 2 else [r * N // world for r in range(world + 1)]
+        lo, hi = bounds[rank], bounds[rank + 1]
+        local = recs[lo:hi]
+        # K-s0 stand-in: local histogram of key bytes 0..1; C1: allreduce
+        pref = local[:, 0].astype(np.int64) * 256 + local[:, 1]
+        lh = np.bincount(pref, minlength=65536).astype(np.int64)
+        gh = torch.from_numpy(lh.copy())
+        tdist.all_reduce(gh)
+        bins, rho, first = ley.ley_dist_plan_splitters(gh.numpy().astype(np.uint64), N, world)
+        # K-s1 stand-in: boundary-bin candidates with global ordinals; C2: all-gather
+        cand = [(bytes(local[i, :10]), lo + i) for i in range(hi - lo) if pref[i] in set(bins)]
+        allc = [None] * world
+        tdist.all_gather_object(allc, cand)
+        cands = sorted(c for part in allc for c in part)
+        spl = []
+        for k in range(world - 1):
+            start = sum(int(gh[b]) for b in sorted(set(bins)) if b < bins[k])
+            spl.append(cands[start + rho[k]])
+        # destinations; K-s2 + whole-bin counts must agree with a direct count
+        dest = np.array([sum(1 for s in spl if s <= (bytes(local[i, :10]), lo + i)) for i in range(hi - lo)],
+                        dtype=np.int64)
+        direct = np.bincount(dest, minlength=world)
+        whole = ley.ley_dist_bin_dest_counts(lh.astype(np.uint64), bins, world)
+        extra = np.zeros(world, dtype=np.int64)
+        for (kb, g) in cand:
+            extra[sum(1 for s in spl if s <= (kb, g))] += 1
+        assert np.array_equal(np.array(whole) + extra, direct)
+        # C3: all-gather the send counts; exchange plan
+        sc = torch.from_numpy(direct.copy())
+        mat = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+        tdist.all_gather(mat, sc)
+        plan = ley.ley_dist_plan_exchange([m.tolist() for m in mat], world, rank)
+        sizes, offs = _closed_form(N, world)
+        assert plan["n_out"] == sizes[rank] and plan["out_offset"] == offs[rank]
+        # K-p stand-in (stable partition) + C4 all-to-all-v
+        order = np.argsort(dest, kind="stable")
+        send = torch.from_numpy(np.ascontiguousarray(local[order]).reshape(-1))
+        recv = torch.empty(plan["n_out"] * 100, dtype=torch.uint8)
+        tdist.all_to_all_single(recv, send, [c * 100 for c in plan["recv_counts"]], [int(c) * 100 for c in direct])
+        # local sort (oracle stands in for the GPU local sort); receive order = global order
+        mine, _ = oracle.sort(recv.numpy())
+        outs = [None] * world
+        tdist.all_gather_object(outs, mine.tobytes())
+        if rank == 0:
+            got = b"".join(outs)
+            q.put(got == oracle.sort(recs.reshape(-1))[0].tobytes())
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dist", ["uniform", "skewed", "all_equal"])
+def test_gloo_two_ranks_host_logic(dist):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, 3001, dist, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
