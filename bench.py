@@ -35,6 +35,11 @@ CONFIGS = {
     "c3": dict(n=200_000_000, seed=2, dist="skewed",
                name="C3 2e8 x 100 B Zipf(1.2) byte0, 8-valued byte1, 2% dup keys, 20 GB (BASELINE.json configs[2])"),
     "c4": dict(n=600_000_000, seed=3, dist="uniform", name="C4 6e8 x 100 B uniform, 60 GB (BASELINE.json configs[3])"),
+    # external path: pinned host in/out; scaled from 6e8/4 GB to 2e8/(4/3) GB (same 15:1 data-to-budget
+    # ratio) so in + out + run scratch (3 x 20 GB pinned) fits the GPU box's 196 GB host RAM
+    "c5": dict(n=200_000_000, seed=4, dist="uniform", budget=(4 << 30) // 3,
+               name="C5 external (scaled): 2e8 x 100 B uniform in pinned host memory, device budget 1.33 GB "
+                    "(BASELINE.json configs[4] ratio 60 GB : 4 GB)"),
 }
 METRIC = "sorted GB/s of 100-byte records"
 # algorithmic bytes per record of each stage: what the step must move
@@ -51,27 +56,35 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML, every 20 ms; B200_PROFILING.md)."""
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.02):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
         while not self._stop.is_set():
             try:
-                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                   capture_output=True, text=True, timeout=5)
-                parts = [x.strip() for x in r.stdout.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                self.samples.append((sm, mx, {k for k, b in bits.items() if reasons & b}, util))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -84,14 +97,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        loaded = [s for s in self.samples if s[6] not in ("0", "[N/A]")] or self.samples
-        sm = [float(s[0]) for s in loaded if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in loaded if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in loaded for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(loaded)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        loaded = [x for x in self.samples if x[3] > 0] or self.samples
+        return {"sm_mhz": statistics.median(x[0] for x in loaded), "sm_max_mhz": max(x[1] for x in loaded),
+                "reasons": sorted(set().union(*[x[2] for x in loaded])), "samples": len(loaded)}
 
 
 def cpu_baseline(cfg, sample_n: int):
@@ -146,12 +155,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample records (0 = min(n, 1e8))")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if not args.cpu_sample:
+        args.cpu_sample = min(cfg["n"], 100_000_000)
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -168,18 +179,48 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = cfg["n"]
     stream = torch.cuda.current_stream()
-    x = torch.empty(n * 100, dtype=torch.uint8, device="cuda")
-    gen.records_cuda(x.data_ptr(), n, cfg["seed"] + 1000 * rank, cfg["dist"], stream=stream.cuda_stream)
-    out = torch.empty_like(x)
+    n_total = cfg["n"]
+    external = "budget" in cfg
+    comm = None
+    if world > 1:
+        # strong scaling: the config's records split into contiguous rank slices
+        lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+        n = hi - lo
+        obj = [ley.ley_comm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = ley.ley_comm_init(world, rank, obj[0], local)
+    else:
+        lo, n = 0, n_total
+    cap = n_total // world + 2 if world > 1 else n
+    if external:
+        x = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
+        out = torch.empty(cap * 100, dtype=torch.uint8).pin_memory()
+        stage = torch.empty(min(n, 50_000_000) * 100, dtype=torch.uint8, device="cuda")
+        for at in range(0, n, 50_000_000):
+            m = min(50_000_000, n - at)
+            gen.records_cuda(stage.data_ptr(), m, cfg["seed"], cfg["dist"], i0=lo + at, stream=stream.cuda_stream)
+            x[at * 100:(at + m) * 100].copy_(stage[: m * 100])
+        del stage
+        torch.cuda.empty_cache()
+    else:
+        x = torch.empty(max(n, 1) * 100, dtype=torch.uint8, device="cuda")
+        gen.records_cuda(x.data_ptr(), n, cfg["seed"], cfg["dist"], i0=lo, stream=stream.cuda_stream)
+        out = torch.empty(max(cap, 1) * 100, dtype=torch.uint8, device="cuda")
+    budget = cfg.get("budget", 0)
+
+    def step():
+        if comm is not None:
+            ley.ley_sort_dist(comm, x, n, out, cap, device_budget_bytes=budget, stream=stream)
+        else:
+            ley.ley_sort(x, out, n, device_budget_bytes=budget, stream=stream)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     for _ in range(max(args.warmup, 0)):
-        ley.ley_sort(x, out, n, stream=stream)
+        step()
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- timed region (device events)
@@ -192,7 +233,7 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            ley.ley_sort(x, out, n, stream=stream)
+            step()
             st, nl = ley.ley_stage_times()
             launches += nl
             for name, ms in st:
@@ -206,33 +247,39 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * n * 100 / (ms / 1e3) / 1e9
+    value = n_total * 100 / (ms / 1e3) / 1e9
 
     peak, peak_src = _peaks()
     avg = {k: statistics.mean(v) for k, v in stage_ms.items()}
-    dominant = max((k for k in avg if k in STAGE_ALG_BYTES), key=lambda k: avg[k])
-    alg = STAGE_ALG_BYTES[dominant] * n
-    achieved = alg / (avg[dominant] / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            tr = json.load(f)
-        ent = tr.get(args.config, {}).get(dominant)
-        if ent:
-            traffic = ent.get("bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dominant,
-                "alg_bytes_per_record": STAGE_ALG_BYTES[dominant], "peak_source": peak_src}
+    roofline = None
+    kern = [k for k in avg if k in STAGE_ALG_BYTES]
+    if kern:
+        dominant = max(kern, key=lambda k: avg[k])
+        alg = STAGE_ALG_BYTES[dominant] * n
+        achieved = alg / (avg[dominant] / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                ent = json.load(f).get(args.config, {}).get(dominant)
+            if ent:
+                traffic = ent.get("bytes_per_launch")
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dominant,
+                    "alg_bytes_per_record": STAGE_ALG_BYTES[dominant], "peak_source": peak_src}
     step_roof_ms = 200 * n / (peak * 1e9) * 1e3
     step_roofline = {"alg_bytes_per_record": 200, "t_roof_ms": round(step_roof_ms, 3),
-                     "frac": round(step_roof_ms / ms, 4), "peak": peak, "unit": "GB/s"}
+                     "frac": round(step_roof_ms / ms, 4), "peak": peak, "unit": "GB/s",
+                     "note": "HBM term only" + (" (external: host-link bound, see DESIGN.md)" if external else "")}
 
     # ---------------------------------------------------------------- e2e through the C ABI, host buffers
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if external:
+        e2e = {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": n * 100 * 2,
+               "d2h_bytes_per_step": n * 100 * 2, "ms_per_step": round(ms, 3), "note": "the timed step is host-to-host"}
+    elif not args.no_e2e and world == 1:
         hin = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
-        hin.copy_(x)
+        hin.copy_(x[: n * 100])
         hout = torch.empty_like(hin).pin_memory()
         ley.ley_sort(hin, hout, n, stream=stream)  # warm (staging arena)
         torch.cuda.synchronize()
@@ -254,18 +301,23 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based generator, SURVEY App. A)",
-            "config": {"workload": cfg["name"], "n_records": n, "record_bytes": 100, "key_bytes": 10,
+            "config": {"workload": cfg["name"], "n_records": n_total, "record_bytes": 100, "key_bytes": 10,
                        "seed": cfg["seed"], "distribution": cfg["dist"],
-                       "l2": "inputs (10 GB+) larger than the 126 MB L2; no flush needed",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                       "device_budget_bytes": budget,
+                       "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7
+                       else "100 MB input: L2 flushed by the next step's 100 MB output + 29 MB scratch",
+                       "parallelism": f"key-range dist x{world} (NCCL)" if world > 1 else "1 GPU"},
             "roofline": roofline, "step_roofline": step_roofline,
             "stages_ms": {k: round(v, 4) for k, v in avg.items()},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        ley.ley_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
 
