@@ -21,7 +21,11 @@ __device__ __forceinline__ void classify_bucket(const Seg& s, const Tunables& tu
   } else if (s.len <= tu.warp_tier_max) {
     list = kListWarp;
   } else if (s.len <= tu.smem_tier_max) {
-    list = s.len <= 512 ? kListMed1 : (s.len <= 2048 ? kListMed2 : (s.len <= 8192 ? kListMed3 : kListMed4));
+    list = s.len <= 512    ? kListMed1
+           : s.len <= 2048 ? kListMed2
+           : s.len <= 8192 ? kListMed3
+           : s.len <= 10240 ? kListMed4
+                            : kListMed5;
   } else {
     uint32_t slot = atomicAdd(big_count, 1u);
     big_out[slot] = s;

@@ -23,11 +23,11 @@ enum ListId : int {
   kListMed1 = 1,   // len <= 512:   one CTA (128 threads), shared memory
   kListMed2 = 2,   // len <= 2048   (256 threads)
   kListMed3 = 3,   // len <= 8192   (512 threads)
-  kListMed4 = 4,   // len <= 16384  (512 threads, 1 CTA/SM)
-  kListPass = 5,   // depth == 10: all key bytes equal -> already in index order
-  kNumKdLists = 6
+  kListMed4 = 4,   // len <= 10240  (1024 threads, 1 CTA/SM; the C4 bucket size)
+  kListMed5 = 5,   // len <= 16384  (512 threads, bucket re-read from L2)
+  kListPass = 6,   // depth == 10: all key bytes equal -> already in index order
+  kNumKdLists = 7
 };
-constexpr uint32_t kMedCap[4] = {512, 2048, 8192, 16384};
 
 struct ListSet {
   Seg* items[kNumKdLists];

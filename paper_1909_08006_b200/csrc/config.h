@@ -22,6 +22,10 @@ constexpr uint32_t kChunk = kSplitThreads * kSplitItems;  // 4096
 
 constexpr int kRadix = 256;
 
+// K-a accumulates hist16 into kHistCopies copies (CTA t -> copy t % kHistCopies) so skewed keys do not
+// serialise on a few L2 atomic addresses; K-b sums the copies.
+constexpr int kHistCopies = 16;
+
 // K-b block tile
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;

@@ -65,7 +65,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
 
   // ---------------------------------------------------------------- zero counters / look-back state
   if ((st = prof.begin("init"))) return st;
-  LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4 * 65536, s));
+  LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4ull * 65536 * L.hist_copies, s));
   LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * 64, s));
   LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
   LEY_CUDA("init", cudaMemsetAsync(split_status, 0, 8 * (size_t)kRadix * L.split_chunks_ub, s));
@@ -73,17 +73,18 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
 
   // ---------------------------------------------------------------- K-a
   if ((st = prof.begin("K-a tile sort"))) return st;
-  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, s));
+  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, s));
   ++launches;
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- K-b
   if ((st = prof.begin("K-b scan"))) return st;
+  LEY_CUDA("K-b scan", launch_hist_reduce(hist16, L.hist_copies, s));
   LEY_CUDA("K-b scan", launch_scan_excl(cnt, off, L.m, scan_status, tickets + 0, off + L.m, s));
   LEY_CUDA("K-b scan", launch_scan_excl(hist16, B16, 65536, scan_status + L.scan_status_words, tickets + 1,
                                         B16 + 65536, s));
   LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
-  launches += 3;
+  launches += 4;
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- K-c (byte 1)

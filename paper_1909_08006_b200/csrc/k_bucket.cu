@@ -135,7 +135,7 @@ __host__ __device__ constexpr size_t kd_smem() {
 //      (tiny) or a warp bitonic network (larger) — Alg. 1's ComparisonSort below tinyBucketThreshold,
 //   4. perm[start + i] = idx of the i-th smallest, coalesced.
 template <uint32_t CAP, int THREADS>
-__global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THREADS) > 4 ? 4 : 6)
+__global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 6)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                 uint32_t* __restrict__ perm, Tunables tu) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
     auto digit = [&](uint64_t t) -> uint32_t { return bits ? (uint32_t)(t >> shift) & mask : 0u; };
 
     uint64_t tr[RITEMS];
-    uint32_t xr[RITEMS], rr[RITEMS], dr[RITEMS];
+    uint32_t xr[RITEMS], rr[RITEMS];
     if (REGS) {
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
@@ -186,12 +186,22 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          dr[j] = digit(tr[j]);
-          rr[j] = atomicAdd(&s_cnt[dr[j]], 1u);
+          rr[j] = atomicAdd(&s_cnt[digit(tr[j])], 1u);
         }
       }
     } else {
-      for (uint32_t i = threadIdx.x; i < s; i += THREADS) atomicAdd(&s_cnt[digit(tp[i])], 1u);
+      // batches of 8 independent loads per thread keep the bucket read latency-tolerant
+      for (uint32_t i0 = threadIdx.x; i0 < s; i0 += 8 * THREADS) {
+        uint64_t tb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t i = i0 + u * THREADS;
+          tb[u] = i < s ? tp[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * THREADS < s) atomicAdd(&s_cnt[digit(tb[u])], 1u);
+      }
     }
     if (threadIdx.x == 0) *s_nbig = 0;
     __syncthreads();
@@ -218,11 +228,9 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t b = s_cnt[dr[j]], e = s_cnt[dr[j] + 1];
-          rr[j] |= (e - b) << 16;  // keep the sub-bucket size next to the rank (both < 2^16)
-          dr[j] = b;               // and its start
-          s_tail[b + (rr[j] & 0xFFFFu)] = tr[j];
-          s_idx[b + (rr[j] & 0xFFFFu)] = xr[j];
+          const uint32_t b = s_cnt[digit(tr[j])];
+          s_tail[b + rr[j]] = tr[j];
+          s_idx[b + rr[j]] = xr[j];
         }
       }
       __syncthreads();
@@ -230,14 +238,15 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t b = dr[j], sz = rr[j] >> 16;
+          const uint32_t d = digit(tr[j]);
+          const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
           if (sz == 1) {
             perm[sg.start + b] = xr[j];
           } else if (sz <= (uint32_t)tu.kd_insert_max) {
             uint32_t rank = 0;
             for (uint32_t m = b; m < b + sz; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
             perm[sg.start + b + rank] = xr[j];
-          } else if ((rr[j] & 0xFFFFu) == 0) {
+          } else if (rr[j] == 0) {
             s_bigl[atomicAdd(s_nbig, 1u)] = digit(tr[j]);
           }
         }
@@ -258,12 +267,26 @@ __global__ void __launch_bounds__(THREADS, (CAP / THREADS) > 8 ? 1 : (CAP / THRE
     // ---- large-CAP path: elements re-read from L2, placed by a second counter pass
     for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_bigl[g] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < s; i += THREADS) {
-      uint64_t t = tp[i];
-      uint32_t d = digit(t);
-      uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
-      s_tail[p] = t;
-      s_idx[p] = ip[i];
+    for (uint32_t i0 = threadIdx.x; i0 < s; i0 += 8 * THREADS) {
+      uint64_t tb[8];
+      uint32_t xb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t i = i0 + u * THREADS;
+        if (i < s) {
+          tb[u] = tp[i];
+          xb[u] = ip[i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (i0 + u * THREADS < s) {
+          const uint32_t d = digit(tb[u]);
+          const uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
+          s_tail[p] = tb[u];
+          s_idx[p] = xb[u];
+        }
+      }
     }
     __syncthreads();
     // comparison sort of every sub-bucket
@@ -343,11 +366,13 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
     return e;
   if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, s)))
     return e;
-  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms, s)))
+    return e;
+  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms, s)))
     return e;
   kd_passthrough<<<sms * 4, 256, 0, s>>>(kd.items[kListPass], kd.counts + kListPass, i0, i1, perm);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (launches) *launches += 6;
+  if (launches) *launches += 7;
   return cudaSuccess;
 }
 

@@ -81,7 +81,22 @@ __global__ void kc_plan_chunks(const uint32_t* __restrict__ B16, uint64_t n, uin
   if (b == 0) cstart[256] = total;
 }
 
+// hist16[b] = sum of the kHistCopies copies (copy 0 is overwritten in place).
+__global__ void kb_hist_reduce(uint32_t* __restrict__ hist, uint32_t copies) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= 65536) return;
+  uint32_t s = 0;
+  for (uint32_t c = 0; c < copies; ++c) s += hist[(size_t)c * 65536 + b];
+  hist[b] = s;
+}
+
 }  // namespace
+
+cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s) {
+  if (copies <= 1) return cudaSuccess;
+  kb_hist_reduce<<<256, 256, 0, s>>>(hist, copies);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
                              uint32_t* total_out, cudaStream_t s) {

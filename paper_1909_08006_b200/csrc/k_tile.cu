@@ -26,7 +26,7 @@ template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles,
                                                          uint64_t* __restrict__ k1_out, uint32_t* __restrict__ w_out,
                                                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
-                                                         uint32_t* __restrict__ hist16) {
+                                                         uint32_t* __restrict__ hist16, uint32_t copies) {
   constexpr int T = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
   const uint32_t cnt_t = (uint32_t)(n - base < (uint64_t)T ? n - base : (uint64_t)T);
 
   for (int i = threadIdx.x; i < WARPS * kRadix; i += THREADS) s_wh[i] = 0;
+  uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
 
   // ---- 1. load keys (all loads issued before use)
   uint32_t a[ITEMS], b[ITEMS], c[ITEMS];
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
     // level-1 bucket sizes: 16-bit prefix (bytes 0..1)
     uint32_t p16 = hi >> 16;
     uint32_t peers16 = peers & warp_peers8((hi >> 16) & 0xFFu, valid);
-    if (valid && __popc(peers16 & lt) == 0) atomicAdd(&hist16[p16], (uint32_t)__popc(peers16));
+    if (valid && __popc(peers16 & lt) == 0) atomicAdd(&hist_copy[p16], (uint32_t)__popc(peers16));
   }
   __syncthreads();
 
@@ -132,12 +133,12 @@ size_t ka_smem_bytes() {
 }
 
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
-                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, cudaStream_t s) {
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, cudaStream_t s) {
   auto kern = ka_tile_sort<kTileThreads, kTileItems>;
   size_t smem = ka_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16);
+  kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies);
   return cudaGetLastError();
 }
 

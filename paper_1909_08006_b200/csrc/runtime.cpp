@@ -104,7 +104,8 @@ InternalLayout plan_internal(uint64_t n) {
   L.off_cnt = take(4 * L.m);
   L.off_off = take(4 * (L.m + 1));
   L.off_lo = take(4 * L.m);
-  L.off_hist16 = take(4 * 65536);
+  L.hist_copies = (uint32_t)std::min<uint64_t>(kHistCopies, std::max<uint64_t>(1, L.tiles / 64));
+  L.off_hist16 = take(4ull * 65536 * L.hist_copies);
   L.off_B16 = take(4 * (65536 + 1));
   L.off_cstart = take(4 * 260);
   L.off_scan_status = take(8 * 2 * L.scan_status_words);

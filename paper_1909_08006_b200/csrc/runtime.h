@@ -57,6 +57,7 @@ struct InternalLayout {
   size_t off_cnt = 0, off_off = 0, off_lo = 0, off_hist16 = 0, off_B16 = 0, off_cstart = 0;
   size_t off_scan_status = 0, off_split_status = 0, off_small = 0, off_plan_a = 0, off_plan_b = 0;
   size_t scan_status_words = 0;
+  uint32_t hist_copies = 1;  // K-a hist16 copies (contention relief under skew)
   size_t bytes = 0;  // total
 };
 InternalLayout plan_internal(uint64_t n);
