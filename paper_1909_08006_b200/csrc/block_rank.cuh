@@ -12,6 +12,9 @@ namespace ley {
 // Lanes of the warp holding the same 8-bit digit (and valid): 8 ballots, one per digit bit (warp
 // multi-split), cheaper than match.any on sm_100a.
 __device__ __forceinline__ uint32_t warp_peers8(uint32_t d, bool valid) {
+#ifdef LEY_RANK_MATCH
+  return __match_any_sync(0xffffffffu, valid ? d : (0x100u | (threadIdx.x & 31)));
+#endif
   uint32_t peers = __ballot_sync(0xffffffffu, valid);
   if (!valid) peers = ~peers;
 #pragma unroll
@@ -21,6 +24,36 @@ __device__ __forceinline__ uint32_t warp_peers8(uint32_t d, bool valid) {
     peers &= set ? bal : ~bal;
   }
   return peers;
+}
+
+// Unstable block-wide ranking by one 8-bit digit: a shared-memory atomic per item gives its position
+// inside its digit group, a block scan of the 256 counts gives the group starts. The order inside a
+// group is whatever the atomics produce — the sort's result does not depend on it, because every later
+// comparison is on the composite (key, ordinal). s_hist: [256] u32; s_tmp: [32] u32.
+template <int THREADS, int ITEMS>
+__device__ __forceinline__ void block_rank_atomic(const uint32_t (&dig)[ITEMS], uint32_t count, uint32_t (&pos)[ITEMS],
+                                                  uint32_t* s_hist, uint32_t* s_tmp, uint32_t& total_d,
+                                                  uint32_t& excl_d) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRadix; i += THREADS) s_hist[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
+    if (e < count) pos[j] = atomicAdd(&s_hist[dig[j]], 1u);
+  }
+  __syncthreads();
+  const uint32_t total = threadIdx.x < kRadix ? s_hist[threadIdx.x] : 0u;
+  const uint32_t excl = block_excl_scan<THREADS>(total, s_tmp, nullptr);
+  if (threadIdx.x < kRadix) s_hist[threadIdx.x] = excl;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
+    if (e < count) pos[j] += s_hist[dig[j]];
+  }
+  total_d = total;
+  excl_d = excl;
 }
 
 // s_wh: [THREADS/32][256] u32 scratch; s_tmp: [32] u32.

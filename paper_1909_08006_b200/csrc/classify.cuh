@@ -1,6 +1,7 @@
 // classify.cuh — route a finished MSD bucket to its tier (Algorithm 1, lines 60-85):
-//   depth == 10                 -> pass-through: every key byte consumed, ties already in index order
-//                                  ("if radix < 10")
+//   (depth counts consumed bytes of the composite key: key bytes 0..9, then the ordinal's 4 bytes, so
+//    a bucket whose 10 key bytes are all equal keeps splitting on its ordinals — P:60/"radix < 10"
+//    ends the key; SURVEY Q12 — and every bucket ends as a singleton at depth 14 at the latest)
 //   len <= warp_tier_max        -> one-warp comparison network ("ComparisonSort(key)" for
 //                                  k < tinyBucketThreshold)
 //   len <= smem_tier_max        -> one CTA in shared memory ("SingleThreadRadixSort" of a small bucket,
@@ -16,9 +17,7 @@ __device__ __forceinline__ void classify_bucket(const Seg& s, const Tunables& tu
                                                 uint32_t* big_count) {
   if (s.len == 0) return;
   int list;
-  if (s.depth >= kKeyBytes) {
-    list = kListPass;
-  } else if (s.len <= tu.warp_tier_max) {
+  if (s.len <= tu.warp_tier_max) {
     list = kListWarp;
   } else if (s.len <= tu.smem_tier_max) {
     list = s.len <= 512    ? kListMed1

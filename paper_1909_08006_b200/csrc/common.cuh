@@ -25,8 +25,7 @@ enum ListId : int {
   kListMed3 = 3,   // len <= 8192   (512 threads)
   kListMed4 = 4,   // len <= 10240  (1024 threads, 1 CTA/SM; the C4 bucket size)
   kListMed5 = 5,   // len <= 16384  (512 threads, bucket re-read from L2)
-  kListPass = 6,   // depth == 10: all key bytes equal -> already in index order
-  kNumKdLists = 7
+  kNumKdLists = 6
 };
 
 struct ListSet {

@@ -46,7 +46,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   uint32_t* B16 = reinterpret_cast<uint32_t*>(base + L.off_B16);
   uint32_t* cstart = reinterpret_cast<uint32_t*>(base + L.off_cstart);
   uint64_t* scan_status = reinterpret_cast<uint64_t*>(base + L.off_scan_status);
-  uint64_t* split_status = reinterpret_cast<uint64_t*>(base + L.off_split_status);
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(base + L.off_cursor);
   uint32_t* small = reinterpret_cast<uint32_t*>(base + L.off_small);
   uint32_t* tickets = small;          // [0..15]
   uint32_t* kd_counts = small + 16;   // [kNumKdLists]
@@ -68,7 +68,6 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4ull * 65536 * L.hist_copies, s));
   LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * 64, s));
   LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
-  LEY_CUDA("init", cudaMemsetAsync(split_status, 0, 8 * (size_t)kRadix * L.split_chunks_ub, s));
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- K-a
@@ -91,7 +90,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   if ((st = prof.begin("K-c split"))) return st;
   LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
                                                reinterpret_cast<uint4*>(base + L.off_plan_a),
-                                               reinterpret_cast<uint2*>(base + L.off_plan_b), split_status,
+                                               reinterpret_cast<uint2*>(base + L.off_plan_b), cursor,
                                                tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s));
   launches += 2;
   if ((st = prof.end())) return st;
@@ -130,11 +129,11 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     const uint64_t child_cap = std::min<uint64_t>((uint64_t)nbig * kRadix, n + 1);
     const uint64_t next_big_cap = std::min<uint64_t>(child_cap, n / (tier + 1) + 1);
     const size_t scan_words = scan_status_words(nbig);
-    // rec layout: nch | cstart2 | seg_hist | seg_excl | noscatter | scan status | split status | tickets
+    // rec layout: nch | cstart2 | seg_hist | seg_excl (= fill cursors) | noscatter | scan status | tickets
     size_t r_nch = 0, r_cst = a256(4ull * (nbig + 1)), r_hist = r_cst + a256(4ull * (nbig + 1));
     size_t r_excl = r_hist + a256(4ull * nbig * kRadix), r_nos = r_excl + a256(4ull * nbig * kRadix);
-    size_t r_scan = r_nos + a256(nbig), r_stat = r_scan + a256(8 * scan_words);
-    size_t r_tick = r_stat + a256(8ull * kRadix * chunks_ub), r_end = r_tick + 256;
+    size_t r_scan = r_nos + a256(nbig);
+    size_t r_tick = r_scan + a256(8 * scan_words), r_end = r_tick + 256;
     if ((st = ensure_buffer(ctx.rec, r_end, "recursion arrays", s))) return st;
     if (child_cap > kd.cap) {
       if ((st = ensure_buffer(ctx.lists, (size_t)kNumKdLists * a256(child_cap * sizeof(Seg)), "K-d lists", s)))
@@ -151,24 +150,22 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     uint32_t* seg_excl = reinterpret_cast<uint32_t*>(rb + r_excl);
     uint8_t* noscatter = rb + r_nos;
     uint64_t* rscan = reinterpret_cast<uint64_t*>(rb + r_scan);
-    uint64_t* rstat = reinterpret_cast<uint64_t*>(rb + r_stat);
     uint32_t* rtick = reinterpret_cast<uint32_t*>(rb + r_tick);
     const Seg* segs = static_cast<const Seg*>(ctx.big[cur].ptr);
     Seg* next_big = static_cast<Seg*>(ctx.big[cur ^ 1].ptr);
 
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(seg_hist, 0, 4ull * nbig * kRadix, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rscan, 0, 8 * scan_words, s));
-    LEY_CUDA("K-c' recursion", cudaMemsetAsync(rstat, 0, 8ull * kRadix * chunks_ub, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rtick, 0, 256, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(kd_counts, 0, 4 * kNumKdLists, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(big_count, 0, 4, s));
     LEY_CUDA("K-c' recursion", launch_kr_nchunks(segs, nbig, nch, s));
     LEY_CUDA("K-c' recursion", launch_scan_excl(nch, cst, nbig, rscan, rtick + 0, cst + nbig, s));
     uint32_t hist_grid = (uint32_t)std::min<uint64_t>(chunks_ub, (uint64_t)sms * 8);
-    LEY_CUDA("K-c' recursion", launch_kr_hist(segs, nbig, cst, hist_grid, At, Bt, seg_hist, s));
+    LEY_CUDA("K-c' recursion", launch_kr_hist(segs, nbig, cst, hist_grid, At, Ai, Bt, Bi, seg_hist, s));
     LEY_CUDA("K-c' recursion",
              launch_kr_plan(segs, nbig, seg_hist, seg_excl, noscatter, tu, kd, next_big, big_count, s));
-    LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rstat, rtick + 1,
+    LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rtick + 1,
                                               (uint32_t)chunks_ub, s));
     launches += 5;
     LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm, tu, sms, s, &launches));

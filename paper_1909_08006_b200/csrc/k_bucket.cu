@@ -65,18 +65,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// ---------------------------------------------------------------------------- pass-through (depth 10)
-__global__ void kd_passthrough(const Seg* __restrict__ list, const uint32_t* __restrict__ count,
-                               const uint32_t* __restrict__ i0, const uint32_t* __restrict__ i1,
-                               uint32_t* __restrict__ perm) {
-  const uint32_t nitems = *count;
-  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const Seg sg = list[it];
-    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
-    for (uint32_t i = threadIdx.x; i < sg.len; i += blockDim.x) perm[sg.start + i] = ip[i];
-  }
-}
-
 // ---------------------------------------------------------------------------- CTA tier
 // In-smem all-ascending bitonic network over [b, e) by one warp; virtual +inf padding beyond e never
 // moves, so compare-exchanges touching it are skipped.
@@ -161,7 +149,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     const uint32_t s = sg.len;
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
     const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
-    const uint32_t avail = 8u * (kKeyBytes - sg.depth);  // unconsumed key bits held in the tail
+    // unconsumed bits of the composite key (tail = key bytes 2..9, then the 32-bit ordinal): key bits
+    // while depth < 10, else ordinal bits (the key bytes are then all equal inside the bucket)
+    const bool on_idx = sg.depth >= kKeyBytes;
+    const uint32_t avail = on_idx ? 8u * (14u - sg.depth) : 8u * (kKeyBytes - sg.depth);
     uint32_t bits = s > 1 ? 32u - __clz(s - 1) : 0u;
     bits = min(bits, (uint32_t)tu.kd_digit_bits);
     bits = min(bits, avail);
@@ -169,7 +160,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     const uint32_t shift = avail - bits;
     const uint32_t nb = 1u << bits;
     const uint32_t mask = nb - 1;
-    auto digit = [&](uint64_t t) -> uint32_t { return bits ? (uint32_t)(t >> shift) & mask : 0u; };
+    auto digit2 = [&](uint64_t t, uint32_t x) -> uint32_t {
+      return bits ? (on_idx ? (x >> shift) & mask : (uint32_t)(t >> shift) & mask) : 0u;
+    };
 
     uint64_t tr[RITEMS];
     uint32_t xr[RITEMS], rr[RITEMS];
@@ -186,21 +179,23 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          rr[j] = atomicAdd(&s_cnt[digit(tr[j])], 1u);
+          rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
         }
       }
     } else {
       // batches of 8 independent loads per thread keep the bucket read latency-tolerant
       for (uint32_t i0 = threadIdx.x; i0 < s; i0 += 8 * THREADS) {
         uint64_t tb[8];
+        uint32_t xb[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t i = i0 + u * THREADS;
           tb[u] = i < s ? tp[i] : 0;
+          xb[u] = (i < s && on_idx) ? ip[i] : 0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (i0 + u * THREADS < s) atomicAdd(&s_cnt[digit(tb[u])], 1u);
+          if (i0 + u * THREADS < s) atomicAdd(&s_cnt[digit2(tb[u], xb[u])], 1u);
       }
     }
     if (threadIdx.x == 0) *s_nbig = 0;
@@ -228,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t b = s_cnt[digit(tr[j])];
+          const uint32_t b = s_cnt[digit2(tr[j], xr[j])];
           s_tail[b + rr[j]] = tr[j];
           s_idx[b + rr[j]] = xr[j];
         }
@@ -238,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t d = digit(tr[j]);
+          const uint32_t d = digit2(tr[j], xr[j]);
           const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
           if (sz == 1) {
             perm[sg.start + b] = xr[j];
@@ -247,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
             for (uint32_t m = b; m < b + sz; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
             perm[sg.start + b + rank] = xr[j];
           } else if (rr[j] == 0) {
-            s_bigl[atomicAdd(s_nbig, 1u)] = digit(tr[j]);
+            s_bigl[atomicAdd(s_nbig, 1u)] = digit2(tr[j], xr[j]);
           }
         }
       }
@@ -281,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (i0 + u * THREADS < s) {
-          const uint32_t d = digit(tb[u]);
+          const uint32_t d = digit2(tb[u], xb[u]);
           const uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
           s_tail[p] = tb[u];
           s_idx[p] = xb[u];
@@ -370,9 +365,7 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
     return e;
   if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms, s)))
     return e;
-  kd_passthrough<<<sms * 4, 256, 0, s>>>(kd.items[kListPass], kd.counts + kListPass, i0, i1, perm);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (launches) *launches += 7;
+  if (launches) *launches += 6;
   return cudaSuccess;
 }
 

@@ -5,15 +5,20 @@
 // and Algorithm 1 lines 59-63 (after the first round every bucket is split again on the next radix;
 // "if k > bigBucketThreshold then MSDRadixSort(key, radix + 1, k)"). SURVEY.md §8a rows a3 and a4.
 //
-// K-c (level 1): byte-0 bucket b is the concatenation, in tile order, of the byte-0 runs K-a left in
-// every tile. Each CTA takes one chunk (kChunk consecutive pairs of one bucket, claimed by atomic ticket
-// in global chunk order), gathers it from the runs, ranks it stably by key byte 1 (warp multi-split),
-// finds its per-digit offset inside the bucket by decoupled look-back over the bucket's earlier chunks,
-// stages the pairs in shared memory in digit order and writes them to their 16-bit bucket
-// B16[b:d] + offset. Output pair: tail = key bytes 2..9 big-endian (u64), idx = global ordinal (u32).
+// K-c (level 1): byte-0 bucket b is the concatenation of the byte-0 runs K-a left in every tile. Each
+// CTA takes kChunk-pair chunks of one bucket (persistent, ticketed), gathers a chunk from the runs, ranks
+// it by key byte 1 (shared-memory atomics), claims each digit's slice of its 16-bit bucket with one global
+// atomic on that bucket's fill cursor (initialised to B16), stages the pairs in shared memory in digit
+// order and writes them out as coalesced runs. Output pair: tail = key bytes 2..9 big-endian (u64),
+// idx = global ordinal (u32).
 //
-// K-c' (level >= 2): the same on contiguous big buckets, digit = key byte `depth`; the bucket's digit
-// histogram comes from kr_hist and its children are classified by kr_plan before the split.
+// The order inside a bucket is whatever the atomics produce: it does not matter, because every later
+// step orders by the composite (key bytes, ordinal) — the ordinal is the least significant part of the
+// sort key, which is what makes the result the stable sort. No look-back is needed.
+//
+// K-c' (level >= 2): the same on contiguous big buckets, digit = key byte `depth` (depth 10..13: byte
+// depth-10 of the big-endian ordinal, for buckets whose 10 key bytes are all equal); the bucket's
+// digit histogram comes from kr_hist and its children are classified by kr_plan before the split.
 #include "block_rank.cuh"
 #include "classify.cuh"
 #include "common.cuh"
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     kc_split_level1(const uint64_t* __restrict__ k1_in, const uint32_t* __restrict__ w_in, uint32_t tiles,
                     const uint32_t* __restrict__ off /*[256*tiles+1]*/, const uint32_t* __restrict__ lo,
                     const uint32_t* __restrict__ B16, const uint32_t* __restrict__ cstart,
-                    const uint4* __restrict__ plan_a, const uint2* __restrict__ plan_b, uint64_t* __restrict__ status,
+                    const uint4* __restrict__ plan_a, const uint2* __restrict__ plan_b, uint32_t* __restrict__ cursor,
                     uint32_t* __restrict__ ticket, uint64_t* __restrict__ tail_out, uint32_t* __restrict__ idx_out) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* region = smem;
@@ -174,8 +179,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();  // run tables dead from here on
 
     uint32_t pos[kItems], total_d, excl_d;
-    block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
-    if (threadIdx.x < kRadix) lookback_publish(status, k, k0, threadIdx.x, total_d);
+        block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+    if (threadIdx.x < kRadix) {
+      const int d = threadIdx.x;
+      const uint32_t base = total_d ? atomicAdd(&cursor[b * 256 + d], total_d) : 0u;
+      s_dst[d] = base - excl_d;
+    }
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       uint32_t e = warp * (32 * kItems) + j * 32 + lane;
@@ -185,11 +194,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         s_idx[p] = (src[j] & ~(kTileRecords - 1)) | (w[j] & 0xFFFFFFu);
         s_dig[p] = (uint8_t)dig[j];
       }
-    }
-    if (threadIdx.x < kRadix) {
-      const int d = threadIdx.x;
-      uint32_t pre = lookback_wait(status, k, k0, d, total_d);
-      s_dst[d] = B16[b * 256 + d] + pre - excl_d;
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
@@ -212,8 +216,10 @@ __device__ __forceinline__ uint32_t chunk_segment(const uint32_t* cstart, uint32
   return s;
 }
 
-__device__ __forceinline__ uint32_t byte_of_tail(uint64_t tail, uint32_t depth) {
-  return (uint32_t)(tail >> (8 * (9 - depth))) & 0xFFu;  // tail = key bytes 2..9
+// Digit `depth` of the composite sort key (key bytes 0..9, then the big-endian ordinal as bytes 10..13):
+// tail = key bytes 2..9, so byte d < 10 is (tail >> 8 (9 - d)); bytes 10..13 come from the ordinal.
+__device__ __forceinline__ uint32_t digit_at(uint64_t tail, uint32_t idx, uint32_t depth) {
+  return depth < 10 ? (uint32_t)(tail >> (8 * (9 - depth))) & 0xFFu : (idx >> (8 * (13 - depth))) & 0xFFu;
 }
 
 __global__ void kr_nchunks(const Seg* __restrict__ segs, uint32_t nseg, uint32_t* __restrict__ nch) {
@@ -223,7 +229,8 @@ __global__ void kr_nchunks(const Seg* __restrict__ segs, uint32_t nseg, uint32_t
 
 __global__ void __launch_bounds__(256)
     kr_hist(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart, uint32_t nchunks_total_ub,
-            const uint64_t* __restrict__ tails0, const uint64_t* __restrict__ tails1, uint32_t* __restrict__ seg_hist) {
+            const uint64_t* __restrict__ tails0, const uint32_t* __restrict__ idx0, const uint64_t* __restrict__ tails1,
+            const uint32_t* __restrict__ idx1, uint32_t* __restrict__ seg_hist) {
   __shared__ uint32_t h[kRadix];
   const uint32_t total = cstart[nseg];
   for (uint32_t k = blockIdx.x; k < total; k += gridDim.x) {
@@ -233,8 +240,13 @@ __global__ void __launch_bounds__(256)
     Seg sg = segs[s];
     uint32_t c = k - cstart[s];
     uint32_t beg = c * kChunk, end = min(sg.len, beg + kChunk);
-    const uint64_t* t = (sg.parity ? tails1 : tails0) + sg.start;
-    for (uint32_t i = beg + threadIdx.x; i < end; i += 256) atomicAdd(&h[byte_of_tail(t[i], sg.depth)], 1u);
+    if (sg.depth < 10) {
+      const uint64_t* t = (sg.parity ? tails1 : tails0) + sg.start;
+      for (uint32_t i = beg + threadIdx.x; i < end; i += 256) atomicAdd(&h[digit_at(t[i], 0, sg.depth)], 1u);
+    } else {
+      const uint32_t* x = (sg.parity ? idx1 : idx0) + sg.start;
+      for (uint32_t i = beg + threadIdx.x; i < end; i += 256) atomicAdd(&h[digit_at(0, x[i], sg.depth)], 1u);
+    }
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&seg_hist[(uint64_t)s * kRadix + threadIdx.x], h[threadIdx.x]);
     __syncthreads();
@@ -242,7 +254,8 @@ __global__ void __launch_bounds__(256)
   (void)nchunks_total_ub;
 }
 
-// One CTA (256 threads) per big segment: bucket offsets, children, constant-digit skip.
+// One CTA (256 threads) per big segment: bucket offsets (also the fill cursors of kr_split), children,
+// constant-digit skip.
 __global__ void __launch_bounds__(256)
     kr_plan(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ seg_hist,
             uint32_t* __restrict__ seg_excl, uint8_t* __restrict__ noscatter, Tunables tu, ListSet kd,
@@ -275,9 +288,8 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(kThreads, 2)
     kr_split(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart,
-             const uint32_t* __restrict__ seg_excl, const uint8_t* __restrict__ noscatter, uint64_t* tails0,
-             uint32_t* idx0, uint64_t* tails1, uint32_t* idx1, uint64_t* __restrict__ status,
-             uint32_t* __restrict__ ticket) {
+             uint32_t* __restrict__ cursor, const uint8_t* __restrict__ noscatter, uint64_t* tails0, uint32_t* idx0,
+             uint64_t* tails1, uint32_t* idx1, uint32_t* __restrict__ ticket) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
@@ -285,66 +297,72 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* s_wh = reinterpret_cast<uint32_t*>(smem + SplitSmem::kRegion);
   uint32_t* s_dst = s_wh + kWarps * kRadix;
   uint32_t* s_misc = s_dst + 256;
-
-  if (threadIdx.x == 0) {
-    uint32_t k = atomicAdd(ticket, 1u);
-    s_misc[32] = k;
-    if (k < cstart[nseg]) {
-      uint32_t s = chunk_segment(cstart, nseg, k);
-      s_misc[33] = s;
-      s_misc[34] = k - cstart[s];
-    }
-  }
-  __syncthreads();
-  const uint32_t k = s_misc[32];
-  if (k >= cstart[nseg]) return;
-  const uint32_t s = s_misc[33], c = s_misc[34];
-  if (noscatter[s]) return;
-  const Seg sg = segs[s];
-  const uint32_t beg = c * kChunk;
-  const uint32_t cnt = min(kChunk, sg.len - beg);
-  const uint64_t* tin = (sg.parity ? tails1 : tails0) + sg.start + beg;
-  const uint32_t* iin = (sg.parity ? idx1 : idx0) + sg.start + beg;
-  uint64_t* tout = (sg.parity ? tails0 : tails1) + sg.start;
-  uint32_t* iout = (sg.parity ? idx0 : idx1) + sg.start;
-
+  const uint32_t total = cstart[nseg];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t tv[kItems];
-  uint32_t iv[kItems], dig[kItems];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-    if (e < cnt) {
-      tv[j] = tin[e];
-      iv[j] = iin[e];
-    } else {
-      tv[j] = 0;
-      iv[j] = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      uint32_t k = atomicAdd(ticket, 1u);
+      s_misc[32] = k;
+      if (k < total) {
+        uint32_t s = chunk_segment(cstart, nseg, k);
+        s_misc[33] = s;
+        s_misc[34] = k - cstart[s];
+      }
     }
-    dig[j] = byte_of_tail(tv[j], sg.depth);
-  }
-  uint32_t pos[kItems], total_d, excl_d;
-  block_rank_digits<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
-  if (threadIdx.x < kRadix) {
-    const int d = threadIdx.x;
-    uint32_t pre = lookback_digit(status, k, k - c, d, total_d);
-    s_dst[d] = seg_excl[(uint64_t)s * kRadix + d] + pre - excl_d;
-  }
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-    if (e < cnt) {
-      uint32_t p = pos[j];
-      s_tail[p] = tv[j];
-      s_idx[p] = iv[j];
-      s_dig[p] = (uint8_t)dig[j];
+    __syncthreads();
+    const uint32_t k = s_misc[32];
+    if (k >= total) return;
+    const uint32_t s = s_misc[33], c = s_misc[34];
+    if (noscatter[s]) {
+      __syncthreads();
+      continue;
     }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-    uint32_t g = s_dst[s_dig[i]] + i;
-    tout[g] = s_tail[i];
-    iout[g] = s_idx[i];
+    const Seg sg = segs[s];
+    const uint32_t beg = c * kChunk;
+    const uint32_t cnt = min(kChunk, sg.len - beg);
+    const uint64_t* tin = (sg.parity ? tails1 : tails0) + sg.start + beg;
+    const uint32_t* iin = (sg.parity ? idx1 : idx0) + sg.start + beg;
+    uint64_t* tout = (sg.parity ? tails0 : tails1) + sg.start;
+    uint32_t* iout = (sg.parity ? idx0 : idx1) + sg.start;
+
+    uint64_t tv[kItems];
+    uint32_t iv[kItems], dig[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+      if (e < cnt) {
+        tv[j] = tin[e];
+        iv[j] = iin[e];
+      } else {
+        tv[j] = 0;
+        iv[j] = 0;
+      }
+      dig[j] = digit_at(tv[j], iv[j], sg.depth);
+    }
+    uint32_t pos[kItems], total_d, excl_d;
+        block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+    if (threadIdx.x < kRadix) {
+      const int d = threadIdx.x;
+      const uint32_t base = total_d ? atomicAdd(&cursor[(uint64_t)s * kRadix + d], total_d) : 0u;
+      s_dst[d] = base - excl_d;
+    }
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      uint32_t e = warp * (32 * kItems) + j * 32 + lane;
+      if (e < cnt) {
+        uint32_t p = pos[j];
+        s_tail[p] = tv[j];
+        s_idx[p] = iv[j];
+        s_dig[p] = (uint8_t)dig[j];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      uint32_t g = s_dst[s_dig[i]] + i;
+      tout[g] = s_tail[i];
+      iout[g] = s_idx[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -354,10 +372,12 @@ size_t split_smem_bytes() { return SplitSmem::kBytes; }
 
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
-                                   uint4* plan_a, uint2* plan_b, uint64_t* status, uint32_t* ticket,
+                                   uint4* plan_a, uint2* plan_b, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s) {
   kc_plan_level1<<<(grid_ub + 255) / 256, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b);
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(cursor, B16, 4 * 65536, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return e;
   size_t smem = SplitSmem::kBytes;
   e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -369,7 +389,7 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
   if (e != cudaSuccess) return e;
   uint32_t grid = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
   if (grid > grid_ub) grid = grid_ub;
-  kc_split_level1<<<grid, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, status,
+  kc_split_level1<<<grid, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, cursor,
                                                ticket, tail_out, idx_out);
   return cudaGetLastError();
 }
@@ -380,8 +400,9 @@ cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cud
 }
 
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
-                           const uint64_t* tails0, const uint64_t* tails1, uint32_t* seg_hist, cudaStream_t s) {
-  kr_hist<<<grid, 256, 0, s>>>(segs, nseg, cstart, grid, tails0, tails1, seg_hist);
+                           const uint64_t* tails0, const uint32_t* idx0, const uint64_t* tails1, const uint32_t* idx1,
+                           uint32_t* seg_hist, cudaStream_t s) {
+  kr_hist<<<grid, 256, 0, s>>>(segs, nseg, cstart, grid, tails0, idx0, tails1, idx1, seg_hist);
   return cudaGetLastError();
 }
 
@@ -392,14 +413,20 @@ cudaError_t launch_kr_plan(const Seg* segs, uint32_t nseg, const uint32_t* seg_h
   return cudaGetLastError();
 }
 
-cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, const uint32_t* seg_excl,
+cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t* cursor,
                             const uint8_t* noscatter, uint64_t* tails0, uint32_t* idx0, uint64_t* tails1,
-                            uint32_t* idx1, uint64_t* status, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s) {
+                            uint32_t* idx1, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s) {
   size_t smem = SplitSmem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kr_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kr_split<<<grid_ub, kThreads, smem, s>>>(segs, nseg, cstart, seg_excl, noscatter, tails0, idx0, tails1, idx1,
-                                           status, ticket);
+  int per_sm = 2, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr_split, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  uint32_t grid = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
+  if (grid > grid_ub) grid = grid_ub;
+  kr_split<<<grid, kThreads, smem, s>>>(segs, nseg, cstart, cursor, noscatter, tails0, idx0, tails1, idx1, ticket);
   return cudaGetLastError();
 }
 

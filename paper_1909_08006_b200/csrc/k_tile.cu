@@ -8,7 +8,8 @@
 //
 // One CTA per tile of kTileRecords records:
 //   1. load key bytes 0..9 of each record (three 4-byte loads; record i sits at byte 100 i, 4-aligned)
-//   2. warp multi-split rank on byte 0 (match.any + popc of lanemask_lt): stable, input order
+//   2. warp multi-split rank on byte 0 (8 ballots + popc of lanemask_lt; measured cheaper here than
+//      shared-memory atomics, which win in K-c)
 //   3. block scan of the 256 x WARPS counts -> tile-local offsets
 //   4. scatter pairs into shared memory in byte-0 order, write them out coalesced:
 //        k1 = key bytes 1..8 big-endian (u64)     w = key byte 9 << 24 | local index (u32)

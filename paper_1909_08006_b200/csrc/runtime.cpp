@@ -109,7 +109,7 @@ InternalLayout plan_internal(uint64_t n) {
   L.off_B16 = take(4 * (65536 + 1));
   L.off_cstart = take(4 * 260);
   L.off_scan_status = take(8 * 2 * L.scan_status_words);
-  L.off_split_status = take(8 * (size_t)kRadix * L.split_chunks_ub);
+  L.off_cursor = take(4 * 65536);
   L.off_small = take(4 * 64);  // tickets + list counters
   L.off_plan_a = take(16 * L.split_chunks_ub);
   L.off_plan_b = take(8 * L.split_chunks_ub);
