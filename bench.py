@@ -43,7 +43,7 @@ CONFIGS = {
 }
 METRIC = "sorted GB/s of 100-byte records"
 # algorithmic bytes per record of each stage: what the step must move
-STAGE_ALG_BYTES = {"K-a tile sort": 10 + 12, "K-c split": 12 + 12, "K-d buckets": 12 + 4, "K-e gather": 4 + 100 + 100}
+STAGE_ALG_BYTES = {"K-a tile sort": 10 + 12, "K-c split": 12 + 12, "K-de sort+gather": 12 + 100 + 100}
 
 
 def _peaks():

@@ -5,8 +5,8 @@
 //   K-c  split every byte-0 bucket on byte 1           (the next round of ParallelRadixSort)
 //   classify level-1 buckets                           (big -> recurse P:62-63; small -> queue P:65-66)
 //   K-d  sort the queued buckets (warp / CTA tiers)    (SingleThreadRadixSort + ComparisonSort)
-//   loop while big buckets remain: K-c' on byte depth (MSDRadixSort(key, radix+1, k)) + K-d
-//   K-e  gather the records by the sorted ordinals     (record scatter of P:104-106)
+//   K-e  ... and, in the same kernels, gather each sorted bucket's records (record scatter)
+//   loop while big buckets remain: K-c' on byte depth (MSDRadixSort(key, radix+1, k)) + K-d/K-e
 //
 // All work is on the caller's stream. The only host synchronisations are one 4-byte read of the
 // big-bucket count per recursion level (usually exactly one per call) and the final completion wait.
@@ -96,7 +96,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- classify level 1, K-d
-  if ((st = prof.begin("K-d buckets"))) return st;
+  if ((st = prof.begin("K-de sort+gather"))) return st;
   uint64_t tier = std::max<uint64_t>(tu.smem_tier_max, tu.warp_tier_max);
   uint64_t big_cap = std::min<uint64_t>(65536, n / (tier + 1) + 1);
   uint32_t kd_cap = (uint32_t)std::min<uint64_t>(65536, n);  // level-1 buckets: at most min(2^16, n) non-empty
@@ -113,9 +113,9 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   bind_lists(kd_cap);
   LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
   ++launches;
-  LEY_CUDA("K-d buckets", launch_kd_all(kd, At, Ai, Bt, Bi, perm, tu, sms, s, &launches));
-  LEY_CUDA("K-d buckets", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
-  LEY_CUDA("K-d buckets", cudaStreamSynchronize(s));
+  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
+  LEY_CUDA("K-de sort+gather", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
   uint32_t nbig = host_cnt[0];
   if ((st = prof.end())) return st;
 
@@ -168,7 +168,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rtick + 1,
                                               (uint32_t)chunks_ub, s));
     launches += 5;
-    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm, tu, sms, s, &launches));
+    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
     LEY_CUDA("K-c' recursion", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
     LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
     nbig = host_cnt[0];
@@ -178,10 +178,6 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     }
   }
 
-  // ---------------------------------------------------------------- K-e
-  if ((st = prof.begin("K-e gather"))) return st;
-  LEY_CUDA("K-e gather", launch_ke_gather(in, perm, n, out, sms, s, &launches));
-  if ((st = prof.end())) return st;
   if (perm_out) {
     cudaPointerAttributes pa{};
     LEY_CUDA("perm", cudaPointerGetAttributes(&pa, perm_out));

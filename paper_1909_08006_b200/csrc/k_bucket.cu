@@ -1,15 +1,25 @@
-// k_bucket.cu — K-d: per-bucket sort of (key-tail, index) pairs, plus level-1 classification.
+// k_bucket.cu — K-d + K-e fused: per-bucket sort of (key-tail, ordinal) pairs, then the record gather
+// of that bucket, plus level-1 classification.
 //
 // PAPER.md §3.1 Algorithm 1 lines 65-85: buckets below bigBucketThreshold go to smallBucketQueue and
 // are finished by one worker each — SingleThreadRadixSort on the next radix, then ComparisonSort for
 // buckets under tinyBucketThreshold ("size is small enough for comparison-based sort to perform
 // more efficient than Radix Sort"). On the GPU a "worker" is a warp (tiny buckets, register bitonic
-// network over the composite (tail, index)) or a CTA (shared-memory counting pass on the next 1..12 key
-// bits, then per-sub-bucket comparison sort). SURVEY.md §8a row a5.
+// network over the composite (tail, ordinal)) or a CTA (shared-memory counting pass on the next 1..12
+// unconsumed bits of the composite key, then an exact rank inside every tiny sub-bucket, or a warp
+// bitonic network for larger ones). SURVEY.md §8a row a5.
 //
-// Every bucket writes perm[start .. start+len) = input ordinals in sorted order. The comparison order is
-// the composite (tail, index), which is the sort's strict total order, so the result does not depend on
-// the (non-deterministic) atomics used to place elements inside a CTA.
+// The same worker then performs the record scatter of its bucket (§3.2, "scatter
+// data records ... given the sorted (key, pointer) tuples"): the bucket's output is
+// the contiguous range out[start, start+len), so each warp takes groups of 32 output records, issues
+// 16-byte cp.async copies of each record's 16-byte-aligned 112-byte window [floor(100 p/16)*16, +112)
+// into its shared-memory staging, re-aligns and writes the group as a coalesced word stream. Fusing the
+// two removes the perm round trip and hides the sort's shared-memory work under other
+// CTAs' gather traffic. Every chunk copy starts inside the input buffer (the window starts at or below
+// the record) and, being 16-byte aligned, never crosses a page.
+//
+// The comparison order is the composite (tail, ordinal) — the sort's strict total order — so the result
+// does not depend on the order in which atomics place elements.
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -19,6 +29,50 @@
 
 namespace ley {
 namespace {
+
+constexpr int kGroup = 32;                     // records per warp gather group
+constexpr int kWindow = 112;                   // 7 x 16-byte chunks hold any 4-byte-aligned 100-byte record
+constexpr int kStageBytes = kGroup * kWindow;  // 3584 B per gathering warp
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void stg_cs_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Records in[perm[i]] -> out_base[i] for i in [0, s) by one warp, groups g0 = first, first + stride, ...
+// of 32 records, through `stage` (kStageBytes, 16-byte aligned). perm lives in shared memory.
+__device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
+                                            const uint8_t* __restrict__ in, uint8_t* __restrict__ out_base,
+                                            uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  for (uint32_t g0 = first; g0 < s; g0 += stride) {
+    const uint32_t cnt = min((uint32_t)kGroup, s - g0);
+    const uint32_t p = lane < (int)cnt ? perm[g0 + lane] : 0u;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const int cidx = q * 32 + lane;
+      const int r = cidx / 7, c = cidx - r * 7;
+      const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
+      if (r < (int)cnt)
+        cp_async16(stage_s + r * kWindow + c * 16,
+                   in + ((((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16));
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out_base + (uint64_t)g0 * kRecordBytes);
+    const uint32_t words = cnt * kRecordWords;
+    for (uint32_t w = lane; w < words; w += 32) {
+      const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
+      const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
+      stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
+    }
+    __syncwarp();
+  }
+}
 
 __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
                                    Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
@@ -32,11 +86,13 @@ __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const ui
 __global__ void __launch_bounds__(256)
     kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                  const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                 uint32_t* __restrict__ perm) {
+                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+  __shared__ __align__(16) uint8_t s_stage[8][kStageBytes];
+  __shared__ uint32_t s_perm[8][32];
   const uint32_t nitems = *count;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems; it += nwarps) {
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + wib; it < nitems; it += nwarps) {
     const Seg sg = list[it];
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
     const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
@@ -61,7 +117,12 @@ __global__ void __launch_bounds__(256)
         }
       }
     }
-    if ((uint32_t)lane < sg.len) perm[sg.start + lane] = x;
+    if ((uint32_t)lane < sg.len) {
+      if (perm) perm[sg.start + lane] = x;
+      s_perm[wib][lane] = x;
+    }
+    __syncwarp();
+    warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib]);
   }
 }
 
@@ -109,42 +170,61 @@ template <uint32_t CAP>
 __host__ __device__ constexpr uint32_t kd_bins() {
   return CAP >= 4096 ? 4096u : CAP;  // <= 2^12 counting bins
 }
-template <uint32_t CAP>
-__host__ __device__ constexpr size_t kd_smem() {
-  return (size_t)CAP * 12 + (size_t)(2 * kd_bins<CAP>() + 1) * 4 + 64 * 4 + 16;
-}
+template <uint32_t CAP, int THREADS>
+struct KdLayout {
+  static constexpr uint32_t BINS = kd_bins<CAP>();
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr bool REGS = CAP / THREADS <= 16;  // bucket held in registers (else re-read from L2)
+  // [s_idx CAP x 4][s_perm CAP x 4 (REGS only)][reusable: s_tail CAP x 8 | s_cnt | s_bigl | s_tmp][stage]
+  static constexpr size_t kIdx = 0;
+  static constexpr size_t kPerm = kIdx + (size_t)CAP * 4;
+  static constexpr size_t kTail = kPerm + (REGS ? (size_t)CAP * 4 : 0);
+  static constexpr size_t kCnt = kTail + (size_t)CAP * 8;
+  static constexpr size_t kBigl = kCnt + (size_t)(BINS + 1) * 4;
+  static constexpr size_t kTmp = kBigl + (size_t)BINS * 4;
+  static constexpr size_t kReuseEnd = kTmp + 64 * 4;
+  static constexpr size_t kReuse = kReuseEnd - kTail;  // free once the bucket is sorted
+  static constexpr int GWARPS_REUSE = (int)(kReuse / kStageBytes);
+  static constexpr bool EXTRA_STAGE = GWARPS_REUSE < 2;  // tiny tiers: separate staging area
+  static constexpr int GWARPS = EXTRA_STAGE ? WARPS : (GWARPS_REUSE >= WARPS ? WARPS : GWARPS_REUSE);
+  static constexpr size_t kStage = EXTRA_STAGE ? kReuseEnd : kTail;
+  static constexpr size_t kBytes = EXTRA_STAGE ? kReuseEnd + (size_t)WARPS * kStageBytes : kReuseEnd;
+};
 
 // One CTA per bucket (len <= CAP), persistent over its list:
-//   1. load the bucket's (tail, idx) pairs (coalesced; kept in registers when CAP/THREADS <= 16,
+//   1. load the bucket's (tail, ordinal) pairs (coalesced; held in registers when CAP/THREADS <= 16,
 //      else re-read from L2),
-//   2. counting pass on the next `bits` unconsumed key bits (shared-memory atomics give each item its
-//      rank inside its sub-bucket), block scan of the 2^bits counters, placement into shared memory,
-//   3. comparison sort of every sub-bucket on the composite (tail, idx): insertion sort by one thread
-//      (tiny) or a warp bitonic network (larger) — Alg. 1's ComparisonSort below tinyBucketThreshold,
-//   4. perm[start + i] = idx of the i-th smallest, coalesced.
+//   2. counting pass on the next `bits` unconsumed bits of the composite key (shared-memory atomics give
+//      each item its rank inside its sub-bucket), block scan of the 2^bits counters, placement,
+//   3. exact rank inside every tiny sub-bucket (count of smaller composites; <= kd_insert_max), a warp
+//      bitonic network for larger ones — Alg. 1's ComparisonSort below tinyBucketThreshold,
+//   4. the bucket's records gathered into out[start, start+len) by the CTA's warps (see file header).
 template <uint32_t CAP, int THREADS>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 6)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                uint32_t* __restrict__ perm, Tunables tu) {
-  constexpr uint32_t BINS = kd_bins<CAP>();
-  constexpr int WARPS = THREADS / 32;
+                uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+  using L = KdLayout<CAP, THREADS>;
+  constexpr uint32_t BINS = L::BINS;
+  constexpr int WARPS = L::WARPS;
   constexpr int ITEMS = CAP / THREADS;
-  constexpr bool REGS = ITEMS <= 16;
+  constexpr bool REGS = L::REGS;
   constexpr int RITEMS = REGS ? ITEMS : 1;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + CAP);
-  uint32_t* s_cnt = s_idx + CAP;            // [BINS + 1]: counts, then exclusive starts
-  uint32_t* s_bigl = s_cnt + BINS + 1;      // [BINS]: sub-buckets needing the warp network
-  uint32_t* s_tmp = s_bigl + BINS;          // [32] scan tmp, [32] = number of big sub-buckets
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + L::kIdx);
+  uint32_t* s_perm = REGS ? reinterpret_cast<uint32_t*>(smem + L::kPerm) : s_idx;  // sorted ordinals
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem + L::kTail);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L::kCnt);    // [BINS + 1]: counts, then starts
+  uint32_t* s_bigl = reinterpret_cast<uint32_t*>(smem + L::kBigl);  // [BINS]: sub-buckets for the network
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem + L::kTmp);    // [32] scan tmp, [32] = #big
   uint32_t* s_nbig = s_tmp + 32;
+  uint8_t* s_stage = smem + L::kStage;                               // gather staging (reuses the sort area)
 
-  for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;
-  __syncthreads();
   const uint32_t nitems = *count;
   const int warp = threadIdx.x >> 5;
   for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;  // was gather staging
+    __syncthreads();
     const Seg sg = list[it];
     const uint32_t s = sg.len;
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
@@ -178,24 +258,22 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) {
-          rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
-        }
+        if (i < s) rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
       }
     } else {
       // batches of 8 independent loads per thread keep the bucket read latency-tolerant
-      for (uint32_t i0 = threadIdx.x; i0 < s; i0 += 8 * THREADS) {
+      for (uint32_t i0b = threadIdx.x; i0b < s; i0b += 8 * THREADS) {
         uint64_t tb[8];
         uint32_t xb[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t i = i0 + u * THREADS;
+          const uint32_t i = i0b + u * THREADS;
           tb[u] = i < s ? tp[i] : 0;
           xb[u] = (i < s && on_idx) ? ip[i] : 0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (i0 + u * THREADS < s) atomicAdd(&s_cnt[digit2(tb[u], xb[u])], 1u);
+          if (i0b + u * THREADS < s) atomicAdd(&s_cnt[digit2(tb[u], xb[u])], 1u);
       }
     }
     if (threadIdx.x == 0) *s_nbig = 0;
@@ -218,7 +296,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     __syncthreads();
     if (REGS) {
       // place, then every item finds its final rank inside its (tiny) sub-bucket by counting the
-      // smaller composites there, and writes its ordinal straight to perm.
+      // smaller composites there
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
@@ -236,13 +314,15 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
           const uint32_t d = digit2(tr[j], xr[j]);
           const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
           if (sz == 1) {
-            perm[sg.start + b] = xr[j];
+            s_perm[b] = xr[j];
           } else if (sz <= (uint32_t)tu.kd_insert_max) {
             uint32_t rank = 0;
-            for (uint32_t m = b; m < b + sz; ++m) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
-            perm[sg.start + b + rank] = xr[j];
+            const uint32_t self = b + rr[j];
+            for (uint32_t m = b; m < b + sz; ++m)
+              if (m != self) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
+            s_perm[b + rank] = xr[j];
           } else if (rr[j] == 0) {
-            s_bigl[atomicAdd(s_nbig, 1u)] = digit2(tr[j], xr[j]);
+            s_bigl[atomicAdd(s_nbig, 1u)] = d;
           }
         }
       }
@@ -252,86 +332,86 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
         const uint32_t g = s_bigl[q];
         const uint32_t b = s_cnt[g], e = s_cnt[g + 1];
         warp_bitonic_smem(s_tail, s_idx, b, e);
-        for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) perm[sg.start + i] = s_idx[i];
+        for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) s_perm[i] = s_idx[i];
       }
-      __syncthreads();  // every warp is done reading the sub-bucket bounds before they are cleared
-      for (uint32_t g = threadIdx.x; g <= nb; g += THREADS) s_cnt[g] = 0;
+    } else {
+      // ---- large-CAP path: elements re-read from L2, placed by a second counter pass
+      for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_bigl[g] = 0;
       __syncthreads();
-      continue;
-    }
-    // ---- large-CAP path: elements re-read from L2, placed by a second counter pass
-    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) s_bigl[g] = 0;
-    __syncthreads();
-    for (uint32_t i0 = threadIdx.x; i0 < s; i0 += 8 * THREADS) {
-      uint64_t tb[8];
-      uint32_t xb[8];
+      for (uint32_t i0b = threadIdx.x; i0b < s; i0b += 8 * THREADS) {
+        uint64_t tb[8];
+        uint32_t xb[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t i = i0 + u * THREADS;
-        if (i < s) {
-          tb[u] = tp[i];
-          xb[u] = ip[i];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (i0 + u * THREADS < s) {
-          const uint32_t d = digit2(tb[u], xb[u]);
-          const uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
-          s_tail[p] = tb[u];
-          s_idx[p] = xb[u];
-        }
-      }
-    }
-    __syncthreads();
-    // comparison sort of every sub-bucket
-    for (uint32_t g = threadIdx.x; g < nb; g += THREADS) {
-      uint32_t b = s_cnt[g], e = s_cnt[g + 1];
-      uint32_t sz = e - b;
-      if (sz <= 1) continue;
-      if (sz <= (uint32_t)tu.kd_insert_max) {
-        for (uint32_t i = b + 1; i < e; ++i) {
-          uint64_t t = s_tail[i];
-          uint32_t x = s_idx[i];
-          uint32_t j = i;
-          while (j > b && pair_less(t, x, s_tail[j - 1], s_idx[j - 1])) {
-            s_tail[j] = s_tail[j - 1];
-            s_idx[j] = s_idx[j - 1];
-            --j;
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t i = i0b + u * THREADS;
+          if (i < s) {
+            tb[u] = tp[i];
+            xb[u] = ip[i];
           }
-          s_tail[j] = t;
-          s_idx[j] = x;
         }
-      } else {
-        s_bigl[atomicAdd(s_nbig, 1u)] = g;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0b + u * THREADS < s) {
+            const uint32_t d = digit2(tb[u], xb[u]);
+            const uint32_t p = s_cnt[d] + atomicAdd(&s_bigl[d], 1u);
+            s_tail[p] = tb[u];
+            s_idx[p] = xb[u];
+          }
+        }
+      }
+      __syncthreads();
+      // comparison sort of every sub-bucket, in place
+      for (uint32_t g = threadIdx.x; g < nb; g += THREADS) {
+        uint32_t b = s_cnt[g], e = s_cnt[g + 1];
+        uint32_t sz = e - b;
+        if (sz <= 1) continue;
+        if (sz <= (uint32_t)tu.kd_insert_max) {
+          for (uint32_t i = b + 1; i < e; ++i) {
+            uint64_t t = s_tail[i];
+            uint32_t x = s_idx[i];
+            uint32_t j = i;
+            while (j > b && pair_less(t, x, s_tail[j - 1], s_idx[j - 1])) {
+              s_tail[j] = s_tail[j - 1];
+              s_idx[j] = s_idx[j - 1];
+              --j;
+            }
+            s_tail[j] = t;
+            s_idx[j] = x;
+          }
+        } else {
+          s_bigl[atomicAdd(s_nbig, 1u)] = g;
+        }
+      }
+      __syncthreads();
+      const uint32_t nbig = *s_nbig;
+      for (uint32_t q = warp; q < nbig; q += WARPS) {
+        uint32_t g = s_bigl[q];
+        warp_bitonic_smem(s_tail, s_idx, s_cnt[g], s_cnt[g + 1]);
       }
     }
-    __syncthreads();
-    const uint32_t nbig = *s_nbig;
-    for (uint32_t q = warp; q < nbig; q += WARPS) {
-      uint32_t g = s_bigl[q];
-      warp_bitonic_smem(s_tail, s_idx, s_cnt[g], s_cnt[g + 1]);
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_idx[i];
-    for (uint32_t g = threadIdx.x; g <= nb; g += THREADS) s_cnt[g] = 0;
-    __syncthreads();
+    __syncthreads();  // sorted ordinals complete; the sort area is free for the gather staging
+    if (perm)
+      for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
+    if (warp < L::GWARPS)
+      warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in,
+                  out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes);
+    __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
 }
 
 template <uint32_t CAP, int THREADS>
 cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                             const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                            cudaStream_t s) {
+                            const uint8_t* in, uint8_t* out, cudaStream_t s) {
   auto kern = kd_cta_sort<CAP, THREADS>;
-  const size_t smem = kd_smem<CAP>();
+  const size_t smem = KdLayout<CAP, THREADS>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu);
+  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out);
   if (getenv("LEY_DEBUG_SYNC")) {
     fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
     cudaError_t e2 = cudaStreamSynchronize(s);
@@ -348,22 +428,27 @@ cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B1
   return cudaGetLastError();
 }
 
-// All K-d tiers for the lists of one level (counts are read on the device; no host sync).
+// All K-d/K-e tiers for the lists of one level (counts are read on the device; no host sync).
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
-                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, cudaStream_t s,
-                          int* launches) {
+                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
+                          uint8_t* out, cudaStream_t s, int* launches) {
   cudaError_t e;
-  kd_warp_sort<<<sms * 8, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm);
+  kd_warp_sort<<<sms * 4, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in, out);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
+                                     out, s)))
     return e;
-  if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
+                                      out, s)))
     return e;
-  if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
+                                      out, s)))
     return e;
-  if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
+                                        in, out, s)))
     return e;
-  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms, s)))
+  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
+                                       in, out, s)))
     return e;
   if (launches) *launches += 6;
   return cudaSuccess;
