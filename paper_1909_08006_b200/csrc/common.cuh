@@ -106,6 +106,36 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, u
   return r;
 }
 
+// Block-wide exclusive max-scan of one u32 per thread (identity 0). `tmp` holds >= 32 words.
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* tmp) {
+  constexpr int WARPS = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x = max(x, y);
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w = max(w, y);
+    }
+    if (lane < WARPS) tmp[lane] = w;  // inclusive per-warp maxima
+  }
+  __syncthreads();
+  uint32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
+  uint32_t r = lane ? prev : 0u;
+  if (warp) r = max(r, tmp[warp - 1]);
+  __syncthreads();
+  return r;
+}
+
 // Composite (key-tail, ordinal) order: the strict total order of the sort.
 __device__ __forceinline__ bool pair_less(uint64_t ta, uint32_t ia, uint64_t tb, uint32_t ib) {
   return ta < tb || (ta == tb && ia < ib);

@@ -126,29 +126,44 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t R = t1 - t0 + 1;
     const uint32_t* off_b = off + (uint64_t)b * tiles;
     const bool table = R <= kMaxRuns / 2;
+    uint32_t src[kItems];  // position of each element in K-a's output
     if (table) {
+      // run table (virtual start, source base: src = base + v) and run-start marks; an inclusive
+      // max-scan of the marks gives every element of the chunk its run without any search
+      uint16_t* s_mark = reinterpret_cast<uint16_t*>(s_off + kMaxRuns / 2);
+      for (uint32_t e = threadIdx.x; e < cnt; e += kThreads) s_mark[e] = 0;
       for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
-        s_off[i] = off_b[t0 + i];
-        s_lo[i] = lo[(uint64_t)(t0 + i) * kRadix + b];
+        const uint32_t vs = off_b[t0 + i];
+        s_off[i] = vs;
+        s_lo[i] = ((t0 + i) << kTileLog2) + lo[(uint64_t)(t0 + i) * kRadix + b] - vs;
       }
-    }
-    __syncthreads();
-
-    // ---- gather the chunk's pairs (element order = virtual order = stable order)
-    uint32_t src[kItems];
-    if (table) {
-      uint32_t r = 0;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
+        const uint32_t vs = s_off[i], ve = (i + 1 < R) ? s_off[i + 1] : off_b[t1 + 1];
+        const uint32_t e = vs > v0 ? vs - v0 : 0u;
+        if (ve > vs && e < cnt) s_mark[e] = (uint16_t)i;
+      }
+      __syncthreads();
+      {
+        constexpr int PER = kChunk / kThreads;  // 8 consecutive marks per thread
+        const uint32_t e0 = threadIdx.x * PER;
+        uint32_t m[PER], run = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          m[q] = e0 + q < cnt ? s_mark[e0 + q] : 0u;
+          run = max(run, m[q]);
+          m[q] = run;
+        }
+        const uint32_t pre = block_excl_max<kThreads>(run, s_misc);
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (e0 + q < cnt) s_mark[e0 + q] = (uint16_t)max(pre, m[q]);
+      }
+      __syncthreads();
 #pragma unroll
       for (int j = 0; j < kItems; ++j) {
         uint32_t e = warp * (32 * kItems) + j * 32 + lane;
-        uint32_t v = v0 + e;
-        src[j] = 0;
-        if (e < cnt) {
-          if (j == 0) r = search_le(s_off, 0, R, v);
-          else
-            while (r + 1 < R && s_off[r + 1] <= v) ++r;
-          src[j] = ((t0 + r) << kTileLog2) + s_lo[r] + (v - s_off[r]);
-        }
+        src[j] = e < cnt ? s_lo[s_mark[e]] + v0 + e : 0u;
       }
     } else {  // very sparse bucket: search the global run table directly
 #pragma unroll
