@@ -13,25 +13,38 @@
 
 namespace ley {
 
-__device__ __forceinline__ void classify_bucket(const Seg& s, const Tunables& tu, const ListSet& kd, Seg* big_out,
-                                                uint32_t* big_count) {
-  if (s.len == 0) return;
-  int list;
-  if (s.len <= tu.warp_tier_max) {
-    list = kListWarp;
-  } else if (s.len <= tu.smem_tier_max) {
-    list = s.len <= 512    ? kListMed1
-           : s.len <= 2048 ? kListMed2
-           : s.len <= 8192 ? kListMed3
-           : s.len <= 10240 ? kListMed4
-                            : kListMed5;
-  } else {
-    uint32_t slot = atomicAdd(big_count, 1u);
-    big_out[slot] = s;
-    return;
+__device__ __forceinline__ int tier_of(uint32_t len, const Tunables& tu) {
+  if (len <= tu.warp_tier_max) return kListWarp;
+  if (len <= tu.smem_tier_max)
+    return len <= 512 ? kListMed1 : len <= 2048 ? kListMed2 : len <= 8192 ? kListMed3 : len <= 10240 ? kListMed4 : kListMed5;
+  return kNumKdLists;  // big: recurse
+}
+
+// Block-wide classification (every thread of the CTA must call it; `valid` marks threads holding a bucket):
+// list appends are aggregated per warp (match.any) and per CTA (shared counters), so each list costs one
+// global atomic per CTA instead of one per bucket — buckets of one level number up to 256 x #segments.
+// s_cnt: >= 16 u32 of shared memory.
+__device__ __forceinline__ void classify_block(const Seg& s, bool valid, const Tunables& tu, const ListSet& kd,
+                                               Seg* big_out, uint32_t* big_count, uint32_t* s_cnt) {
+  const int list = (valid && s.len) ? tier_of(s.len, tu) : -1;
+  if (threadIdx.x < 16) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t peers = __match_any_sync(0xffffffffu, list);
+  const int leader = __ffs(peers) - 1;
+  const uint32_t rank = __popc(peers & lanemask_lt());
+  uint32_t wbase = 0;
+  if (list >= 0 && rank == 0) wbase = atomicAdd(&s_cnt[list], (uint32_t)__popc(peers));
+  wbase = __shfl_sync(0xffffffffu, wbase, leader);
+  __syncthreads();
+  if (threadIdx.x <= kNumKdLists && s_cnt[threadIdx.x])
+    s_cnt[8 + threadIdx.x] =
+        atomicAdd(threadIdx.x == kNumKdLists ? big_count : &kd.counts[threadIdx.x], s_cnt[threadIdx.x]);
+  __syncthreads();
+  if (list >= 0) {
+    const uint32_t slot = s_cnt[8 + list] + wbase + rank;
+    if (list == kNumKdLists) big_out[slot] = s;
+    else kd.items[list][slot] = s;
   }
-  uint32_t slot = atomicAdd(&kd.counts[list], 1u);
-  kd.items[list][slot] = s;
 }
 
 }  // namespace ley

@@ -16,15 +16,24 @@ constexpr uint32_t kTileLog2 = 12;
 static_assert((1u << kTileLog2) == kTileRecords, "tile must be a power of two");
 
 // K-c / K-c' chunk: THREADS x ITEMS (key-tail, index) pairs.
-constexpr int kSplitThreads = 512;
-constexpr int kSplitItems = 8;
+#ifndef LEY_SPLIT_THREADS
+#define LEY_SPLIT_THREADS 512
+#define LEY_SPLIT_ITEMS 8
+#define LEY_SPLIT_MINB 2
+#endif
+constexpr int kSplitThreads = LEY_SPLIT_THREADS;
+constexpr int kSplitItems = LEY_SPLIT_ITEMS;
+constexpr int kSplitMinBlocks = LEY_SPLIT_MINB;
 constexpr uint32_t kChunk = kSplitThreads * kSplitItems;  // 4096
 
 constexpr int kRadix = 256;
 
 // K-a accumulates hist16 into kHistCopies copies (CTA t -> copy t % kHistCopies) so skewed keys do not
 // serialise on a few L2 atomic addresses; K-b sums the copies.
-constexpr int kHistCopies = 16;
+#ifndef LEY_HIST_COPIES
+#define LEY_HIST_COPIES 16
+#endif
+constexpr int kHistCopies = LEY_HIST_COPIES;
 
 // K-b block tile
 constexpr int kScanThreads = 256;

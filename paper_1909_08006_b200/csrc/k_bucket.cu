@@ -76,10 +76,10 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
 
 __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
                                    Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= 65536) return;
-  Seg s{B16[p], hist16[p], 2u, 1u};
-  classify_bucket(s, tu, kd, big_out, big_count);
+  __shared__ uint32_t s_cnt[16];
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers exactly 65536 buckets
+  const Seg s{B16[p], hist16[p], 2u, 1u};
+  classify_block(s, true, tu, kd, big_out, big_count, s_cnt);
 }
 
 // ---------------------------------------------------------------------------- warp tier (len <= 32)
@@ -185,10 +185,11 @@ struct KdLayout {
   static constexpr size_t kReuseEnd = kTmp + 64 * 4;
   static constexpr size_t kReuse = kReuseEnd - kTail;  // free once the bucket is sorted
   static constexpr int GWARPS_REUSE = (int)(kReuse / kStageBytes);
-  static constexpr bool EXTRA_STAGE = GWARPS_REUSE < 2;  // tiny tiers: separate staging area
+  static constexpr bool EXTRA_STAGE = GWARPS_REUSE < WARPS;  // small tiers: every warp gets its own stage
   static constexpr int GWARPS = EXTRA_STAGE ? WARPS : (GWARPS_REUSE >= WARPS ? WARPS : GWARPS_REUSE);
-  static constexpr size_t kStage = EXTRA_STAGE ? kReuseEnd : kTail;
-  static constexpr size_t kBytes = EXTRA_STAGE ? kReuseEnd + (size_t)WARPS * kStageBytes : kReuseEnd;
+  static constexpr size_t kStage = EXTRA_STAGE ? (kReuseEnd + 127) & ~size_t(127) : kTail;  // cp.async: 16-B aligned
+  static constexpr size_t kBytes = EXTRA_STAGE ? kStage + (size_t)WARPS * kStageBytes : kReuseEnd;
+  static_assert(kStage % 16 == 0, "gather staging must be 16-byte aligned");
 };
 
 // One CTA per bucket (len <= CAP), persistent over its list:
@@ -200,7 +201,7 @@ struct KdLayout {
 //      bitonic network for larger ones — Alg. 1's ComparisonSort below tinyBucketThreshold,
 //   4. the bucket's records gathered into out[start, start+len) by the CTA's warps (see file header).
 template <uint32_t CAP, int THREADS>
-__global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 6)
+__global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 8)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                 uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {

@@ -82,7 +82,7 @@ __global__ void kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles,
 
 constexpr uint32_t kMaxRuns = (uint32_t)((kChunk * 13 + 16) / 8);  // run table fits the staging region
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
     kc_split_level1(const uint64_t* __restrict__ k1_in, const uint32_t* __restrict__ w_in, uint32_t tiles,
                     const uint32_t* __restrict__ off /*[256*tiles+1]*/, const uint32_t* __restrict__ lo,
                     const uint32_t* __restrict__ B16, const uint32_t* __restrict__ cstart,
@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(256)
             uint32_t* __restrict__ seg_excl, uint8_t* __restrict__ noscatter, Tunables tu, ListSet kd,
             Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
   __shared__ uint32_t s_tmp[32];
+  __shared__ uint32_t s_cnt[16];
   __shared__ uint32_t s_single;
   const uint32_t s = blockIdx.x;
   const Seg sg = segs[s];
@@ -286,22 +287,14 @@ __global__ void __launch_bounds__(256)
   if (h == sg.len) s_single = 1;  // one digit holds the whole bucket: nothing to move
   uint32_t ex = block_excl_scan<256>(h, s_tmp, nullptr);
   seg_excl[(uint64_t)s * kRadix + d] = ex;
-  if (s_single) {
-    if (d == 0) {
-      noscatter[s] = 1;
-      Seg ch{sg.start, sg.len, sg.depth + 1, sg.parity};
-      classify_bucket(ch, tu, kd, big_out, big_count);
-    }
-  } else {
-    if (d == 0) noscatter[s] = 0;
-    if (h) {
-      Seg ch{sg.start + ex, h, sg.depth + 1, sg.parity ^ 1u};
-      classify_bucket(ch, tu, kd, big_out, big_count);
-    }
-  }
+  const bool single = s_single != 0;
+  if (d == 0) noscatter[s] = single ? 1 : 0;
+  const Seg ch = single ? Seg{sg.start, sg.len, sg.depth + 1, sg.parity}
+                        : Seg{sg.start + ex, h, sg.depth + 1, sg.parity ^ 1u};
+  classify_block(ch, single ? d == 0 : h != 0, tu, kd, big_out, big_count, s_cnt);
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
     kr_split(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart,
              uint32_t* __restrict__ cursor, const uint8_t* __restrict__ noscatter, uint64_t* tails0, uint32_t* idx0,
              uint64_t* tails1, uint32_t* idx1, uint32_t* __restrict__ ticket) {

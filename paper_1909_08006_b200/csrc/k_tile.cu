@@ -23,6 +23,12 @@
 namespace ley {
 namespace {
 
+__device__ __forceinline__ uint32_t ld_ef_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles,
                                                          uint64_t* __restrict__ k1_out, uint32_t* __restrict__ w_out,
@@ -44,6 +50,11 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
   for (int i = threadIdx.x; i < WARPS * kRadix; i += THREADS) s_wh[i] = 0;
   uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
 
+  // L2 policies: the record lines are read once (evict first — measured: without it ~25% of them are
+  // fetched twice, 128 vs 103 B/record of DRAM reads at C2); the hist16 copies are hot (evict last).
+  uint64_t pol_ef, pol_el;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
   // ---- 1. load keys (all loads issued before use)
   uint32_t a[ITEMS], b[ITEMS], c[ITEMS];
 #pragma unroll
@@ -51,9 +62,9 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
     uint32_t r = warp * (32 * ITEMS) + j * 32 + lane;
     if (r < cnt_t) {
       const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (base + r) * kRecordBytes);
-      a[j] = __ldg(p);
-      b[j] = __ldg(p + 1);
-      c[j] = __ldg(p + 2);
+      a[j] = ld_ef_u32(p, pol_ef);
+      b[j] = ld_ef_u32(p + 1, pol_ef);
+      c[j] = ld_ef_u32(p + 2, pol_ef);
     } else {
       a[j] = b[j] = c[j] = 0;
     }
@@ -80,7 +91,9 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
     // level-1 bucket sizes: 16-bit prefix (bytes 0..1)
     uint32_t p16 = hi >> 16;
     uint32_t peers16 = peers & warp_peers8((hi >> 16) & 0xFFu, valid);
-    if (valid && __popc(peers16 & lt) == 0) atomicAdd(&hist_copy[p16], (uint32_t)__popc(peers16));
+    if (valid && __popc(peers16 & lt) == 0)
+      asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(&hist_copy[p16]),
+                   "r"((uint32_t)__popc(peers16)), "l"(pol_el) : "memory");
   }
   __syncthreads();
 

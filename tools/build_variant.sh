@@ -10,6 +10,6 @@ cd $T/csrc
 for f in *.cu; do nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I$ROOT/include -I. -I$NCCL/include -Xcompiler -fPIC --expt-relaxed-constexpr $FLAGS -c $f -o $f.o 2>/dev/null & done
 for f in *.cpp; do g++ -O3 -std=c++17 -fPIC -I$ROOT/include -I. -I/usr/local/cuda/include -I$NCCL/include -c $f -o $f.o & done
 wait
-mkdir -p $ROOT/variants
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/variants/libley_$NAME.so *.o -L$NCCL/lib -l:libnccl.so.2 -Xlinker -rpath,$NCCL/lib
-echo built variants/libley_$NAME.so
+mkdir -p $ROOT/vlib
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/vlib/libley_$NAME.so *.o -L$NCCL/lib -l:libnccl.so.2 -Xlinker -rpath,$NCCL/lib
+echo built vlib/libley_$NAME.so

@@ -91,6 +91,95 @@ __global__ void mb_copy(const uint4* __restrict__ in, uint4* __restrict__ out, u
     __stcs(out + i, __ldcs(in + i));
 }
 
+
+// gather variant: mode bit0 = L1-cached 16-B loads (ld.global.v4) instead of cp.async.cg;
+// bit1 = blocked assignment (CTA c handles output groups [c*chunk_groups, (c+1)*chunk_groups) per round)
+__global__ void __launch_bounds__(256) mb_gather2(const uint8_t* __restrict__ in, const uint32_t* __restrict__ perm,
+                                                  uint8_t* __restrict__ out, uint64_t n, int mode, uint32_t chunk_groups) {
+  __shared__ __align__(16) uint8_t stage[8][32 * kWin];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t ss = (uint32_t)__cvta_generic_to_shared(stage[w]);
+  const uint64_t ngroups = (n + 31) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * 8;
+  for (uint64_t it = (uint64_t)blockIdx.x * 8 + w;; it += nw) {
+    uint64_t g;
+    if (mode & 2) {
+      // blocked: round r = it / nw covers gridDim.x * chunk_groups groups; CTA c its chunk
+      const uint64_t r = it / nw, c = blockIdx.x;
+      const uint64_t k = (it % nw) - c * 8;  // 0..7 : warp index in CTA
+      (void)k;
+      const uint64_t base = r * gridDim.x * (uint64_t)chunk_groups + c * chunk_groups;
+      // each warp loops over its share of the CTA chunk inside this round
+      bool any = false;
+      for (uint32_t q = w; q < chunk_groups; q += 8) {
+        g = base + q;
+        if (g >= ngroups) break;
+        any = true;
+        const uint64_t j0 = g * 32;
+        const uint32_t cnt = (uint32_t)min((uint64_t)32, n - j0);
+        const uint32_t p = lane < (int)cnt ? perm[j0 + lane] : 0u;
+        if (mode & 1) {
+          for (int qq = 0; qq < 7; ++qq) {
+            const int ci = qq * 32 + lane, rr = ci / 7, cc = ci - rr * 7;
+            const uint32_t pr = __shfl_sync(0xffffffffu, p, rr);
+            if (rr < (int)cnt)
+              *reinterpret_cast<uint4*>(stage[w] + rr * kWin + cc * 16) =
+                  *reinterpret_cast<const uint4*>(in + (((uint64_t)pr * 100) & ~15ull) + cc * 16);
+          }
+        } else {
+          for (int qq = 0; qq < 7; ++qq) {
+            const int ci = qq * 32 + lane, rr = ci / 7, cc = ci - rr * 7;
+            const uint32_t pr = __shfl_sync(0xffffffffu, p, rr);
+            if (rr < (int)cnt) cp_async16(ss + rr * kWin + cc * 16, in + (((uint64_t)pr * 100) & ~15ull) + cc * 16);
+          }
+          cp_async_wait_all();
+        }
+        __syncwarp();
+        uint32_t* dst = reinterpret_cast<uint32_t*>(out + j0 * 100);
+        for (uint32_t x = lane; x < cnt * 25; x += 32) {
+          const uint32_t r2 = x / 25, o = x - r2 * 25;
+          const uint32_t pr = __shfl_sync(__activemask(), p, r2);
+          dst[x] = *reinterpret_cast<const uint32_t*>(stage[w] + r2 * kWin + ((pr * 4u) & 15u) + 4 * o);
+        }
+        __syncwarp();
+      }
+      if (!any) return;
+      continue;
+    }
+    g = it;
+    if (g >= ngroups) return;
+    const uint64_t j0 = g * 32;
+    const uint32_t cnt = (uint32_t)min((uint64_t)32, n - j0);
+    const uint32_t p = lane < (int)cnt ? perm[j0 + lane] : 0u;
+    if (mode & 1) {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const int ci = q * 32 + lane, r = ci / 7, c = ci - r * 7;
+        const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
+        if (r < (int)cnt)
+          *reinterpret_cast<uint4*>(stage[w] + r * kWin + c * 16) =
+              *reinterpret_cast<const uint4*>(in + (((uint64_t)pr * 100) & ~15ull) + c * 16);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const int ci = q * 32 + lane, r = ci / 7, c = ci - r * 7;
+        const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
+        if (r < (int)cnt) cp_async16(ss + r * kWin + c * 16, in + (((uint64_t)pr * 100) & ~15ull) + c * 16);
+      }
+      cp_async_wait_all();
+    }
+    __syncwarp();
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + j0 * 100);
+    for (uint32_t x = lane; x < cnt * 25; x += 32) {
+      const uint32_t r = x / 25, o = x - r * 25;
+      const uint32_t pr = __shfl_sync(__activemask(), p, r);
+      dst[x] = *reinterpret_cast<const uint32_t*>(stage[w] + r * kWin + ((pr * 4u) & 15u) + 4 * o);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -102,6 +191,7 @@ int mb_run(int which, const void* in, void* out, const uint32_t* idx, uint32_t* 
     case 2: mb_scatter_idx<<<grid, 256, 0, s>>>(idx, idx_out, n); break;
     case 3: mb_keys<<<grid, 256, 0, s>>>((const uint8_t*)in, idx_out, n); break;
     case 4: mb_copy<<<grid, 256, 0, s>>>((const uint4*)in, (uint4*)out, n * 100 / 16); break;
+    default: mb_gather2<<<grid, 256, 0, s>>>((const uint8_t*)in, idx, (uint8_t*)out, n, (which - 10) & 3, (uint32_t)((which - 10) >> 2)); break;
   }
   return (int)cudaGetLastError();
 }

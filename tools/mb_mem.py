@@ -89,3 +89,14 @@ for w in (24_576, 393_216, 1_572_864):
     rep(f"gather window {w * 100 / 1e6:.1f}MB", t(0, pw, g), 204)
     rep(f"scatter window {w * 100 / 1e6:.1f}MB", t(1, inverse(pw), g), 204)
     del pw
+
+# L2-reuse study: which = 10 + mode + 4 * chunk_groups (mode bit0 L1 loads, bit1 blocked CTA chunks)
+if "l2" in only:
+    for w in (32, 256, 4096, 24_576):
+        pw = win_perm(w)
+        for mode in (0, 1):
+            rep(f"gather2 m{mode} window {w}", t(10 + mode, pw, g), 204)
+        if w >= 256:
+            for mode in (2, 3):
+                rep(f"gather2 m{mode} blocked window {w}", t(10 + mode + 4 * (w // 32), pw, g), 204)
+        del pw
