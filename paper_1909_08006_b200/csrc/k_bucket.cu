@@ -74,6 +74,8 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
   }
 }
 
+constexpr int kGatherStages = 1;  // groups in flight per gathering warp
+
 __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
                                    Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
   __shared__ uint32_t s_cnt[16];
@@ -183,13 +185,17 @@ struct KdLayout {
   static constexpr size_t kBigl = kCnt + (size_t)(BINS + 1) * 4;
   static constexpr size_t kTmp = kBigl + (size_t)BINS * 4;
   static constexpr size_t kReuseEnd = kTmp + 64 * 4;
-  static constexpr size_t kReuse = kReuseEnd - kTail;  // free once the bucket is sorted
-  static constexpr int GWARPS_REUSE = (int)(kReuse / kStageBytes);
-  static constexpr bool EXTRA_STAGE = GWARPS_REUSE < WARPS;  // small tiers: every warp gets its own stage
-  static constexpr int GWARPS = EXTRA_STAGE ? WARPS : (GWARPS_REUSE >= WARPS ? WARPS : GWARPS_REUSE);
-  static constexpr size_t kStage = EXTRA_STAGE ? (kReuseEnd + 127) & ~size_t(127) : kTail;  // cp.async: 16-B aligned
-  static constexpr size_t kBytes = EXTRA_STAGE ? kStage + (size_t)WARPS * kStageBytes : kReuseEnd;
+  // gather staging: every warp gets kGatherStages groups, overlapping the sort area (free once the bucket
+  // is sorted) and extending past it where the sort area is smaller
+  static constexpr size_t kWarpStage = (size_t)kGatherStages * kStageBytes;
+  static constexpr size_t kSmemMax = 227 * 1024 - 1024;  // dynamic; leaves room for the static mbarriers
+  static constexpr int GWARPS_FIT = (int)((kSmemMax - kTail) / kWarpStage);
+  static constexpr int GWARPS = GWARPS_FIT < WARPS ? GWARPS_FIT : WARPS;
+  static constexpr size_t kStage = kTail;
+  static constexpr size_t kStageEnd = kStage + (size_t)GWARPS * kWarpStage;
+  static constexpr size_t kBytes = kStageEnd > kReuseEnd ? kStageEnd : kReuseEnd;
   static_assert(kStage % 16 == 0, "gather staging must be 16-byte aligned");
+  static_assert(GWARPS >= 1 && kBytes <= kSmemMax, "K-de tier does not fit shared memory");
 };
 
 // One CTA per bucket (len <= CAP), persistent over its list:

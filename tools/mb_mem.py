@@ -100,3 +100,25 @@ if "l2" in only:
             for mode in (2, 3):
                 rep(f"gather2 m{mode} blocked window {w}", t(10 + mode + 4 * (w // 32), pw, g), 204)
         del pw
+
+if "g3" in only:
+    for grid_mult in (4, 8):
+        rep(f"gather cp.async x{grid_mult}/SM", t(0, perm, sms * grid_mult), 204)
+    for grid_mult in (2, 4, 6, 8):
+        rep(f"gather reg x{grid_mult}/SM", t(5, perm, sms * grid_mult), 204)
+    rep("gather bulk S2 x3/SM", t(6, perm, sms * 3), 204)
+    rep("gather bulk S2 x2/SM", t(6, perm, sms * 2), 204)
+    rep("gather bulk S3 x2/SM", t(8, perm, sms * 2), 204)
+    rep("gather bulk S4 x1/SM", t(7, perm, sms * 1), 204)
+
+if "g4" in only:
+    rep("gather cp.async x8/SM", t(0, perm, sms * 8), 204)
+    rep("gather bulk S2 x3/SM", t(6, perm, sms * 3), 204)
+    # TMA-store variant: smem per CTA = 8 x (S x 3584 + 6400)
+    for st, mults in ((1, (2, 4)), (2, (2, 3)), (3, (2,))):
+        for m in mults:
+            rep(f"gather tma S{st} x{m}/SM", t(19 + st, perm, sms * m), 204)
+    # correctness of the tma variant: compare with the plain gather
+    t(0, perm, sms * 8, reps=1); ref = out.clone()
+    t(21, perm, sms * 2, reps=1)
+    print("tma variant matches:", bool(torch.equal(ref, out)))
