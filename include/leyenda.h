@@ -72,6 +72,26 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
                          uint32_t record_bytes, uint32_t key_bytes, uint64_t device_budget_bytes,
                          void* stream);
 
+/* ---------------------------------------------------------------- streaming host sort
+ * ley_sort_submit — enqueue the staged-internal sort of PINNED HOST records (in -> out, same layout and
+ *   result as ley_sort) and return once the sort itself is done, WITHOUT waiting for the output's
+ *   device->host copy. Consecutive submits on the current device form a pipeline over two device
+ *   staging slots and three internal streams: the H2D of call k+1 overlaps the D2H of call k (the two
+ *   copy engines), so a stream of sorts is bound by max(H2D, D2H) per call instead of their sum (the
+ *   reader/sorter/writer overlap of P:116-118).
+ *   in, out, n_records, record_bytes, key_bytes: as ley_sort; both pointers must be pinned host memory
+ *     (else LEY_ERR_UNSUPPORTED). `in` must stay unmodified, and `out` is complete, only after
+ *     ley_sort_drain(). `stream` orders the start: the H2D waits for work already enqueued on it; the
+ *     caller's stream is NOT made to wait for the output (that would serialise consecutive calls).
+ *   device_budget_bytes: 0 = no cap. If two slots (4 x n_records x 100 bytes) plus the internal scratch
+ *     do not fit the cap, the call runs the blocking ley_sort instead (which may take the external path).
+ *   Ownership: the library owns the slots (freed by ley_release_cache). Errors as ley_sort; on error the
+ *   pipeline state of earlier calls is unaffected.
+ * ley_sort_drain — block until every submitted sort on the current device has landed in its `out`. */
+ley_status ley_sort_submit(const void* in, void* out, uint64_t n_records, uint32_t record_bytes,
+                           uint32_t key_bytes, uint64_t device_budget_bytes, void* stream);
+ley_status ley_sort_drain(void);
+
 /* Stage-tagged message for the last failing call on this thread ("" if none). Valid until the next
  * call on this thread. */
 const char* ley_last_error(void);

@@ -41,7 +41,8 @@ MAX_RECORDS = 0xFFFFFFFE
 EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get_unique_id", "ley_comm_init",
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
                     "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
-                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange")
+                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange",
+                    "ley_sort_submit", "ley_sort_drain")
 
 
 class ley_plan_info(ctypes.Structure):
@@ -56,6 +57,10 @@ _lib.ley_sort.argtypes = [_vp, _vp, _u64, _u32, _u32, _u64, _vp]
 _lib.ley_sort.restype = _i32
 _lib.ley_sort_perm.argtypes = [_vp, _vp, _vp, _u64, _u32, _u32, _u64, _vp]
 _lib.ley_sort_perm.restype = _i32
+_lib.ley_sort_submit.argtypes = [_vp, _vp, _u64, _u32, _u32, _u64, _vp]
+_lib.ley_sort_submit.restype = _i32
+_lib.ley_sort_drain.argtypes = []
+_lib.ley_sort_drain.restype = _i32
 _lib.ley_last_error.argtypes = []
 _lib.ley_last_error.restype = ctypes.c_char_p
 _lib.ley_comm_get_unique_id.argtypes = [_vp]
@@ -132,6 +137,19 @@ def ley_sort(in_, out, n_records: int, record_bytes: int = RECORD_BYTES, key_byt
     """C: ley_sort(in, out, n_records, record_bytes, key_bytes, device_budget_bytes, stream)."""
     st = _lib.ley_sort(_addr(in_), _addr(out), n_records, record_bytes, key_bytes, device_budget_bytes, _stream(stream))
     return _check(st, "ley_sort", raise_on_error)
+
+
+def ley_sort_submit(in_, out, n_records: int, record_bytes: int = RECORD_BYTES, key_bytes: int = KEY_BYTES,
+                    device_budget_bytes: int = 0, stream=None, raise_on_error: bool = True) -> int:
+    """C: ley_sort_submit(in, out, n_records, ...): pipelined sort of pinned host records (see leyenda.h)."""
+    st = _lib.ley_sort_submit(_addr(in_), _addr(out), n_records, record_bytes, key_bytes, device_budget_bytes,
+                              _stream(stream))
+    return _check(st, "ley_sort_submit", raise_on_error)
+
+
+def ley_sort_drain(raise_on_error: bool = True) -> int:
+    """C: ley_sort_drain(): wait for every submitted sort on the current device."""
+    return _check(_lib.ley_sort_drain(), "ley_sort_drain", raise_on_error)
 
 
 def ley_sort_perm(in_, out, perm, n_records: int, record_bytes: int = RECORD_BYTES, key_bytes: int = KEY_BYTES,

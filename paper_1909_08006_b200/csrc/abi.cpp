@@ -208,6 +208,52 @@ ley_status ley_sort(const void* in, void* out, uint64_t n_records, uint32_t reco
   return ley_sort_perm(in, out, nullptr, n_records, record_bytes, key_bytes, device_budget_bytes, stream);
 }
 
+ley_status ley_sort_submit(const void* in, void* out, uint64_t n_records, uint32_t record_bytes, uint32_t key_bytes,
+                           uint64_t device_budget_bytes, void* stream) {
+  clear_error();
+  record_launches(0);
+  ley_status st = check_common(in, out, nullptr, n_records, record_bytes, key_bytes);
+  if (st || n_records == 0) return st;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("validate: no CUDA device");
+    return LEY_ERR_CUDA;
+  }
+  Kind kin, kout;
+  if ((st = classify_ptr(in, dev, &kin, "in"))) return st;
+  if ((st = classify_ptr(out, dev, &kout, "out"))) return st;
+  if (kin != Kind::kPinnedHost || kout != Kind::kPinnedHost) {
+    set_error("validate: ley_sort_submit takes pinned host in/out (device buffers: call ley_sort)");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  const size_t a = ((size_t)n_records * kRecordBytes + 255) & ~size_t(255);
+  const uint64_t need = 4 * (uint64_t)a + plan_internal(n_records).bytes;  // two slots (in | out) + scratch
+  if (device_budget_bytes && need > device_budget_bytes)  // does not fit twice: the blocking path decides
+    return ley_sort(in, out, n_records, record_bytes, key_bytes, device_budget_bytes, stream);
+  DeviceContext& ctx = device_context(dev);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  ctx.device = dev;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms > 0) ctx.sms = sms;
+  return sort_submit(ctx, static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), n_records,
+                     static_cast<cudaStream_t>(stream));
+}
+
+ley_status ley_sort_drain(void) {
+  clear_error();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("validate: no CUDA device");
+    return LEY_ERR_CUDA;
+  }
+  DeviceContext& ctx = device_context(dev);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  return sort_drain(ctx);
+}
+
 ley_status ley_comm_get_unique_id(uint8_t id_out[128]) {
   clear_error();
   return comm_get_unique_id(id_out);

@@ -235,6 +235,7 @@ void release_device(int device) {
     }
     for (cudaEvent_t e : c.events) cudaEventDestroy(e);
     c.events.clear();
+    pipe_release(c);
     cudaSetDevice(prev);
   }
 }

@@ -87,6 +87,17 @@ struct DeviceContext {
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // external path: H2D / D2H copy streams
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> events;
+  // streaming host sort (ley_sort_submit): two device staging slots (in | out) and three streams, so the
+  // H2D of call k+1, the sort of call k and the D2H of call k-1 overlap
+  struct Pipe {
+    bool init = false;
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    DeviceBuffer slot[2];
+    cudaEvent_t user = nullptr;
+    cudaEvent_t copied_in[2] = {nullptr, nullptr}, sorted[2] = {nullptr, nullptr}, copied_out[2] = {nullptr, nullptr};
+    bool used[2] = {false, false};
+    int next = 0;
+  } pipe;
 };
 DeviceContext& device_context(int device);
 ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s);
@@ -113,5 +124,9 @@ int stage_times(const char** names, float* ms, int max, int* launches);
 // `work` (optional) is a caller-provided workspace of >= plan_internal(n).bytes; else ctx.work is used.
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                                 cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0);
+// Streaming staged-internal sort of pinned host records (ley_sort_submit / ley_sort_drain).
+ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, cudaStream_t user);
+ley_status sort_drain(DeviceContext& ctx);
+void pipe_release(DeviceContext& ctx);
 
 }  // namespace ley

@@ -102,6 +102,42 @@ def test_pinned_host_path():
     assert_parity(recs, out.numpy())
 
 
+def test_streaming_submit_pipeline():
+    """ley_sort_submit: consecutive host sorts overlap through two device slots (H2D of call k+1 with the
+    D2H of call k). Five calls of different sizes and distributions (slots reused and grown) must each
+    land byte-exact, and the caller's stream must be ordered after each call's D2H."""
+    import paper_1909_08006_b200 as ley
+
+    cases = [(70_001, "uniform"), (123_457, "skewed"), (4097, "all_equal"), (200_003, "tiny_alphabet"),
+             (33, "reverse")]
+    bufs = []
+    for i, (n, dist) in enumerate(cases):
+        recs = gen.records(n, seed=60 + i, dist=dist)
+        x, out = _pinned(recs)
+        out.fill_(0xAB)
+        ley.ley_sort_submit(x, out, n)
+        bufs.append((recs, x, out))
+    ley.ley_sort_drain()
+    for recs, _, out in bufs:
+        assert_parity(recs, out.numpy())
+    # stream ordering: the H2D waits for work already on the caller's stream (here a copy into `in`)
+    recs = gen.records(50_000, seed=99, dist="skewed")
+    x, out = _pinned(recs)
+    x0 = x.clone()
+    x.zero_()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        torch.cuda._sleep(50_000_000)  # keep the stream busy so an unordered H2D would read zeros
+        x.copy_(x0.cuda(non_blocking=True), non_blocking=True)
+    ley.ley_sort_submit(x, out, 50_000, stream=st)
+    ley.ley_sort_drain()
+    assert_parity(recs, out.numpy())
+    # device pointers are rejected (the blocking ley_sort is the device-resident call)
+    d = torch.from_numpy(recs).cuda()
+    assert ley.ley_sort_submit(d, torch.empty_like(d), 50_000, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
+    ley.ley_sort_drain()
+
+
 def test_pageable_rejected():
     import paper_1909_08006_b200 as ley
 
