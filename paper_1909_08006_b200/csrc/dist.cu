@@ -349,7 +349,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
   if (sms > 0) ctx.sms = sms;
-  if (!ctx.host_pinned) LEY_CUDA("dist", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  if (!ctx.host_pinned) LEY_CUDA("dist", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
   if (n_local && (!in_local || !out_local)) {
     set_error("dist: NULL in/out with n_local > 0");
     return LEY_ERR_INVALID_ARGUMENT;
@@ -502,7 +502,7 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms > 0) ctx.sms = sms;
-  if (!ctx.host_pinned) LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  if (!ctx.host_pinned) LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
   std::vector<std::unique_ptr<RankState>> R(G);
   Plan P;
   P.G = G;

@@ -11,17 +11,23 @@
 // B200 mapping (device memory capped by device_budget_bytes, P:19's memory limit):
 //   a10 run generation: run r = input records [r C, (r+1) C) -> H2D -> internal sort (K-a..K-e) -> D2H
 //       into pinned host run scratch; every S-th record of each sorted run is kept on the device as a
-//       sample. H2D of run r+1 overlaps D2H of run r (two copy streams, full-duplex PCIe).
+//       sample. Two device slots: while run r sorts, run r+1 streams in and run r-1 streams out (two
+//       copy streams, full-duplex PCIe), so each direction of the host link stays busy.
 //   a11 partition location: the samples are sorted (the internal sort again: sample order = (key, run,
 //       pos)), every q-th one becomes a splitter, and K-loc binary-searches every sorted run for every
 //       splitter directly in pinned host memory (zero-copy) -> exact slice bounds split[p][r].
 //   a12 merge: partition p's R slices are copied H2D (concatenated in run order), turned into 16-byte
 //       composite keys (key bytes 0..9, position in the concatenation = (run, pos) order), merged by a
 //       ceil(log2 R)-level tree of 2-way merge-path merges (K-m), gathered (K-e style, device-local) and
-//       copied D2H to out at the partition's offset. D2H of p overlaps H2D of p+1.
+//       copied D2H to out at the partition's offset. Two slots again: partition p+1's slices stream in
+//       while p merges and p-1 streams out.
 // Ties: records with equal keys from different runs come out in run order, within a run in position
 // order — i.e. by global input index, which is the stable order.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -165,6 +171,64 @@ __global__ void ext_gather(const uint32_t* __restrict__ slice, const uint64_t* _
   }
 }
 
+// LEY_TRACE_EXT=1: events around every copy / sort of the external path; per-category busy time and
+// span printed to stderr at the end (diagnostics only; never on by default).
+struct ExtTrace {
+  bool on = getenv("LEY_TRACE_EXT") != nullptr;
+  cudaEvent_t origin = nullptr;
+  struct Span { const char* cat; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  void start(cudaStream_t st) {
+    if (!on) return;
+    cudaEventCreate(&origin);
+    cudaEventRecord(origin, st);
+  }
+  size_t begin(const char* cat, cudaStream_t st) {
+    if (!on) return 0;
+    Span sp{cat, nullptr, nullptr};
+    cudaEventCreate(&sp.a);
+    cudaEventCreate(&sp.b);
+    cudaEventRecord(sp.a, st);
+    spans.push_back(sp);
+    return spans.size() - 1;
+  }
+  void end(size_t i, cudaStream_t st) {
+    if (on) cudaEventRecord(spans[i].b, st);
+  }
+  void report() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    std::vector<std::string> cats;
+    for (auto& sp : spans) {
+      bool seen = false;
+      for (auto& c : cats) seen |= c == sp.cat;
+      if (!seen) cats.push_back(sp.cat);
+    }
+    for (auto& c : cats) {
+      float busy = 0, first = 1e30f, last = 0;
+      int cnt = 0;
+      for (auto& sp : spans) {
+        if (c != sp.cat) continue;
+        float a = 0, b = 0, d = 0;
+        cudaEventElapsedTime(&a, origin, sp.a);
+        cudaEventElapsedTime(&b, origin, sp.b);
+        cudaEventElapsedTime(&d, sp.a, sp.b);
+        busy += d;
+        first = std::min(first, a);
+        last = std::max(last, b);
+        ++cnt;
+      }
+      fprintf(stderr, "[ext trace] %-12s n=%4d busy %8.2f ms  span [%8.2f, %8.2f] ms\n", c.c_str(), cnt, busy, first,
+              last);
+    }
+    for (auto& sp : spans) {
+      cudaEventDestroy(sp.a);
+      cudaEventDestroy(sp.b);
+    }
+    cudaEventDestroy(origin);
+  }
+};
+
 unsigned grid_for(uint64_t work, int sms, int per_sm = 8) {
   uint64_t b = (work + 255) / 256;
   uint64_t cap = (uint64_t)sms * per_sm;
@@ -199,18 +263,20 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   }
   const size_t sz_run = a256(C * kRecordBytes);
   const size_t sz_samples = a256(nsamp * kRecordBytes);
-  const size_t phase1 = 2 * sz_run + a256(LC.bytes) + 2 * sz_samples + a256(4 * nsamp) + a256(4 * C) +
+  const size_t phase1 = 4 * sz_run + a256(LC.bytes) + 2 * sz_samples + a256(4 * nsamp) + 2 * a256(4 * C) +
                         a256(plan_internal(nsamp).bytes);
   if ((st = ensure_buffer(ctx.ext, phase1, "external buffers", s))) return st;
   uint8_t* eb = static_cast<uint8_t*>(ctx.ext.ptr);
-  uint8_t* d_in = eb;
-  uint8_t* d_out = d_in + sz_run;
-  uint8_t* d_work = d_out + sz_run;
+  uint8_t* d_in[2] = {eb, eb + sz_run};
+  uint8_t* d_out[2] = {eb + 2 * sz_run, eb + 3 * sz_run};
+  uint8_t* d_work = eb + 4 * sz_run;
   uint8_t* d_samp = d_work + a256(LC.bytes);
   uint8_t* d_samp_sorted = d_samp + sz_samples;
   uint32_t* d_samp_perm = reinterpret_cast<uint32_t*>(d_samp_sorted + sz_samples);
-  uint32_t* d_run_perm = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_samp_perm) + a256(4 * nsamp));
-  uint8_t* d_work2 = reinterpret_cast<uint8_t*>(d_run_perm) + a256(4 * C);
+  uint32_t* d_run_perm[2];
+  d_run_perm[0] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_samp_perm) + a256(4 * nsamp));
+  d_run_perm[1] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_run_perm[0]) + a256(4 * C));
+  uint8_t* d_work2 = reinterpret_cast<uint8_t*>(d_run_perm[1]) + a256(4 * C);
 
   // pinned host run scratch (records, and global ordinals when perm is requested)
   const size_t scratch_bytes = (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0);
@@ -228,58 +294,81 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
 
   if (!ctx.copy_stream[0]) {
     for (int i = 0; i < 2; ++i) LEY_CUDA("external", cudaStreamCreateWithFlags(&ctx.copy_stream[i], cudaStreamNonBlocking));
-    for (int i = 0; i < 4; ++i) LEY_CUDA("external", cudaEventCreateWithFlags(&ctx.ev[i], cudaEventDisableTiming));
+    for (int i = 0; i < DeviceContext::kExtEvents; ++i)
+      LEY_CUDA("external", cudaEventCreateWithFlags(&ctx.ev[i], cudaEventDisableTiming));
   }
   cudaStream_t h2d = ctx.copy_stream[0], d2h = ctx.copy_stream[1];
-  cudaEvent_t ev_start = ctx.ev[0], ev_in = ctx.ev[1], ev_sorted = ctx.ev[2], ev_out = ctx.ev[3];
+  // per slot: input landed, slot sorted (input free, output ready), output copied out (output free)
+  cudaEvent_t ev_start = ctx.ev[0];
+  cudaEvent_t ev_in[2] = {ctx.ev[1], ctx.ev[2]}, ev_sorted[2] = {ctx.ev[3], ctx.ev[4]},
+              ev_out[2] = {ctx.ev[5], ctx.ev[6]};
 
   // ---------------------------------------------------------------- a10: run generation
   if ((st = prof.begin("ext run generation"))) return st;
+  ExtTrace tr;
+  tr.start(s);
   LEY_CUDA("ext runs", cudaEventRecord(ev_start, s));
   LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_start, 0));
   LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_start, 0));
   Profiler quiet;  // inner sorts are not profiled stage by stage
   quiet.ctx = &ctx;
   quiet.stream = s;
+  // H2D of run r into slot r & 1, once run r-2 (same slot) has been sorted
+  auto issue_run_h2d = [&](uint32_t r) -> ley_status {
+    const int sl = r & 1;
+    if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_sorted[sl], 0));
+    const size_t t_h = tr.begin("run H2D", h2d);
+    LEY_CUDA("ext H2D", cudaMemcpyAsync(d_in[sl], in + run_off[r] * kRecordBytes, run_len[r] * kRecordBytes,
+                                        cudaMemcpyHostToDevice, h2d));
+    tr.end(t_h, h2d);
+    LEY_CUDA("ext runs", cudaEventRecord(ev_in[sl], h2d));
+    return LEY_OK;
+  };
+  if ((st = issue_run_h2d(0))) return st;
   for (uint32_t r = 0; r < R; ++r) {
     const uint64_t len = run_len[r];
-    // d_in is free once the previous run's sort finished (ev_sorted on s)
-    if (r > 0) LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_sorted, 0));
-    LEY_CUDA("ext H2D", cudaMemcpyAsync(d_in, in + run_off[r] * kRecordBytes, len * kRecordBytes,
-                                        cudaMemcpyHostToDevice, h2d));
-    LEY_CUDA("ext runs", cudaEventRecord(ev_in, h2d));
-    LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_in, 0));
-    // d_out is free once the previous run's D2H finished
-    if (r > 0) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out, 0));
-    st = sort_internal_device(ctx, d_in, d_out, perm_out ? d_run_perm : nullptr, len, s, quiet, d_work, LC.bytes);
+    const int sl = r & 1;
+    // queue the next run's input before this run's sort blocks the host on its own stream
+    if (r + 1 < R && (st = issue_run_h2d(r + 1))) return st;
+    LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_in[sl], 0));
+    if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_out[sl] copied out
+    const size_t t_s = tr.begin("run sort", s);
+    st = sort_internal_device(ctx, d_in[sl], d_out[sl], perm_out ? d_run_perm[sl] : nullptr, len, s, quiet, d_work,
+                              LC.bytes);
     if (st) return st;
+    tr.end(t_s, s);
     prof.launches += quiet.launches;
     quiet.launches = 0;
     ext_take_samples<<<grid_for((len + S - 1) / S * kRecordWords, sms), 256, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(d_out), len, (uint32_t)S, reinterpret_cast<uint32_t*>(d_samp), samp_base[r]);
+        reinterpret_cast<const uint32_t*>(d_out[sl]), len, (uint32_t)S, reinterpret_cast<uint32_t*>(d_samp),
+        samp_base[r]);
     LEY_CUDA("ext samples", cudaGetLastError());
     prof.launches += 1;
     if (perm_out) {
-      ext_add_base<<<grid_for(len, sms), 256, 0, s>>>(d_run_perm, len, (uint32_t)run_off[r]);
+      ext_add_base<<<grid_for(len, sms), 256, 0, s>>>(d_run_perm[sl], len, (uint32_t)run_off[r]);
       LEY_CUDA("ext perm", cudaGetLastError());
       prof.launches += 1;
     }
-    LEY_CUDA("ext runs", cudaEventRecord(ev_sorted, s));
-    LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_sorted, 0));
-    LEY_CUDA("ext D2H", cudaMemcpyAsync(h_runs + run_off[r] * kRecordBytes, d_out, len * kRecordBytes,
+    LEY_CUDA("ext runs", cudaEventRecord(ev_sorted[sl], s));
+    LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
+    const size_t t_d = tr.begin("run D2H", d2h);
+    LEY_CUDA("ext D2H", cudaMemcpyAsync(h_runs + run_off[r] * kRecordBytes, d_out[sl], len * kRecordBytes,
                                         cudaMemcpyDeviceToHost, d2h));
+    tr.end(t_d, d2h);
     if (perm_out)
-      LEY_CUDA("ext D2H", cudaMemcpyAsync(h_perm + run_off[r], d_run_perm, len * 4, cudaMemcpyDeviceToHost, d2h));
-    LEY_CUDA("ext runs", cudaEventRecord(ev_out, d2h));
+      LEY_CUDA("ext D2H", cudaMemcpyAsync(h_perm + run_off[r], d_run_perm[sl], len * 4, cudaMemcpyDeviceToHost, d2h));
+    LEY_CUDA("ext runs", cudaEventRecord(ev_out[sl], d2h));
   }
-  LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out, 0));
+  LEY_CUDA("ext runs", cudaEventRecord(ev_start, d2h));  // every run copied out
+  LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_start, 0));
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- a11: splitters and slice bounds
   if ((st = prof.begin("ext partition"))) return st;
-  // merge-phase device plan: a partition of m records needs slice (100 m) + out (100 m) + 2 x 16 m
-  // composites (+ 8 m perm); keep it inside the same budget as phase 1.
-  const size_t per_rec = 2 * kRecordBytes + 32 + (perm_out ? 8 : 0);
+  // merge-phase device plan: a partition of m records needs two slots of slice (100 m) + out (100 m)
+  // (partition p+1 streams in and p-1 streams out while p merges) + 2 x 16 m composites (+ 16 m perm);
+  // keep it inside the same budget as phase 1.
+  const size_t per_rec = 4 * kRecordBytes + 32 + (perm_out ? 16 : 0);
   const size_t lists = 7ull * 16 * std::min<uint64_t>(65536, C) + (2u << 20);
   const size_t avail = std::max<size_t>(budget > lists ? budget - lists : 0, per_rec * 1024);
   uint64_t m_target = std::max<uint64_t>(1024, avail / per_rec);
@@ -342,82 +431,126 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   if ((st = prof.begin("ext merge"))) return st;
   const size_t sz_slice = a256(m_max * kRecordBytes);
   const size_t sz_comp = a256(m_max * 8);
-  const size_t phase2 = 2 * sz_slice + 4 * sz_comp + (perm_out ? 2 * a256(m_max * 4) : 0) + a256(8 * (R + 1));
+  const size_t sz_p = perm_out ? a256(m_max * 4) : 0;
+  std::vector<uint32_t> parts;  // non-empty partitions, merged in order
+  for (uint32_t p = 0; p < P; ++p)
+    if (part_off[p + 1] > part_off[p]) parts.push_back(p);
+  // merge-tree boundaries of every level of every partition, computed once on the host and copied to the
+  // device in one transfer (no host round trip between levels): level 0 = the R slice starts in the
+  // concatenation; level l+1 keeps every other boundary of level l (adjacent pairs merged)
+  const size_t bstride = 2 * (size_t)(R + 1) + 64;
+  std::vector<uint64_t> hb(parts.size() * bstride, 0);
+  std::vector<std::vector<std::pair<size_t, uint32_t>>> levels(parts.size());  // (offset in hb, K)
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const uint32_t p = parts[i];
+    std::vector<uint64_t> cur(R + 1);
+    uint64_t at = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      cur[r] = at;
+      at += split[(size_t)(p + 1) * R + r] - split[(size_t)p * R + r];
+    }
+    cur[R] = at;
+    size_t o = i * bstride;
+    std::copy(cur.begin(), cur.end(), hb.begin() + o);  // level 0 also gives the slice offsets
+    while (cur.size() > 2) {
+      std::copy(cur.begin(), cur.end(), hb.begin() + o);
+      levels[i].push_back({o, (uint32_t)cur.size() - 1});
+      o += cur.size();
+      std::vector<uint64_t> nxt;
+      for (size_t k = 0; k < cur.size(); k += 2) nxt.push_back(cur[k]);
+      if (nxt.back() != cur.back()) nxt.push_back(cur.back());
+      cur.swap(nxt);
+    }
+  }
+  const size_t phase2 = 4 * sz_slice + 4 * sz_comp + 4 * sz_p + a256(8 * hb.size());
   if (phase2 > ctx.ext.cap) {
     if ((st = ensure_buffer(ctx.ext, phase2, "external merge buffers", s))) return st;
   }
   eb = static_cast<uint8_t*>(ctx.ext.ptr);
-  uint8_t* d_slice = eb;
-  uint8_t* d_mout = d_slice + sz_slice;
-  uint64_t* c_h[2] = {reinterpret_cast<uint64_t*>(d_mout + sz_slice), nullptr};
-  uint64_t* c_l[2] = {reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_h[0]) + sz_comp), nullptr};
-  c_h[1] = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_l[0]) + sz_comp);
-  c_l[1] = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(c_h[1]) + sz_comp);
-  uint8_t* after = reinterpret_cast<uint8_t*>(c_l[1]) + sz_comp;
-  uint32_t* d_pslice = perm_out ? reinterpret_cast<uint32_t*>(after) : nullptr;
-  uint32_t* d_pout = perm_out ? reinterpret_cast<uint32_t*>(after + a256(m_max * 4)) : nullptr;
-  uint64_t* d_bnd = reinterpret_cast<uint64_t*>(after + (perm_out ? 2 * a256(m_max * 4) : 0));
-  std::vector<uint64_t> bnd(R + 1);
-  bool first = true;
-  for (uint32_t p = 0; p < P; ++p) {
-    const uint64_t m = part_off[p + 1] - part_off[p];
-    if (m == 0) continue;
-    // slices H2D (d_slice free once the previous partition's gather finished)
-    if (!first) LEY_CUDA("ext merge", cudaStreamWaitEvent(h2d, ev_sorted, 0));
-    uint64_t at = 0;
+  uint8_t* d_slice[2] = {eb, eb + sz_slice};
+  uint8_t* d_mout[2] = {eb + 2 * sz_slice, eb + 3 * sz_slice};
+  uint8_t* cb = eb + 4 * sz_slice;
+  uint64_t* c_h[2] = {reinterpret_cast<uint64_t*>(cb), reinterpret_cast<uint64_t*>(cb + 2 * sz_comp)};
+  uint64_t* c_l[2] = {reinterpret_cast<uint64_t*>(cb + sz_comp), reinterpret_cast<uint64_t*>(cb + 3 * sz_comp)};
+  uint8_t* pb = cb + 4 * sz_comp;
+  uint32_t* d_pslice[2] = {nullptr, nullptr};
+  uint32_t* d_pout[2] = {nullptr, nullptr};
+  if (perm_out) {
+    for (int i = 0; i < 2; ++i) {
+      d_pslice[i] = reinterpret_cast<uint32_t*>(pb + i * sz_p);
+      d_pout[i] = reinterpret_cast<uint32_t*>(pb + (2 + i) * sz_p);
+    }
+  }
+  uint64_t* d_bnd = reinterpret_cast<uint64_t*>(pb + 4 * sz_p);
+  LEY_CUDA("ext merge", cudaMemcpyAsync(d_bnd, hb.data(), 8 * hb.size(), cudaMemcpyHostToDevice, s));
+  LEY_CUDA("ext merge", cudaStreamSynchronize(s));
+  // H2D of the i-th partition's R slices into slot i & 1, once partition i-2 (same slot) is gathered
+  auto issue_slices = [&](size_t i) -> ley_status {
+    const uint32_t p = parts[i];
+    const int sl = i & 1;
+    if (i >= 2) LEY_CUDA("ext merge", cudaStreamWaitEvent(h2d, ev_sorted[sl], 0));
+    const uint64_t* off0 = hb.data() + i * bstride;  // slice r lands at off0[r]
+    const size_t t_mh = tr.begin("merge H2D", h2d);
     for (uint32_t r = 0; r < R; ++r) {
       const uint64_t lo = split[(size_t)p * R + r], hi = split[(size_t)(p + 1) * R + r];
-      bnd[r] = at;
+      const uint64_t at = off0[r];
       if (hi > lo) {
-        LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice + at * kRecordBytes,
+        LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice[sl] + at * kRecordBytes,
                                                   h_runs + (run_off[r] + lo) * kRecordBytes, (hi - lo) * kRecordBytes,
                                                   cudaMemcpyHostToDevice, h2d));
         if (perm_out)
-          LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice + at, h_perm + run_off[r] + lo, (hi - lo) * 4,
+          LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice[sl] + at, h_perm + run_off[r] + lo, (hi - lo) * 4,
                                                     cudaMemcpyHostToDevice, h2d));
       }
-      at += hi - lo;
     }
-    bnd[R] = at;
-    LEY_CUDA("ext merge", cudaEventRecord(ev_in, h2d));
-    LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_in, 0));
-    if (!first) LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out, 0));  // d_mout free
-    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice, m, c_h[0], c_l[0]);
+    tr.end(t_mh, h2d);
+    LEY_CUDA("ext merge", cudaEventRecord(ev_in[sl], h2d));
+    return LEY_OK;
+  };
+  // the slices are read from the host run scratch: every run's D2H (which s has waited for) comes first
+  LEY_CUDA("ext merge", cudaEventRecord(ctx.ev[7], s));
+  LEY_CUDA("ext merge", cudaStreamWaitEvent(h2d, ctx.ev[7], 0));
+  if (!parts.empty() && (st = issue_slices(0))) return st;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const uint32_t p = parts[i];
+    const int sl = i & 1;
+    const uint64_t m = part_off[p + 1] - part_off[p];
+    if (i + 1 < parts.size() && (st = issue_slices(i + 1))) return st;  // queued ahead of this merge
+    LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_in[sl], 0));
+    if (i >= 2) LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_mout[sl] copied out
+    const size_t t_mm = tr.begin("merge K-m", s);
+    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice[sl], m, c_h[0], c_l[0]);
     LEY_CUDA("K-m merge", cudaGetLastError());
     prof.launches += 1;
-    // merge tree over the R run slices
-    std::vector<uint64_t> cur(bnd.begin(), bnd.end());
+    // merge tree over the R run slices: one launch per level, boundaries already on the device
     int src = 0;
-    while (cur.size() > 2) {
-      const uint32_t K = (uint32_t)cur.size() - 1;
-      LEY_CUDA("K-m merge", cudaMemcpyAsync(d_bnd, cur.data(), 8 * cur.size(), cudaMemcpyHostToDevice, s));
+    for (const auto& lv : levels[i]) {
       const uint64_t threads = (m + kMergeItems - 1) / kMergeItems;
       ext_merge_level<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(c_h[src], c_l[src], c_h[src ^ 1], c_l[src ^ 1],
-                                                                        m, d_bnd, K);
+                                                                        m, d_bnd + lv.first, lv.second);
       LEY_CUDA("K-m merge", cudaGetLastError());
       prof.launches += 1;
-      // host copy of the boundaries must outlive the async H2D: wait for it before reusing `cur`
-      LEY_CUDA("K-m merge", cudaStreamSynchronize(s));
-      std::vector<uint64_t> nxt;
-      for (size_t i = 0; i < cur.size(); i += 2) nxt.push_back(cur[i]);
-      if (nxt.back() != cur.back()) nxt.push_back(cur.back());
-      cur.swap(nxt);
       src ^= 1;
     }
-    ext_gather<<<grid_for(m * kRecordWords, sms), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(d_slice), c_l[src], m,
-                                                               reinterpret_cast<uint32_t*>(d_mout), d_pslice, d_pout);
+    ext_gather<<<grid_for(m * kRecordWords, sms), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(d_slice[sl]), c_l[src],
+                                                               m, reinterpret_cast<uint32_t*>(d_mout[sl]), d_pslice[sl],
+                                                               d_pout[sl]);
     LEY_CUDA("K-e gather", cudaGetLastError());
     prof.launches += 1;
-    LEY_CUDA("ext merge", cudaEventRecord(ev_sorted, s));
-    LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ev_sorted, 0));
-    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + part_off[p] * kRecordBytes, d_mout, m * kRecordBytes,
+    LEY_CUDA("ext merge", cudaEventRecord(ev_sorted[sl], s));
+    LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
+    tr.end(t_mm, s);
+    const size_t t_md = tr.begin("merge D2H", d2h);
+    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + part_off[p] * kRecordBytes, d_mout[sl], m * kRecordBytes,
                                               cudaMemcpyDeviceToHost, d2h));
+    tr.end(t_md, d2h);
     if (perm_out)
-      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + part_off[p], d_pout, m * 4, cudaMemcpyDeviceToHost, d2h));
-    LEY_CUDA("ext merge", cudaEventRecord(ev_out, d2h));
-    first = false;
+      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + part_off[p], d_pout[sl], m * 4, cudaMemcpyDeviceToHost, d2h));
+    LEY_CUDA("ext merge", cudaEventRecord(ev_out[sl], d2h));
   }
-  LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out, 0));
+  LEY_CUDA("ext merge", cudaEventRecord(ev_start, d2h));
+  LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_start, 0));
+  tr.report();
   if ((st = prof.end())) return st;
   return LEY_OK;
 }

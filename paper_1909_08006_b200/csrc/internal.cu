@@ -32,7 +32,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     set_error("internal: caller workspace too small");
     return LEY_ERR_BUDGET;
   }
-  if (!ctx.host_pinned) LEY_CUDA("setup", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocDefault));
+  if (!ctx.host_pinned) LEY_CUDA("setup", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
   uint8_t* base = static_cast<uint8_t*>(work);
   uint64_t* At = reinterpret_cast<uint64_t*>(base + L.off_At);
   uint32_t* Ai = reinterpret_cast<uint32_t*>(base + L.off_Ai);
@@ -51,7 +51,9 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   uint32_t* tickets = small;          // [0..15]
   uint32_t* kd_counts = small + 16;   // [kNumKdLists]
   uint32_t* big_count = small + 32;   // [1]
-  uint32_t* host_cnt = static_cast<uint32_t*>(ctx.host_pinned);
+  volatile uint32_t* host_cnt = static_cast<volatile uint32_t*>(ctx.host_pinned);
+  uint32_t* host_cnt_dev = nullptr;  // its device alias: counters are published by a kernel store
+  LEY_CUDA("setup", cudaHostGetDevicePointer((void**)&host_cnt_dev, ctx.host_pinned, 0));
 
   const Options o = options_snapshot();
   Tunables tu;
@@ -114,7 +116,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
   ++launches;
   LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
-  LEY_CUDA("K-de sort+gather", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
   LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
   uint32_t nbig = host_cnt[0];
   if ((st = prof.end())) return st;
@@ -169,7 +171,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
                                               (uint32_t)chunks_ub, s));
     launches += 5;
     LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
-    LEY_CUDA("K-c' recursion", cudaMemcpyAsync(host_cnt, big_count, 4, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-c' recursion", launch_publish_u32(big_count, host_cnt_dev, s));
     LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
     nbig = host_cnt[0];
     cur ^= 1;

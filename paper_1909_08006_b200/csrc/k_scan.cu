@@ -90,7 +90,17 @@ __global__ void kb_hist_reduce(uint32_t* __restrict__ hist, uint32_t copies) {
   hist[b] = s;
 }
 
+// Copy one device counter into mapped pinned host memory with a store from the SM: the host reads a
+// recursion level's big-bucket count without a copy-engine transfer, which would queue behind a large
+// D2H on the copy engine (the streaming and external paths overlap sorts with such copies).
+__global__ void kb_publish_u32(const uint32_t* __restrict__ src, volatile uint32_t* dst) { *dst = *src; }
+
 }  // namespace
+
+cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, cudaStream_t s) {
+  kb_publish_u32<<<1, 1, 0, s>>>(src, host_mapped_dev);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s) {
   if (copies <= 1) return cudaSuccess;

@@ -18,6 +18,7 @@ cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint
                              uint32_t* total_out, cudaStream_t s);
 uint64_t scan_status_words(uint64_t m);
 cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s);
+cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, cudaStream_t s);
 cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
                                   cudaStream_t s);
 

@@ -118,15 +118,16 @@ InternalLayout plan_internal(uint64_t n) {
 }
 
 // External path: the largest run C (records) whose run-generation working set fits the
-// budget: run in + run out (200 C) + the internal sort's workspace and K-d lists for C records + the run's
-// perm (4 C) + the sample buffers (every S-th record of every run, S = min(4096, C/16)) + 2 MB slack.
+// budget: two slots of run in + run out (400 C; run r+1 streams in and run r-1 streams out while run r
+// sorts) + the internal sort's workspace and K-d lists for C records + two runs' perms (8 C) + the
+// sample buffers (every S-th record of every run, S = min(4096, C/16)) + 2 MB slack.
 uint64_t external_run_need(uint64_t n, uint64_t C) {
   if (C == 0) return 0;
   const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>(4096, C / 16));
   const uint64_t runs = (n + C - 1) / C;
   const uint64_t nsamp = runs * ((C + S - 1) / S);
   const uint64_t lists = 6ull * 16 * std::min<uint64_t>(65536, C) + 16ull * std::min<uint64_t>(65536, C);
-  return 204 * C + plan_internal(C).bytes + lists + 2 * 100 * nsamp + 4 * nsamp + plan_internal(nsamp).bytes +
+  return 408 * C + plan_internal(C).bytes + lists + 2 * 100 * nsamp + 4 * nsamp + plan_internal(nsamp).bytes +
          (2ull << 20);
 }
 
@@ -229,7 +230,7 @@ void release_device(int device) {
       if (c.copy_stream[i]) cudaStreamDestroy(c.copy_stream[i]);
       c.copy_stream[i] = nullptr;
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < DeviceContext::kExtEvents; ++i) {
       if (c.ev[i]) cudaEventDestroy(c.ev[i]);
       c.ev[i] = nullptr;
     }

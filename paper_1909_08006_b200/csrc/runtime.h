@@ -85,7 +85,8 @@ struct DeviceContext {
   void* host_scratch = nullptr;  // external path: pinned (mapped) host run scratch
   size_t host_scratch_cap = 0;
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // external path: H2D / D2H copy streams
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kExtEvents = 8;
+  cudaEvent_t ev[kExtEvents] = {};
   std::vector<cudaEvent_t> events;
   // streaming host sort (ley_sort_submit): two device staging slots (in | out) and three streams, so the
   // H2D of call k+1, the sort of call k and the D2H of call k-1 overlap
