@@ -156,7 +156,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample records (0 = min(n, 1e8))")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -259,10 +259,10 @@ def main():
         achieved = alg / (avg[dominant] / 1e3) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and world == 1:
             with open(tp) as f:
                 ent = json.load(f).get(args.config, {}).get(dominant)
-            if ent:
+            if ent:  # DRAM bytes of the stage's launches in one call (ncu; tools/ncu_traffic.py)
                 traffic = ent.get("bytes_per_launch")
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dominant,

@@ -122,9 +122,6 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- recursion on big buckets
-  if (nbig) {
-    if ((st = prof.begin("K-c' recursion"))) return st;
-  }
   int cur = 0;
   while (nbig) {
     const uint64_t chunks_ub = n / kChunk + nbig + 1;
@@ -156,6 +153,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     const Seg* segs = static_cast<const Seg*>(ctx.big[cur].ptr);
     Seg* next_big = static_cast<Seg*>(ctx.big[cur ^ 1].ptr);
 
+    if ((st = prof.begin("K-c' split"))) return st;
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(seg_hist, 0, 4ull * nbig * kRadix, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rscan, 0, 8 * scan_words, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rtick, 0, 256, s));
@@ -170,14 +168,14 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rtick + 1,
                                               (uint32_t)chunks_ub, s));
     launches += 5;
+    if ((st = prof.end())) return st;
+    if ((st = prof.begin("K-de sort+gather"))) return st;
     LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
     LEY_CUDA("K-c' recursion", launch_publish_u32(big_count, host_cnt_dev, s));
     LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
     nbig = host_cnt[0];
     cur ^= 1;
-    if (!nbig) {
-      if ((st = prof.end())) return st;
-    }
+    if ((st = prof.end())) return st;
   }
 
   if (perm_out) {

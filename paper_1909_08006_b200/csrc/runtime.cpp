@@ -277,11 +277,17 @@ void Profiler::finish() {
   g_stages.ms.clear();
   g_stages.launches = launches;
   if (!on) return;
+  // stages that recur (one per MSD recursion level) are summed under their name, in first-use order
   for (size_t i = 0; i < names.size() && i < ev_end.size(); ++i) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->events[ev_begin[i]], ctx->events[ev_end[i]]);
-    g_stages.names.push_back(names[i]);
-    g_stages.ms.push_back(ms);
+    size_t k = 0;
+    while (k < g_stages.names.size() && strcmp(g_stages.names[k], names[i]) != 0) ++k;
+    if (k == g_stages.names.size()) {
+      g_stages.names.push_back(names[i]);
+      g_stages.ms.push_back(0.f);
+    }
+    g_stages.ms[k] += ms;
   }
 }
 
