@@ -56,37 +56,47 @@ def _peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled during the timed region (NVML, every 20 ms; B200_PROFILING.md)."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML, every 5 ms; B200_PROFILING.md)."""
 
-    def __init__(self, index: int, period: float = 0.02):
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
         self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    _BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+    _nv = None
+
+    def _init(self):
         try:
             import pynvml
 
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nv = (pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
         except Exception:
+            self._nv = None
+
+    def _sample_once(self):
+        if self._nv is None:
             return
-        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
-                "sw_power_cap": 0x4}
+        try:
+            pynvml, h, mx = self._nv
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+            self.samples.append((sm, mx, {k for k, b in self._BITS.items() if reasons & b}, util))
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
-                self.samples.append((sm, mx, {k for k, b in bits.items() if reasons & b}, util))
-            except Exception:
-                pass
+            self._sample_once()
             self._stop.wait(self.period)
 
     def __enter__(self):
+        self._init()  # NVML handle ready before the timed region starts
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -94,6 +104,8 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples:  # a timed region shorter than the first sample: one sample as it ends
+            self._sample_once()
 
     def summary(self):
         if not self.samples:
