@@ -192,6 +192,90 @@ def test_c3_full_size_certificate():
     assert oracle.multiset_hash(h_in) == oracle.multiset_hash(h_out)
 
 
+def _certify_on_device(x: torch.Tensor, out: torch.Tensor, perm: torch.Tensor, n: int, step: int = 20_000_000):
+    """The certificate (perm is a permutation; out[j] == in[perm[j]]; (key, perm) strictly increasing) with
+    plain torch ops on the device, in chunks — for sizes whose host copy would not fit. Independent of the
+    library's kernels; together the three properties pin the output to the oracle's."""
+    X, O = x.view(n, 100), out.view(n, 100)
+    seen = torch.zeros(n, dtype=torch.bool, device="cuda")
+    prev = None
+    w = torch.tensor([1 << (8 * (6 - i)) for i in range(7)], dtype=torch.int64, device="cuda")
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        pc = perm[a:b].to(torch.int64)
+        assert int(pc.min()) >= 0 and int(pc.max()) < n
+        seen[pc] = True
+        assert torch.equal(O[a:b], X[pc]), f"out != in[perm] in [{a}, {b})"
+        kb = O[a:b, :10].to(torch.int64)
+        hi = (kb[:, :7] * w).sum(1)                                     # key bytes 0..6
+        lo = ((kb[:, 7] << 16) | (kb[:, 8] << 8) | kb[:, 9]) << 32 | pc  # bytes 7..9, then the ordinal
+        if prev is not None:
+            hi = torch.cat([prev[0], hi])
+            lo = torch.cat([prev[1], lo])
+        inc = (hi[1:] > hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] > lo[:-1]))
+        assert bool(inc.all()), f"(key, ordinal) not strictly increasing in [{a}, {b})"
+        prev = (hi[-1:], lo[-1:])
+    assert bool(seen.all()), "perm is not a permutation"
+
+
+def test_device_certificate_rejects_corruption():
+    """The device-side certifier used at full size must reject every single-defect corruption: swapped
+    records, a swapped tie (unstable order), a payload byte flip, a duplicated ordinal."""
+    import paper_1909_08006_b200 as ley
+
+    n = 100_003
+    x = device_records(n, seed=5, dist="three_keys")
+    out = torch.empty_like(x)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ley.ley_sort_perm(x, out, perm, n)
+    torch.cuda.synchronize()
+    _certify_on_device(x, out, perm, n, step=30_000)
+
+    def bad(mut):
+        o, p = out.clone(), perm.clone()
+        mut(o.view(n, 100), p)
+        with pytest.raises(AssertionError):
+            _certify_on_device(x, o, p, n, step=30_000)
+
+    def swap_rows(o, p, i, j):
+        o[[i, j]] = o[[j, i]]
+        p[[i, j]] = p[[j, i]]
+
+    bad(lambda o, p: swap_rows(o, p, 10, 90_000))     # out of key order
+    bad(lambda o, p: swap_rows(o, p, 40_000, 40_001))  # adjacent equal keys (three_keys): unstable tie
+    bad(lambda o, p: o[777].__setitem__(55, o[777, 55] ^ 1))  # payload edit
+    bad(lambda o, p: p.__setitem__(5, p[6]))           # not a permutation
+
+
+@pytest.mark.slow
+def test_c4_full_size_certificate():
+    """BASELINE.json configs[3] at full size (6e8 records = 60 GB, seed 3), the bench's launch
+    configuration: certified on the device (in + out + perm + scratch fit the 180 GB HBM), and the oracle
+    sorts a 2M-record slice of the same input to the same bytes as the GPU."""
+    import paper_1909_08006_b200 as ley
+
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' cached blocks: in + out + perm + scratch need ~140 GB
+    ley.ley_release_cache(-1)
+    n = 600_000_000
+    x = device_records(n, seed=3)
+    out = torch.empty_like(x)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ley.ley_sort_perm(x, out, perm, n)
+    torch.cuda.synchronize()
+    _certify_on_device(x, out, perm, n)
+    sl = x[: 2_000_000 * 100].cpu().numpy()
+    del out, perm
+    torch.cuda.empty_cache()
+    o2, p2 = gpu_sort(sl)
+    assert_parity(sl, o2, p2)
+    del x
+    torch.cuda.empty_cache()
+    ley.ley_release_cache(-1)
+
+
 # ------------------------------------------------------------------ external path (SURVEY §8a a10-a12)
 def _pinned(recs):
     x = torch.from_numpy(recs).pin_memory()
