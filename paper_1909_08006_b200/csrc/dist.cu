@@ -131,8 +131,11 @@ struct RankState {
   uint64_t send_counts[kMaxRanks] = {0};
   uint64_t recv_counts[kMaxRanks], recv_off[kMaxRanks], send_off[kMaxRanks];
   uint64_t n_out = 0, out_off = 0;
+  // grow-only caches, so repeated sorts allocate nothing on the hot path
+  DeviceBuffer cand_buf, split_buf, recv_buf;
   ~RankState() {
-    if (buf.ptr) cudaFree(buf.ptr);
+    for (DeviceBuffer* b : {&buf, &cand_buf, &split_buf, &recv_buf})
+      if (b->ptr) cudaFree(b->ptr);
   }
 };
 
@@ -201,14 +204,13 @@ ley_status phase2_candidates(RankState& r, const Plan& P) {
 
 // Given all candidates concatenated in rank order (device records + ordinals), find the exact splitters.
 ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* all_cand, const uint32_t* all_gidx,
-                            uint64_t total_cand, Plan& P) {
+                            uint64_t total_cand, Plan& P, DeviceBuffer& tmp) {
   const int nspl = P.G - 1;
   if (nspl == 0) return LEY_OK;
-  DeviceBuffer tmp;
   const InternalLayout L = plan_internal(total_cand);
   const size_t bytes = a256(total_cand * kRecordBytes) + a256(4 * total_cand) + a256(L.bytes);
-  LEY_CUDA("K-s splitters", cudaMalloc(&tmp.ptr, bytes));
-  std::unique_ptr<void, decltype(&cudaFree)> guard(tmp.ptr, &cudaFree);
+  ley_status est = ensure_buffer(tmp, bytes, "K-s splitters", s);
+  if (est) return est;
   uint8_t* sorted = static_cast<uint8_t*>(tmp.ptr);
   uint32_t* perm = reinterpret_cast<uint32_t*>(sorted + a256(total_cand * kRecordBytes));
   uint8_t* work = reinterpret_cast<uint8_t*>(perm) + a256(4 * total_cand);
@@ -416,12 +418,10 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
       total += counts[i];
     }
     // padded allgather of candidate records and ordinals, then compaction into rank order
-    DeviceBuffer cb;
     const size_t rec_b = a256(maxc * kRecordBytes), gid_b = a256(4 * maxc);
     const size_t bytes = (size_t)G * (rec_b + gid_b) + rec_b + gid_b + a256(total * kRecordBytes) + a256(4 * total);
-    LEY_CUDA("dist cand", cudaMalloc(&cb.ptr, std::max<size_t>(bytes, 256)));
-    std::unique_ptr<void, decltype(&cudaFree)> g2(cb.ptr, &cudaFree);
-    uint8_t* base = static_cast<uint8_t*>(cb.ptr);
+    if ((st = ensure_buffer(r.cand_buf, std::max<size_t>(bytes, 256), "dist cand", s))) return st;
+    uint8_t* base = static_cast<uint8_t*>(r.cand_buf.ptr);
     uint8_t* all_rec = base;                                   // G x rec_b
     uint8_t* all_gid = all_rec + (size_t)G * rec_b;            // G x gid_b
     uint8_t* my_rec = all_gid + (size_t)G * gid_b;
@@ -444,7 +444,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
       }
       at += counts[i];
     }
-    if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P))) return st;
+    if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P, r.split_buf))) return st;
     LEY_CUDA("dist cand", cudaStreamSynchronize(s));
   }
   // P4 + C3: send counts
@@ -460,11 +460,9 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   // P5 + C4: partition and all-to-all-v
   if ((st = phase5_partition(r, P))) return st;
   const uint8_t* recv = r.in;
-  DeviceBuffer rb;
-  std::unique_ptr<void, decltype(&cudaFree)> g3(nullptr, &cudaFree);
   if (G > 1) {
-    LEY_CUDA("dist exchange", cudaMalloc(&rb.ptr, std::max<size_t>(r.n_out * kRecordBytes, 256)));
-    g3.reset(rb.ptr);
+    if ((st = ensure_buffer(r.recv_buf, std::max<size_t>(r.n_out * kRecordBytes, 256), "dist exchange", s))) return st;
+    DeviceBuffer& rb = r.recv_buf;
     LEY_NCCL("dist exchange", ncclGroupStart());
     for (int peer = 0; peer < G; ++peer) {
       const uint64_t sc = P.send_matrix[(size_t)r.rank * G + peer];
@@ -560,7 +558,7 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
       }
       at += c;
     }
-    if ((st = phase3_splitters(ctx, s, cat, gid, total, P))) return st;
+    if ((st = phase3_splitters(ctx, s, cat, gid, total, P, R[0]->split_buf))) return st;
   }
   // P4 + C3
   P.send_matrix.assign((size_t)G * G, 0);
