@@ -40,6 +40,7 @@ struct Tunables {
   uint32_t smem_tier_max = kSmemTierMax;
   int kd_digit_bits = kKdMaxBits;
   int kd_insert_max = 16;
+  int kd_ws = 1;  // warp-specialised sort/gather tiers (kd_ws_sort) instead of the alternating kd_cta_sort
 };
 
 // ------------------------------------------------------------------ device helpers

@@ -61,6 +61,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   tu.smem_tier_max = (uint32_t)o.smem_tier_max;
   tu.kd_digit_bits = (int)o.kd_digit_bits;
   tu.kd_insert_max = (int)o.kd_insert_max;
+  tu.kd_ws = (int)o.kd_ws;
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;

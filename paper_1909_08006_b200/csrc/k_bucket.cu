@@ -427,6 +427,272 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}"
+               ::"r"(a), "r"(parity) : "memory");
+}
+// TMA bulk copy global -> shared, completion counted in bytes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+// ---------------------------------------------------------------------------- warp-specialised tier
+// The fused kernel above alternates: all warps sort a bucket, then all warps gather it, so a CTA issues no
+// record reads while it sorts. Here a CTA splits into a sort group (ST threads) and a gather group (GW
+// warps) that run concurrently on consecutive buckets of the CTA's list through a two-slot ring of sorted
+// ordinals: the sort group sorts bucket k+1 while the gather warps stream bucket k, each warp keeping two
+// 32-record groups in flight (cp.async double buffering). Hand-off by named barriers (bar.arrive /
+// bar.sync, producer/consumer counts): FULL[q] sort -> gather, EMPTY[q] gather -> sort.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int kBarSort = 1, kBarFull = 2, kBarEmpty = 4;  // ids 1, 2-3, 4-5 (0 is __syncthreads)
+
+// exclusive scan over a group of THREADS threads (tid = group-local index) synchronised by barrier `bar`
+template <int THREADS>
+__device__ __forceinline__ uint32_t group_excl_scan(uint32_t v, uint32_t* tmp, int tid, int bar) {
+  constexpr int WARPS = THREADS / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  nbar_sync(bar, THREADS);
+  if (warp == 0) {
+    uint32_t w = lane < WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < WARPS) tmp[lane] = w;
+  }
+  nbar_sync(bar, THREADS);
+  const uint32_t r = (warp ? tmp[warp - 1] : 0u) + x - v;
+  nbar_sync(bar, THREADS);
+  return r;
+}
+
+template <uint32_t CAP, int ST, int GW>
+struct WsLayout {
+  static constexpr uint32_t BINS = CAP < 1024 ? CAP : 1024;
+  static constexpr size_t kIdx = 0;                                   // u32[CAP]
+  static constexpr size_t kTail = kIdx + (size_t)CAP * 4;             // u64[CAP]
+  static constexpr size_t kCnt = kTail + (size_t)CAP * 8;             // u32[BINS + 1]
+  static constexpr size_t kBigl = kCnt + (size_t)(BINS + 1) * 4;      // u32[BINS]
+  static constexpr size_t kTmp = kBigl + (size_t)BINS * 4;            // u32[64]
+  static constexpr size_t kRing = (kTmp + 64 * 4 + 15) & ~size_t(15);  // u32[2][CAP]
+  static constexpr size_t kDesc = kRing + 2 * (size_t)CAP * 4;        // uint2[2]
+  static constexpr size_t kStage = (kDesc + 16 + 127) & ~size_t(127);  // [GW][2][kStageBytes]
+  static constexpr size_t kBytes = kStage + (size_t)GW * 2 * kStageBytes;
+};
+
+template <uint32_t CAP, int ST, int GW>
+__global__ void __launch_bounds__(ST + 32 * GW, 2)
+    kd_ws_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
+               const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
+               uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+  using L = WsLayout<CAP, ST, GW>;
+  constexpr uint32_t BINS = L::BINS;
+  constexpr int ITEMS = CAP / ST;
+  constexpr int NT = ST + 32 * GW;
+  constexpr int SW = ST / 32;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + L::kIdx);
+  uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem + L::kTail);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L::kCnt);
+  uint32_t* s_bigl = reinterpret_cast<uint32_t*>(smem + L::kBigl);
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem + L::kTmp);
+  uint32_t* s_nbig = s_tmp + 32;
+  uint32_t* s_ring = reinterpret_cast<uint32_t*>(smem + L::kRing);
+  uint2* s_desc = reinterpret_cast<uint2*>(smem + L::kDesc);
+  const uint32_t nitems = *count;
+  const int tid = threadIdx.x;
+
+  if (tid < ST) {
+    // ================================================================ sort group
+    const int warp = tid >> 5;
+    uint32_t k = 0;
+    for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
+      const int q = k & 1;
+      uint32_t* s_perm = s_ring + q * CAP;
+      if (k >= 2) nbar_sync(kBarEmpty + q, NT);  // the gather warps released slot q (bucket k-2)
+      for (uint32_t g = tid; g <= BINS; g += ST) s_cnt[g] = 0;
+      if (tid == 0) *s_nbig = 0;
+      nbar_sync(kBarSort, ST);
+      const Seg sg = list[it];
+      const uint32_t s = sg.len;
+      const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
+      const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
+      const bool on_idx = sg.depth >= kKeyBytes;
+      const uint32_t avail = on_idx ? 8u * (14u - sg.depth) : 8u * (kKeyBytes - sg.depth);
+      uint32_t bits = s > 1 ? 32u - __clz(s - 1) : 0u;
+      bits = min(bits, (uint32_t)tu.kd_digit_bits);
+      bits = min(bits, avail);
+      bits = min(bits, 31u - __clz(BINS));
+      const uint32_t shift = avail - bits;
+      const uint32_t nb = 1u << bits;
+      const uint32_t mask = nb - 1;
+      auto digit2 = [&](uint64_t t, uint32_t x) -> uint32_t {
+        return bits ? (on_idx ? (x >> shift) & mask : (uint32_t)(t >> shift) & mask) : 0u;
+      };
+      uint64_t tr[ITEMS];
+      uint32_t xr[ITEMS], rr[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * ST + tid;
+        if (i < s) {
+          tr[j] = tp[i];
+          xr[j] = ip[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * ST + tid;
+        if (i < s) rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
+      }
+      nbar_sync(kBarSort, ST);
+      {
+        const uint32_t per = (nb + ST - 1) / ST;
+        const uint32_t g0 = tid * per, g1 = min(nb, g0 + per);
+        uint32_t sum = 0;
+        for (uint32_t g = g0; g < g1; ++g) sum += s_cnt[g];
+        uint32_t run = group_excl_scan<ST>(sum, s_tmp, tid, kBarSort);
+        for (uint32_t g = g0; g < g1; ++g) {
+          const uint32_t c = s_cnt[g];
+          s_cnt[g] = run;
+          run += c;
+        }
+        if (tid == 0) s_cnt[nb] = s;
+      }
+      nbar_sync(kBarSort, ST);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * ST + tid;
+        if (i < s) {
+          const uint32_t b = s_cnt[digit2(tr[j], xr[j])];
+          s_tail[b + rr[j]] = tr[j];
+          s_idx[b + rr[j]] = xr[j];
+        }
+      }
+      nbar_sync(kBarSort, ST);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * ST + tid;
+        if (i < s) {
+          const uint32_t d = digit2(tr[j], xr[j]);
+          const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
+          if (sz == 1) {
+            s_perm[b] = xr[j];
+          } else if (sz <= (uint32_t)tu.kd_insert_max) {
+            uint32_t rank = 0;
+            const uint32_t self = b + rr[j];
+            for (uint32_t m = b; m < b + sz; ++m)
+              if (m != self) rank += pair_less(s_tail[m], s_idx[m], tr[j], xr[j]) ? 1u : 0u;
+            s_perm[b + rank] = xr[j];
+          } else if (rr[j] == 0) {
+            s_bigl[atomicAdd(s_nbig, 1u)] = d;
+          }
+        }
+      }
+      nbar_sync(kBarSort, ST);
+      const uint32_t nbig = *s_nbig;
+      for (uint32_t qq = warp; qq < nbig; qq += SW) {
+        const uint32_t g = s_bigl[qq];
+        const uint32_t b = s_cnt[g], e = s_cnt[g + 1];
+        warp_bitonic_smem(s_tail, s_idx, b, e);
+        for (uint32_t i = b + (tid & 31); i < e; i += 32) s_perm[i] = s_idx[i];
+      }
+      nbar_sync(kBarSort, ST);
+      if (perm)
+        for (uint32_t i = tid; i < s; i += ST) perm[sg.start + i] = s_perm[i];
+      if (tid == 0) s_desc[q] = make_uint2(sg.start, s);
+      __threadfence_block();
+      nbar_arrive(kBarFull + q, NT);  // bucket k is in slot q
+    }
+    // consume the gather group's last releases so no barrier is left with pending arrivals
+    for (uint32_t kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) nbar_sync(kBarEmpty + (kk & 1), NT);
+  } else {
+    // ================================================================ gather group
+    const int gw = (tid - ST) >> 5, lane = tid & 31;
+    uint8_t* stage = smem + L::kStage + (size_t)gw * 2 * kStageBytes;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+    __shared__ __align__(8) uint64_t s_mb[GW][2];
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&s_mb[gw][0]);
+    if (lane < 2) mbar_init(mb0 + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t phases = 0;
+    uint32_t k = 0;
+    for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
+      const int q = k & 1;
+      nbar_sync(kBarFull + q, NT);
+      const uint2 d = s_desc[q];
+      const uint32_t* pr = s_ring + q * CAP;
+      const uint32_t len = d.y;
+      uint8_t* ob = out + (uint64_t)d.x * kRecordBytes;
+      auto issue = [&](uint32_t g0, int st) {
+        const uint32_t cnt = min((uint32_t)kGroup, len - g0);
+        if (lane == 0) mbar_expect_tx(mb0 + 8 * st, cnt * kWindow);
+        __syncwarp();
+        if (lane < (int)cnt)
+          bulk_g2s(stage_s + st * kStageBytes + lane * kWindow,
+                   in + (((uint64_t)pr[g0 + lane] * kRecordBytes) & ~uint64_t(15)), kWindow, mb0 + 8 * st);
+      };
+      const uint32_t first = (uint32_t)gw * kGroup, stride = (uint32_t)GW * kGroup;
+      int st = 0;
+      if (first < len) issue(first, 0);
+      for (uint32_t g0 = first; g0 < len; g0 += stride) {
+        const uint32_t gn = g0 + stride;
+        if (gn < len) issue(gn, st ^ 1);
+        mbar_wait(mb0 + 8 * st, (phases >> st) & 1u);
+        phases ^= 1u << st;
+        __syncwarp();
+        const uint32_t cnt = min((uint32_t)kGroup, len - g0);
+        const uint8_t* sb = stage + st * kStageBytes;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(ob + (uint64_t)g0 * kRecordBytes);
+        const uint32_t words = cnt * kRecordWords;
+        for (uint32_t w = lane; w < words; w += 32) {
+          const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
+          const uint32_t off = (pr[g0 + r] * 4u) & 15u;
+          stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWindow + off + 4 * o));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        st ^= 1;
+      }
+      nbar_arrive(kBarEmpty + q, NT);  // slot q may be refilled
+    }
+  }
+}
+
+template <uint32_t CAP, int ST, int GW>
+cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
+                           const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
+                           const uint8_t* in, uint8_t* out, cudaStream_t s) {
+  auto kern = kd_ws_sort<CAP, ST, GW>;
+  const size_t smem = WsLayout<CAP, ST, GW>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST + 32 * GW, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
@@ -442,12 +708,19 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
   cudaError_t e;
   kd_warp_sort<<<sms * 4, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in, out);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
+  // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
   if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
                                      out, s)))
     return e;
-  if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
-                                      out, s)))
+  if (tu.kd_ws) {
+    if ((e = launch_ws_sort<2048, 256, 8>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
+                                          out, s)))
+      return e;
+  } else if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu,
+                                             sms, in, out, s))) {
     return e;
+  }
   if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
                                       out, s)))
     return e;

@@ -59,6 +59,17 @@ def test_c1_config():
     assert_parity(recs, out, perm)
 
 
+@pytest.mark.parametrize("ws", [1, 0])
+def test_medium_buckets_both_kd_forms(ws):
+    """16-bit buckets of ~1500 records (the C2 shape, scaled down by sorting on a 2-byte constant prefix
+    plus one varying byte: prefix2 sends everything into one level-1 bucket, recursion splits it into
+    ~1K-record buckets) through the warp-specialised K-d+K-e tier and the alternating one."""
+    recs = gen.records(300_007, seed=12, dist="prefix2")
+    with Options(kd_ws=ws):
+        out, perm = gpu_sort(recs)
+    assert_parity(recs, out, perm)
+
+
 def test_zero_records():
     import paper_1909_08006_b200 as ley
 
@@ -71,6 +82,8 @@ def test_zero_records():
     dict(kd_digit_bits=0, kd_insert_max=64),         # insertion sort on whole small buckets
     dict(smem_tier_max=600),                         # many big buckets -> byte-2 level
     dict(warp_tier_max=4, kd_insert_max=1),          # warp bitonic for every sub-bucket
+    dict(kd_ws=0),                                   # alternating sort/gather CTAs instead of warp-specialised
+    dict(kd_ws=0, kd_digit_bits=0),
 ])
 @pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "byte9"])
 def test_forced_thresholds(opts, dist):
