@@ -164,6 +164,10 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    bucket (Alg. 1 ComparisonSort)                   (0..12, default 12)
  *   "kd_insert_max"  K-d: sub-buckets up to this size use per-thread insertion sort, larger ones a
  *                    warp bitonic network (tinyBucketThreshold)       (1..64, default 16)
+ *   "kd_ws"          1 = warp-specialised K-d+K-e for 513..2048-record buckets (sort warps feed gather
+ *                    warps through a ring; TMA bulk record copies), 0 = alternating sort/gather CTAs
+ *   "ka_stream"      1 = K-a streams records through a TMA bulk-copy ring (one persistent CTA per SM),
+ *                    0 = one CTA per tile with direct key loads
  *   "profile"        1 = record CUDA events around every stage (ley_stage_times)
  *   "ext_run_records" external path: force the run size (records; 0 = from the budget)
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */

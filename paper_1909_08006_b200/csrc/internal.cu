@@ -75,7 +75,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
 
   // ---------------------------------------------------------------- K-a
   if ((st = prof.begin("K-a tile sort"))) return st;
-  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, s));
+  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, o.ka_stream != 0, s));
   ++launches;
   if ((st = prof.end())) return st;
 

@@ -140,6 +140,174 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
   }
 }
 
+// ---------------------------------------------------------------------------- streaming K-a
+// Same per-tile work as ka_tile_sort, restructured so the SM's record reads never wait for its compute:
+// one persistent CTA per SM streams its tiles' records through a 3-slot shared-memory ring of 512-record
+// pieces (51.2 KB each) with TMA bulk copies (cp.async.bulk + mbarrier); the key words of piece j of a
+// tile land in item j of every thread (record r = j * 512 + tid), so while a tile is ranked, scattered
+// and written, the first pieces of the next tile are already arriving.
+constexpr int kPiece = kTileThreads;                        // records per piece (one per thread)
+constexpr int kPieces = kTileRecords / kPiece;              // pieces per tile (= kTileItems)
+constexpr int kRing = 3;
+constexpr uint32_t kPieceBytes = kPiece * kRecordBytes;     // 51200
+static_assert(kPieces == kTileItems, "one piece per item");
+
+__device__ __forceinline__ void ka_mbar_init(uint32_t a, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void ka_mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ka_mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}"
+               ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void ka_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(pol) : "memory");
+}
+
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS, 1)
+    ka_tile_stream(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles, uint64_t* __restrict__ k1_out,
+                   uint32_t* __restrict__ w_out, uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
+                   uint32_t* __restrict__ hist16, uint32_t copies) {
+  constexpr int T = THREADS * ITEMS;
+  constexpr int WARPS = THREADS / 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* s_ring = smem;                                                        // [kRing][kPieceBytes]
+  uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem + kRing * kPieceBytes);     // [T]
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                        // [T]
+  uint32_t* s_wh = s_w + T;                                                     // [WARPS][256]
+  uint32_t* s_tmp = s_wh + WARPS * kRadix;                                      // [32]
+  __shared__ __align__(8) uint64_t s_full[kRing];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
+  uint64_t pol_ef, pol_el;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
+  const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(s_ring);
+  if (tid < kRing) ka_mbar_init(full0 + 8 * tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  // global piece P of this CTA = (its tile i = P / kPieces, piece j = P % kPieces)
+  const uint32_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t total_pieces = my_tiles * kPieces;
+  auto issue = [&](uint32_t P) {  // thread 0 only
+    const uint32_t t = blockIdx.x + (P / kPieces) * gridDim.x;
+    const uint64_t r0 = (uint64_t)t * T + (uint64_t)(P % kPieces) * kPiece;
+    const uint32_t slot = P % kRing;
+    uint32_t bytes = 0;
+    if (r0 < n) {
+      const uint64_t c = n - r0 < (uint64_t)kPiece ? n - r0 : (uint64_t)kPiece;
+      bytes = (uint32_t)((c * kRecordBytes) & ~uint64_t(15));  // keys of every record included (tail <= 12 B)
+    }
+    if (bytes) {
+      ka_mbar_expect_tx(full0 + 8 * slot, bytes);
+      ka_bulk_g2s(ring0 + slot * kPieceBytes, in + r0 * kRecordBytes, bytes, full0 + 8 * slot, pol_ef);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * slot) : "memory");
+    }
+  };
+  if (tid == 0)
+    for (uint32_t P = 0; P < (uint32_t)kRing && P < total_pieces; ++P) issue(P);
+
+  for (uint32_t i = 0; i < my_tiles; ++i) {
+    const uint32_t t = blockIdx.x + i * gridDim.x;
+    const uint64_t base = (uint64_t)t * T;
+    const uint32_t cnt_t = (uint32_t)(n - base < (uint64_t)T ? n - base : (uint64_t)T);
+    for (int q = tid; q < WARPS * kRadix; q += THREADS) s_wh[q] = 0;
+    // ---- 1. keys of piece j -> item j (record r = j * THREADS + tid)
+    uint32_t a[ITEMS], b[ITEMS], c[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t P = i * kPieces + j;
+      const uint32_t slot = P % kRing;
+      ka_mbar_wait(full0 + 8 * slot, (P / kRing) & 1u);
+      const uint32_t r = j * THREADS + tid;
+      if (r < cnt_t) {
+        const uint32_t* kw = reinterpret_cast<const uint32_t*>(s_ring + slot * kPieceBytes + tid * kRecordBytes);
+        a[j] = kw[0];
+        b[j] = kw[1];
+        c[j] = kw[2];
+      } else {
+        a[j] = b[j] = c[j] = 0;
+      }
+      __syncthreads();  // every thread has its key words: the slot may be refilled
+      if (tid == 0 && P + kRing < total_pieces) issue(P + kRing);
+    }
+
+    // ---- 2. warp multi-split ranking on byte 0
+    uint32_t rank[ITEMS];
+    uint32_t* wh = s_wh + warp * kRadix;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t r = j * THREADS + tid;
+      const bool valid = r < cnt_t;
+      const uint32_t hi = bswap32(a[j]);
+      const uint32_t d = hi >> 24;
+      const uint32_t peers = warp_peers8(d, valid);
+      const uint32_t before = __popc(peers & lt);
+      const uint32_t cur = valid ? wh[d] : 0;
+      __syncwarp();
+      if (valid && before == 0) wh[d] = cur + __popc(peers);
+      __syncwarp();
+      rank[j] = cur + before;
+      const uint32_t p16 = hi >> 16;
+      const uint32_t peers16 = peers & warp_peers8((hi >> 16) & 0xFFu, valid);
+      if (valid && __popc(peers16 & lt) == 0)
+        asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(&hist_copy[p16]),
+                     "r"((uint32_t)__popc(peers16)), "l"(pol_el) : "memory");
+    }
+    __syncthreads();
+
+    // ---- 3. per-digit totals over warps, tile exclusive offsets
+    uint32_t total = 0;
+    if (tid < kRadix) {
+#pragma unroll 4
+      for (int w = 0; w < WARPS; ++w) {
+        const uint32_t v = s_wh[w * kRadix + tid];
+        s_wh[w * kRadix + tid] = total;
+        total += v;
+      }
+    }
+    const uint32_t excl = block_excl_scan<THREADS>(tid < kRadix ? total : 0, s_tmp, nullptr);
+    if (tid < kRadix) {
+#pragma unroll 4
+      for (int w = 0; w < WARPS; ++w) s_wh[w * kRadix + tid] += excl;
+      cnt[(uint64_t)tid * tiles + t] = total;
+      lo[(uint64_t)t * kRadix + tid] = excl;
+    }
+    __syncthreads();
+
+    // ---- 4. scatter into shared memory in byte-0 order
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t r = j * THREADS + tid;
+      if (r < cnt_t) {
+        const uint32_t hi = bswap32(a[j]);
+        const uint32_t d = hi >> 24;
+        const uint32_t pos = wh[d] + rank[j];
+        const uint64_t kk = ((uint64_t)hi << 32) | bswap32(b[j]);
+        s_k1[pos] = (kk << 8) | (c[j] & 0xFFu);
+        s_w[pos] = ((c[j] >> 8) & 0xFFu) << 24 | r;
+      }
+    }
+    __syncthreads();
+
+    // ---- 5. coalesced write-out
+    for (uint32_t q = tid; q < cnt_t; q += THREADS) {
+      k1_out[base + q] = s_k1[q];
+      w_out[base + q] = s_w[q];
+    }
+    __syncthreads();  // staging and per-warp counters reused by the next tile
+  }
+}
+
 }  // namespace
 
 size_t ka_smem_bytes() {
@@ -147,11 +315,25 @@ size_t ka_smem_bytes() {
 }
 
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
-                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, cudaStream_t s) {
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
+                                cudaStream_t s) {
   auto kern = ka_tile_sort<kTileThreads, kTileItems>;
   size_t smem = ka_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (stream_form) {
+    auto sk = ka_tile_stream<kTileThreads, kTileItems>;
+    const size_t ssm = (size_t)kRing * kPieceBytes + (size_t)kTileRecords * 12 +
+                       (size_t)(kTileThreads / 32) * kRadix * 4 + 32 * 4;
+    e = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
+    sk<<<grid, kTileThreads, ssm, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies);
+    return cudaGetLastError();
+  }
   kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies);
   return cudaGetLastError();
 }

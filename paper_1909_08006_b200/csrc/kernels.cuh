@@ -11,7 +11,8 @@ namespace ley {
 // K-a (k_tile.cu)
 size_t ka_smem_bytes();
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
-                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, cudaStream_t s);
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
+                                cudaStream_t s);
 
 // K-b (k_scan.cu)
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,

@@ -41,6 +41,7 @@ struct Options {
   int64_t kd_digit_bits = 12;
   int64_t kd_insert_max = 16;
   int64_t kd_ws = 1;
+  int64_t ka_stream = 1;
   int64_t profile = 0;
   int64_t ext_run_records = 0;
   int64_t l2_fetch_bytes = 0;  // 0 = leave the device default; else cudaLimitMaxL2FetchGranularity

@@ -44,6 +44,17 @@ def test_uniform_sizes(n):
     assert_parity(recs, out, perm)
 
 
+@pytest.mark.parametrize("n", [1, 511, 513, 4095, 4097, 600_001, 606_209])
+def test_ka_forms_ragged(n):
+    """Both K-a forms on ragged sizes: partial 512-record pieces (bulk copies rounded down to 16 bytes),
+    partial tiles, and more tiles than SMs (several tiles per persistent CTA)."""
+    recs = gen.records(n, seed=n + 1, dist="skewed")
+    for ks in (1, 0):
+        with Options(ka_stream=ks):
+            out, perm = gpu_sort(recs)
+        assert_parity(recs, out, perm)
+
+
 @pytest.mark.parametrize("dist", DISTS)
 @pytest.mark.parametrize("n", [4097, 100_003])
 def test_distributions(dist, n):
@@ -84,6 +95,7 @@ def test_zero_records():
     dict(warp_tier_max=4, kd_insert_max=1),          # warp bitonic for every sub-bucket
     dict(kd_ws=0),                                   # alternating sort/gather CTAs instead of warp-specialised
     dict(kd_ws=0, kd_digit_bits=0),
+    dict(ka_stream=0),                               # K-a: one CTA per tile, direct key loads
 ])
 @pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "byte9"])
 def test_forced_thresholds(opts, dist):
