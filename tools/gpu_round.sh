@@ -15,5 +15,5 @@ for spec in "c1 1e6 uniform 0" "c2 1e8 uniform 1" "c3 2e8 skewed 2" "c4 6e8 unif
     python tools/profile_step.py --n $2 --dist $3 --seed $4 --steps 1 --warmup 1 > gpurun_out/ncu_$1.log 2>&1
 done
 python tools/profile_step.py --n 1e8 --steps 1 --warmup 1 > gpurun_out/plain_full.log 2>&1 && \
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:kd_cta_sort -s 1 -c 1 \
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"kd_ws_sort|ka_tile_stream" -s 2 -c 2 \
   -o gpurun_out/full_kde_c2 python tools/profile_step.py --n 1e8 --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1

@@ -11,7 +11,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = [("ka_tile_sort", "K-a tile sort"), ("kb_", "K-b scan"), ("kc_plan_chunks", "K-b scan"),
+STAGE = [("ka_tile", "K-a tile sort"), ("kb_", "K-b scan"), ("kc_plan_chunks", "K-b scan"),
          ("kc_", "K-c split"), ("kr_", "K-c' split"), ("kd_", "K-de sort+gather")]
 
 
@@ -33,7 +33,7 @@ def summarise(path, n):
         key = (int(r[hdr["ID"]]), r[hdr["Kernel Name"]])
         data.setdefault(key, {})[r[hdr["Metric Name"]]] = float(r[hdr["Metric Value"]].replace(",", ""))
     launches = sorted(data.items())
-    firsts = [i for i, ((_, k), _) in enumerate(launches) if "ka_tile_sort" in k]
+    firsts = [i for i, ((_, k), _) in enumerate(launches) if "ka_tile" in k]
     sel = launches[firsts[1]:] if len(firsts) > 1 else launches
     out = {}
     for (_, k), m in sel:
