@@ -219,7 +219,9 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
   quiet.stream = s;
   ley_status st = sort_internal_device(ctx, all_cand, sorted, perm, total_cand, s, quiet, work, L.bytes);
   if (st) return st;
-  // first sorted index of each boundary bin = candidates in smaller boundary bins
+  // first sorted index of each boundary bin = candidates in smaller boundary bins; all splitters' key
+  // bytes and sorted positions are read back in one batch, then their global ordinals in a second
+  std::vector<uint64_t> at(nspl);
   for (int k = 0; k < nspl; ++k) {
     uint64_t start = 0;
     std::vector<uint32_t> seen;
@@ -229,19 +231,25 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
         seen.push_back(P.bins[j]);
       }
     }
-    const uint64_t at = start + P.rho[k];
-    uint8_t key[12] = {0};
-    uint32_t p = 0, g = 0;
-    LEY_CUDA("K-s splitters", cudaMemcpyAsync(key, sorted + at * kRecordBytes, 10, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&p, perm + at, 4, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
-    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&g, all_gidx + p, 4, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
+    at[k] = start + P.rho[k];
+  }
+  uint8_t keys[kMaxRanks][12] = {};
+  uint32_t pidx[kMaxRanks] = {}, gidx[kMaxRanks] = {};
+  for (int k = 0; k < nspl; ++k) {
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(keys[k], sorted + at[k] * kRecordBytes, 10, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&pidx[k], perm + at[k], 4, cudaMemcpyDeviceToHost, s));
+  }
+  LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
+  for (int k = 0; k < nspl; ++k)
+    LEY_CUDA("K-s splitters", cudaMemcpyAsync(&gidx[k], all_gidx + pidx[k], 4, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("K-s splitters", cudaStreamSynchronize(s));
+  for (int k = 0; k < nspl; ++k) {
+    const uint8_t* key = keys[k];
     DistSplitter& d = P.spl[k];
     d.hi = ((uint32_t)key[0] << 24) | ((uint32_t)key[1] << 16) | ((uint32_t)key[2] << 8) | key[3];
     d.mid = ((uint32_t)key[4] << 24) | ((uint32_t)key[5] << 16) | ((uint32_t)key[6] << 8) | key[7];
     d.lo16 = ((uint32_t)key[8] << 8) | key[9];
-    d.gidx = g;
+    d.gidx = gidx[k];
   }
   return LEY_OK;
 }
