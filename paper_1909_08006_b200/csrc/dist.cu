@@ -123,6 +123,7 @@ struct RankState {
   DistSplitter* d_spl = nullptr;     // [kMaxRanks]
   uint32_t* d_bins = nullptr;        // [kMaxRanks]
   uint8_t* d_send = nullptr;         // n records
+  uint16_t* d_pref = nullptr;        // n 16-bit key prefixes (K-s0 -> K-s1)
   uint8_t* d_recv = nullptr;         // received records
   uint64_t recv_cap = 0;
   // host side
@@ -159,7 +160,7 @@ ley_status rank_alloc(RankState& r) {
   const size_t o_hist = take(4 * 65536), o_status = take(8 * status_words), o_small = take(256),
                o_cand = take(cand_cap * kRecordBytes), o_cgidx = take(4 * cand_cap), o_dcount = take(8 * kMaxRanks),
                o_sbase = take(8 * kMaxRanks), o_spl = take(sizeof(DistSplitter) * kMaxRanks),
-               o_bins = take(4 * kMaxRanks), o_send = take(n * kRecordBytes);
+               o_bins = take(4 * kMaxRanks), o_send = take(n * kRecordBytes), o_pref = take(2 * n);
   if (r.buf.cap < o) {
     if (r.buf.ptr) cudaFree(r.buf.ptr);
     r.buf.ptr = nullptr;
@@ -178,13 +179,14 @@ ley_status rank_alloc(RankState& r) {
   r.d_spl = reinterpret_cast<DistSplitter*>(b + o_spl);
   r.d_bins = reinterpret_cast<uint32_t*>(b + o_bins);
   r.d_send = b + o_send;
+  r.d_pref = reinterpret_cast<uint16_t*>(b + o_pref);
   return LEY_OK;
 }
 
 // ---------------------------------------------------------------------------- phases (one rank)
 ley_status phase1_hist(RankState& r) {
   LEY_CUDA("K-s0 hist", cudaMemsetAsync(r.d_hist, 0, 4 * 65536, r.s));
-  LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.ctx->sms, r.s));
+  LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.d_pref, r.ctx->sms, r.s));
   return LEY_OK;
 }
 
@@ -193,7 +195,7 @@ ley_status phase2_candidates(RankState& r, const Plan& P) {
   LEY_CUDA("K-s1 candidates", cudaMemcpyAsync(r.d_bins, P.bins, 4 * std::max(nspl, 1), cudaMemcpyHostToDevice, r.s));
   LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_small, 0, 256, r.s));
   LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_status, 0, 8 * (ks_candidate_tiles(r.n) + 1), r.s));
-  LEY_CUDA("K-s1 candidates", launch_ks_candidates(r.in, r.n, (uint32_t)r.gbase, r.d_bins, nspl, r.d_status,
+  LEY_CUDA("K-s1 candidates", launch_ks_candidates(r.in, r.d_pref, r.n, (uint32_t)r.gbase, r.d_bins, nspl, r.d_status,
                                                    r.d_small + 0, r.d_cand, r.d_cand_gidx, r.d_small + 1, r.s));
   uint32_t* h = static_cast<uint32_t*>(r.ctx->host_pinned);
   LEY_CUDA("K-s1 candidates", cudaMemcpyAsync(h, r.d_small + 1, 4, cudaMemcpyDeviceToHost, r.s));

@@ -53,14 +53,18 @@ __device__ __forceinline__ uint32_t dest_of(uint32_t hi, uint32_t mid, uint32_t 
 }
 
 // ------------------------------------------------------------------------------------------ K-s0
-__global__ void __launch_bounds__(256) ks_hist16(const uint8_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ hist) {
+// Also keeps every record's 16-bit prefix (2 B/record, coalesced) so that K-s1 finds the boundary-bin
+// records from the prefixes instead of reading every record's key line again (~100 B/record).
+__global__ void __launch_bounds__(256) ks_hist16(const uint8_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ hist,
+                                                 uint16_t* __restrict__ pref) {
   const uint32_t lt = lanemask_lt();
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = base + threadIdx.x;
     const bool valid = i < n;
-    uint32_t hi = 0, mid, lo16;
-    if (valid) load_key(in, i, hi, mid, lo16);
+    uint32_t hi = 0;
+    if (valid) hi = bswap32(__ldg(reinterpret_cast<const uint32_t*>(in + i * kRecordBytes)));
     const uint32_t p16 = hi >> 16;
+    if (valid) pref[i] = (uint16_t)p16;
     const uint32_t peers = warp_peers8(p16 & 0xFFu, valid) & warp_peers8(p16 >> 8, valid);
     if (valid && __popc(peers & lt) == 0) atomicAdd(&hist[p16], (uint32_t)__popc(peers));
   }
@@ -72,7 +76,8 @@ constexpr int kCandItems = 8;
 constexpr uint32_t kCandTile = kCandThreads * kCandItems;
 
 __global__ void __launch_bounds__(kCandThreads)
-    ks_candidates(const uint8_t* __restrict__ in, uint64_t n, uint32_t gbase, const uint32_t* __restrict__ bins,
+    ks_candidates(const uint8_t* __restrict__ in, const uint16_t* __restrict__ pref16, uint64_t n, uint32_t gbase,
+                  const uint32_t* __restrict__ bins,
                   int nbins, uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, uint8_t* __restrict__ cand,
                   uint32_t* __restrict__ cand_gidx, uint32_t* __restrict__ cand_count) {
   __shared__ uint32_t s_tmp[32];
@@ -90,8 +95,7 @@ __global__ void __launch_bounds__(kCandThreads)
   for (int j = 0; j < kCandItems; ++j) {
     const uint64_t i = base + threadIdx.x * kCandItems + j;
     if (i < n) {
-      const uint32_t p16 = __ldg(reinterpret_cast<const uint32_t*>(in + i * kRecordBytes));
-      const uint32_t pref = ((p16 & 0xFFu) << 8) | ((p16 >> 8) & 0xFFu);
+      const uint32_t pref = __ldg(pref16 + i);
       bool f = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) f |= (pref == s_bins[k]);
@@ -283,19 +287,20 @@ unsigned grid_cap(uint64_t items, int per_block, int sms, int per_sm) {
 
 }  // namespace
 
-cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, int sms, cudaStream_t s) {
+cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, int sms, cudaStream_t s) {
   if (!n) return cudaSuccess;
-  ks_hist16<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(in, n, hist);
+  ks_hist16<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(in, n, hist, pref);
   return cudaGetLastError();
 }
 
 uint64_t ks_candidate_tiles(uint64_t n) { return (n + kCandTile - 1) / kCandTile; }
 
-cudaError_t launch_ks_candidates(const uint8_t* in, uint64_t n, uint32_t gbase, const uint32_t* bins, int nbins,
+cudaError_t launch_ks_candidates(const uint8_t* in, const uint16_t* pref, uint64_t n, uint32_t gbase,
+                                 const uint32_t* bins, int nbins,
                                  uint64_t* status, uint32_t* ticket, uint8_t* cand, uint32_t* cand_gidx,
                                  uint32_t* cand_count, cudaStream_t s) {
   if (!n) return cudaSuccess;
-  ks_candidates<<<(unsigned)ks_candidate_tiles(n), kCandThreads, 0, s>>>(in, n, gbase, bins, nbins, status, ticket,
+  ks_candidates<<<(unsigned)ks_candidate_tiles(n), kCandThreads, 0, s>>>(in, pref, n, gbase, bins, nbins, status, ticket,
                                                                           cand, cand_gidx, cand_count);
   return cudaGetLastError();
 }

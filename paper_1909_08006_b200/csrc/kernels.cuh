@@ -49,9 +49,10 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
                           uint8_t* out, cudaStream_t s, int* launches);
 
 // multi-GPU (k_dist.cu)
-cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, int sms, cudaStream_t s);
+cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, int sms, cudaStream_t s);
 uint64_t ks_candidate_tiles(uint64_t n);
-cudaError_t launch_ks_candidates(const uint8_t* in, uint64_t n, uint32_t gbase, const uint32_t* bins, int nbins,
+cudaError_t launch_ks_candidates(const uint8_t* in, const uint16_t* pref, uint64_t n, uint32_t gbase,
+                                 const uint32_t* bins, int nbins,
                                  uint64_t* status, uint32_t* ticket, uint8_t* cand, uint32_t* cand_gidx,
                                  uint32_t* cand_count, cudaStream_t s);
 cudaError_t launch_ks_dest_counts(const uint8_t* cand, const uint32_t* cand_gidx, uint32_t ncand,
