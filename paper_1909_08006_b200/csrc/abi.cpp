@@ -231,12 +231,9 @@ ley_status ley_sort_submit(const void* in, void* out, uint64_t n_records, uint32
   const uint64_t need = 4 * (uint64_t)a + plan_internal(n_records).bytes;  // two slots (in | out) + scratch
   if (device_budget_bytes && need > device_budget_bytes)  // does not fit twice: the blocking path decides
     return ley_sort(in, out, n_records, record_bytes, key_bytes, device_budget_bytes, stream);
-  DeviceContext& ctx = device_context(dev);
-  std::lock_guard<std::mutex> guard(ctx.mu);
-  ctx.device = dev;
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (sms > 0) ctx.sms = sms;
+  DeviceContext& ctx = device_context(dev);  // (device index and SM count are set on creation)
+  // the pipeline has its own lock; its worker takes ctx.mu for each sort. Not taking ctx.mu here keeps a
+  // submit from waiting for the previous call's sort to finish.
   return sort_submit(ctx, static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), n_records,
                      static_cast<cudaStream_t>(stream));
 }
@@ -250,7 +247,6 @@ ley_status ley_sort_drain(void) {
     return LEY_ERR_CUDA;
   }
   DeviceContext& ctx = device_context(dev);
-  std::lock_guard<std::mutex> guard(ctx.mu);
   return sort_drain(ctx);
 }
 

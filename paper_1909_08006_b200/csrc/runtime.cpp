@@ -183,6 +183,11 @@ DeviceContext& device_context(int device) {
   if (!g_ctx[device]) {
     g_ctx[device].reset(new DeviceContext());
     g_ctx[device]->device = device;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+      g_ctx[device]->sms = sms;
+    else
+      cudaGetLastError();
   }
   return *g_ctx[device];
 }
@@ -214,6 +219,7 @@ void release_device(int device) {
     if (device >= 0 && d != device) continue;
     if (!g_ctx[d]) continue;
     DeviceContext& c = *g_ctx[d];
+    pipe_release(c);  // stops the streaming worker first (it takes c.mu for its sorts)
     std::lock_guard<std::mutex> g2(c.mu);
     int prev = 0;
     cudaGetDevice(&prev);
@@ -238,7 +244,6 @@ void release_device(int device) {
     }
     for (cudaEvent_t e : c.events) cudaEventDestroy(e);
     c.events.clear();
-    pipe_release(c);
     cudaSetDevice(prev);
   }
 }

@@ -5,7 +5,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <condition_variable>
+#include <deque>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -90,16 +93,41 @@ struct DeviceContext {
   static constexpr int kExtEvents = 8;
   cudaEvent_t ev[kExtEvents] = {};
   std::vector<cudaEvent_t> events;
-  // streaming host sort (ley_sort_submit): two device staging slots (in | out) and three streams, so the
-  // H2D of call k+1, the sort of call k and the D2H of call k-1 overlap
+  // streaming host sort (ley_sort_submit): two device staging slots (in | out), three streams and a
+  // worker thread, so the H2D of call k+1, the sort of call k and the D2H of call k-1 all overlap
   struct Pipe {
+    struct Job {
+      uint64_t k;
+      uint8_t* din;
+      uint8_t* dout;
+      uint8_t* out;
+      uint64_t n;
+    };
     bool init = false;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     DeviceBuffer slot[2];
     cudaEvent_t user = nullptr;
     cudaEvent_t copied_in[2] = {nullptr, nullptr}, sorted[2] = {nullptr, nullptr}, copied_out[2] = {nullptr, nullptr};
-    bool used[2] = {false, false};
-    int next = 0;
+    uint64_t submitted = 0;   // calls whose H2D is enqueued (call k uses slot k & 1)
+    uint64_t sort_done = 0;   // calls whose sort + D2H the worker has enqueued (in order)
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<Job> q;
+    std::thread worker;
+    bool stop = false, busy = false;
+    ley_status err = LEY_OK;
+    std::string err_msg;
+    ~Pipe() {  // process exit: stop the worker (no CUDA calls here)
+      if (worker.joinable()) {
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          stop = true;
+          q.clear();
+        }
+        cv.notify_all();
+        worker.join();
+      }
+    }
   } pipe;
 };
 DeviceContext& device_context(int device);
