@@ -161,6 +161,14 @@ def test_streaming_submit_pipeline():
     d = torch.from_numpy(recs).cuda()
     assert ley.ley_sort_submit(d, torch.empty_like(d), 50_000, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
     ley.ley_sort_drain()
+    # releasing the cache stops the pipeline's worker; the next submit starts a fresh one; drain is idempotent
+    ley.ley_release_cache(-1)
+    ley.ley_sort_drain()
+    out.fill_(0)
+    ley.ley_sort_submit(x, out, 50_000)
+    ley.ley_release_cache(-1)  # with a call in flight: its sort and copy complete before the worker stops
+    assert_parity(recs, out.numpy())
+    ley.ley_sort_drain()
 
 
 def test_pageable_rejected():
