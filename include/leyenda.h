@@ -179,10 +179,30 @@ ley_status ley_get_option(const char* name, int64_t* value);
  * is written to *launches. */
 int ley_stage_times(const char** names, float* ms, int max, int* launches);
 
+/* Device memory held by the library (all devices; the cached arena, staging slots, dist buffers) and its
+ * high-water mark since the last reset (reset_peak != 0 resets it to the current value). Lets callers and
+ * tests check that a call stayed within device_budget_bytes. */
+ley_status ley_device_bytes(uint64_t* current_bytes, uint64_t* peak_bytes, int reset_peak);
+
 /* Free the cached arena of `device` (-1 = all devices). */
 ley_status ley_release_cache(int device);
 
 uint32_t ley_version(void); /* (major << 16) | minor */
+
+/* ---------------------------------------------------------------- kernel verification hooks
+ * Single kernels of the path on caller-provided DEVICE buffers, checked by the tests
+ * against CPU models. Synchronous. Not performance paths.
+ * ley_test_scan_excl — K-b, the decoupled-look-back exclusive scan ("where each key should be
+ *   placed"): out[i] = sum of in[0..i), out[m] = total. in: u32[m]; out: u32[m + 1].
+ * ley_test_tile_sort — K-a on n records (P:59 ParallelRadixSort radix 0, P:102 extraction), 4096-record
+ *   tiles t = 0..T-1, T = ceil(n / 4096): k1/w = u64[n] / u32[n] (each tile's pairs in byte-0 order:
+ *   k1 = key bytes 1..8 big-endian, w = key byte 9 << 24 | index inside the tile), cnt = u32[256 * T]
+ *   (cnt[b * T + t] = records of tile t with byte 0 = b), lo = u32[T * 256] (tile-local exclusive offsets),
+ *   hist16 = u32[65536] (zeroed, then the count of every 2-byte prefix). stream_form: 1 = the streaming
+ *   form (TMA ring), 0 = one CTA per tile. */
+ley_status ley_test_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, void* stream);
+ley_status ley_test_tile_sort(const void* in, uint64_t n, uint64_t* k1, uint32_t* w, uint32_t* cnt, uint32_t* lo,
+                              uint32_t* hist16, int stream_form, void* stream);
 
 #ifdef __cplusplus
 }

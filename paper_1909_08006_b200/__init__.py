@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
                     "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
                     "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange",
-                    "ley_sort_submit", "ley_sort_drain")
+                    "ley_sort_submit", "ley_sort_drain", "ley_test_scan_excl", "ley_test_tile_sort", "ley_device_bytes")
 
 
 class ley_plan_info(ctypes.Structure):
@@ -61,6 +61,12 @@ _lib.ley_sort_submit.argtypes = [_vp, _vp, _u64, _u32, _u32, _u64, _vp]
 _lib.ley_sort_submit.restype = _i32
 _lib.ley_sort_drain.argtypes = []
 _lib.ley_sort_drain.restype = _i32
+_lib.ley_test_scan_excl.argtypes = [_vp, _vp, _u64, _vp]
+_lib.ley_test_scan_excl.restype = _i32
+_lib.ley_test_tile_sort.argtypes = [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _i32, _vp]
+_lib.ley_test_tile_sort.restype = _i32
+_lib.ley_device_bytes.argtypes = [ctypes.POINTER(_u64), ctypes.POINTER(_u64), _i32]
+_lib.ley_device_bytes.restype = _i32
 _lib.ley_last_error.argtypes = []
 _lib.ley_last_error.restype = ctypes.c_char_p
 _lib.ley_comm_get_unique_id.argtypes = [_vp]
@@ -277,3 +283,22 @@ def ley_dist_plan_exchange(send_counts, nranks: int, rank: int):
 
 def library_path() -> str:
     return _LIB_PATH
+
+
+def ley_test_scan_excl(in_, out, m: int, stream=None) -> int:
+    """C: ley_test_scan_excl(in, out, m, stream) — K-b alone (verification hook)."""
+    return _check(_lib.ley_test_scan_excl(_addr(in_), _addr(out), m, _stream(stream)), "ley_test_scan_excl", True)
+
+
+def ley_test_tile_sort(in_, n: int, k1, w, cnt, lo, hist16, stream_form: int = 1, stream=None) -> int:
+    """C: ley_test_tile_sort(in, n, k1, w, cnt, lo, hist16, stream_form, stream) — K-a alone (verification hook)."""
+    st = _lib.ley_test_tile_sort(_addr(in_), n, _addr(k1), _addr(w), _addr(cnt), _addr(lo), _addr(hist16),
+                                 stream_form, _stream(stream))
+    return _check(st, "ley_test_tile_sort", True)
+
+
+def ley_device_bytes(reset_peak: bool = False) -> tuple[int, int]:
+    """C: ley_device_bytes(&current, &peak, reset_peak) -> (current, peak) bytes held by the library."""
+    cur, peak = _u64(), _u64()
+    _check(_lib.ley_device_bytes(ctypes.byref(cur), ctypes.byref(peak), int(reset_peak)), "ley_device_bytes", True)
+    return cur.value, peak.value

@@ -119,6 +119,12 @@ int ley_stage_times(const char** names, float* ms, int max, int* launches) {
   return stage_times(names, ms, max, launches);
 }
 
+ley_status ley_device_bytes(uint64_t* current_bytes, uint64_t* peak_bytes, int reset_peak) {
+  clear_error();
+  device_bytes(current_bytes, peak_bytes, reset_peak != 0);
+  return LEY_OK;
+}
+
 ley_status ley_release_cache(int device) {
   clear_error();
   release_device(device);

@@ -136,7 +136,10 @@ struct RankState {
   DeviceBuffer cand_buf, split_buf, recv_buf;
   ~RankState() {
     for (DeviceBuffer* b : {&buf, &cand_buf, &split_buf, &recv_buf})
-      if (b->ptr) cudaFree(b->ptr);
+      if (b->ptr) {
+        cudaFree(b->ptr);
+        track_device_bytes(-(int64_t)b->cap);
+      }
   }
 };
 
@@ -162,11 +165,15 @@ ley_status rank_alloc(RankState& r) {
                o_sbase = take(8 * kMaxRanks), o_spl = take(sizeof(DistSplitter) * kMaxRanks),
                o_bins = take(4 * kMaxRanks), o_send = take(n * kRecordBytes), o_pref = take(2 * n);
   if (r.buf.cap < o) {
-    if (r.buf.ptr) cudaFree(r.buf.ptr);
+    if (r.buf.ptr) {
+      cudaFree(r.buf.ptr);
+      track_device_bytes(-(int64_t)r.buf.cap);
+    }
     r.buf.ptr = nullptr;
     r.buf.cap = 0;
     LEY_CUDA("dist alloc", cudaMalloc(&r.buf.ptr, o));
     r.buf.cap = o;
+    track_device_bytes((int64_t)o);
   }
   uint8_t* b = static_cast<uint8_t*>(r.buf.ptr);
   r.d_hist = reinterpret_cast<uint32_t*>(b + o_hist);

@@ -252,7 +252,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   // ---------------------------------------------------------------- device buffer plan (within budget)
   // run generation: run in (100 C) + run out (100 C) + internal workspace(C) + samples
   const InternalLayout LC = plan_internal(C);
-  const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>(4096, C / 16));  // sample stride
+  const uint64_t S = external_sample_stride(n, C, budget);  // sample stride (bounds every partition)
   uint64_t nsamp = 0;
   std::vector<uint64_t> run_off(R), run_len(R), samp_base(R);
   for (uint32_t r = 0; r < R; ++r) {
@@ -368,11 +368,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   // merge-phase device plan: a partition of m records needs two slots of slice (100 m) + out (100 m)
   // (partition p+1 streams in and p-1 streams out while p merges) + 2 x 16 m composites (+ 16 m perm);
   // keep it inside the same budget as phase 1.
-  const size_t per_rec = 4 * kRecordBytes + 32 + (perm_out ? 16 : 0);
-  const size_t lists = 7ull * 16 * std::min<uint64_t>(65536, C) + (2u << 20);
-  const size_t avail = std::max<size_t>(budget > lists ? budget - lists : 0, per_rec * 1024);
-  uint64_t m_target = std::max<uint64_t>(1024, avail / per_rec);
-  // samples between splitters q: partition size <= (q + R) * S
+  const uint64_t m_target = external_merge_target(C, budget);
   uint64_t q = m_target / S > 2ull * R ? m_target / S - R : std::max<uint64_t>(1, m_target / (2 * S));
   if (q == 0) q = 1;
   const uint32_t P = (uint32_t)std::max<uint64_t>(1, (nsamp + q - 1) / q);

@@ -1,6 +1,8 @@
 // runtime.cpp — errors, options, planning, device arena and profiling for libleyenda (host C++).
 #include "runtime.h"
 
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -119,13 +121,32 @@ InternalLayout plan_internal(uint64_t n) {
   return L;
 }
 
-// External path: the largest run C (records) whose run-generation working set fits the
-// budget: two slots of run in + run out (400 C; run r+1 streams in and run r-1 streams out while run r
-// sorts) + the internal sort's workspace and K-d lists for C records + two runs' perms (8 C) + the
-// sample buffers (every S-th record of every run, S = min(4096, C/16)) + 2 MB slack.
-uint64_t external_run_need(uint64_t n, uint64_t C) {
+// External path planning, shared by the planner and the driver.
+// Phase 2 (merge): a partition of m records needs two slots of slice + output (400 m), composites (32 m)
+// and perms (16 m, when requested): m_target = (budget - K-d lists - 2 MB) / 448.
+// Sample stride S: every S-th record of every sorted run is a sample; a partition between two splitters
+// holds at most (q + R) S records (q samples apart, plus up to one sample interval from each of the R
+// runs), so S <= m_target / (2 R) keeps every partition within m_target.
+uint64_t external_merge_target(uint64_t C, uint64_t budget) {
+  const uint64_t lists = 7ull * 16 * std::min<uint64_t>(65536, C) + (2ull << 20);
+  const uint64_t per_rec = 4 * kRecordBytes + 32 + 16;
+  const uint64_t avail = std::max<uint64_t>(budget > lists ? budget - lists : 0, per_rec * 1024);
+  return std::max<uint64_t>(1024, avail / per_rec);
+}
+uint64_t external_sample_stride(uint64_t n, uint64_t C, uint64_t budget) {
+  if (C == 0) return 1;
+  const uint64_t R = (n + C - 1) / C;
+  uint64_t S = std::min<uint64_t>(4096, C / 16);
+  if (budget) S = std::min<uint64_t>(S, external_merge_target(C, budget) / (2 * R));
+  return std::max<uint64_t>(1, S);
+}
+// Phase 1 (runs): the largest run C (records) whose run-generation working set fits the budget: two
+// slots of run in + run out (400 C; run r+1 streams in and run r-1 streams out while run r sorts) + the
+// internal sort's workspace and K-d lists for C records + two runs' perms (8 C) + the samples and their
+// sort + 2 MB slack.
+uint64_t external_run_need(uint64_t n, uint64_t C, uint64_t budget) {
   if (C == 0) return 0;
-  const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>(4096, C / 16));
+  const uint64_t S = external_sample_stride(n, C, budget);
   const uint64_t runs = (n + C - 1) / C;
   const uint64_t nsamp = runs * ((C + S - 1) / S);
   const uint64_t lists = 6ull * 16 * std::min<uint64_t>(65536, C) + 16ull * std::min<uint64_t>(65536, C);
@@ -139,7 +160,7 @@ uint64_t external_run_records(uint64_t n, uint64_t budget) {
   uint64_t lo = 0, hi = std::min<uint64_t>(n, 0xFFFFFFFEull);
   while (lo < hi) {
     uint64_t mid = lo + (hi - lo + 1) / 2;
-    if (external_run_need(n, mid) <= budget) lo = mid; else hi = mid - 1;
+    if (external_run_need(n, mid, budget) <= budget) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -192,11 +213,28 @@ DeviceContext& device_context(int device) {
   return *g_ctx[device];
 }
 
+// Device bytes held by the library's cached buffers (all devices) and their high-water mark.
+namespace {
+std::atomic<uint64_t> g_dev_bytes{0}, g_dev_peak{0};
+}
+void track_device_bytes(int64_t delta) {
+  const uint64_t now = g_dev_bytes.fetch_add((uint64_t)delta) + (uint64_t)delta;
+  uint64_t pk = g_dev_peak.load();
+  while (now > pk && !g_dev_peak.compare_exchange_weak(pk, now)) {
+  }
+}
+void device_bytes(uint64_t* current, uint64_t* peak, bool reset_peak) {
+  if (current) *current = g_dev_bytes.load();
+  if (peak) *peak = g_dev_peak.load();
+  if (reset_peak) g_dev_peak.store(g_dev_bytes.load());
+}
+
 ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s) {
   if (b.cap >= bytes && b.ptr) return LEY_OK;
   if (b.ptr) {
     LEY_CUDA(what, cudaStreamSynchronize(s));
     LEY_CUDA(what, cudaFree(b.ptr));
+    track_device_bytes(-(int64_t)b.cap);
     b.ptr = nullptr;
     b.cap = 0;
   }
@@ -210,6 +248,9 @@ ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaSt
     return LEY_ERR_CUDA;
   }
   b.cap = want;
+  track_device_bytes((int64_t)want);
+  if (getenv("LEY_DEBUG_ALLOC")) fprintf(stderr, "[ley alloc] %s: %zu bytes (held %llu)\n", what, want,
+                                         (unsigned long long)g_dev_bytes.load());
   return LEY_OK;
 }
 
@@ -225,7 +266,10 @@ void release_device(int device) {
     cudaGetDevice(&prev);
     cudaSetDevice(d);
     for (DeviceBuffer* b : {&c.work, &c.lists, &c.big[0], &c.big[1], &c.rec, &c.stage, &c.ext}) {
-      if (b->ptr) cudaFree(b->ptr);
+      if (b->ptr) {
+        cudaFree(b->ptr);
+        track_device_bytes(-(int64_t)b->cap);
+      }
       b->ptr = nullptr;
       b->cap = 0;
     }

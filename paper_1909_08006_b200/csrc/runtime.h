@@ -68,6 +68,8 @@ struct InternalLayout {
 InternalLayout plan_internal(uint64_t n);
 ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info);
 uint64_t external_run_records(uint64_t n, uint64_t budget);
+uint64_t external_merge_target(uint64_t C, uint64_t budget);
+uint64_t external_sample_stride(uint64_t n, uint64_t C, uint64_t budget);
 
 // ------------------------------------------------------------------ device arena
 // A growable cached buffer per (device, slot). Growth frees and reallocates (stream synchronised first).
@@ -132,6 +134,9 @@ struct DeviceContext {
 };
 DeviceContext& device_context(int device);
 ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s);
+// library device-memory accounting (ensure_buffer and the few direct allocations report here)
+void track_device_bytes(int64_t delta);
+void device_bytes(uint64_t* current, uint64_t* peak, bool reset_peak);
 void release_device(int device);
 
 // ------------------------------------------------------------------ profiling

@@ -142,7 +142,10 @@ void pipe_release(DeviceContext& c) {
   for (cudaStream_t st : {P.h2d, P.comp, P.d2h})
     if (st) cudaStreamSynchronize(st);
   for (int i = 0; i < 2; ++i) {
-    if (P.slot[i].ptr) cudaFree(P.slot[i].ptr);
+    if (P.slot[i].ptr) {
+      cudaFree(P.slot[i].ptr);
+      track_device_bytes(-(int64_t)P.slot[i].cap);
+    }
     P.slot[i] = DeviceBuffer{};
     for (cudaEvent_t* e : {&P.copied_in[i], &P.sorted[i], &P.copied_out[i]}) {
       if (*e) cudaEventDestroy(*e);

@@ -351,6 +351,26 @@ def test_external_equals_internal_and_single_run():
     assert np.array_equal(out1.numpy(), out_int)
 
 
+def test_external_device_memory_within_budget():
+    """The external path's device high-water mark stays within device_budget_bytes (SURVEY §4 item 6;
+    P:19's memory limit), measured by the library's own allocation accounting (ley_device_bytes) over a
+    cold call, for budgets from a few runs to many."""
+    import paper_1909_08006_b200 as ley
+
+    n = 1_000_000
+    recs = gen.records(n, seed=44)
+    x, out = _pinned(recs)
+    for budget in (12 << 20, 24 << 20, 96 << 20):
+        ley.ley_release_cache(-1)
+        cur, _ = ley.ley_device_bytes(reset_peak=True)
+        assert cur == 0
+        ley.ley_sort(x, out, n, device_budget_bytes=budget)
+        _, peak = ley.ley_device_bytes()
+        assert peak <= budget, f"library held {peak} bytes under a {budget}-byte budget"
+        assert_parity(recs, out.numpy())
+    ley.ley_release_cache(-1)
+
+
 def test_external_budget_too_small():
     import paper_1909_08006_b200 as ley
 
