@@ -174,8 +174,9 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
 
   if (kin == Kind::kDevice) {
     InternalLayout L = plan_internal(n_records);
-    if (device_budget_bytes && L.bytes > device_budget_bytes) {
-      set_error("plan: internal path needs " + std::to_string(L.bytes) + " bytes of device scratch, budget is " +
+    const uint64_t need = L.bytes + internal_aux_bytes(n_records);
+    if (device_budget_bytes && need > device_budget_bytes) {
+      set_error("plan: internal path needs " + std::to_string(need) + " bytes of device scratch, budget is " +
                 std::to_string(device_budget_bytes));
       return LEY_ERR_BUDGET;
     }

@@ -27,6 +27,7 @@ enum ListId : int {
   kListMed5 = 5,   // len <= 16384  (512 threads, bucket re-read from L2)
   kNumKdLists = 6
 };
+static_assert(kNumKdLists == kNumKdListsHost, "host planning mirrors the K-d list count");
 
 struct ListSet {
   Seg* items[kNumKdLists];

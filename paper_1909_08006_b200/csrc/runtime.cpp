@@ -165,6 +165,15 @@ uint64_t external_run_records(uint64_t n, uint64_t budget) {
   return lo;
 }
 
+// Device bytes the internal path holds outside its workspace: the K-d work lists (6 tiers of 16-byte
+// bucket descriptors, level 1: one per 16-bit bucket; deeper levels: at most 256 children of each of the
+// <= n / 16385 big buckets), the big-bucket lists and the recursion arrays (each at least 1 MB).
+uint64_t internal_aux_bytes(uint64_t n) {
+  const uint64_t buckets = std::max<uint64_t>(std::min<uint64_t>(65536, n), n / 64 + 1);
+  return (uint64_t)kNumKdListsHost * align256(16 * buckets) + 2 * std::max<uint64_t>(1 << 20, 16 * (n / 16385 + 1)) +
+         std::max<uint64_t>(1 << 20, n / 8 + (64 << 10));
+}
+
 ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info) {
   if (!info) {
     set_error("ley_plan_query: NULL info");
@@ -180,8 +189,8 @@ ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info) {
   info->tile_records = kTileRecords;
   info->tiles = L.tiles;
   info->chunk_records = kChunk;
-  info->internal_scratch = L.bytes;
-  info->staged_bytes = L.bytes + 2 * align256(100 * n);
+  info->internal_scratch = L.bytes + internal_aux_bytes(n);
+  info->staged_bytes = info->internal_scratch + 2 * align256(100 * n);
   info->host_path = (budget == 0 || info->staged_bytes <= budget) ? 0 : 1;
   if (info->host_path == 1) {
     info->run_records = external_run_records(n, budget);

@@ -66,6 +66,7 @@ struct InternalLayout {
   size_t bytes = 0;  // total
 };
 InternalLayout plan_internal(uint64_t n);
+uint64_t internal_aux_bytes(uint64_t n);
 ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info);
 uint64_t external_run_records(uint64_t n, uint64_t budget);
 uint64_t external_merge_target(uint64_t C, uint64_t budget);

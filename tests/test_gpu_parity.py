@@ -179,6 +179,24 @@ def test_pageable_rejected():
     assert ley.ley_sort(recs, out, 1000, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
 
 
+def test_internal_device_memory_within_budget():
+    """Device pointers: the library's high-water mark stays within the scratch ley_plan_query reports (the
+    budget check uses the same figure), including skew that recurses through several MSD levels."""
+    import paper_1909_08006_b200 as ley
+
+    for n, dist in [(300_007, "skewed"), (250_000, "prefix2"), (200_000, "tiny_alphabet")]:
+        need = ley.ley_plan_query(n)["internal_scratch"]
+        x = device_records(n, seed=5, dist=dist)
+        out = torch.empty_like(x)
+        ley.ley_release_cache(-1)
+        ley.ley_device_bytes(reset_peak=True)
+        ley.ley_sort(x, out, n, device_budget_bytes=need)
+        _, peak = ley.ley_device_bytes()
+        assert peak <= need, (dist, peak, need)
+        assert ley.ley_sort(x, out, n, device_budget_bytes=need - 1, raise_on_error=False) == ley.LEY_ERR_BUDGET
+    ley.ley_release_cache(-1)
+
+
 def test_device_budget_too_small():
     import paper_1909_08006_b200 as ley
 
