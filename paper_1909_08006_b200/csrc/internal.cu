@@ -93,7 +93,8 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   if ((st = prof.begin("K-c split"))) return st;
   LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
                                                reinterpret_cast<uint4*>(base + L.off_plan_a),
-                                               reinterpret_cast<uint2*>(base + L.off_plan_b), cursor,
+                                               reinterpret_cast<uint2*>(base + L.off_plan_b),
+                                               reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
                                                tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s));
   launches += 2;
   if ((st = prof.end())) return st;

@@ -27,7 +27,7 @@ cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chun
 size_t split_smem_bytes();
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
-                                   uint4* plan_a, uint2* plan_b, uint32_t* cursor, uint32_t* ticket,
+                                   uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s);
 cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,

@@ -117,6 +117,7 @@ InternalLayout plan_internal(uint64_t n) {
   L.off_small = take(4 * 64);  // tickets + list counters
   L.off_plan_a = take(16 * L.split_chunks_ub);
   L.off_plan_b = take(8 * L.split_chunks_ub);
+  L.off_order = take(4 * L.split_chunks_ub);  // K-c chunk processing order
   L.bytes = o;
   return L;
 }

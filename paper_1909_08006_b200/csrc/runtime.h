@@ -60,7 +60,7 @@ struct InternalLayout {
   // byte offsets inside the workspace
   size_t off_At = 0, off_Ai = 0, off_Bt = 0, off_Bi = 0, off_perm = 0;
   size_t off_cnt = 0, off_off = 0, off_lo = 0, off_hist16 = 0, off_B16 = 0, off_cstart = 0;
-  size_t off_scan_status = 0, off_cursor = 0, off_small = 0, off_plan_a = 0, off_plan_b = 0;
+  size_t off_scan_status = 0, off_cursor = 0, off_small = 0, off_plan_a = 0, off_plan_b = 0, off_order = 0;
   size_t scan_status_words = 0;
   uint32_t hist_copies = 1;  // K-a hist16 copies (contention relief under skew)
   size_t bytes = 0;  // total
