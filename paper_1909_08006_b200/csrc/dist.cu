@@ -132,6 +132,7 @@ struct RankState {
   uint64_t send_counts[kMaxRanks] = {0};
   uint64_t recv_counts[kMaxRanks], recv_off[kMaxRanks], send_off[kMaxRanks];
   uint64_t n_out = 0, out_off = 0;
+  int launches = 0;  // kernels this rank launched in the current sort (reported by ley_stage_times)
   // grow-only caches, so repeated sorts allocate nothing on the hot path
   DeviceBuffer cand_buf, split_buf, recv_buf;
   ~RankState() {
@@ -152,6 +153,7 @@ struct Plan {
   uint64_t rho[kMaxRanks] = {0}, first[kMaxRanks] = {0};
   DistSplitter spl[kMaxRanks];
   std::vector<uint64_t> send_matrix;  // G x G
+  int launches = 0;                   // replicated-phase kernels (the candidate sort)
 };
 
 ley_status rank_alloc(RankState& r) {
@@ -194,6 +196,7 @@ ley_status rank_alloc(RankState& r) {
 ley_status phase1_hist(RankState& r) {
   LEY_CUDA("K-s0 hist", cudaMemsetAsync(r.d_hist, 0, 4 * 65536, r.s));
   LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.d_pref, r.ctx->sms, r.s));
+  r.launches += 1;
   return LEY_OK;
 }
 
@@ -202,6 +205,7 @@ ley_status phase2_candidates(RankState& r, const Plan& P) {
   LEY_CUDA("K-s1 candidates", cudaMemcpyAsync(r.d_bins, P.bins, 4 * std::max(nspl, 1), cudaMemcpyHostToDevice, r.s));
   LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_small, 0, 256, r.s));
   LEY_CUDA("K-s1 candidates", cudaMemsetAsync(r.d_status, 0, 8 * (ks_candidate_tiles(r.n) + 1), r.s));
+  r.launches += 1;
   LEY_CUDA("K-s1 candidates", launch_ks_candidates(r.in, r.d_pref, r.n, (uint32_t)r.gbase, r.d_bins, nspl, r.d_status,
                                                    r.d_small + 0, r.d_cand, r.d_cand_gidx, r.d_small + 1, r.s));
   uint32_t* h = static_cast<uint32_t*>(r.ctx->host_pinned);
@@ -228,6 +232,7 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
   quiet.stream = s;
   ley_status st = sort_internal_device(ctx, all_cand, sorted, perm, total_cand, s, quiet, work, L.bytes);
   if (st) return st;
+  P.launches += quiet.launches;
   // first sorted index of each boundary bin = candidates in smaller boundary bins; all splitters' key
   // bytes and sorted positions are read back in one batch, then their global ordinals in a second
   std::vector<uint64_t> at(nspl);
@@ -269,6 +274,7 @@ ley_status phase4_counts(RankState& r, const Plan& P) {
   if (nspl == 0) return LEY_OK;
   LEY_CUDA("K-s2 counts", cudaMemcpyAsync(r.d_spl, P.spl, sizeof(DistSplitter) * nspl, cudaMemcpyHostToDevice, r.s));
   LEY_CUDA("K-s2 counts", cudaMemsetAsync(r.d_dcount, 0, 8 * kMaxRanks, r.s));
+  r.launches += 1;
   LEY_CUDA("K-s2 counts", launch_ks_dest_counts(r.d_cand, r.d_cand_gidx, r.ncand, r.d_spl, nspl, r.d_dcount,
                                                 r.ctx->sms, r.s));
   unsigned long long c[kMaxRanks];
@@ -290,6 +296,7 @@ ley_status phase5_partition(RankState& r, const Plan& P) {
   LEY_CUDA("K-p partition", cudaMemcpyAsync(r.d_sendbase, r.send_off, 8 * G, cudaMemcpyHostToDevice, r.s));
   LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_small, 0, 256, r.s));
   LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_status, 0, 8 * (kp_tiles(r.n) * kMaxRanks + 1), r.s));
+  r.launches += 1;
   LEY_CUDA("K-p partition", launch_kp_partition(r.in, r.n, (uint32_t)r.gbase, r.d_spl, G - 1, r.d_sendbase,
                                                 r.d_status, r.d_small + 2, r.d_send, r.s));
   return LEY_OK;
@@ -300,7 +307,9 @@ ley_status phase6_local_sort(RankState& r, const uint8_t* recv) {
   quiet.ctx = r.ctx;
   quiet.stream = r.s;
   if (r.n_out == 0) return LEY_OK;
-  return sort_internal_device(*r.ctx, recv, r.out, nullptr, r.n_out, r.s, quiet);
+  const ley_status st = sort_internal_device(*r.ctx, recv, r.out, nullptr, r.n_out, r.s, quiet);
+  r.launches += quiet.launches;
+  return st;
 }
 
 void host_hist(RankState& r) {
@@ -374,6 +383,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     return LEY_ERR_INVALID_ARGUMENT;
   }
   RankState& r = comm->state;
+  r.launches = 0;
   r.rank = comm->rank;
   r.ctx = &ctx;
   r.s = s;
@@ -498,6 +508,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   LEY_CUDA("dist", cudaStreamSynchronize(s));
   *n_out_local = r.n_out;
   *out_global_offset = r.out_off;
+  record_launches(r.launches + P.launches);
   return LEY_OK;
 }
 

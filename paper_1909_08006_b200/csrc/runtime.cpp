@@ -352,7 +352,11 @@ void Profiler::finish() {
   }
 }
 
-void record_launches(int launches) { g_stages.launches = launches; }
+void record_launches(int launches) {  // a call without stage profiling: no stale stage list
+  g_stages.names.clear();
+  g_stages.ms.clear();
+  g_stages.launches = launches;
+}
 
 int stage_times(const char** names, float* ms, int max, int* launches) {
   int k = 0;

@@ -103,6 +103,8 @@ def test_nccl_world_size_one(cuda_ok):
         torch.cuda.synchronize()
         assert (n_out, off) == (n, 0)
         assert np.array_equal(out.cpu().numpy(), oracle.sort(recs)[0])
+        _, launches = ley.ley_stage_times()
+        assert launches > 5  # the kernels this rank launched (the bench's gpu_launches at N > 1)
     finally:
         ley.ley_comm_destroy(comm)
 
