@@ -415,6 +415,20 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     set_error("dist: total records > 2^32-2");
     return LEY_ERR_TOO_LARGE;
   }
+  if (G == 1) {  // one rank owns every key: no histogram, splitters or exchange, just the local sort
+    r.n_out = n_local;
+    r.out_off = 0;
+    if (r.n_out > r.cap) {
+      set_error("dist: out_capacity_records is smaller than n_local");
+      return LEY_ERR_CAPACITY;
+    }
+    if ((st = phase6_local_sort(r, r.in))) return st;
+    LEY_CUDA("dist", cudaStreamSynchronize(s));
+    *n_out_local = r.n_out;
+    *out_global_offset = 0;
+    record_launches(r.launches);
+    return LEY_OK;
+  }
   if ((st = phase1_hist(r))) return st;
   host_hist(r);
   // global histogram (u32 sums: N < 2^32), in place: the local one is already on the host
