@@ -172,6 +172,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the NCCL key-range path even at one GPU (checks it)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="with --dist at one GPU: also run the splitter/partition/exchange phases (dist_exchange_g1)")
+    ap.add_argument("--alltoall", action="store_true", help="dist: K-p into a send buffer + NCCL all-to-all-v "
+                                                            "instead of the fused exchange (dist_fused=0)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if not args.cpu_sample:
@@ -186,6 +190,10 @@ def main():
     import gen
     import paper_1909_08006_b200 as ley
 
+    if args.exchange:
+        ley.ley_set_option("dist_exchange_g1", 1)
+    if args.alltoall:
+        ley.ley_set_option("dist_fused", 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -370,7 +378,10 @@ def main():
                        "device_budget_bytes": budget,
                        "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7
                        else "100 MB input: L2 flushed by the next step's 100 MB output + 29 MB scratch",
-                       "parallelism": f"key-range dist x{world} (NCCL)" if comm is not None else "1 GPU"},
+                       "parallelism": (f"key-range dist x{world} (NCCL, " +
+                                       ("all-to-all-v" if args.alltoall else "fused partition+exchange") +
+                                       (", exchange at G=1" if args.exchange else "") + ")")
+                       if comm is not None else "1 GPU"},
             "roofline": roofline, "step_roofline": step_roofline,
             "stages_ms": {k: round(v, 4) for k, v in avg.items()},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

@@ -145,10 +145,17 @@ GEN_HD void gen_key(uint8_t key[10], uint64_t seed, uint64_t i, int dist, const 
   }
 }
 
-/* Full 100-byte record i. Payload bytes 10..99 = bytes 10..99 of the uniform stream of record i. */
+/* Full 100-byte record i. Payload bytes 10..99 = bytes 10..99 of the uniform stream of record i;
+ * ASCII records (the paper's 20 GB set is ASCII) map every payload byte into 0x20..0x7E too and
+ * end in CR LF, so the whole record is printable text. */
 GEN_HD void gen_record(uint8_t rec[100], uint64_t seed, uint64_t i, int dist, const uint64_t* zt) {
   uint8_t tmp[104];
   for (int w = 0; w < 13; ++w) gen_put_le64(tmp + 8 * w, gen_W(seed, i, (uint32_t)w), 8);
   gen_key(tmp, seed, i, dist, zt);
+  if (dist == GEN_ASCII) {
+    for (int b = 10; b < 98; ++b) tmp[b] = (uint8_t)(0x20 + (((uint32_t)tmp[b] * 95u) >> 8));
+    tmp[98] = '\r';
+    tmp[99] = '\n';
+  }
   for (int b = 0; b < 100; ++b) rec[b] = tmp[b];
 }

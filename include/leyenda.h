@@ -131,12 +131,16 @@ ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const
  *  ley_dist_bin_dest_counts: per-destination record counts of a rank's WHOLE bins (bins that hold no
  *    splitter); boundary-bin records are counted separately against the exact splitters.
  *  ley_dist_plan_exchange: G x G send-count matrix [src][dst] -> this rank's receive counts/offsets (in
- *    source-rank order), send offsets, output size and global output offset. */
+ *    source-rank order), send offsets, output size and global output offset.
+ *  ley_dist_dest_offsets: the same matrix -> for every destination d, the record offset inside d's
+ *    receive buffer where this (source) rank's run starts; the fused exchange (option "dist_fused") has
+ *    K-p store there directly. Equals ley_dist_plan_exchange(d).recv_offsets[rank]. */
 int ley_dist_plan_splitters(const uint64_t* global_hist16, uint64_t n_total, int nranks, uint32_t* bins,
                             uint64_t* rank_in_bin, uint64_t* bin_first);
 void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins, int nranks, uint64_t* counts);
 void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
                             uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset);
+void ley_dist_dest_offsets(const uint64_t* send_counts, int nranks, int rank, uint64_t* dst_offsets);
 
 /* ---------------------------------------------------------------- introspection and tuning */
 
@@ -168,6 +172,11 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    warps through a ring; TMA bulk record copies), 0 = alternating sort/gather CTAs
  *   "ka_stream"      1 = K-a streams records through a TMA bulk-copy ring (one persistent CTA per SM),
  *                    0 = one CTA per tile with direct key loads
+ *   "dist_fused"     ley_sort_dist / loopback: 1 = fused partition + exchange — K-p stores every record
+ *                    straight into its owner's receive window (NCCL symmetric memory over NVLink;
+ *                    SURVEY §8f NEXT 1), 0 = K-p into a local send buffer, then an NCCL all-to-all-v
+ *   "dist_exchange_g1" 1 = run the splitter, partition and exchange phases even with one rank (tests the
+ *                    exchange path on a single GPU), 0 = one rank sorts locally
  *   "profile"        1 = record CUDA events around every stage (ley_stage_times)
  *   "ext_run_records" external path: force the run size (records; 0 = from the budget)
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */

@@ -41,7 +41,7 @@ MAX_RECORDS = 0xFFFFFFFE
 EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get_unique_id", "ley_comm_init",
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
                     "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
-                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange",
+                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange", "ley_dist_dest_offsets",
                     "ley_sort_submit", "ley_sort_drain", "ley_test_scan_excl", "ley_test_tile_sort", "ley_device_bytes")
 
 
@@ -101,6 +101,8 @@ _lib.ley_dist_bin_dest_counts.argtypes = [_pu64, ctypes.POINTER(_u32), _i32, _pu
 _lib.ley_dist_bin_dest_counts.restype = None
 _lib.ley_dist_plan_exchange.argtypes = [_pu64, _i32, _i32, _pu64, _pu64, _pu64, _pu64, _pu64]
 _lib.ley_dist_plan_exchange.restype = None
+_lib.ley_dist_dest_offsets.argtypes = [_pu64, _i32, _i32, _pu64]
+_lib.ley_dist_dest_offsets.restype = None
 
 
 class LeyendaError(RuntimeError):
@@ -279,6 +281,15 @@ def ley_dist_plan_exchange(send_counts, nranks: int, rank: int):
     _lib.ley_dist_plan_exchange(m, nranks, rank, rc, ro, so, ctypes.byref(n_out), ctypes.byref(off))
     return dict(recv_counts=list(rc), recv_offsets=list(ro), send_offsets=list(so), n_out=n_out.value,
                 out_offset=off.value)
+
+
+def ley_dist_dest_offsets(send_counts, nranks: int, rank: int):
+    """send_counts: nranks x nranks [src][dst] -> where this rank's run starts in each destination's buffer."""
+    flat = [int(x) for row in send_counts for x in row]
+    m = (_u64 * (nranks * nranks))(*flat)
+    d = (_u64 * nranks)()
+    _lib.ley_dist_dest_offsets(m, nranks, rank, d)
+    return list(d)
 
 
 def library_path() -> str:

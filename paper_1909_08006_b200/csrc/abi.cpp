@@ -25,6 +25,7 @@ int dist_plan_splitters(const uint64_t* hist, uint64_t N, int G, uint32_t* bins,
 void dist_bin_dest_counts(const uint64_t* local_hist, const uint32_t* bins, int nspl, uint64_t* counts);
 void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* recv_counts, uint64_t* recv_off,
                         uint64_t* send_off, uint64_t* n_out, uint64_t* out_off);
+void dist_dest_offsets(const uint64_t* send_counts, int G, int rank, uint64_t* dst_off);
 }  // namespace ley
 
 using namespace ley;
@@ -317,6 +318,10 @@ void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins
 void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
                             uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset) {
   dist_plan_exchange(send_counts, nranks, rank, recv_counts, recv_offsets, send_offsets, n_out, out_offset);
+}
+
+void ley_dist_dest_offsets(const uint64_t* send_counts, int nranks, int rank, uint64_t* dst_offsets) {
+  dist_dest_offsets(send_counts, nranks, rank, dst_offsets);
 }
 
 }  // extern "C"

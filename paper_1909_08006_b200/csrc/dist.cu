@@ -88,6 +88,16 @@ void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* 
   *out_off = before;
 }
 
+// Fused exchange: where source rank `rank`'s run starts inside each destination's receive buffer
+// (records) = what lower source ranks send to that destination (receive order = source rank order).
+void dist_dest_offsets(const uint64_t* send_counts, int G, int rank, uint64_t* dst_off) {
+  for (int d = 0; d < G; ++d) {
+    uint64_t acc = 0;
+    for (int s = 0; s < rank; ++s) acc += send_counts[(size_t)s * G + d];
+    dst_off[d] = acc;
+  }
+}
+
 namespace {
 
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -119,10 +129,10 @@ struct RankState {
   uint8_t* d_cand = nullptr;         // local candidates (records)
   uint32_t* d_cand_gidx = nullptr;
   unsigned long long* d_dcount = nullptr;  // [kMaxRanks]
-  uint64_t* d_sendbase = nullptr;    // [kMaxRanks]
+  uint64_t* d_doff = nullptr;        // [kMaxRanks] K-p: start of this rank's run at each destination
+  uint8_t** d_dptr = nullptr;        // [kMaxRanks] K-p: destination bases (send buffer or receive windows)
   DistSplitter* d_spl = nullptr;     // [kMaxRanks]
   uint32_t* d_bins = nullptr;        // [kMaxRanks]
-  uint8_t* d_send = nullptr;         // n records
   uint16_t* d_pref = nullptr;        // n 16-bit key prefixes (K-s0 -> K-s1)
   uint8_t* d_recv = nullptr;         // received records
   uint64_t recv_cap = 0;
@@ -134,9 +144,9 @@ struct RankState {
   uint64_t n_out = 0, out_off = 0;
   int launches = 0;  // kernels this rank launched in the current sort (reported by ley_stage_times)
   // grow-only caches, so repeated sorts allocate nothing on the hot path
-  DeviceBuffer cand_buf, split_buf, recv_buf;
+  DeviceBuffer cand_buf, split_buf, recv_buf, send_buf;
   ~RankState() {
-    for (DeviceBuffer* b : {&buf, &cand_buf, &split_buf, &recv_buf})
+    for (DeviceBuffer* b : {&buf, &cand_buf, &split_buf, &recv_buf, &send_buf})
       if (b->ptr) {
         cudaFree(b->ptr);
         track_device_bytes(-(int64_t)b->cap);
@@ -164,8 +174,8 @@ ley_status rank_alloc(RankState& r) {
   auto take = [&](size_t b) { size_t at = o; o += a256(b); return at; };
   const size_t o_hist = take(4 * 65536), o_status = take(8 * status_words), o_small = take(256),
                o_cand = take(cand_cap * kRecordBytes), o_cgidx = take(4 * cand_cap), o_dcount = take(8 * kMaxRanks),
-               o_sbase = take(8 * kMaxRanks), o_spl = take(sizeof(DistSplitter) * kMaxRanks),
-               o_bins = take(4 * kMaxRanks), o_send = take(n * kRecordBytes), o_pref = take(2 * n);
+               o_doff = take(8 * kMaxRanks), o_dptr = take(8 * kMaxRanks),
+               o_spl = take(sizeof(DistSplitter) * kMaxRanks), o_bins = take(4 * kMaxRanks), o_pref = take(2 * n);
   if (r.buf.cap < o) {
     if (r.buf.ptr) {
       cudaFree(r.buf.ptr);
@@ -184,10 +194,10 @@ ley_status rank_alloc(RankState& r) {
   r.d_cand = b + o_cand;
   r.d_cand_gidx = reinterpret_cast<uint32_t*>(b + o_cgidx);
   r.d_dcount = reinterpret_cast<unsigned long long*>(b + o_dcount);
-  r.d_sendbase = reinterpret_cast<uint64_t*>(b + o_sbase);
+  r.d_doff = reinterpret_cast<uint64_t*>(b + o_doff);
+  r.d_dptr = reinterpret_cast<uint8_t**>(b + o_dptr);
   r.d_spl = reinterpret_cast<DistSplitter*>(b + o_spl);
   r.d_bins = reinterpret_cast<uint32_t*>(b + o_bins);
-  r.d_send = b + o_send;
   r.d_pref = reinterpret_cast<uint16_t*>(b + o_pref);
   return LEY_OK;
 }
@@ -284,22 +294,43 @@ ley_status phase4_counts(RankState& r, const Plan& P) {
   return LEY_OK;
 }
 
-ley_status phase5_partition(RankState& r, const Plan& P) {
-  const int G = P.G;
-  dist_plan_exchange(P.send_matrix.data(), G, r.rank, r.recv_counts, r.recv_off, r.send_off, &r.n_out, &r.out_off);
+// P5a: the exchange plan of this rank (receive layout, send segments, its output range).
+ley_status phase5_plan(RankState& r, const Plan& P) {
+  dist_plan_exchange(P.send_matrix.data(), P.G, r.rank, r.recv_counts, r.recv_off, r.send_off, &r.n_out, &r.out_off);
   if (r.n_out > r.cap) {
     set_error("dist: rank " + std::to_string(r.rank) + " must hold " + std::to_string(r.n_out) +
               " records but out_capacity_records is " + std::to_string(r.cap));
     return LEY_ERR_CAPACITY;
   }
-  if (G == 1) return LEY_OK;
-  LEY_CUDA("K-p partition", cudaMemcpyAsync(r.d_sendbase, r.send_off, 8 * G, cudaMemcpyHostToDevice, r.s));
+  return LEY_OK;
+}
+
+// P5b: K-p. Destination d's run of this rank starts at record off[d] of base d: bases come either as a
+// host array (copied into r.d_dptr) or as a device array already filled (peer window pointers).
+ley_status phase5_partition(RankState& r, const Plan& P, uint8_t* const* host_bases, uint8_t* const* dev_bases,
+                            const uint64_t* off, bool remote) {
+  const int G = P.G;
+  if (host_bases) {
+    LEY_CUDA("K-p partition", cudaMemcpyAsync(r.d_dptr, host_bases, 8 * G, cudaMemcpyHostToDevice, r.s));
+    dev_bases = r.d_dptr;
+  }
+  LEY_CUDA("K-p partition", cudaMemcpyAsync(r.d_doff, off, 8 * G, cudaMemcpyHostToDevice, r.s));
   LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_small, 0, 256, r.s));
   LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_status, 0, 8 * (kp_tiles(r.n) * kMaxRanks + 1), r.s));
   r.launches += 1;
-  LEY_CUDA("K-p partition", launch_kp_partition(r.in, r.n, (uint32_t)r.gbase, r.d_spl, G - 1, r.d_sendbase,
-                                                r.d_status, r.d_small + 2, r.d_send, r.s));
+  LEY_CUDA("K-p partition", launch_kp_partition(r.in, r.n, (uint32_t)r.gbase, r.d_spl, G - 1, dev_bases, r.d_doff,
+                                                r.d_status, r.d_small + 2, remote, r.s));
   return LEY_OK;
+}
+
+// K-p into this rank's own send buffer (segments at send_off), for the all-to-all-v transports.
+ley_status phase5_partition_send(RankState& r, const Plan& P) {
+  if (!r.n) return LEY_OK;
+  ley_status st = ensure_buffer(r.send_buf, r.n * kRecordBytes, "dist send buffer", r.s);
+  if (st) return st;
+  uint8_t* bases[kMaxRanks];
+  for (int d = 0; d < P.G; ++d) bases[d] = static_cast<uint8_t*>(r.send_buf.ptr);
+  return phase5_partition(r, P, bases, nullptr, r.send_off, false);
 }
 
 ley_status phase6_local_sort(RankState& r, const uint8_t* recv) {
@@ -327,9 +358,53 @@ struct ley_comm {
   int nranks = 0, rank = 0, device = 0;
   ncclComm_t nccl = nullptr;
   ley::RankState state;
+  // fused exchange: this rank's receive window (ncclMemAlloc + symmetric registration; same size on every
+  // rank) and the device array of every rank's window pointer as seen from this GPU
+  void* win_buf = nullptr;
+  size_t win_cap = 0;
+  ncclWindow_t win = nullptr;
+  uint8_t** d_peers = nullptr;
 };
 
 namespace ley {
+
+cudaError_t launch_peer_pointers(ncclWindow_t win, int G, uint8_t** out, cudaStream_t s);  // k_exchange.cu
+
+namespace {
+
+void window_release(ley_comm* c) {
+  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+  if (c->win_buf) {
+    ncclMemFree(c->win_buf);
+    track_device_bytes(-(int64_t)c->win_cap);
+  }
+  c->win = nullptr;
+  c->win_buf = nullptr;
+  c->win_cap = 0;
+}
+
+// Collective: every rank calls it with the same `bytes` (derived from the replicated send matrix), so
+// they all (re)register together. Grow-only with 25% headroom, so repeated sorts register once.
+ley_status window_ensure(ley_comm* c, size_t bytes, cudaStream_t s) {
+  if (c->win && c->win_cap >= bytes) return LEY_OK;
+  LEY_CUDA("dist window", cudaStreamSynchronize(s));  // nothing may still use the old window
+  window_release(c);
+  size_t cap = bytes + bytes / 4;
+  cap = (cap + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+  LEY_NCCL("dist window", ncclMemAlloc(&c->win_buf, cap));
+  c->win_cap = cap;
+  track_device_bytes((int64_t)cap);
+  LEY_NCCL("dist window", ncclCommWindowRegister(c->nccl, c->win_buf, cap, &c->win, NCCL_WIN_COLL_SYMMETRIC));
+  if (!c->d_peers) LEY_CUDA("dist window", cudaMalloc(&c->d_peers, 8 * kMaxRanks));
+  LEY_CUDA("dist window", launch_peer_pointers(c->win, c->nranks, c->d_peers, s));
+  // this rank's own run goes through its local mapping: stores through the window's flat (LSA) mapping
+  // of local memory measured slower (C2 at G=1: K-p 9.0 vs 7.3 ms)
+  LEY_CUDA("dist window", cudaMemcpyAsync(c->d_peers + c->rank, &c->win_buf, 8, cudaMemcpyHostToDevice, s));
+  LEY_CUDA("dist window", cudaStreamSynchronize(s));
+  return LEY_OK;
+}
+
+}  // namespace
 
 ley_status comm_get_unique_id(uint8_t id_out[128]) {
   if (!id_out) {
@@ -362,6 +437,10 @@ ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128
 
 ley_status comm_destroy(ley_comm* comm) {
   if (!comm) return LEY_OK;
+  cudaSetDevice(comm->device);
+  cudaDeviceSynchronize();
+  window_release(comm);
+  if (comm->d_peers) cudaFree(comm->d_peers);
   if (comm->nccl) ncclCommDestroy(comm->nccl);
   delete comm;
   return LEY_OK;
@@ -395,6 +474,11 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   if (st) return st;
   Plan P;
   P.G = G;
+  const Options opts = options_snapshot();
+  Profiler prof;  // per-phase device times when the "profile" option is on (ley_stage_times)
+  prof.on = opts.profile != 0;
+  prof.stream = s;
+  prof.ctx = &ctx;
   // C1: allgather n_local, allreduce hist16
   uint64_t* d_tmp = reinterpret_cast<uint64_t*>(r.d_status);  // status area reused as collective scratch
   {
@@ -415,20 +499,23 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     set_error("dist: total records > 2^32-2");
     return LEY_ERR_TOO_LARGE;
   }
-  if (G == 1) {  // one rank owns every key: no histogram, splitters or exchange, just the local sort
+  const bool exchange = G > 1 || opts.dist_exchange_g1;
+  if (!exchange) {  // one rank owns every key: no histogram, splitters or exchange, just the local sort
     r.n_out = n_local;
     r.out_off = 0;
     if (r.n_out > r.cap) {
       set_error("dist: out_capacity_records is smaller than n_local");
       return LEY_ERR_CAPACITY;
     }
-    if ((st = phase6_local_sort(r, r.in))) return st;
+    if ((st = prof.begin("D5 local sort")) || (st = phase6_local_sort(r, r.in)) || (st = prof.end())) return st;
     LEY_CUDA("dist", cudaStreamSynchronize(s));
     *n_out_local = r.n_out;
     *out_global_offset = 0;
-    record_launches(r.launches);
+    prof.launches = r.launches;
+    prof.finish();
     return LEY_OK;
   }
+  if ((st = prof.begin("D1 hist16+allreduce"))) return st;
   if ((st = phase1_hist(r))) return st;
   host_hist(r);
   // global histogram (u32 sums: N < 2^32), in place: the local one is already on the host
@@ -437,6 +524,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   LEY_CUDA("dist", cudaMemcpyAsync(gh.data(), r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, s));
   LEY_CUDA("dist", cudaStreamSynchronize(s));
   P.ghist.assign(gh.begin(), gh.end());
+  if ((st = prof.end()) || (st = prof.begin("D2 splitters"))) return st;
   if (P.N && dist_plan_splitters(P.ghist.data(), P.N, G, P.bins, P.rho, P.first)) {
     set_error("dist: splitter planning failed");
     return LEY_ERR_INVALID_ARGUMENT;
@@ -489,6 +577,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     LEY_CUDA("dist cand", cudaStreamSynchronize(s));
   }
   // P4 + C3: send counts
+  if ((st = prof.end()) || (st = prof.begin("D3 send counts"))) return st;
   if ((st = phase4_counts(r, P))) return st;
   P.send_matrix.assign((size_t)G * G, 0);
   {
@@ -498,17 +587,37 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     LEY_CUDA("dist", cudaMemcpyAsync(P.send_matrix.data(), d_m, 8ull * G * G, cudaMemcpyDeviceToHost, s));
     LEY_CUDA("dist", cudaStreamSynchronize(s));
   }
-  // P5 + C4: partition and all-to-all-v
-  if ((st = phase5_partition(r, P))) return st;
-  const uint8_t* recv = r.in;
-  if (G > 1) {
+  // P5 + C4: partition and exchange
+  if ((st = prof.end()) || (st = prof.begin("D4 partition"))) return st;
+  if ((st = phase5_plan(r, P))) return st;
+  const uint8_t* recv = nullptr;
+  if (opts.dist_fused) {
+    // fused: K-p stores each destination run straight into its owner's symmetric
+    // window over NVLink; one tiny all-reduce afterwards orders every rank's stores before any local sort
+    uint64_t most = 0;
+    for (int d = 0; d < G; ++d) {
+      uint64_t in_d = 0;
+      for (int src = 0; src < G; ++src) in_d += P.send_matrix[(size_t)src * G + d];
+      most = std::max(most, in_d);
+    }
+    if ((st = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s))) return st;
+    uint64_t dst_off[kMaxRanks];
+    dist_dest_offsets(P.send_matrix.data(), G, r.rank, dst_off);
+    if (r.n && (st = phase5_partition(r, P, nullptr, comm->d_peers, dst_off, G > 1))) return st;
+    if ((st = prof.end()) || (st = prof.begin("D4b exchange"))) return st;
+    LEY_NCCL("dist exchange", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
+    recv = static_cast<const uint8_t*>(comm->win_buf);
+  } else {
+    if ((st = phase5_partition_send(r, P))) return st;
+    if ((st = prof.end()) || (st = prof.begin("D4b exchange"))) return st;
     if ((st = ensure_buffer(r.recv_buf, std::max<size_t>(r.n_out * kRecordBytes, 256), "dist exchange", s))) return st;
     DeviceBuffer& rb = r.recv_buf;
+    const uint8_t* send = static_cast<const uint8_t*>(r.send_buf.ptr);
     LEY_NCCL("dist exchange", ncclGroupStart());
     for (int peer = 0; peer < G; ++peer) {
       const uint64_t sc = P.send_matrix[(size_t)r.rank * G + peer];
       if (sc)
-        LEY_NCCL("dist exchange", ncclSend(r.d_send + r.send_off[peer] * kRecordBytes, sc * kRecordBytes, ncclUint8,
+        LEY_NCCL("dist exchange", ncclSend(send + r.send_off[peer] * kRecordBytes, sc * kRecordBytes, ncclUint8,
                                            peer, comm->nccl, s));
       if (r.recv_counts[peer])
         LEY_NCCL("dist exchange", ncclRecv(static_cast<uint8_t*>(rb.ptr) + r.recv_off[peer] * kRecordBytes,
@@ -518,11 +627,14 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     recv = static_cast<uint8_t*>(rb.ptr);
   }
   // P6: local sort of the received range
+  if ((st = prof.end()) || (st = prof.begin("D5 local sort"))) return st;
   if ((st = phase6_local_sort(r, recv))) return st;
+  if ((st = prof.end())) return st;
   LEY_CUDA("dist", cudaStreamSynchronize(s));
   *n_out_local = r.n_out;
   *out_global_offset = r.out_off;
-  record_launches(r.launches + P.launches);
+  prof.launches = r.launches + P.launches;
+  prof.finish();
   return LEY_OK;
 }
 
@@ -608,28 +720,41 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
     if ((st = phase4_counts(*R[i], P))) return st;
     for (int d = 0; d < G; ++d) P.send_matrix[(size_t)i * G + d] = R[i]->send_counts[d];
   }
-  // P5 + C4
-  for (int i = 0; i < G; ++i)
-    if ((st = phase5_partition(*R[i], P))) return st;
+  // P5 + C4: every rank's receive buffer exists before any K-p runs; fused: K-p of rank i writes its
+  // runs straight into the receivers' buffers (the kernels never wait on one another); else K-p into a
+  // send buffer and device copies stand in for the all-to-all-v
+  const Options opts = options_snapshot();
   std::vector<std::unique_ptr<void, decltype(&cudaFree)>> recvs;
+  std::vector<uint8_t*> rbuf(G);
+  for (int i = 0; i < G; ++i) {
+    if ((st = phase5_plan(*R[i], P))) return st;
+    void* p = nullptr;
+    LEY_CUDA("loopback exchange", cudaMalloc(&p, std::max<size_t>(R[i]->n_out * kRecordBytes, 256)));
+    recvs.emplace_back(p, &cudaFree);
+    rbuf[i] = static_cast<uint8_t*>(p);
+  }
   for (int i = 0; i < G; ++i) {
     RankState& r = *R[i];
-    const uint8_t* recv = r.in;
-    if (G > 1) {
-      void* p = nullptr;
-      LEY_CUDA("loopback exchange", cudaMalloc(&p, std::max<size_t>(r.n_out * kRecordBytes, 256)));
-      recvs.emplace_back(p, &cudaFree);
-      for (int src = 0; src < G; ++src) {
-        const uint64_t c = r.recv_counts[src];
+    if (!r.n) continue;
+    if (opts.dist_fused) {
+      uint64_t dst_off[kMaxRanks];
+      dist_dest_offsets(P.send_matrix.data(), G, i, dst_off);
+      if ((st = phase5_partition(r, P, rbuf.data(), nullptr, dst_off, false))) return st;
+    } else {
+      if ((st = phase5_partition_send(r, P))) return st;
+      for (int d = 0; d < G; ++d) {
+        const uint64_t c = P.send_matrix[(size_t)i * G + d];
         if (c)
           LEY_CUDA("loopback exchange",
-                   cudaMemcpyAsync(static_cast<uint8_t*>(p) + r.recv_off[src] * kRecordBytes,
-                                   R[src]->d_send + R[src]->send_off[i] * kRecordBytes, c * kRecordBytes,
-                                   cudaMemcpyDeviceToDevice, s));
+                   cudaMemcpyAsync(rbuf[d] + R[d]->recv_off[i] * kRecordBytes,
+                                   static_cast<uint8_t*>(r.send_buf.ptr) + r.send_off[d] * kRecordBytes,
+                                   c * kRecordBytes, cudaMemcpyDeviceToDevice, s));
       }
-      recv = static_cast<uint8_t*>(p);
     }
-    if ((st = phase6_local_sort(r, recv))) return st;
+  }
+  for (int i = 0; i < G; ++i) {
+    RankState& r = *R[i];
+    if ((st = phase6_local_sort(r, rbuf[i]))) return st;
     LEY_CUDA("loopback", cudaStreamSynchronize(s));
     n_out[i] = r.n_out;
     out_off[i] = r.out_off;

@@ -12,7 +12,11 @@
 //   K-p   kp_partition    stable partition of full records into G destination segments: a 256-record
 //                         tile is staged in shared memory, ranked by destination (ballots), offset by a
 //                         per-destination decoupled look-back over tiles, and written back in
-//                         destination order as coalesced word streams
+//                         destination order as coalesced word streams. Each destination run goes to
+//                         dst_base[d] + dst_off[d]: the local send buffer (then an NCCL all-to-all), or
+//                         — the fused exchange — straight into rank d's receive window
+//                         over NVLink (NCCL symmetric memory, k_exchange.cu), so the exchange overlaps the
+//                         partition tile by tile and the 200 B/record send-buffer round trip disappears
 // Destination of a record = number of splitters s_k (k = 1..G-1) with s_k <= (key, global ordinal):
 // the exact splitter s_k is the element of global sorted rank floor(k N / G).
 #include "block_rank.cuh"
@@ -165,8 +169,8 @@ constexpr uint32_t kPartTile = 256;  // records per tile (one per thread)
 
 __global__ void __launch_bounds__(kPartThreads)
     kp_partition(const uint8_t* __restrict__ in, uint64_t n, uint32_t gbase, const DistSplitter* __restrict__ spl,
-                 int nspl, const uint64_t* __restrict__ send_base, uint64_t* __restrict__ status,
-                 uint32_t* __restrict__ ticket, uint8_t* __restrict__ send) {
+                 int nspl, uint8_t* const* __restrict__ dst_base, const uint64_t* __restrict__ dst_off,
+                 uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, int remote) {
   extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* s_rec = s_dyn;                                 // tile in input order
   uint32_t* s_out = s_dyn + kPartTile * kRecordWords;      // tile in destination order
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(kPartThreads)
   __shared__ uint32_t s_wc[kPartThreads / 32][kMaxRanks];
   __shared__ uint32_t s_dcnt[kMaxRanks], s_dex[kMaxRanks];
   __shared__ uint64_t s_dst[kMaxRanks];
+  __shared__ uint8_t* s_dptr[kMaxRanks];
   __shared__ uint32_t s_t;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < (unsigned)nspl) s_spl[threadIdx.x] = spl[threadIdx.x];
@@ -256,7 +261,8 @@ __global__ void __launch_bounds__(kPartThreads)
       }
       st_relaxed_u64(st, kFlagPrefix | (uint64_t)(pre + agg));
     }
-    s_dst[k] = send_base[k] + pre;
+    s_dst[k] = dst_off[k] + pre;
+    s_dptr[k] = dst_base[k];
   }
   // stage in destination order
   if (valid) {
@@ -271,9 +277,17 @@ __global__ void __launch_bounds__(kPartThreads)
   for (int k = 0; k <= nspl; ++k) {
     const uint32_t c = s_dcnt[k];
     if (!c) continue;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(send + s_dst[k] * kRecordBytes);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_dptr[k] + s_dst[k] * kRecordBytes);
     const uint32_t* src = s_out + s_dex[k] * kRecordWords;
     for (uint32_t w = threadIdx.x; w < c * kRecordWords; w += kPartThreads) dst[w] = src[w];
+  }
+  // fused exchange: the stores above went to peers' receive windows over NVLink. One system-scope fence
+  // per CTA, after the barrier that orders every thread's stores before it (fences are cumulative), so
+  // they are performed before the grid completes and the host's ordering collective runs (a fence per
+  // thread cost ~30% of the kernel: membar stalls)
+  if (remote) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
   }
   (void)lane;
 }
@@ -316,14 +330,14 @@ cudaError_t launch_ks_dest_counts(const uint8_t* cand, const uint32_t* cand_gidx
 uint64_t kp_tiles(uint64_t n) { return (n + kPartTile - 1) / kPartTile; }
 
 cudaError_t launch_kp_partition(const uint8_t* in, uint64_t n, uint32_t gbase, const DistSplitter* spl, int nspl,
-                                const uint64_t* send_base, uint64_t* status, uint32_t* ticket, uint8_t* send,
-                                cudaStream_t s) {
+                                uint8_t* const* dst_base, const uint64_t* dst_off, uint64_t* status, uint32_t* ticket,
+                                bool remote, cudaStream_t s) {
   if (!n) return cudaSuccess;
   const size_t smem = 2ull * kPartTile * kRecordBytes;
   cudaError_t e = cudaFuncSetAttribute(kp_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kp_partition<<<(unsigned)kp_tiles(n), kPartThreads, smem, s>>>(in, n, gbase, spl, nspl, send_base, status, ticket,
-                                                                  send);
+  kp_partition<<<(unsigned)kp_tiles(n), kPartThreads, smem, s>>>(in, n, gbase, spl, nspl, dst_base, dst_off, status,
+                                                                  ticket, remote ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -59,8 +59,10 @@ cudaError_t launch_ks_dest_counts(const uint8_t* cand, const uint32_t* cand_gidx
                                   const DistSplitter* spl, int nspl, unsigned long long* counts, int sms,
                                   cudaStream_t s);
 uint64_t kp_tiles(uint64_t n);
+// dst_base[d] / dst_off[d] (device arrays, kMaxRanks): where destination d's run starts (records);
+// remote = the bases are peers' windows (adds a system-scope fence before the grid completes)
 cudaError_t launch_kp_partition(const uint8_t* in, uint64_t n, uint32_t gbase, const DistSplitter* spl, int nspl,
-                                const uint64_t* send_base, uint64_t* status, uint32_t* ticket, uint8_t* send,
-                                cudaStream_t s);
+                                uint8_t* const* dst_base, const uint64_t* dst_off, uint64_t* status, uint32_t* ticket,
+                                bool remote, cudaStream_t s);
 
 }  // namespace ley

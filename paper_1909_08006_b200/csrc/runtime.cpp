@@ -36,6 +36,8 @@ const OptDesc kOpts[] = {
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"kd_ws", &Options::kd_ws, 0, 1},
     {"ka_stream", &Options::ka_stream, 0, 1},
+    {"dist_fused", &Options::dist_fused, 0, 1},
+    {"dist_exchange_g1", &Options::dist_exchange_g1, 0, 1},
     {"profile", &Options::profile, 0, 1},
     {"ext_run_records", &Options::ext_run_records, 0, (int64_t)0xFFFFFFFEll},
     {"l2_fetch_bytes", &Options::l2_fetch_bytes, 0, 128},

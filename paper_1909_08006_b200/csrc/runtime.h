@@ -45,6 +45,8 @@ struct Options {
   int64_t kd_insert_max = 16;
   int64_t kd_ws = 1;
   int64_t ka_stream = 1;
+  int64_t dist_fused = 1;        // K-p stores into peers' NCCL symmetric windows (0: send buffer + all-to-all)
+  int64_t dist_exchange_g1 = 0;  // run splitters/partition/exchange even when G == 1 (test hook)
   int64_t profile = 0;
   int64_t ext_run_records = 0;
   int64_t l2_fetch_bytes = 0;  // 0 = leave the device default; else cudaLimitMaxL2FetchGranularity

@@ -1,7 +1,9 @@
 """Multi-GPU key-range sort.
 
 * -m gpu: the loopback transport runs the real G-rank algorithm (K-s0/K-s1/K-s2/K-p kernels, plans, local
-  sort) on one B200 with device copies standing in for NCCL; and the NCCL path itself at world size 1.
+  sort) on one B200, with K-p storing straight into every receiver's buffer (fused exchange, the
+  kernels never wait on one another) or device copies standing in for the all-to-all; and the NCCL path
+  itself at world size 1, including its exchange phase (symmetric window or send/recv to itself).
   Checks: concatenation of the ranks' outputs == oracle of the concatenated input; closed-form sizes
   n_out(r) = floor((r+1)N/G) - floor(rN/G) and offsets floor(rN/G) (exact splitters).
 * -m "not gpu": two gloo processes run the host-side planning of the library (ley_dist_plan_splitters,
@@ -23,10 +25,20 @@ def _closed_form(N, G):
 
 
 # ----------------------------------------------------------------------------------------- GPU
+@pytest.fixture(params=[1, 0], ids=["fused", "alltoall"])
+def exchange_mode(request):
+    """dist_fused=1: K-p stores into the receivers' buffers; 0: send buffer + all-to-all-v."""
+    import paper_1909_08006_b200 as ley
+
+    ley.ley_set_option("dist_fused", request.param)
+    yield request.param
+    ley.ley_set_option("dist_fused", 1)
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("dist", ["uniform", "skewed", "all_equal", "tiny_alphabet", "sorted", "reverse"])
-def test_loopback_matches_oracle(cuda_ok, G, dist):
+def test_loopback_matches_oracle(cuda_ok, exchange_mode, G, dist):
     import torch
 
     import paper_1909_08006_b200 as ley
@@ -60,7 +72,7 @@ def test_loopback_matches_oracle(cuda_ok, G, dist):
 
 
 @pytest.mark.gpu
-def test_loopback_tiny_and_capacity(cuda_ok):
+def test_loopback_tiny_and_capacity(cuda_ok, exchange_mode):
     import torch
 
     import paper_1909_08006_b200 as ley
@@ -86,27 +98,33 @@ def test_loopback_tiny_and_capacity(cuda_ok):
 
 
 @pytest.mark.gpu
-def test_nccl_world_size_one(cuda_ok):
-    """The NCCL path itself (communicator of one rank): equals ley_sort."""
+@pytest.mark.parametrize("exchange_g1", [0, 1], ids=["local", "exchange"])
+def test_nccl_world_size_one(cuda_ok, exchange_mode, exchange_g1):
+    """The NCCL path itself (communicator of one rank): equals ley_sort. With dist_exchange_g1 the rank
+    also runs K-s0, K-p and the exchange: fused = ncclMemAlloc + symmetric window registration, the
+    device-API peer-pointer table (its own entry is the local mapping), K-p storing into the window and
+    the ordering all-reduce; else NCCL send/recv to itself. Growing n re-registers the window."""
     import torch
 
     import paper_1909_08006_b200 as ley
 
-    n = 50_003
-    recs = gen.records(n, seed=61, dist="skewed")
+    ley.ley_set_option("dist_exchange_g1", exchange_g1)
     uid = ley.ley_comm_get_unique_id()
     comm = ley.ley_comm_init(1, 0, uid, 0)
     try:
-        x = torch.from_numpy(recs).cuda()
-        out = torch.empty_like(x)
-        n_out, off = ley.ley_sort_dist(comm, x, n, out, n)
-        torch.cuda.synchronize()
-        assert (n_out, off) == (n, 0)
-        assert np.array_equal(out.cpu().numpy(), oracle.sort(recs)[0])
-        _, launches = ley.ley_stage_times()
-        assert launches > 5  # the kernels this rank launched (the bench's gpu_launches at N > 1)
+        for n, dist in ((50_003, "skewed"), (20_000, "uniform"), (300_001, "three_keys")):
+            recs = gen.records(n, seed=61, dist=dist)
+            x = torch.from_numpy(recs).cuda()
+            out = torch.empty_like(x)
+            n_out, off = ley.ley_sort_dist(comm, x, n, out, n)
+            torch.cuda.synchronize()
+            assert (n_out, off) == (n, 0)
+            assert np.array_equal(out.cpu().numpy(), oracle.sort(recs)[0])
+            _, launches = ley.ley_stage_times()
+            assert launches > 5  # the kernels this rank launched (the bench's gpu_launches at N > 1)
     finally:
         ley.ley_comm_destroy(comm)
+        ley.ley_set_option("dist_exchange_g1", 0)
 
 
 # ----------------------------------------------------------------------------------------- CPU (gloo)
@@ -166,6 +184,27 @@ def _gloo_worker(rank, world, port, N, dist, q):
         send = torch.from_numpy(np.ascontiguousarray(local[order]).reshape(-1))
         recv = torch.empty(plan["n_out"] * 100, dtype=torch.uint8)
         tdist.all_to_all_single(recv, send, [c * 100 for c in plan["recv_counts"]], [int(c) * 100 for c in direct])
+        # the fused exchange's placement: every source writes its run for d at ley_dist_dest_offsets(...)[d]
+        # of d's buffer; gathered here as (dest, offset, bytes), the pieces must tile each receive buffer
+        # exactly and reproduce the all-to-all's result
+        mlist = [m.tolist() for m in mat]
+        doff = ley.ley_dist_dest_offsets(mlist, world, rank)
+        seg = np.concatenate([[0], np.cumsum(direct)])
+        pieces = [(d, doff[d], np.ascontiguousarray(local[order][seg[d]:seg[d + 1]]).tobytes()) for d in range(world)]
+        allp = [None] * world
+        tdist.all_gather_object(allp, pieces)
+        placed = bytearray(plan["n_out"] * 100)
+        cover = np.zeros(plan["n_out"], dtype=np.int64)
+        for src_pieces in allp:
+            for d, o, b in src_pieces:
+                if d != rank:
+                    continue
+                placed[o * 100:o * 100 + len(b)] = b
+                cover[o:o + len(b) // 100] += 1
+        assert (cover == 1).all()
+        assert bytes(placed) == recv.numpy().tobytes()
+        for d in range(world):
+            assert doff[d] == ley.ley_dist_plan_exchange(mlist, world, d)["recv_offsets"][rank]
         # local sort (oracle stands in for the GPU local sort); receive order = global order
         mine, _ = oracle.sort(recv.numpy())
         outs = [None] * world

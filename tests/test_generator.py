@@ -71,5 +71,9 @@ def test_edge_distributions():
     assert (b9[:, :9] == b9[0, :9]).all() and len(set(b9[:, 9].tolist())) > 200
     a = gen.keys(n, 1, "ascii")
     assert a.min() >= 0x20 and a.max() <= 0x7E
+    assert len(np.unique(a[:, 0])) == 95  # all 95 printable values occur as a first byte
+    r = gen.records(n, 1, "ascii").reshape(n, 100)
+    assert r[:, :98].min() >= 0x20 and r[:, :98].max() <= 0x7E
+    assert (r[:, 98] == 13).all() and (r[:, 99] == 10).all()  # CR LF line ends (P:126 ASCII set)
     t = gen.keys(n, 1, "tiny_alphabet")
     assert set(np.unique(t).tolist()) <= {0, 1, 255}

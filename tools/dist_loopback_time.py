@@ -14,12 +14,16 @@ ins = [x[bounds[r] * 100: bounds[r + 1] * 100] for r in range(G)]
 cap = n // G + 2
 outs = [torch.empty(cap * 100, dtype=torch.uint8, device="cuda") for _ in range(G)]
 args = (ins, [bounds[r + 1] - bounds[r] for r in range(G)], outs, [cap] * G)
-ley.ley_sort_dist_loopback(*args)
-torch.cuda.synchronize()
-for rep in range(3):
-    t0 = time.perf_counter()
-    res = ley.ley_sort_dist_loopback(*args)
+for fused in (0, 1, 0, 1):
+    ley.ley_set_option("dist_fused", fused)
+    ley.ley_sort_dist_loopback(*args)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    print(f"G={G} n={n}: {dt * 1e3:.2f} ms total, {dt * 1e3 / G:.2f} ms per rank-equivalent; n_out {[r[0] for r in res][:3]}...",
-          flush=True)
+    best = 1e9
+    for rep in range(3):
+        t0 = time.perf_counter()
+        res = ley.ley_sort_dist_loopback(*args)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    print(f"dist_fused={fused} G={G} n={n}: best {best * 1e3:.2f} ms total, {best * 1e3 / G:.2f} ms per "
+          f"rank-equivalent; n_out {[r[0] for r in res][:3]}...", flush=True)
+ley.ley_set_option("dist_fused", 1)
