@@ -40,6 +40,12 @@ CONFIGS = {
     "c5": dict(n=200_000_000, seed=4, dist="uniform", budget=(4 << 30) // 3,
                name="C5 external (scaled): 2e8 x 100 B uniform in pinned host memory, device budget 1.33 GB "
                     "(BASELINE.json configs[4] ratio 60 GB : 4 GB)"),
+    # SURVEY §8f NEXT 4 workload variants (the paper's third data set: 20 GB, uniform, ASCII)
+    "c6": dict(n=200_000_000, seed=5, dist="ascii",
+               name="C6 ASCII 2e8 x 100 B printable records + CR LF, 20 GB, device-resident (P:126 20 GB set)"),
+    "c7": dict(n=200_000_000, seed=5, dist="ascii", budget=30_000_000_000,
+               name="C7 partial in-memory: ASCII 2e8 x 100 B in pinned host memory, device budget 30 GB "
+                    "(P:126 / Table 2: 20 GB of data, 30 GB of memory)"),
 }
 METRIC = "sorted GB/s of 100-byte records"
 # algorithmic bytes per record of each stage: what the step must move

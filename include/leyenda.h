@@ -145,8 +145,11 @@ void ley_dist_dest_offsets(const uint64_t* send_counts, int nranks, int rank, ui
 /* ---------------------------------------------------------------- introspection and tuning */
 
 /* Host-only plan query (no CUDA calls): device bytes the library allocates to sort n_records on one
- * GPU in-core (internal path), and the path ley_sort would choose for host pointers under `budget`
- * (0 = staged internal, 1 = external). Lets tests and callers size budgets. */
+ * GPU in-core (internal path), and the path ley_sort would choose for host pointers under `budget`:
+ * 0 = staged internal (in and out both staged on the device: staged_bytes), else 2 = resident input,
+ * streamed output (the paper's "partial in-memory" regime: the input staged whole, sorted in
+ * perm-only mode, the output gathered window by window and copied out: resident_bytes), else
+ * 1 = external. Lets tests and callers size budgets. */
 typedef struct {
   uint64_t n_records;
   uint64_t tile_records;        /* K-a tile (records)                                    */
@@ -154,9 +157,10 @@ typedef struct {
   uint64_t chunk_records;       /* K-c / K-c' chunk (pairs)                              */
   uint64_t internal_scratch;    /* bytes of library device memory for the internal path  */
   uint64_t staged_bytes;        /* internal_scratch + in/out staging (host pointers)     */
-  int32_t host_path;            /* 0 = staged internal, 1 = external                    */
+  int32_t host_path;            /* 0 = staged internal, 1 = external, 2 = resident      */
   uint64_t run_records;         /* external: records per sorted run                      */
   uint64_t runs;                /* external: number of runs                              */
+  uint64_t resident_bytes;      /* path 2: scratch + input + perm + 2 output windows     */
 } ley_plan_info;
 ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_plan_info* info);
 
@@ -179,6 +183,9 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    exchange path on a single GPU), 0 = one rank sorts locally
  *   "profile"        1 = record CUDA events around every stage (ley_stage_times)
  *   "ext_run_records" external path: force the run size (records; 0 = from the budget)
+ *   "resident_path"  1 = host pointers may take path 2 (resident input, streamed output) when in + out
+ *                    do not both fit the budget but the input does; 0 = such sorts go external
+ *   "resident_chunk_records" path 2 output window (records; 0 = 2^21; never above ceil(n / 4))
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
 ley_status ley_set_option(const char* name, int64_t value);
 ley_status ley_get_option(const char* name, int64_t* value);

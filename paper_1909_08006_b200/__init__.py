@@ -49,7 +49,7 @@ class ley_plan_info(ctypes.Structure):
     _fields_ = [("n_records", ctypes.c_uint64), ("tile_records", ctypes.c_uint64), ("tiles", ctypes.c_uint64),
                 ("chunk_records", ctypes.c_uint64), ("internal_scratch", ctypes.c_uint64),
                 ("staged_bytes", ctypes.c_uint64), ("host_path", ctypes.c_int32), ("run_records", ctypes.c_uint64),
-                ("runs", ctypes.c_uint64)]
+                ("runs", ctypes.c_uint64), ("resident_bytes", ctypes.c_uint64)]
 
 
 _u64, _u32, _i32, _i64, _vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p

@@ -200,6 +200,8 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
       if ((st = prof.begin("D2H"))) return st;
       LEY_CUDA("D2H", cudaMemcpyAsync(out8, dout, bytes, cudaMemcpyDeviceToHost, s));
       if ((st = prof.end())) return st;
+    } else if (info.host_path == 2) {
+      st = sort_resident_host(ctx, in8, out8, perm, n_records, s, prof);
     } else {
       st = sort_external_host(ctx, in8, out8, perm, n_records, device_budget_bytes, s, prof);
     }

@@ -292,11 +292,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   uint8_t* h_runs_dev = nullptr;
   LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&h_runs_dev, h_runs, 0));
 
-  if (!ctx.copy_stream[0]) {
-    for (int i = 0; i < 2; ++i) LEY_CUDA("external", cudaStreamCreateWithFlags(&ctx.copy_stream[i], cudaStreamNonBlocking));
-    for (int i = 0; i < DeviceContext::kExtEvents; ++i)
-      LEY_CUDA("external", cudaEventCreateWithFlags(&ctx.ev[i], cudaEventDisableTiming));
-  }
+  if (ley_status est = ensure_copy_streams(ctx)) return est;
   cudaStream_t h2d = ctx.copy_stream[0], d2h = ctx.copy_stream[1];
   // per slot: input landed, slot sorted (input free, output ready), output copied out (output free)
   cudaEvent_t ev_start = ctx.ev[0];

@@ -25,6 +25,10 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
                                 cudaStream_t s, Profiler& prof, void* work, size_t work_bytes) {
   const InternalLayout L = plan_internal(n);
   ley_status st;
+  if (!out && !perm_out) {  // out == nullptr is the perm-only mode (K-d without the fused gather)
+    set_error("internal: neither out nor perm requested");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
   if (!work) {
     if ((st = ensure_buffer(ctx.work, L.bytes, "workspace", s))) return st;
     work = ctx.work.ptr;

@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(256)
       s_perm[wib][lane] = x;
     }
     __syncwarp();
-    warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib]);
+    if (out)  // (perm-only mode: the resident host path gathers later, chunk by chunk)
+      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib]);
   }
 }
 
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     __syncthreads();  // sorted ordinals complete; the sort area is free for the gather staging
     if (perm)
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
-    if (warp < L::GWARPS)
+    if (out && warp < L::GWARPS)
       warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in,
                   out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes);
     __syncthreads();  // staging (and s_perm) reused by the next bucket
@@ -713,7 +714,7 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
   if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
                                      out, s)))
     return e;
-  if (tu.kd_ws) {
+  if (tu.kd_ws && out) {  // (no gather warps to feed in perm-only mode)
     if ((e = launch_ws_sort<2048, 256, 8>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
                                           out, s)))
       return e;

@@ -43,10 +43,15 @@ cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* csta
 // K-d (k_bucket.cu)
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
                                       const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
-// K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null).
+// K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
+// out == nullptr: perm-only, no gather).
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
                           uint8_t* out, cudaStream_t s, int* launches);
+
+// K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
+cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
+                             cudaStream_t s);
 
 // multi-GPU (k_dist.cu)
 cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, int sms, cudaStream_t s);

@@ -36,6 +36,8 @@ const OptDesc kOpts[] = {
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"kd_ws", &Options::kd_ws, 0, 1},
     {"ka_stream", &Options::ka_stream, 0, 1},
+    {"resident_path", &Options::resident_path, 0, 1},
+    {"resident_chunk_records", &Options::resident_chunk_records, 0, (int64_t)0xFFFFFFFEll},
     {"dist_fused", &Options::dist_fused, 0, 1},
     {"dist_exchange_g1", &Options::dist_exchange_g1, 0, 1},
     {"profile", &Options::profile, 0, 1},
@@ -177,6 +179,26 @@ uint64_t internal_aux_bytes(uint64_t n) {
          std::max<uint64_t>(1 << 20, n / 8 + (64 << 10));
 }
 
+ley_status ensure_copy_streams(DeviceContext& ctx) {
+  if (ctx.copy_stream[0]) return LEY_OK;
+  for (int i = 0; i < 2; ++i) LEY_CUDA("copy streams", cudaStreamCreateWithFlags(&ctx.copy_stream[i], cudaStreamNonBlocking));
+  for (int i = 0; i < DeviceContext::kExtEvents; ++i)
+    LEY_CUDA("copy streams", cudaEventCreateWithFlags(&ctx.ev[i], cudaEventDisableTiming));
+  return LEY_OK;
+}
+
+uint64_t resident_chunk_records(uint64_t n) {
+  const int64_t o = options_snapshot().resident_chunk_records;
+  const uint64_t c = o > 0 ? (uint64_t)o : (uint64_t)1 << 21;  // 210 MB windows: full-speed D2H copies
+  // at most a quarter of n, so the two windows stay below the output buffer the staged path would need
+  return std::max<uint64_t>(1, std::min<uint64_t>((n + 3) / 4, c));
+}
+
+uint64_t resident_bytes(uint64_t n) {
+  return plan_internal(n).bytes + internal_aux_bytes(n) + align256(100 * n) + align256(4 * n) +
+         2 * align256(100 * resident_chunk_records(n));
+}
+
 ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info) {
   if (!info) {
     set_error("ley_plan_query: NULL info");
@@ -194,7 +216,13 @@ ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info) {
   info->chunk_records = kChunk;
   info->internal_scratch = L.bytes + internal_aux_bytes(n);
   info->staged_bytes = info->internal_scratch + 2 * align256(100 * n);
-  info->host_path = (budget == 0 || info->staged_bytes <= budget) ? 0 : 1;
+  info->resident_bytes = resident_bytes(n);
+  if (budget == 0 || info->staged_bytes <= budget)
+    info->host_path = 0;
+  else if (options_snapshot().resident_path && info->resident_bytes <= budget)
+    info->host_path = 2;
+  else
+    info->host_path = 1;
   if (info->host_path == 1) {
     info->run_records = external_run_records(n, budget);
     info->runs = info->run_records ? (n + info->run_records - 1) / info->run_records : 0;

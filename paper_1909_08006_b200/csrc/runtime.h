@@ -45,6 +45,8 @@ struct Options {
   int64_t kd_insert_max = 16;
   int64_t kd_ws = 1;
   int64_t ka_stream = 1;
+  int64_t resident_path = 1;        // host pointers: allow path 2 (resident input, streamed output)
+  int64_t resident_chunk_records = 0;  // path 2 output window (records; 0 = 2^21)
   int64_t dist_fused = 1;        // K-p stores into peers' NCCL symmetric windows (0: send buffer + all-to-all)
   int64_t dist_exchange_g1 = 0;  // run splitters/partition/exchange even when G == 1 (test hook)
   int64_t profile = 0;
@@ -71,6 +73,8 @@ InternalLayout plan_internal(uint64_t n);
 uint64_t internal_aux_bytes(uint64_t n);
 ley_status plan_query(uint64_t n, uint64_t budget, ley_plan_info* info);
 uint64_t external_run_records(uint64_t n, uint64_t budget);
+uint64_t resident_chunk_records(uint64_t n);  // path 2 output window
+uint64_t resident_bytes(uint64_t n);          // path 2 device bytes (scratch + input + perm + 2 windows)
 uint64_t external_merge_target(uint64_t C, uint64_t budget);
 uint64_t external_sample_stride(uint64_t n, uint64_t C, uint64_t budget);
 
@@ -164,6 +168,11 @@ int stage_times(const char** names, float* ms, int max, int* launches);
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                                 cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0);
 // Streaming staged-internal sort of pinned host records (ley_sort_submit / ley_sort_drain).
+// Host path 2 (resident.cu): input staged whole on the device, sorted in perm-only mode, output gathered
+// window by window into two device staging buffers and copied to the caller's pinned memory.
+ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                              cudaStream_t s, Profiler& prof);
+ley_status ensure_copy_streams(DeviceContext& ctx);  // ctx.copy_stream[2] + ctx.ev (external / resident)
 ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, cudaStream_t user);
 ley_status sort_drain(DeviceContext& ctx);
 void pipe_release(DeviceContext& ctx);

@@ -70,6 +70,18 @@ def test_plan_query(ley):
     assert 1 <= e["run_records"] < 600_000_000
     assert e["runs"] == -(-600_000_000 // e["run_records"])
     assert 200 * e["run_records"] + ley.ley_plan_query(e["run_records"])["internal_scratch"] <= 4 << 30
+    # between the two: the input fits but input + output do not -> path 2 (resident input, streamed
+    # output); its device bytes = scratch + 100 n (input) + 4 n (perm) + two output windows
+    r = ley.ley_plan_query(200_000_000, 30_000_000_000)
+    assert r["host_path"] == 2 and r["resident_bytes"] <= 30_000_000_000 < r["staged_bytes"]
+    assert r["resident_bytes"] == (r["internal_scratch"] + 100 * 200_000_000 + 4 * 200_000_000 +
+                                   2 * 100 * (1 << 21))
+    assert ley.ley_plan_query(200_000_000, r["resident_bytes"] - 1)["host_path"] == 1
+    ley.ley_set_option("resident_path", 0)
+    try:
+        assert ley.ley_plan_query(200_000_000, 30_000_000_000)["host_path"] == 1
+    finally:
+        ley.ley_set_option("resident_path", 1)
     with pytest.raises(ley.LeyendaError):
         ley.ley_plan_query(2**32)
 

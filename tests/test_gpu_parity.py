@@ -127,6 +127,47 @@ def test_pinned_host_path():
     assert_parity(recs, out.numpy())
 
 
+@pytest.mark.parametrize("dist,n,chunk", [
+    ("uniform", 700_001, 100_000),     # 7 full windows + a ragged one
+    ("skewed", 500_000, 64_000),       # recursion + ties, window edges inside tie runs
+    ("ascii", 300_007, 1 << 21),       # default window size, capped at n / 4 for small n
+    ("all_equal", 150_000, 40_960),    # output == input
+    ("reverse", 99_999, 32_768),
+])
+def test_resident_host_path(dist, n, chunk):
+    """Host path 2, resident input + streamed output (the paper's partial in-memory regime): under a
+    budget that holds the input but not input + output, the sort runs in perm-only mode and K-e gathers
+    the output window by window into two device windows copied to pinned host memory. Byte-exact with
+    the oracle (out and perm), and the library's device high-water mark stays within the budget."""
+    import paper_1909_08006_b200 as ley
+
+    with Options(resident_chunk_records=chunk):
+        plan = ley.ley_plan_query(n, 1)
+        budget = plan["resident_bytes"]
+        plan = ley.ley_plan_query(n, budget)
+        assert plan["host_path"] == 2 and budget < plan["staged_bytes"], plan
+        recs = gen.records(n, seed=71, dist=dist)
+        x = torch.from_numpy(recs).pin_memory()
+        out = torch.empty_like(x).pin_memory()
+        perm = torch.empty(n, dtype=torch.int32).pin_memory()
+        ley.ley_release_cache(-1)
+        ley.ley_device_bytes(reset_peak=True)
+        ley.ley_sort_perm(x, out, perm, n, device_budget_bytes=budget)
+        _, peak = ley.ley_device_bytes()
+        assert peak <= budget, (peak, budget)
+        assert_parity(recs, out.numpy(), perm.numpy().view(np.uint32))
+        # the plain call (no perm) and the path switch off (-> external) give the same bytes
+        out2 = torch.empty_like(x).pin_memory()
+        ley.ley_sort(x, out2, n, device_budget_bytes=budget)
+        assert torch.equal(out, out2)
+        with Options(resident_path=0):
+            assert ley.ley_plan_query(n, budget)["host_path"] == 1
+            out3 = torch.empty_like(x).pin_memory()
+            ley.ley_sort(x, out3, n, device_budget_bytes=budget)
+        assert torch.equal(out, out3)
+    ley.ley_release_cache(-1)
+
+
 def test_streaming_submit_pipeline():
     """ley_sort_submit: consecutive host sorts overlap through two device slots (H2D of call k+1 with the
     D2H of call k). Five calls of different sizes and distributions (slots reused and grown) must each
@@ -323,6 +364,52 @@ def test_c4_full_size_certificate():
     o2, p2 = gpu_sort(sl)
     assert_parity(sl, o2, p2)
     del x
+    torch.cuda.empty_cache()
+    ley.ley_release_cache(-1)
+
+
+@pytest.mark.slow
+def test_ascii_20gb_and_partial_in_memory():
+    """SURVEY §8f NEXT 4 workloads at full size. (1) The paper's 20 GB ASCII set ("ASCII for 20 GB
+    dataset"): 2e8 printable records ending in CR LF, 95 live values per key byte, so every 16-bit bucket
+    (~22K records) recurses on byte 2 — sorted on the device and certified there. (2) The paper's
+    "partial in-memory" regime (Table 2's 30 GB memory for 20 GB of data): the same records
+    in pinned host memory under a 30 GB device budget — the input fits, input + output do not — take host
+    path 2 (resident input, streamed output), and with that path switched off the external path (a few
+    large runs); both outputs must equal the certified device result byte for byte."""
+    import gc
+
+    import paper_1909_08006_b200 as ley
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    ley.ley_release_cache(-1)
+    n, budget = 200_000_000, 30_000_000_000
+    x = device_records(n, seed=5, dist="ascii")
+    out = torch.empty_like(x)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ley.ley_sort_perm(x, out, perm, n)
+    torch.cuda.synchronize()
+    _certify_on_device(x, out, perm, n)
+    del perm
+    plan = ley.ley_plan_query(n, budget)
+    assert plan["host_path"] == 2, plan
+    h_in = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
+    h_in.copy_(x)
+    del x
+    torch.cuda.empty_cache()
+    ley.ley_release_cache(-1)
+    h_out = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
+    step = 20_000_000 * 100
+    for resident in (1, 0):
+        with Options(resident_path=resident):
+            p = ley.ley_plan_query(n, budget)
+            assert p["host_path"] == (2 if resident else 1) and (resident or 2 <= p["runs"] <= 8), p
+            h_out.zero_()
+            ley.ley_sort(h_in, h_out, n, device_budget_bytes=budget)
+        for a in range(0, n * 100, step):
+            assert torch.equal(h_out[a:a + step].cuda(), out[a:a + step]), f"path {p['host_path']} != device at {a}"
+    del out, h_in, h_out
     torch.cuda.empty_cache()
     ley.ley_release_cache(-1)
 
