@@ -50,6 +50,10 @@ def _lib():
         lib.oracle_is_sorted.restype = i32
         lib.oracle_certify.argtypes = [vp, vp, vp, u64]
         lib.oracle_certify.restype = u64
+        lib.oracle_sort_kb.argtypes = [vp, vp, vp, u64, i32, i32]
+        lib.oracle_sort_kb.restype = i32
+        lib.oracle_certify_kb.argtypes = [vp, vp, vp, u64, i32]
+        lib.oracle_certify_kb.restype = u64
         _LIB = lib
     return _LIB
 
@@ -65,18 +69,24 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def sort(recs, threads: int = 0, want_perm: bool = True):
-    """Stable ascending sort of 100-byte records by the unsigned 10-byte key (ties by index).
+def sort(recs, threads: int = 0, want_perm: bool = True, key_bytes: int = 10):
+    """Stable ascending sort of 100-byte records by the unsigned key = bytes [0, key_bytes) (ties by index).
 
     Returns (out, perm): out is a (n*100,) uint8 array, perm[j] the input index of output record j.
+    key_bytes = 10 (the paper's records) uses the (key, pointer) tuple sort; other sizes (P:164
+    flexible key sizes, 1..100) compare the records themselves.
     """
     a = _flat(recs)
     n = a.size // RECORD_BYTES
     out = np.empty_like(a)
     perm = np.empty(n, dtype=np.uint32) if want_perm else None
-    rc = _lib().oracle_sort(_ptr(a), _ptr(out), _ptr(perm) if perm is not None else None, n, threads)
+    pp = _ptr(perm) if perm is not None else None
+    if key_bytes == 10:
+        rc = _lib().oracle_sort(_ptr(a), _ptr(out), pp, n, threads)
+    else:
+        rc = _lib().oracle_sort_kb(_ptr(a), _ptr(out), pp, n, key_bytes, threads)
     if rc:
-        raise ValueError("oracle_sort: n out of range")
+        raise ValueError(f"oracle_sort: n or key_bytes out of range (rc {rc})")
     return out, perm
 
 
@@ -125,7 +135,7 @@ def is_sorted(recs) -> bool:
     return bool(_lib().oracle_is_sorted(_ptr(a), a.size // RECORD_BYTES))
 
 
-def certify(inp, out, perm) -> int:
+def certify(inp, out, perm, key_bytes: int = 10) -> int:
     """0 if (perm is a permutation, out[j] == in[perm[j]], (key, perm) strictly increasing); else
     1 + first failing position (n + 1 for a non-permutation)."""
     a, b = _flat(inp), _flat(out)
@@ -133,7 +143,9 @@ def certify(inp, out, perm) -> int:
     n = a.size // RECORD_BYTES
     if b.size != a.size or p.size != n:
         raise ValueError("certify: size mismatch")
-    return int(_lib().oracle_certify(_ptr(a), _ptr(b), _ptr(p), n))
+    if key_bytes == 10:
+        return int(_lib().oracle_certify(_ptr(a), _ptr(b), _ptr(p), n))
+    return int(_lib().oracle_certify_kb(_ptr(a), _ptr(b), _ptr(p), n, key_bytes))
 
 
 def mod128(x: int) -> int:

@@ -17,6 +17,10 @@
  *                 sort E by (memcmp(key) , then index)       -- library comparison sort
  *                 perm[j] = E[j].idx;  out[j] = in[perm[j]]  -- the record scatter of P:104-106
  *
+ * oracle_sort_kb / oracle_certify_kb: the same definition with key = bytes [0, key_bytes) (§5
+ * P:164 flexible key sizes), pinned by brute force for 1..100-byte keys, Python's stable sort on the
+ * prefix, and agreement with oracle_sort at key_bytes = 10.
+ *
  * Pins (tests/test_oracle.py, -m "not gpu"): brute force over all n! orders for n <= 7, an insertion
  * sort written in Python, Python's stable sorted() on the key alone, closed forms (all-equal ->
  * identity, sorted -> identity, strictly decreasing -> reversal, single-byte-position keys), the §2.2
@@ -209,6 +213,37 @@ int oracle_sorted_digest(const uint8_t* in, uint64_t n, uint64_t out[2], int thr
   return 0;
 }
 
+/* Flexible key size (§5, "flexible key sizes"): the same definition
+ * with the key = record bytes [0, key_bytes), 1 <= key_bytes <= 100, compared as unsigned bytes, ties by
+ * original index. Written separately from oracle_sort (a comparison of the records themselves, no
+ * tuple extraction), so the key_bytes = 10 case also cross-checks the tuple path. Returns 0 on success,
+ * 1 if n is out of range, 2 if key_bytes is. */
+int oracle_sort_kb(const uint8_t* in, uint8_t* out, uint32_t* perm, uint64_t n, int key_bytes, int threads) {
+  if (n > 0xFFFFFFFEULL) return 1;
+  if (key_bytes < 1 || key_bytes > 100) return 2;
+  if (n == 0) return 0;
+  if (threads <= 0) threads = omp_get_max_threads();
+  std::vector<uint32_t> idx(n);
+  for (uint64_t i = 0; i < n; ++i) idx[i] = (uint32_t)i;
+  const size_t k = (size_t)key_bytes;
+  auto less = [in, k](uint32_t a, uint32_t b) {
+    int c = memcmp(in + 100 * (uint64_t)a, in + 100 * (uint64_t)b, k);
+    return c != 0 ? c < 0 : a < b;
+  };
+  if (n < 200000 || threads == 1) {
+    std::sort(idx.begin(), idx.end(), less);
+  } else {
+    omp_set_num_threads(threads);
+    __gnu_parallel::sort(idx.begin(), idx.end(), less);
+  }
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int64_t j = 0; j < (int64_t)n; ++j) {
+    if (perm) perm[j] = idx[j];
+    if (out) memcpy(out + 100 * (uint64_t)j, in + 100 * (uint64_t)idx[j], 100);
+  }
+  return 0;
+}
+
 /* 1 if the keys of recs are non-decreasing (unsigned lexicographic), else 0. */
 int oracle_is_sorted(const uint8_t* recs, uint64_t n) {
   for (uint64_t j = 1; j < n; ++j)
@@ -219,7 +254,13 @@ int oracle_is_sorted(const uint8_t* recs, uint64_t n) {
 /* Certificate: returns 0 if (a) perm is a permutation of [0,n), (b) out[j] == in[perm[j]] for all j,
  * (c) (key(out[j]), perm[j]) is strictly increasing in j. Together these force out == oracle output.
  * Otherwise returns 1 + the first failing j (or n+1 for a non-permutation). */
+uint64_t oracle_certify_kb(const uint8_t* in, const uint8_t* out, const uint32_t* perm, uint64_t n, int key_bytes);
 uint64_t oracle_certify(const uint8_t* in, const uint8_t* out, const uint32_t* perm, uint64_t n) {
+  return oracle_certify_kb(in, out, perm, n, 10);
+}
+
+/* The certificate with key = bytes [0, key_bytes). */
+uint64_t oracle_certify_kb(const uint8_t* in, const uint8_t* out, const uint32_t* perm, uint64_t n, int key_bytes) {
   std::vector<uint8_t> seen(n, 0);
   for (uint64_t j = 0; j < n; ++j) {
     if (perm[j] >= n || seen[perm[j]]) return n + 1;
@@ -228,7 +269,7 @@ uint64_t oracle_certify(const uint8_t* in, const uint8_t* out, const uint32_t* p
   for (uint64_t j = 0; j < n; ++j) {
     if (memcmp(out + 100 * j, in + 100 * (uint64_t)perm[j], 100) != 0) return j + 1;
     if (j > 0) {
-      int c = memcmp(out + 100 * (j - 1), out + 100 * j, 10);
+      int c = memcmp(out + 100 * (j - 1), out + 100 * j, (size_t)key_bytes);
       if (c > 0 || (c == 0 && perm[j - 1] >= perm[j])) return j + 1;
     }
   }

@@ -209,3 +209,67 @@ def test_certificate():
     o4 = out.copy()
     o4[150] ^= 0xFF
     assert oracle.certify(recs, o4, perm) == 2
+
+
+# ---------------------------------------------------------------- flexible key sizes (NEXT 4)
+@pytest.mark.parametrize("k", [1, 3, 9, 10, 11, 37, 100])
+def test_key_bytes_brute_force(k):
+    """Key = record bytes [0, k) (§5 P:164 "flexible key sizes"): for n <= 6 every arrangement
+    is enumerated; exactly one has (key prefix, index) strictly increasing and it is the oracle's. Bytes
+    over {0x00, 0x01, 0xFF} in the whole record, so a comparison that reads too few or too many key
+    bytes (an off-by-one in k) picks a different winner."""
+    for n in range(7):
+        for seed in range(3):
+            rng = random.Random(77 * k + 10 * n + seed)
+            a = np.array([[rng.choice((0x00, 0x01, 0xFF)) for _ in range(100)] for _ in range(n)],
+                         dtype=np.uint8).reshape(-1)
+            recs = a.reshape(n, 100) if n else a.reshape(0, 100)
+            keys = [bytes(recs[i, :k]) for i in range(n)]
+            winners = [list(p) for p in itertools.permutations(range(n))
+                       if all((keys[p[j]], p[j]) < (keys[p[j + 1]], p[j + 1]) for j in range(n - 1))]
+            assert len(winners) == 1
+            _, perm = oracle.sort(a, key_bytes=k)
+            assert list(perm) == winners[0]
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 10, 12, 100])
+def test_key_bytes_python_stable_sort(k):
+    """Python's stable sorted() on the k-byte prefix alone gives the oracle's order (a dropped or reversed
+    index tie-break, or a wrong prefix length, fails); tiny-alphabet keys make long tie runs."""
+    recs = gen.records(6000, seed=13, dist="tiny_alphabet").reshape(-1, 100)
+    recs[:, 10:40] = recs[:, :30] % 3  # low-entropy bytes beyond the 10-byte key too
+    keys = [bytes(recs[i, :k]) for i in range(recs.shape[0])]
+    expect = sorted(range(len(keys)), key=lambda i: keys[i])
+    out, perm = oracle.sort(recs, key_bytes=k)
+    assert list(perm) == expect
+    assert np.array_equal(out.reshape(-1, 100), recs[expect])
+    assert oracle.certify(recs, out, perm, key_bytes=k) == 0
+
+
+def test_key_bytes_ten_matches_tuple_path():
+    """The record-comparison oracle (oracle_sort_kb) at k = 10 equals the (key, pointer) tuple oracle:
+    two independent implementations of the same definition."""
+    import ctypes
+
+    for dist in ("uniform", "skewed", "three_keys", "byte9"):
+        recs = gen.records(20000, seed=17, dist=dist)
+        _, p10 = oracle.sort(recs)
+        perm = np.empty(20000, dtype=np.uint32)
+        rc = oracle._lib().oracle_sort_kb(recs.ctypes.data_as(ctypes.c_void_p), None,
+                                          perm.ctypes.data_as(ctypes.c_void_p), 20000, 10, 0)
+        assert rc == 0 and np.array_equal(perm, p10)
+
+
+def test_key_bytes_certificate_is_prefix_aware():
+    """The 10-byte order is not a valid 1-byte-key result (ties on byte 0 must fall back to the index),
+    and vice versa: the k-aware certificate tells them apart."""
+    recs = gen.records(5000, seed=19, dist="uniform")
+    o10, p10 = oracle.sort(recs)
+    o1, p1 = oracle.sort(recs, key_bytes=1)
+    assert oracle.certify(recs, o10, p10) == 0 and oracle.certify(recs, o1, p1, key_bytes=1) == 0
+    assert oracle.certify(recs, o10, p10, key_bytes=1) != 0
+    assert oracle.certify(recs, o1, p1) != 0
+    with pytest.raises(ValueError):
+        oracle.sort(recs, key_bytes=0)
+    with pytest.raises(ValueError):
+        oracle.sort(recs, key_bytes=101)
