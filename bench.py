@@ -121,19 +121,29 @@ class ClockSampler:
                 "reasons": sorted(set().union(*[x[2] for x in loaded])), "samples": len(loaded)}
 
 
-def cpu_baseline(cfg, sample_n: int):
+def _oracle_step(recs, threads, key_bytes):
+    """One oracle sort; (extract, sort, gather) seconds for the paper's 10-byte keys, else None."""
+    import oracle
+
+    if key_bytes == 10:
+        return oracle.sort_timed(recs, threads=threads)[1]
+    oracle.sort(recs, threads=threads, want_perm=False, key_bytes=key_bytes)
+    return None
+
+
+def cpu_baseline(cfg, sample_n: int, key_bytes: int = 10):
     """The oracle as it stands (oracle/), timed on this host's cores on a bounded sample."""
     import gen
-    import oracle
 
     recs = gen.records(sample_n, cfg["seed"], cfg["dist"])
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    _, (te, ts, tg) = oracle.sort_timed(recs, threads=threads)
+    st = _oracle_step(recs, threads, key_bytes)
     dt = time.perf_counter() - t0
+    stages = (f"extract {st[0]:.2f} s, sort {st[1]:.2f} s, gather {st[2]:.2f} s (__gnu_parallel::sort, OpenMP)"
+              if st else f"record-comparison sort on {key_bytes}-byte keys (__gnu_parallel::sort, OpenMP)")
     return {"value": round(sample_n * 100 / dt / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {sample_n:,} records of {cfg['name'].split(' (')[0]} (same generator/seed); "
-                      f"extract {te:.2f} s, sort {ts:.2f} s, gather {tg:.2f} s (__gnu_parallel::sort, OpenMP)",
+            "sample": f"first {sample_n:,} records of {cfg['name'].split(' (')[0]} (same generator/seed); {stages}",
             "seconds": round(dt, 3)}
 
 
@@ -142,24 +152,24 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     import gen
-    import oracle
 
     sample_n = args.cpu_sample
     recs = gen.records(sample_n, cfg["seed"], cfg["dist"])
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        oracle.sort_timed(recs[: min(sample_n, 1_000_000) * 100], threads=threads)
+        _oracle_step(recs[: min(sample_n, 1_000_000) * 100], threads, args.key_bytes)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.sort_timed(recs, threads=threads)
+        _oracle_step(recs, threads, args.key_bytes)
         times.append(time.perf_counter() - t0)
     t = statistics.mean(times)
     v = sample_n * 100 / t / 1e9
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg["name"], "n_records": cfg["n"], "sample_records": sample_n},
+            "config": {"workload": cfg["name"], "n_records": cfg["n"], "sample_records": sample_n,
+                       "key_bytes": args.key_bytes},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
                              "sample": f"first {sample_n:,} records of the workload per step"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -180,6 +190,8 @@ def main():
     ap.add_argument("--dist", action="store_true", help="use the NCCL key-range path even at one GPU (checks it)")
     ap.add_argument("--exchange", action="store_true",
                     help="with --dist at one GPU: also run the splitter/partition/exchange phases (dist_exchange_g1)")
+    ap.add_argument("--key-bytes", type=int, default=10,
+                    help="key = record bytes [0, k), 1..100 (P:164 flexible key sizes; default the paper's 10)")
     ap.add_argument("--alltoall", action="store_true", help="dist: K-p into a send buffer + NCCL all-to-all-v "
                                                             "instead of the fused exchange (dist_fused=0)")
     args = ap.parse_args()
@@ -239,9 +251,9 @@ def main():
 
     def step():
         if comm is not None:
-            ley.ley_sort_dist(comm, x, n, out, cap, device_budget_bytes=budget, stream=stream)
+            ley.ley_sort_dist(comm, x, n, out, cap, key_bytes=args.key_bytes, device_budget_bytes=budget, stream=stream)
         else:
-            ley.ley_sort(x, out, n, device_budget_bytes=budget, stream=stream)
+            ley.ley_sort(x, out, n, key_bytes=args.key_bytes, device_budget_bytes=budget, stream=stream)
 
     def barrier():
         if world > 1:
@@ -314,7 +326,8 @@ def main():
 
         def e2e_step():
             x[: n * 100].copy_(hin, non_blocking=True)
-            n_out, _ = ley.ley_sort_dist(comm, x, n, out, cap, device_budget_bytes=budget, stream=stream)
+            n_out, _ = ley.ley_sort_dist(comm, x, n, out, cap, key_bytes=args.key_bytes, device_budget_bytes=budget,
+                                         stream=stream)
             hout[: n_out * 100].copy_(out[: n_out * 100], non_blocking=True)
             return n_out
 
@@ -348,19 +361,19 @@ def main():
         def timed(call, steps):
             f0.record(stream)
             for _ in range(steps):
-                call(hin, hout, n, stream=stream)
+                call(hin, hout, n, key_bytes=args.key_bytes, stream=stream)
             f1.record(stream)
             torch.cuda.synchronize()
             return f0.elapsed_time(f1) / steps
 
         # (1) the public streaming call: H2D of step k+1 overlaps the D2H of step k (ley_sort_submit)
-        ley.ley_sort_submit(hin, hout, n, stream=stream)  # warm: allocates the two device slots
+        ley.ley_sort_submit(hin, hout, n, key_bytes=args.key_bytes, stream=stream)  # warm: the two device slots
         ley.ley_sort_drain()
         ems = timed(ley.ley_sort_submit, args.e2e_steps)
         ley.ley_sort_drain()
         # (2) the blocking call, one sort at a time (H2D + sort + D2H serialised)
         ley.ley_release_cache(-1)
-        ley.ley_sort(hin, hout, n, stream=stream)
+        ley.ley_sort(hin, hout, n, key_bytes=args.key_bytes, stream=stream)
         bms = timed(ley.ley_sort, max(2, args.e2e_steps // 3))
         e2e = {"value": round(n * 100 / (ems / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * 100,
                "d2h_bytes_per_step": n * 100, "ms_per_step": round(ems, 3), "steps": args.e2e_steps,
@@ -371,7 +384,7 @@ def main():
 
     cpu = None
     if not args.no_cpu and rank == 0:
-        cpu = cpu_baseline(cfg, args.cpu_sample)
+        cpu = cpu_baseline(cfg, args.cpu_sample, args.key_bytes)
 
     if rank == 0:
         line = {
@@ -379,7 +392,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based generator, SURVEY App. A)",
-            "config": {"workload": cfg["name"], "n_records": n_total, "record_bytes": 100, "key_bytes": 10,
+            "config": {"workload": cfg["name"] + ("" if args.key_bytes == 10 else f", {args.key_bytes}-byte keys (P:164)"),
+                       "n_records": n_total, "record_bytes": 100, "key_bytes": args.key_bytes,
                        "seed": cfg["seed"], "distribution": cfg["dist"],
                        "device_budget_bytes": budget,
                        "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7

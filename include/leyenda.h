@@ -36,8 +36,9 @@ typedef enum {
   LEY_OK = 0,
   LEY_ERR_INVALID_ARGUMENT = 1, /* NULL with n>0; in/out (or perm) overlap; base not 16-byte aligned;
                                    pointer on another device; unknown option name                      */
-  LEY_ERR_UNSUPPORTED = 2,      /* record_bytes != 100 or key_bytes != 10 (v1); pageable or managed
-                                   memory; in/out of different kinds (one host, one device)           */
+  LEY_ERR_UNSUPPORTED = 2,      /* record_bytes != 100; key_bytes outside 1..100 (1..10 on the external
+                                   and multi-GPU paths, see ley_sort); pageable or managed memory;
+                                   in/out of different kinds (one host, one device)                   */
   LEY_ERR_BUDGET = 3,           /* device_budget_bytes below the minimum working set of every path   */
   LEY_ERR_TOO_LARGE = 4,        /* n_records > 2^32 - 2 (u32 ordinals plus one sentinel) */
   LEY_ERR_CAPACITY = 5,         /* dist: out_capacity_records < records this rank must hold          */
@@ -53,12 +54,21 @@ typedef enum {
  *   in, out       : both DEVICE pointers on the current device (internal path: K-a .. K-e, §8a rows
  *                   a1-a6), or both PINNED HOST pointers (cudaHostAlloc / cudaHostRegister). Host
  *                   pointers take the staged-internal path when the working set fits
- *                   device_budget_bytes, else the external path (run generation + merge-path K-way
- *                   merge). Layout: n_records * record_bytes contiguous bytes, record i at
+ *                   device_budget_bytes, else the resident path (input staged, output streamed out;
+ *                   the paper's partial in-memory regime) when the input fits, else the external path
+ *                   (run generation + merge-path K-way merge). ley_plan_query tells which.
+ *                   Layout: n_records * record_bytes contiguous bytes, record i at
  *                   byte offset i*record_bytes, key = its first key_bytes bytes. 16-byte aligned bases.
  *                   Out-of-place only ("from the key to the tmp array"); `in` is never written.
  *   n_records     : 0 .. 2^32-2.
- *   record_bytes  : must be 100.   key_bytes: must be 10.
+ *   record_bytes  : must be 100.
+ *   key_bytes     : the key is record bytes [0, key_bytes), 1..100: the paper's 10 and its
+ *                   "flexible key sizes". <= 10: one pass; bytes [key_bytes, 10) of the sort
+ *                   key carry the ordinal, so equal keys keep input order. > 10: LSD passes over the
+ *                   10-byte windows (last window first), each stable, so the result is the same
+ *                   stable order; they need an extra n_records x 100-byte device buffer (+ 8 bytes per
+ *                   record with perm), device pointers or the staged host path (else
+ *                   LEY_ERR_UNSUPPORTED: the external and resident paths take keys of <= 10 bytes).
  *   device_budget_bytes : cap on device memory the LIBRARY allocates for this call (caller buffers
  *                   excluded); 0 = no cap (P:19's memory limit; BJ configs[4] "4 GB per GPU").
  *   stream        : a cudaStream_t (0 = legacy default stream). Work is ordered after prior work on
@@ -104,7 +114,7 @@ const char* ley_last_error(void);
  * (sum of n_local over ranks < r) + i. On return rank r holds global sorted positions
  * [*out_global_offset, *out_global_offset + *n_out_local) with exact splitters:
  * n_out_local(r) = floor((r+1) n / G) - floor(r n / G). Concatenating ranks 0..G-1 equals ley_sort of
- * the concatenated input. */
+ * the concatenated input. key_bytes: 1..10 (shorter keys compare as their prefix). */
 typedef struct ley_comm ley_comm;
 ley_status ley_comm_get_unique_id(uint8_t id_out[128]);  /* rank 0; broadcast it (e.g. torch PG)  */
 ley_status ley_comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);

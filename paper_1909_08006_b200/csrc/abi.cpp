@@ -13,14 +13,16 @@
 
 namespace ley {
 ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                              uint64_t budget, cudaStream_t s, Profiler& prof);
+                              uint64_t budget, uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
-                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, cudaStream_t s);
+                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
+                     cudaStream_t s);
 ley_status comm_get_unique_id(uint8_t id_out[128]);
 ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);
 ley_status comm_destroy(ley_comm* comm);
 ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
-                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, cudaStream_t s);
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint32_t key_bytes,
+                              cudaStream_t s);
 int dist_plan_splitters(const uint64_t* hist, uint64_t N, int G, uint32_t* bins, uint64_t* rho, uint64_t* first);
 void dist_bin_dest_counts(const uint64_t* local_hist, const uint32_t* bins, int nspl, uint64_t* counts);
 void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* recv_counts, uint64_t* recv_off,
@@ -67,11 +69,18 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
-ley_status check_common(const void* in, const void* out, const void* perm, uint64_t n, uint32_t rb, uint32_t kb) {
-  if (rb != kRecordBytes || kb != kKeyBytes) {
-    set_error("validate: only record_bytes=100, key_bytes=10 are supported (P:126)");
+// Records are 100 bytes. Keys: record bytes [0, key_bytes), 1 <= key_bytes <= 100 — the paper's
+// 10 and its "flexible key sizes".
+ley_status check_record_key(uint32_t rb, uint32_t kb, uint32_t max_kb) {
+  if (rb != kRecordBytes || kb < 1 || kb > max_kb) {
+    set_error("validate: record_bytes must be 100 and key_bytes 1.." + std::to_string(max_kb) + " on this path (P:126, P:164)");
     return LEY_ERR_UNSUPPORTED;
   }
+  return LEY_OK;
+}
+
+ley_status check_common(const void* in, const void* out, const void* perm, uint64_t n, uint32_t rb, uint32_t kb) {
+  if (ley_status st = check_record_key(rb, kb, kRecordBytes)) return st;
   if (n == 0) return LEY_OK;
   if (n > LEY_MAX_RECORDS) {
     set_error("validate: n_records > 2^32-2 (u32 ordinals)");
@@ -99,7 +108,7 @@ extern "C" {
 
 const char* ley_last_error(void) { return last_error(); }
 
-uint32_t ley_version(void) { return (1u << 16) | 0u; }
+uint32_t ley_version(void) { return (1u << 16) | 1u; }  // 1.1: key_bytes 1..100, host path 2
 
 ley_status ley_set_option(const char* name, int64_t value) {
   clear_error();
@@ -175,16 +184,25 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
 
   if (kin == Kind::kDevice) {
     InternalLayout L = plan_internal(n_records);
-    const uint64_t need = L.bytes + internal_aux_bytes(n_records);
+    const uint64_t need = L.bytes + internal_aux_bytes(n_records) + keypass_bytes(n_records, key_bytes, perm != nullptr);
     if (device_budget_bytes && need > device_budget_bytes) {
       set_error("plan: internal path needs " + std::to_string(need) + " bytes of device scratch, budget is " +
                 std::to_string(device_budget_bytes));
       return LEY_ERR_BUDGET;
     }
-    st = sort_internal_device(ctx, in8, out8, perm, n_records, s, prof);
+    st = sort_internal_device(ctx, in8, out8, perm, n_records, s, prof, nullptr, 0, key_bytes);
   } else {
     ley_plan_info info;
     plan_query(n_records, device_budget_bytes, &info);
+    if (key_bytes > kKeyBytes) {  // multi-pass keys: the staged path only (it needs a device output)
+      const uint64_t need = info.staged_bytes + keypass_bytes(n_records, key_bytes, perm != nullptr);
+      if (device_budget_bytes && need > device_budget_bytes) {
+        set_error("plan: keys longer than 10 bytes on host pointers take the staged path, which needs " +
+                  std::to_string(need) + " device bytes; budget is " + std::to_string(device_budget_bytes));
+        return LEY_ERR_UNSUPPORTED;
+      }
+      info.host_path = 0;
+    }
     if (info.host_path == 0) {
       // staged internal: H2D, internal sort, D2H
       const size_t bytes = (size_t)n_records * kRecordBytes;
@@ -195,15 +213,15 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
       if ((st = prof.begin("H2D"))) return st;
       LEY_CUDA("H2D", cudaMemcpyAsync(din, in8, bytes, cudaMemcpyHostToDevice, s));
       if ((st = prof.end())) return st;
-      st = sort_internal_device(ctx, din, dout, perm, n_records, s, prof);
+      st = sort_internal_device(ctx, din, dout, perm, n_records, s, prof, nullptr, 0, key_bytes);
       if (st) return st;
       if ((st = prof.begin("D2H"))) return st;
       LEY_CUDA("D2H", cudaMemcpyAsync(out8, dout, bytes, cudaMemcpyDeviceToHost, s));
       if ((st = prof.end())) return st;
     } else if (info.host_path == 2) {
-      st = sort_resident_host(ctx, in8, out8, perm, n_records, s, prof);
+      st = sort_resident_host(ctx, in8, out8, perm, n_records, key_bytes, s, prof);
     } else {
-      st = sort_external_host(ctx, in8, out8, perm, n_records, device_budget_bytes, s, prof);
+      st = sort_external_host(ctx, in8, out8, perm, n_records, device_budget_bytes, key_bytes, s, prof);
     }
   }
   if (st) return st;
@@ -238,13 +256,14 @@ ley_status ley_sort_submit(const void* in, void* out, uint64_t n_records, uint32
     return LEY_ERR_UNSUPPORTED;
   }
   const size_t a = ((size_t)n_records * kRecordBytes + 255) & ~size_t(255);
-  const uint64_t need = 4 * (uint64_t)a + plan_internal(n_records).bytes;  // two slots (in | out) + scratch
+  const uint64_t need = 4 * (uint64_t)a + plan_internal(n_records).bytes +  // two slots (in | out) + scratch
+                        keypass_bytes(n_records, key_bytes, false);
   if (device_budget_bytes && need > device_budget_bytes)  // does not fit twice: the blocking path decides
     return ley_sort(in, out, n_records, record_bytes, key_bytes, device_budget_bytes, stream);
   DeviceContext& ctx = device_context(dev);  // (device index and SM count are set on creation)
   // the pipeline has its own lock; its worker takes ctx.mu for each sort. Not taking ctx.mu here keeps a
   // submit from waiting for the previous call's sort to finish.
-  return sort_submit(ctx, static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), n_records,
+  return sort_submit(ctx, static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), n_records, key_bytes,
                      static_cast<cudaStream_t>(stream));
 }
 
@@ -274,16 +293,13 @@ ley_status ley_sort_dist(ley_comm* comm, const void* in_local, uint64_t n_local,
                          uint64_t out_capacity_records, uint64_t* n_out_local, uint64_t* out_global_offset,
                          uint32_t record_bytes, uint32_t key_bytes, uint64_t device_budget_bytes, void* stream) {
   clear_error();
-  if (record_bytes != kRecordBytes || key_bytes != kKeyBytes) {
-    set_error("validate: only record_bytes=100, key_bytes=10 are supported (P:126)");
-    return LEY_ERR_UNSUPPORTED;
-  }
+  if (ley_status st = check_record_key(record_bytes, key_bytes, kKeyBytes)) return st;
   if (!comm || !n_out_local || !out_global_offset) {
     set_error("validate: NULL comm / n_out_local / out_global_offset");
     return LEY_ERR_INVALID_ARGUMENT;
   }
   return dist_sort(comm, in_local, n_local, out_local, out_capacity_records, n_out_local, out_global_offset,
-                   device_budget_bytes, static_cast<cudaStream_t>(stream));
+                   device_budget_bytes, key_bytes, static_cast<cudaStream_t>(stream));
 }
 
 ley_status ley_comm_destroy(ley_comm* comm) {
@@ -295,16 +311,13 @@ ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const
                                   void* const* out_local, const uint64_t* out_capacity_records, uint64_t* n_out_local,
                                   uint64_t* out_global_offset, uint32_t record_bytes, uint32_t key_bytes, void* stream) {
   clear_error();
-  if (record_bytes != kRecordBytes || key_bytes != kKeyBytes) {
-    set_error("validate: only record_bytes=100, key_bytes=10 are supported (P:126)");
-    return LEY_ERR_UNSUPPORTED;
-  }
+  if (ley_status st = check_record_key(record_bytes, key_bytes, kKeyBytes)) return st;
   if (!in_local || !n_local || !out_local || !out_capacity_records || !n_out_local || !out_global_offset) {
     set_error("validate: NULL argument array");
     return LEY_ERR_INVALID_ARGUMENT;
   }
   return dist_sort_loopback(nranks, in_local, n_local, out_local, out_capacity_records, n_out_local,
-                            out_global_offset, static_cast<cudaStream_t>(stream));
+                            out_global_offset, key_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int ley_dist_plan_splitters(const uint64_t* global_hist16, uint64_t n_total, int nranks, uint32_t* bins,

@@ -54,4 +54,17 @@ struct DistSplitter {
   uint32_t hi, mid, lo16, gidx;
 };
 
+// Keys shorter than 10 bytes: the bits of key bytes [key_bytes, 10) in (hi, mid, lo16) are masked
+// off wherever the multi-GPU path compares keys, so equal prefixes fall to the global ordinal.
+struct DistKeyMask {
+  uint32_t hi = ~0u, mid = ~0u, lo16 = 0xFFFFu;
+};
+inline DistKeyMask dist_key_mask(uint32_t kb) {
+  DistKeyMask m;
+  m.hi = kb >= 4 ? ~0u : ~(~0u >> (8 * kb));
+  m.mid = kb >= 8 ? ~0u : (kb <= 4 ? 0u : ~(~0u >> (8 * (kb - 4))));
+  m.lo16 = kb >= 10 ? 0xFFFFu : (kb == 9 ? 0xFF00u : 0u);
+  return m;
+}
+
 }  // namespace ley

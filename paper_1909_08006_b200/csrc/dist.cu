@@ -121,6 +121,8 @@ struct RankState {
   uint8_t* out = nullptr;
   uint64_t cap = 0;
   uint64_t gbase = 0;
+  uint32_t key_bytes = 10;  // keys = record bytes [0, key_bytes), 1..10
+  DistKeyMask km;
   // device scratch (one buffer)
   DeviceBuffer buf;
   uint32_t* d_hist = nullptr;        // [65536]
@@ -205,7 +207,7 @@ ley_status rank_alloc(RankState& r) {
 // ---------------------------------------------------------------------------- phases (one rank)
 ley_status phase1_hist(RankState& r) {
   LEY_CUDA("K-s0 hist", cudaMemsetAsync(r.d_hist, 0, 4 * 65536, r.s));
-  LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.d_pref, r.ctx->sms, r.s));
+  LEY_CUDA("K-s0 hist", launch_ks_hist16(r.in, r.n, r.d_hist, r.d_pref, r.km, r.ctx->sms, r.s));
   r.launches += 1;
   return LEY_OK;
 }
@@ -227,7 +229,7 @@ ley_status phase2_candidates(RankState& r, const Plan& P) {
 
 // Given all candidates concatenated in rank order (device records + ordinals), find the exact splitters.
 ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* all_cand, const uint32_t* all_gidx,
-                            uint64_t total_cand, Plan& P, DeviceBuffer& tmp) {
+                            uint64_t total_cand, Plan& P, DeviceBuffer& tmp, uint32_t key_bytes) {
   const int nspl = P.G - 1;
   if (nspl == 0) return LEY_OK;
   const InternalLayout L = plan_internal(total_cand);
@@ -240,7 +242,7 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
   Profiler quiet;
   quiet.ctx = &ctx;
   quiet.stream = s;
-  ley_status st = sort_internal_device(ctx, all_cand, sorted, perm, total_cand, s, quiet, work, L.bytes);
+  ley_status st = sort_internal_device(ctx, all_cand, sorted, perm, total_cand, s, quiet, work, L.bytes, key_bytes);
   if (st) return st;
   P.launches += quiet.launches;
   // first sorted index of each boundary bin = candidates in smaller boundary bins; all splitters' key
@@ -273,6 +275,10 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
     d.hi = ((uint32_t)key[0] << 24) | ((uint32_t)key[1] << 16) | ((uint32_t)key[2] << 8) | key[3];
     d.mid = ((uint32_t)key[4] << 24) | ((uint32_t)key[5] << 16) | ((uint32_t)key[6] << 8) | key[7];
     d.lo16 = ((uint32_t)key[8] << 8) | key[9];
+    const DistKeyMask km = dist_key_mask(key_bytes);
+    d.hi &= km.hi;
+    d.mid &= km.mid;
+    d.lo16 &= km.lo16;
     d.gidx = gidx[k];
   }
   return LEY_OK;
@@ -286,7 +292,7 @@ ley_status phase4_counts(RankState& r, const Plan& P) {
   LEY_CUDA("K-s2 counts", cudaMemsetAsync(r.d_dcount, 0, 8 * kMaxRanks, r.s));
   r.launches += 1;
   LEY_CUDA("K-s2 counts", launch_ks_dest_counts(r.d_cand, r.d_cand_gidx, r.ncand, r.d_spl, nspl, r.d_dcount,
-                                                r.ctx->sms, r.s));
+                                                r.km, r.ctx->sms, r.s));
   unsigned long long c[kMaxRanks];
   LEY_CUDA("K-s2 counts", cudaMemcpyAsync(c, r.d_dcount, 8 * kMaxRanks, cudaMemcpyDeviceToHost, r.s));
   LEY_CUDA("K-s2 counts", cudaStreamSynchronize(r.s));
@@ -319,7 +325,7 @@ ley_status phase5_partition(RankState& r, const Plan& P, uint8_t* const* host_ba
   LEY_CUDA("K-p partition", cudaMemsetAsync(r.d_status, 0, 8 * (kp_tiles(r.n) * kMaxRanks + 1), r.s));
   r.launches += 1;
   LEY_CUDA("K-p partition", launch_kp_partition(r.in, r.n, (uint32_t)r.gbase, r.d_spl, G - 1, dev_bases, r.d_doff,
-                                                r.d_status, r.d_small + 2, remote, r.s));
+                                                r.d_status, r.d_small + 2, remote, r.km, r.s));
   return LEY_OK;
 }
 
@@ -338,7 +344,7 @@ ley_status phase6_local_sort(RankState& r, const uint8_t* recv) {
   quiet.ctx = r.ctx;
   quiet.stream = r.s;
   if (r.n_out == 0) return LEY_OK;
-  const ley_status st = sort_internal_device(*r.ctx, recv, r.out, nullptr, r.n_out, r.s, quiet);
+  const ley_status st = sort_internal_device(*r.ctx, recv, r.out, nullptr, r.n_out, r.s, quiet, nullptr, 0, r.key_bytes);
   r.launches += quiet.launches;
   return st;
 }
@@ -447,7 +453,8 @@ ley_status comm_destroy(ley_comm* comm) {
 }
 
 ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
-                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, cudaStream_t s) {
+                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
+                     cudaStream_t s) {
   (void)budget;
   const int G = comm->nranks;
   LEY_CUDA("dist", cudaSetDevice(comm->device));
@@ -470,6 +477,8 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   r.n = n_local;
   r.out = static_cast<uint8_t*>(out_local);
   r.cap = out_capacity;
+  r.key_bytes = key_bytes;
+  r.km = dist_key_mask(key_bytes);
   ley_status st = rank_alloc(r);
   if (st) return st;
   Plan P;
@@ -573,7 +582,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
       }
       at += counts[i];
     }
-    if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P, r.split_buf))) return st;
+    if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P, r.split_buf, key_bytes))) return st;
     LEY_CUDA("dist cand", cudaStreamSynchronize(s));
   }
   // P4 + C3: send counts
@@ -642,7 +651,8 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
 // All G ranks on the current device in one process; collectives are host-side reductions and device
 // copies. Exercises exactly the kernels and plans of dist_sort (test hook).
 ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
-                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, cudaStream_t s) {
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint32_t key_bytes,
+                              cudaStream_t s) {
   if (G < 1 || G > kMaxRanks) {
     set_error("loopback: 1 <= G <= 8");
     return LEY_ERR_INVALID_ARGUMENT;
@@ -670,6 +680,8 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
     r.n = n_local[i];
     r.out = static_cast<uint8_t*>(out[i]);
     r.cap = caps[i];
+    r.key_bytes = key_bytes;
+    r.km = dist_key_mask(key_bytes);
     r.gbase = P.N;
     P.N += n_local[i];
     if ((st = rank_alloc(r))) return st;
@@ -712,7 +724,7 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
       }
       at += c;
     }
-    if ((st = phase3_splitters(ctx, s, cat, gid, total, P, R[0]->split_buf))) return st;
+    if ((st = phase3_splitters(ctx, s, cat, gid, total, P, R[0]->split_buf, key_bytes))) return st;
   }
   // P4 + C3
   P.send_matrix.assign((size_t)G * G, 0);

@@ -63,8 +63,9 @@ struct Splitter {
   uint64_t pos;      // its position in that run
 };
 
-__device__ __forceinline__ int cmp_key10(const uint8_t* a, const uint8_t* b) {
-  for (int i = 0; i < 10; ++i) {
+// keys of kb <= 10 bytes (P:164 flexible key sizes): bytes [kb, 10) never decide
+__device__ __forceinline__ int cmp_key(const uint8_t* a, const uint8_t* b, uint32_t kb) {
+  for (uint32_t i = 0; i < kb; ++i) {
     if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
   }
   return 0;
@@ -74,7 +75,7 @@ __device__ __forceinline__ int cmp_key10(const uint8_t* a, const uint8_t* b) {
 // Binary search over the sorted run, reading keys from pinned host scratch (zero-copy).
 __global__ void ext_locate(const uint8_t* __restrict__ scratch_dev, const uint64_t* __restrict__ run_off,
                            const uint64_t* __restrict__ run_len, uint32_t R, const Splitter* __restrict__ spl,
-                           uint32_t nspl, uint64_t* __restrict__ split) {
+                           uint32_t nspl, uint32_t kb, uint64_t* __restrict__ split) {
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (uint64_t)nspl * R) return;
   const uint32_t p = (uint32_t)(id / R), r = (uint32_t)(id % R);
@@ -87,21 +88,24 @@ __global__ void ext_locate(const uint8_t* __restrict__ scratch_dev, const uint64
     const uint8_t* rec = base + mid * kRecordBytes;
 #pragma unroll
     for (int i = 0; i < 10; ++i) k[i] = rec[i];
-    const int c = cmp_key10(k, sp.key);
+    const int c = cmp_key(k, sp.key, kb);
     const bool before = c < 0 || (c == 0 && (r < sp.run || (r == sp.run && mid < sp.pos)));
     if (before) lo = mid + 1; else hi = mid;
   }
   split[id] = lo;
 }
 
-// composite key of element i of the concatenated slice buffer: (key bytes 0..7 BE, bytes 8..9 << 48 | i)
-__global__ void ext_make_comp(const uint8_t* __restrict__ recs, uint64_t m, uint64_t* __restrict__ hi,
+// composite key of element i of the concatenated slice buffer: (key bytes 0..7 BE, bytes 8..9 << 48 | i),
+// key bytes [kb, 10) zeroed (keys shorter than 10 bytes: ties then fall to (run, pos) = the slice order)
+__global__ void ext_make_comp(const uint8_t* __restrict__ recs, uint64_t m, uint32_t kb, uint64_t* __restrict__ hi,
                               uint64_t* __restrict__ lo) {
+  const uint64_t mhi = kb >= 8 ? ~0ull : ~(~0ull >> (8 * kb));
+  const uint64_t mlo = kb >= 10 ? 0xFFFFull : (kb == 9 ? 0xFF00ull : 0ull);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(recs + i * kRecordBytes);
     const uint32_t a = w[0], b = w[1], c = w[2];
-    hi[i] = ((uint64_t)bswap32(a) << 32) | bswap32(b);
-    lo[i] = ((uint64_t)(((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) << 48) | i;
+    hi[i] = (((uint64_t)bswap32(a) << 32) | bswap32(b)) & mhi;
+    lo[i] = ((uint64_t)(((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) & mlo) << 48 | i;
   }
 }
 
@@ -239,8 +243,13 @@ unsigned grid_for(uint64_t work, int sms, int per_sm = 8) {
 
 // ---------------------------------------------------------------------------------------- driver
 ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                              uint64_t budget, cudaStream_t s, Profiler& prof) {
+                              uint64_t budget, uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
   ley_status st;
+  if (key_bytes > kKeyBytes) {  // the merge compares 10-byte composites (K-m)
+    set_error("external: keys longer than 10 bytes are not supported on the external path (raise the budget "
+              "to the staged path's ley_plan_query().staged_bytes)");
+    return LEY_ERR_UNSUPPORTED;
+  }
   const uint64_t C = external_run_records(n, budget);
   if (C < 1024 && C < n) {
     set_error("external: device_budget_bytes " + std::to_string(budget) +
@@ -330,7 +339,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
     if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_out[sl] copied out
     const size_t t_s = tr.begin("run sort", s);
     st = sort_internal_device(ctx, d_in[sl], d_out[sl], perm_out ? d_run_perm[sl] : nullptr, len, s, quiet, d_work,
-                              LC.bytes);
+                              LC.bytes, key_bytes);
     if (st) return st;
     tr.end(t_s, s);
     prof.launches += quiet.launches;
@@ -376,7 +385,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   }
   if (P > 1) {
     st = sort_internal_device(ctx, d_samp, d_samp_sorted, d_samp_perm, nsamp, s, quiet, d_work2,
-                              plan_internal(nsamp).bytes);
+                              plan_internal(nsamp).bytes, key_bytes);
     if (st) return st;
     prof.launches += quiet.launches;
     quiet.launches = 0;
@@ -403,7 +412,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
     LEY_CUDA("ext locate", cudaMemcpyAsync(d_runlen, run_len.data(), 8 * R, cudaMemcpyHostToDevice, s));
     const uint64_t nthreads = (uint64_t)(P - 1) * R;
     ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
-                                                                  d_split);
+                                                                  key_bytes, d_split);
     LEY_CUDA("ext locate", cudaGetLastError());
     prof.launches += 1;
     LEY_CUDA("ext locate", cudaMemcpyAsync(split.data() + R, d_split, 8 * nthreads, cudaMemcpyDeviceToHost, s));
@@ -511,7 +520,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
     LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_in[sl], 0));
     if (i >= 2) LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_mout[sl] copied out
     const size_t t_mm = tr.begin("merge K-m", s);
-    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice[sl], m, c_h[0], c_l[0]);
+    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice[sl], m, key_bytes, c_h[0], c_l[0]);
     LEY_CUDA("K-m merge", cudaGetLastError());
     prof.launches += 1;
     // merge tree over the R run slices: one launch per level, boundaries already on the device

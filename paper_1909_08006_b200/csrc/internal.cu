@@ -21,8 +21,10 @@ namespace {
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
-ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                                cudaStream_t s, Profiler& prof, void* work, size_t work_bytes) {
+namespace {
+// One pass of the internal sort (K-a .. K-e) ordered by the key window `key`.
+ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                     cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, KeySpec key) {
   const InternalLayout L = plan_internal(n);
   ley_status st;
   if (!out && !perm_out) {  // out == nullptr is the perm-only mode (K-d without the fused gather)
@@ -79,7 +81,8 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
 
   // ---------------------------------------------------------------- K-a
   if ((st = prof.begin("K-a tile sort"))) return st;
-  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, o.ka_stream != 0, s));
+  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, o.ka_stream != 0,
+                                                key, s));
   ++launches;
   if ((st = prof.end())) return st;
 
@@ -189,6 +192,58 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     LEY_CUDA("perm", cudaPointerGetAttributes(&pa, perm_out));
     cudaMemcpyKind kind = pa.type == cudaMemoryTypeDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     LEY_CUDA("perm", cudaMemcpyAsync(perm_out, perm, 4 * n, kind, s));
+  }
+  return LEY_OK;
+}
+
+}  // namespace
+
+uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm) {
+  if (key_bytes <= kKeyBytes) return 0;
+  return a256(n * kRecordBytes) + (perm ? 2 * a256(4 * n) : 0);
+}
+
+// Keys of up to 10 bytes: one pass. Longer keys (§5, flexible key sizes): LSD over the
+// 10-byte windows, the last (possibly partial) window first. Each pass is stable with respect to its own
+// input order (the ordinal is the position in that input), so after the pass on window 0 the records
+// are in (window 0, window 1, ..., original index) order. Passes alternate between out and a scratch
+// buffer so the last one lands in out; with perm, the passes' permutations are composed on the device.
+ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                                cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, uint32_t key_bytes) {
+  if (key_bytes < 1 || key_bytes > kRecordBytes) {
+    set_error("internal: key_bytes must be in [1, 100]");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  if (key_bytes <= kKeyBytes) return sort_pass(ctx, in, out, perm_out, n, s, prof, work, work_bytes, KeySpec{0, key_bytes});
+  if (!out) {
+    set_error("internal: keys longer than 10 bytes need an output buffer (multi-pass)");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  const uint32_t W = (key_bytes + kKeyBytes - 1) / kKeyBytes;
+  ley_status st = ensure_buffer(ctx.keypass, keypass_bytes(n, key_bytes, perm_out != nullptr), "key passes", s);
+  if (st) return st;
+  uint8_t* tmp = static_cast<uint8_t*>(ctx.keypass.ptr);
+  uint32_t* pa = perm_out ? reinterpret_cast<uint32_t*>(tmp + a256(n * kRecordBytes)) : nullptr;
+  uint32_t* pb = perm_out ? pa + a256(4 * n) / 4 : nullptr;
+  const uint8_t* src = in;
+  for (uint32_t p = 0; p < W; ++p) {
+    const uint32_t w = W - 1 - p;
+    const KeySpec ks{kKeyBytes * w, std::min<uint32_t>(kKeyBytes, key_bytes - kKeyBytes * w)};
+    uint8_t* dst = (w % 2 == 0) ? out : tmp;
+    uint32_t* pcur = perm_out ? (p == 0 ? pa : pb) : nullptr;
+    if ((st = sort_pass(ctx, src, dst, pcur, n, s, prof, work, work_bytes, ks))) return st;
+    if (perm_out && p > 0) {  // total order so far: pb[j] = pa[pb[j]]
+      LEY_CUDA("key passes", launch_compose_perm(pa, pb, n, ctx.sms, s));
+      ++prof.launches;
+      std::swap(pa, pb);
+    }
+    src = dst;
+  }
+  if (perm_out) {
+    cudaPointerAttributes pa_attr{};
+    LEY_CUDA("perm", cudaPointerGetAttributes(&pa_attr, perm_out));
+    const cudaMemcpyKind kind = pa_attr.type == cudaMemoryTypeDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    LEY_CUDA("perm", cudaMemcpyAsync(perm_out, pa, 4 * n, kind, s));
   }
   return LEY_OK;
 }

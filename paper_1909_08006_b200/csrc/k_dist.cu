@@ -27,12 +27,13 @@ namespace ley {
 
 namespace {
 
-__device__ __forceinline__ void load_key(const uint8_t* in, uint64_t i, uint32_t& hi, uint32_t& mid, uint32_t& lo16) {
+__device__ __forceinline__ void load_key(const uint8_t* in, uint64_t i, uint32_t& hi, uint32_t& mid, uint32_t& lo16,
+                                         const DistKeyMask& km) {
   const uint32_t* p = reinterpret_cast<const uint32_t*>(in + i * kRecordBytes);
-  hi = bswap32(__ldg(p));        // key bytes 0..3
-  mid = bswap32(__ldg(p + 1));   // 4..7
+  hi = bswap32(__ldg(p)) & km.hi;        // key bytes 0..3
+  mid = bswap32(__ldg(p + 1)) & km.mid;  // 4..7
   const uint32_t c = __ldg(p + 2);
-  lo16 = ((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu);  // bytes 8..9
+  lo16 = (((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) & km.lo16;  // bytes 8..9
 }
 
 __device__ __forceinline__ int splitter_cmp(uint32_t hi, uint32_t mid, uint32_t lo16, uint32_t gidx,
@@ -60,13 +61,13 @@ __device__ __forceinline__ uint32_t dest_of(uint32_t hi, uint32_t mid, uint32_t 
 // Also keeps every record's 16-bit prefix (2 B/record, coalesced) so that K-s1 finds the boundary-bin
 // records from the prefixes instead of reading every record's key line again (~100 B/record).
 __global__ void __launch_bounds__(256) ks_hist16(const uint8_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ hist,
-                                                 uint16_t* __restrict__ pref) {
+                                                 uint16_t* __restrict__ pref, uint32_t mask_hi) {
   const uint32_t lt = lanemask_lt();
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = base + threadIdx.x;
     const bool valid = i < n;
     uint32_t hi = 0;
-    if (valid) hi = bswap32(__ldg(reinterpret_cast<const uint32_t*>(in + i * kRecordBytes)));
+    if (valid) hi = bswap32(__ldg(reinterpret_cast<const uint32_t*>(in + i * kRecordBytes))) & mask_hi;
     const uint32_t p16 = hi >> 16;
     if (valid) pref[i] = (uint16_t)p16;
     const uint32_t peers = warp_peers8(p16 & 0xFFu, valid) & warp_peers8(p16 >> 8, valid);
@@ -150,13 +151,13 @@ __global__ void __launch_bounds__(kCandThreads)
 // ------------------------------------------------------------------------------------------ K-s2
 __global__ void ks_dest_counts(const uint8_t* __restrict__ cand, const uint32_t* __restrict__ cand_gidx,
                                uint32_t ncand, const DistSplitter* __restrict__ spl, int nspl,
-                               unsigned long long* __restrict__ counts) {
+                               unsigned long long* __restrict__ counts, DistKeyMask km) {
   __shared__ unsigned long long s_c[kMaxRanks];
   if (threadIdx.x < kMaxRanks) s_c[threadIdx.x] = 0;
   __syncthreads();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ncand; i += gridDim.x * blockDim.x) {
     uint32_t hi, mid, lo16;
-    load_key(cand, i, hi, mid, lo16);
+    load_key(cand, i, hi, mid, lo16, km);
     atomicAdd(&s_c[dest_of(hi, mid, lo16, cand_gidx[i], spl, nspl)], 1ull);
   }
   __syncthreads();
@@ -170,7 +171,7 @@ constexpr uint32_t kPartTile = 256;  // records per tile (one per thread)
 __global__ void __launch_bounds__(kPartThreads)
     kp_partition(const uint8_t* __restrict__ in, uint64_t n, uint32_t gbase, const DistSplitter* __restrict__ spl,
                  int nspl, uint8_t* const* __restrict__ dst_base, const uint64_t* __restrict__ dst_off,
-                 uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, int remote) {
+                 uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, int remote, DistKeyMask km) {
   extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* s_rec = s_dyn;                                 // tile in input order
   uint32_t* s_out = s_dyn + kPartTile * kRecordWords;      // tile in destination order
@@ -205,8 +206,8 @@ __global__ void __launch_bounds__(kPartThreads)
   if (valid) {
     const uint32_t* r = s_rec + i * kRecordWords;
     const uint32_t c = r[2];
-    d = dest_of(bswap32(r[0]), bswap32(r[1]), ((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu), gbase + (uint32_t)(base + i),
-                s_spl, nspl);
+    d = dest_of(bswap32(r[0]) & km.hi, bswap32(r[1]) & km.mid, (((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) & km.lo16,
+                gbase + (uint32_t)(base + i), s_spl, nspl);
   }
   // stable rank by destination (3 ballots: destinations < 8)
   uint32_t peers = __ballot_sync(0xffffffffu, valid);
@@ -301,9 +302,10 @@ unsigned grid_cap(uint64_t items, int per_block, int sms, int per_sm) {
 
 }  // namespace
 
-cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, int sms, cudaStream_t s) {
+cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, DistKeyMask km, int sms,
+                             cudaStream_t s) {
   if (!n) return cudaSuccess;
-  ks_hist16<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(in, n, hist, pref);
+  ks_hist16<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(in, n, hist, pref, km.hi);
   return cudaGetLastError();
 }
 
@@ -320,10 +322,10 @@ cudaError_t launch_ks_candidates(const uint8_t* in, const uint16_t* pref, uint64
 }
 
 cudaError_t launch_ks_dest_counts(const uint8_t* cand, const uint32_t* cand_gidx, uint32_t ncand,
-                                  const DistSplitter* spl, int nspl, unsigned long long* counts, int sms,
-                                  cudaStream_t s) {
+                                  const DistSplitter* spl, int nspl, unsigned long long* counts, DistKeyMask km,
+                                  int sms, cudaStream_t s) {
   if (!ncand) return cudaSuccess;
-  ks_dest_counts<<<grid_cap(ncand, 256, sms, 4), 256, 0, s>>>(cand, cand_gidx, ncand, spl, nspl, counts);
+  ks_dest_counts<<<grid_cap(ncand, 256, sms, 4), 256, 0, s>>>(cand, cand_gidx, ncand, spl, nspl, counts, km);
   return cudaGetLastError();
 }
 
@@ -331,13 +333,13 @@ uint64_t kp_tiles(uint64_t n) { return (n + kPartTile - 1) / kPartTile; }
 
 cudaError_t launch_kp_partition(const uint8_t* in, uint64_t n, uint32_t gbase, const DistSplitter* spl, int nspl,
                                 uint8_t* const* dst_base, const uint64_t* dst_off, uint64_t* status, uint32_t* ticket,
-                                bool remote, cudaStream_t s) {
+                                bool remote, DistKeyMask km, cudaStream_t s) {
   if (!n) return cudaSuccess;
   const size_t smem = 2ull * kPartTile * kRecordBytes;
   cudaError_t e = cudaFuncSetAttribute(kp_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kp_partition<<<(unsigned)kp_tiles(n), kPartThreads, smem, s>>>(in, n, gbase, spl, nspl, dst_base, dst_off, status,
-                                                                  ticket, remote ? 1 : 0);
+                                                                  ticket, remote ? 1 : 0, km);
   return cudaGetLastError();
 }
 

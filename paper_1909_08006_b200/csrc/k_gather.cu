@@ -43,7 +43,20 @@ __global__ void __launch_bounds__(kGatherThreads) ke_gather(const uint8_t* __res
   }
 }
 
+__global__ void ke_compose_perm(const uint32_t* __restrict__ prev, uint32_t* __restrict__ cur, uint64_t n) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+    cur[j] = __ldg(prev + cur[j]);
+}
+
 }  // namespace
+
+cudaError_t launch_compose_perm(const uint32_t* prev, uint32_t* cur, uint64_t n, int sms, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+  ke_compose_perm<<<(unsigned)blocks, 256, 0, s>>>(prev, cur, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
                              cudaStream_t s) {

@@ -29,11 +29,39 @@ __device__ __forceinline__ uint32_t ld_ef_u32(const uint32_t* p, uint64_t pol) {
   return v;
 }
 
+// Flexible keys (§5). K-a sorts on a 10-byte key window at record byte
+// key.off (a multiple of 10: words key.off/4 .. +2, shifted by 16 bits when key.off % 4 == 2); a key of
+// more than 10 bytes is sorted LSD over its windows, last window first (internal.cu). A window of
+// key.len < 10 bytes (a short key, or the last window of a long one) has its bytes [len, 10) replaced by
+// the big-endian ordinal (its top bytes if fewer than 4 remain): (composite, ordinal) order is then
+// (key, ordinal) order, and equal keys stop recursing as soon as the ordinal bytes are reached.
+__device__ __forceinline__ void ka_window(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t w2, uint32_t sh) {
+  // in: a, b, w2 = words key.off/4 .. +2; out: a, b = window bytes 0..7, c = window bytes 8..9 (low 16)
+  if (sh) {
+    a = __funnelshift_r(a, b, sh);
+    b = __funnelshift_r(b, w2, sh);
+    c = w2 >> sh;
+  } else {
+    c = w2;
+  }
+}
+
+__device__ __forceinline__ void ka_compose(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t len, uint32_t ord) {
+  unsigned __int128 K = ((unsigned __int128)bswap32(a) << 48) | ((unsigned __int128)bswap32(b) << 16) |
+                        (((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu));
+  const uint32_t free_bits = 8u * (10u - len);  // 8 .. 72
+  K = (K >> free_bits) << free_bits;
+  K |= free_bits >= 32 ? ((unsigned __int128)ord << (free_bits - 32)) : (unsigned __int128)(ord >> (32 - free_bits));
+  a = bswap32((uint32_t)(K >> 48));
+  b = bswap32((uint32_t)(K >> 16));
+  c = (c & 0xFFFF0000u) | (((uint32_t)K >> 8) & 0xFFu) | (((uint32_t)K & 0xFFu) << 8);
+}
+
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles,
                                                          uint64_t* __restrict__ k1_out, uint32_t* __restrict__ w_out,
                                                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
-                                                         uint32_t* __restrict__ hist16, uint32_t copies) {
+                                                         uint32_t* __restrict__ hist16, uint32_t copies, KeySpec key) {
   constexpr int T = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -61,12 +89,19 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
   for (int j = 0; j < ITEMS; ++j) {
     uint32_t r = warp * (32 * ITEMS) + j * 32 + lane;
     if (r < cnt_t) {
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (base + r) * kRecordBytes);
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (base + r) * kRecordBytes) + key.off / 4;
       a[j] = ld_ef_u32(p, pol_ef);
       b[j] = ld_ef_u32(p + 1, pol_ef);
       c[j] = ld_ef_u32(p + 2, pol_ef);
     } else {
       a[j] = b[j] = c[j] = 0;
+    }
+  }
+  if (key.off | (key.len - 10u)) {  // (uniform) a key window other than the paper's bytes 0..9
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      ka_window(a[j], b[j], c[j], c[j], (key.off & 3u) * 8u);
+      if (key.len < 10) ka_compose(a[j], b[j], c[j], key.len, (uint32_t)(base + warp * (32 * ITEMS) + j * 32 + lane));
     }
   }
   __syncthreads();
@@ -171,7 +206,7 @@ template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, 1)
     ka_tile_stream(const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles, uint64_t* __restrict__ k1_out,
                    uint32_t* __restrict__ w_out, uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
-                   uint32_t* __restrict__ hist16, uint32_t copies) {
+                   uint32_t* __restrict__ hist16, uint32_t copies, uint32_t key_len) {
   constexpr int T = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -233,6 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         a[j] = kw[0];
         b[j] = kw[1];
         c[j] = kw[2];
+        if (key_len < 10) ka_compose(a[j], b[j], c[j], key_len, (uint32_t)(base + r));
       } else {
         a[j] = b[j] = c[j] = 0;
       }
@@ -316,12 +352,12 @@ size_t ka_smem_bytes() {
 
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
                                 uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
-                                cudaStream_t s) {
+                                KeySpec key, cudaStream_t s) {
   auto kern = ka_tile_sort<kTileThreads, kTileItems>;
   size_t smem = ka_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (stream_form) {
+  if (stream_form && key.off == 0) {  // (the ring copies whole records but keys only from bytes 0..11)
     auto sk = ka_tile_stream<kTileThreads, kTileItems>;
     const size_t ssm = (size_t)kRing * kPieceBytes + (size_t)kTileRecords * 12 +
                        (size_t)(kTileThreads / 32) * kRadix * 4 + 32 * 4;
@@ -331,10 +367,10 @@ cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, u
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    sk<<<grid, kTileThreads, ssm, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies);
+    sk<<<grid, kTileThreads, ssm, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key.len);
     return cudaGetLastError();
   }
-  kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies);
+  kern<<<tiles, kTileThreads, smem, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key);
   return cudaGetLastError();
 }
 

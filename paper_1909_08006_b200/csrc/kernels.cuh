@@ -8,11 +8,18 @@
 
 namespace ley {
 
+// The 10-byte key window one sort pass orders by: record bytes [off, off + len), off a multiple of 10,
+// 1 <= len <= 10 (len < 10: bytes [len, 10) of the window carry the ordinal; k_tile.cu)
+struct KeySpec {
+  uint32_t off = 0;
+  uint32_t len = 10;
+};
+
 // K-a (k_tile.cu)
 size_t ka_smem_bytes();
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
                                 uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
-                                cudaStream_t s);
+                                KeySpec key, cudaStream_t s);
 
 // K-b (k_scan.cu)
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
@@ -52,22 +59,25 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
 // K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
                              cudaStream_t s);
+// multi-pass keys: cur[j] = prev[cur[j]] (the permutation of the passes so far, k_gather.cu)
+cudaError_t launch_compose_perm(const uint32_t* prev, uint32_t* cur, uint64_t n, int sms, cudaStream_t s);
 
 // multi-GPU (k_dist.cu)
-cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, int sms, cudaStream_t s);
+cudaError_t launch_ks_hist16(const uint8_t* in, uint64_t n, uint32_t* hist, uint16_t* pref, DistKeyMask km, int sms,
+                             cudaStream_t s);
 uint64_t ks_candidate_tiles(uint64_t n);
 cudaError_t launch_ks_candidates(const uint8_t* in, const uint16_t* pref, uint64_t n, uint32_t gbase,
                                  const uint32_t* bins, int nbins,
                                  uint64_t* status, uint32_t* ticket, uint8_t* cand, uint32_t* cand_gidx,
                                  uint32_t* cand_count, cudaStream_t s);
 cudaError_t launch_ks_dest_counts(const uint8_t* cand, const uint32_t* cand_gidx, uint32_t ncand,
-                                  const DistSplitter* spl, int nspl, unsigned long long* counts, int sms,
-                                  cudaStream_t s);
+                                  const DistSplitter* spl, int nspl, unsigned long long* counts, DistKeyMask km,
+                                  int sms, cudaStream_t s);
 uint64_t kp_tiles(uint64_t n);
 // dst_base[d] / dst_off[d] (device arrays, kMaxRanks): where destination d's run starts (records);
 // remote = the bases are peers' windows (adds a system-scope fence before the grid completes)
 cudaError_t launch_kp_partition(const uint8_t* in, uint64_t n, uint32_t gbase, const DistSplitter* spl, int nspl,
                                 uint8_t* const* dst_base, const uint64_t* dst_off, uint64_t* status, uint32_t* ticket,
-                                bool remote, cudaStream_t s);
+                                bool remote, DistKeyMask km, cudaStream_t s);
 
 }  // namespace ley

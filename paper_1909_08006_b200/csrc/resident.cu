@@ -23,7 +23,7 @@ inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                              cudaStream_t s, Profiler& prof) {
+                              uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
   const uint64_t C = resident_chunk_records(n);
   const size_t a_in = a256((size_t)n * kRecordBytes), a_perm = a256(4 * (size_t)n), a_win = a256(C * kRecordBytes);
   ley_status st = ensure_buffer(ctx.stage, a_in + a_perm + 2 * a_win, "resident staging", s);
@@ -38,7 +38,7 @@ ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   if ((st = prof.begin("H2D"))) return st;
   LEY_CUDA("resident H2D", cudaMemcpyAsync(din, in, (size_t)n * kRecordBytes, cudaMemcpyHostToDevice, s));
   if ((st = prof.end())) return st;
-  if ((st = sort_internal_device(ctx, din, nullptr, dperm, n, s, prof))) return st;
+  if ((st = sort_internal_device(ctx, din, nullptr, dperm, n, s, prof, nullptr, 0, key_bytes))) return st;
   if (perm_out) LEY_CUDA("resident perm", cudaMemcpyAsync(perm_out, dperm, 4 * n, cudaMemcpyDeviceToHost, s));
 
   if ((st = prof.begin("K-e gather+D2H"))) return st;

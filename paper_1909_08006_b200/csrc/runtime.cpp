@@ -305,7 +305,7 @@ void release_device(int device) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(d);
-    for (DeviceBuffer* b : {&c.work, &c.lists, &c.big[0], &c.big[1], &c.rec, &c.stage, &c.ext}) {
+    for (DeviceBuffer* b : {&c.work, &c.lists, &c.big[0], &c.big[1], &c.rec, &c.stage, &c.ext, &c.keypass}) {
       if (b->ptr) {
         cudaFree(b->ptr);
         track_device_bytes(-(int64_t)b->cap);

@@ -95,6 +95,7 @@ struct DeviceContext {
   DeviceBuffer rec;       // recursion-level arrays (chunk starts, histograms, look-back status)
   DeviceBuffer stage;     // staged input/output for host pointers
   DeviceBuffer ext;       // external path device buffers
+  DeviceBuffer keypass;   // keys > 10 bytes: the other record buffer of the LSD window passes (+ perms)
   void* host_pinned = nullptr;  // small pinned host scratch (counters)
   void* host_scratch = nullptr;  // external path: pinned (mapped) host run scratch
   size_t host_scratch_cap = 0;
@@ -111,6 +112,7 @@ struct DeviceContext {
       uint8_t* dout;
       uint8_t* out;
       uint64_t n;
+      uint32_t key_bytes;
     };
     bool init = false;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
@@ -165,15 +167,20 @@ int stage_times(const char** names, float* ms, int max, int* launches);
 // ------------------------------------------------------------------ drivers
 // Internal sort of device-resident records (K-a .. K-e). perm_out may be null.
 // `work` (optional) is a caller-provided workspace of >= plan_internal(n).bytes; else ctx.work is used.
+// key_bytes (1..100): the key is record bytes [0, key_bytes) (> 10: LSD passes over 10-byte windows,
+// scratch keypass_bytes from ctx.keypass; perm-only mode (out == nullptr) needs key_bytes <= 10).
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                                cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0);
+                                cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0,
+                                uint32_t key_bytes = 10);
+uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm);
 // Streaming staged-internal sort of pinned host records (ley_sort_submit / ley_sort_drain).
 // Host path 2 (resident.cu): input staged whole on the device, sorted in perm-only mode, output gathered
 // window by window into two device staging buffers and copied to the caller's pinned memory.
 ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                              cudaStream_t s, Profiler& prof);
+                              uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status ensure_copy_streams(DeviceContext& ctx);  // ctx.copy_stream[2] + ctx.ev (external / resident)
-ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, cudaStream_t user);
+ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, uint32_t key_bytes,
+                       cudaStream_t user);
 ley_status sort_drain(DeviceContext& ctx);
 void pipe_release(DeviceContext& ctx);
 

@@ -93,7 +93,7 @@ void worker_main(DeviceContext* ctx) {
       g_trace.mark((uint64_t)(6 * job.k + 2), P.comp);
       if (!st) {
         Profiler prof;  // stage timing is not recorded on the streaming path
-        st = sort_internal_device(*ctx, job.din, job.dout, nullptr, job.n, P.comp, prof);
+        st = sort_internal_device(*ctx, job.din, job.dout, nullptr, job.n, P.comp, prof, nullptr, 0, job.key_bytes);
         if (st) msg = last_error();
       }
       g_trace.mark((uint64_t)(6 * job.k + 3), P.comp);
@@ -166,7 +166,8 @@ void pipe_release(DeviceContext& c) {
   P.init = false;
 }
 
-ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, cudaStream_t user) {
+ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, uint32_t key_bytes,
+                       cudaStream_t user) {
   auto& P = ctx.pipe;
   std::unique_lock<std::mutex> lk(P.mu);
   if (ley_status st = take_error(P)) return st;
@@ -204,7 +205,7 @@ ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint
   LEY_CUDA("submit H2D", cudaMemcpyAsync(din, in, bytes, cudaMemcpyHostToDevice, P.h2d));
   g_trace.mark((uint64_t)(6 * k + 1), P.h2d);
   LEY_CUDA("submit H2D", cudaEventRecord(P.copied_in[s], P.h2d));
-  P.q.push_back(DeviceContext::Pipe::Job{k, din, dout, out, n});
+  P.q.push_back(DeviceContext::Pipe::Job{k, din, dout, out, n, key_bytes});
   P.submitted = k + 1;
   lk.unlock();
   P.cv.notify_all();

@@ -37,14 +37,18 @@ def test_exports_every_declared_symbol(ley):
 
 
 def test_version(ley):
-    assert ley.ley_version() == (1, 0)
+    assert ley.ley_version() == (1, 1)
 
 
 def test_validation_before_cuda(ley):
-    # record/key geometry other than 100/10 -> UNSUPPORTED, even with n = 0
+    # records other than 100 bytes or keys outside 1..100 bytes -> UNSUPPORTED, even
+    # with n = 0
     assert ley.ley_sort(0, 0, 0, 99, 10, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
-    assert "record_bytes=100" in ley.ley_last_error()
-    assert ley.ley_sort(0, 0, 10, 100, 8, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
+    assert "record_bytes must be 100" in ley.ley_last_error()
+    for kb in (0, 101):
+        assert ley.ley_sort(0, 0, 0, 100, kb, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
+    # a shorter key is valid: the NULL pointers are what is wrong
+    assert ley.ley_sort(0, 0, 10, 100, 8, raise_on_error=False) == ley.LEY_ERR_INVALID_ARGUMENT
     # n = 0 is OK and touches nothing
     assert ley.ley_sort(0, 0, 0, raise_on_error=False) == ley.LEY_OK
     assert ley.ley_last_error() == ""

@@ -1,0 +1,152 @@
+"""Flexible key sizes (§5 P:164 "flexible key sizes ... a prefix generator for all types of keys";
+SURVEY.md §8f NEXT 4): key = record bytes [0, key_bytes), 1..100, stable by input index.
+
+Keys of <= 10 bytes run one pass whose sort key carries the ordinal in its unused bytes; longer keys run
+LSD passes over the 10-byte windows. Every result is compared byte for byte (records and permutation) with
+the oracle's record-comparison sort (oracle.sort(..., key_bytes=k), pinned in tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _records(n, seed, dist):
+    """Generator records with low-entropy bytes 10..39 (copies of key bytes mod 3), so keys longer than
+    10 bytes keep long tie runs for their later windows to break."""
+    r = gen.records(n, seed=seed, dist=dist).reshape(n, 100)
+    r[:, 10:40] = r[:, 0:30] % 3
+    return np.ascontiguousarray(r.reshape(-1))
+
+
+def _expect(recs, k):
+    return oracle.sort(recs, key_bytes=k)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 9, 10, 11, 15, 20, 37, 100])
+@pytest.mark.parametrize("dist", ["uniform", "tiny_alphabet", "three_keys"])
+def test_device_path(cuda_ok, k, dist):
+    import paper_1909_08006_b200 as ley
+
+    n = 150_003
+    recs = _records(n, 90 + k, dist)
+    x = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ley.ley_sort_perm(x, out, perm, n, key_bytes=k)
+    exp, eperm = _expect(recs, k)
+    assert np.array_equal(out.cpu().numpy(), exp)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), eperm)
+    out2 = torch.empty_like(x)
+    ley.ley_sort(x, out2, n, key_bytes=k)  # no perm: the multi-pass path without compositions
+    assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("k", [1, 4, 12])
+def test_large_and_skewed(cuda_ok, k):
+    """Skewed C3-style keys at 2M records (recursion below the key prefix) with short and long keys."""
+    import paper_1909_08006_b200 as ley
+
+    n = 2_000_000
+    recs = _records(n, 7, "skewed")
+    x = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x)
+    ley.ley_sort(x, out, n, key_bytes=k)
+    assert np.array_equal(out.cpu().numpy(), _expect(recs, k)[0])
+
+
+def test_host_paths(cuda_ok):
+    """Staged (k = 20), resident (k = 4), external (k = 3 and 9) and streaming (k = 15) host paths; the
+    external and resident paths refuse keys longer than 10 bytes."""
+    import paper_1909_08006_b200 as ley
+
+    n = 400_001
+    recs = _records(n, 5, "tiny_alphabet")
+    x = torch.from_numpy(recs).pin_memory()
+
+    def run(k, budget=0):
+        out = torch.empty_like(x).pin_memory()
+        perm = torch.empty(n, dtype=torch.int32).pin_memory()
+        ley.ley_sort_perm(x, out, perm, n, key_bytes=k, device_budget_bytes=budget)
+        exp, eperm = _expect(recs, k)
+        assert np.array_equal(out.numpy(), exp), k
+        assert np.array_equal(perm.numpy().view(np.uint32), eperm), k
+
+    run(20)                                                  # staged
+    res_budget = ley.ley_plan_query(n, 1)["resident_bytes"]
+    assert ley.ley_plan_query(n, res_budget)["host_path"] == 2
+    run(4, res_budget)                                       # resident
+    for k in (3, 9):
+        run(k, 12 << 20)                                     # external, several runs
+    out = torch.empty_like(x).pin_memory()
+    assert ley.ley_sort(x, out, n, key_bytes=11, device_budget_bytes=12 << 20,
+                        raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
+    # streaming submit
+    outs = [torch.empty_like(x).pin_memory() for _ in range(2)]
+    for o in outs:
+        ley.ley_sort_submit(x, o, n, key_bytes=15)
+    ley.ley_sort_drain()
+    exp = _expect(recs, 15)[0]
+    for o in outs:
+        assert np.array_equal(o.numpy(), exp)
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("k", [1, 2, 5])
+def test_dist_loopback(cuda_ok, fused, k):
+    """The multi-GPU algorithm (loopback, G = 4, one empty rank) with short keys: splitters, destinations
+    and the local sorts all compare the k-byte prefix, ties by global ordinal."""
+    import paper_1909_08006_b200 as ley
+
+    ley.ley_set_option("dist_fused", fused)
+    try:
+        G, N = 4, 80_001
+        recs = _records(N, 11 + k, "tiny_alphabet")
+        n_local = [30_000, 0, 25_000, N - 55_000]
+        ins, outs, at = [], [], 0
+        for r in range(G):
+            part = recs[at * 100:(at + n_local[r]) * 100]
+            at += n_local[r]
+            ins.append(torch.from_numpy(part.copy()).cuda() if n_local[r] else torch.empty(100, dtype=torch.uint8,
+                                                                                           device="cuda"))
+            outs.append(torch.empty((N // G + 2) * 100, dtype=torch.uint8, device="cuda"))
+        res = ley.ley_sort_dist_loopback(ins, n_local, outs, [N // G + 2] * G, key_bytes=k)
+        assert [x[0] for x in res] == [((r + 1) * N // G) - (r * N // G) for r in range(G)]
+        got = np.concatenate([outs[r][: res[r][0] * 100].cpu().numpy() for r in range(G)])
+        assert np.array_equal(got, _expect(recs, k)[0])
+    finally:
+        ley.ley_set_option("dist_fused", 1)
+
+
+def test_nccl_world_one_exchange(cuda_ok):
+    import paper_1909_08006_b200 as ley
+
+    ley.ley_set_option("dist_exchange_g1", 1)
+    comm = ley.ley_comm_init(1, 0, ley.ley_comm_get_unique_id(), 0)
+    try:
+        n = 60_007
+        recs = _records(n, 3, "three_keys")
+        x = torch.from_numpy(recs).cuda()
+        out = torch.empty_like(x)
+        n_out, off = ley.ley_sort_dist(comm, x, n, out, n, key_bytes=3)
+        assert (n_out, off) == (n, 0)
+        assert np.array_equal(out.cpu().numpy(), _expect(recs, 3)[0])
+        with pytest.raises(ley.LeyendaError) as ei:
+            ley.ley_sort_dist(comm, x, n, out, n, key_bytes=11)
+        assert ei.value.status == ley.LEY_ERR_UNSUPPORTED
+    finally:
+        ley.ley_comm_destroy(comm)
+        ley.ley_set_option("dist_exchange_g1", 0)
+
+
+def test_invalid_key_bytes(cuda_ok):
+    import paper_1909_08006_b200 as ley
+
+    x = torch.zeros(100 * 10, dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(x)
+    for k in (0, 101):
+        assert ley.ley_sort(x, out, 10, key_bytes=k, raise_on_error=False) == ley.LEY_ERR_UNSUPPORTED
