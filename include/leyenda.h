@@ -114,7 +114,11 @@ const char* ley_last_error(void);
  * (sum of n_local over ranks < r) + i. On return rank r holds global sorted positions
  * [*out_global_offset, *out_global_offset + *n_out_local) with exact splitters:
  * n_out_local(r) = floor((r+1) n / G) - floor(r n / G). Concatenating ranks 0..G-1 equals ley_sort of
- * the concatenated input. key_bytes: 1..10 (shorter keys compare as their prefix). */
+ * the concatenated input. key_bytes: 1..10 (shorter keys compare as their prefix).
+ * in_local/out_local: device memory on the comm's device, or pinned host memory on EVERY rank — then each
+ * rank's slice and output capacity are staged on its device (H2D, the device path, D2H of its range) if
+ * they fit device_budget_bytes on every rank, else all ranks return LEY_ERR_UNSUPPORTED (the
+ * multi-GPU external path, is not built). */
 typedef struct ley_comm ley_comm;
 ley_status ley_comm_get_unique_id(uint8_t id_out[128]);  /* rank 0; broadcast it (e.g. torch PG)  */
 ley_status ley_comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);

@@ -370,6 +370,7 @@ struct ley_comm {
   size_t win_cap = 0;
   ncclWindow_t win = nullptr;
   uint8_t** d_peers = nullptr;
+  ley::DeviceBuffer stage;  // pinned host slices: the device copy of this rank's input and output
 };
 
 namespace ley {
@@ -447,15 +448,19 @@ ley_status comm_destroy(ley_comm* comm) {
   cudaDeviceSynchronize();
   window_release(comm);
   if (comm->d_peers) cudaFree(comm->d_peers);
+  if (comm->stage.ptr) {
+    cudaFree(comm->stage.ptr);
+    track_device_bytes(-(int64_t)comm->stage.cap);
+  }
   if (comm->nccl) ncclCommDestroy(comm->nccl);
   delete comm;
   return LEY_OK;
 }
 
-ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
-                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
-                     cudaStream_t s) {
-  (void)budget;
+namespace {
+ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local,
+                            uint64_t out_capacity, uint64_t* n_out_local, uint64_t* out_global_offset,
+                            uint32_t key_bytes, cudaStream_t s) {
   const int G = comm->nranks;
   LEY_CUDA("dist", cudaSetDevice(comm->device));
   DeviceContext& ctx = device_context(comm->device);
@@ -644,6 +649,71 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   *out_global_offset = r.out_off;
   prof.launches = r.launches + P.launches;
   prof.finish();
+  return LEY_OK;
+}
+
+}  // namespace
+
+// Pointer kinds: both device pointers (the NCCL path proper), or both pinned host pointers — staged: this
+// rank's slice is copied into a comm-owned device buffer, sorted by the device path, and its output range
+// copied back. Every rank first agrees (one all-reduce) that its staging fits its budget, so a rank that
+// cannot proceed never leaves the others waiting in a collective.
+ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
+                     uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
+                     cudaStream_t s) {
+  LEY_CUDA("dist", cudaSetDevice(comm->device));
+  int kind = -1;  // 0 device, 1 pinned host
+  const void* ptrs[2] = {n_local ? in_local : nullptr, out_capacity ? out_local : nullptr};
+  for (const void* p : ptrs) {
+    if (!p) continue;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("dist: cudaPointerGetAttributes failed");
+      return LEY_ERR_CUDA;
+    }
+    int k = a.type == cudaMemoryTypeDevice && a.device == comm->device ? 0 : (a.type == cudaMemoryTypeHost ? 1 : 2);
+    if (k == 2 || (kind >= 0 && k != kind)) {
+      set_error("dist: in_local/out_local must both be device memory on the comm's device or both pinned host memory");
+      return LEY_ERR_UNSUPPORTED;
+    }
+    kind = k;
+  }
+  if (kind != 1)
+    return dist_sort_device(comm, in_local, n_local, out_local, out_capacity, n_out_local, out_global_offset,
+                            key_bytes, s);
+  const size_t a_in = a256(n_local * kRecordBytes), a_out = a256(out_capacity * kRecordBytes);
+  const bool fits = !budget || a_in + a_out <= budget;
+  {
+    DeviceContext& ctx = device_context(comm->device);
+    std::lock_guard<std::mutex> guard(ctx.mu);
+    uint64_t* flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
+    if (!flag) {  // first call on this comm: scratch for the agreement
+      if (ley_status st = rank_alloc(comm->state)) return st;
+      flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
+    }
+    const uint64_t bad = fits ? 0 : 1;
+    LEY_CUDA("dist staging", cudaMemcpyAsync(flag, &bad, 8, cudaMemcpyHostToDevice, s));
+    LEY_NCCL("dist staging", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
+    uint64_t any = 0;
+    LEY_CUDA("dist staging", cudaMemcpyAsync(&any, flag, 8, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("dist staging", cudaStreamSynchronize(s));
+    if (any) {
+      set_error("dist: pinned host slices are staged on the device, and a rank's slice + output capacity exceed "
+                "its device_budget_bytes (the multi-GPU external path is not built)");
+      return LEY_ERR_UNSUPPORTED;
+    }
+    if (ley_status st = ensure_buffer(comm->stage, std::max<size_t>(a_in + a_out, 256), "dist staging", s)) return st;
+  }
+  uint8_t* din = static_cast<uint8_t*>(comm->stage.ptr);
+  uint8_t* dout = din + a_in;
+  if (n_local)
+    LEY_CUDA("dist H2D", cudaMemcpyAsync(din, in_local, n_local * kRecordBytes, cudaMemcpyHostToDevice, s));
+  ley_status st = dist_sort_device(comm, din, n_local, dout, out_capacity, n_out_local, out_global_offset, key_bytes, s);
+  if (st) return st;
+  if (*n_out_local)
+    LEY_CUDA("dist D2H", cudaMemcpyAsync(out_local, dout, *n_out_local * kRecordBytes, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("dist D2H", cudaStreamSynchronize(s));
   return LEY_OK;
 }
 

@@ -127,6 +127,37 @@ def test_nccl_world_size_one(cuda_ok, exchange_mode, exchange_g1):
         ley.ley_set_option("dist_exchange_g1", 0)
 
 
+@pytest.mark.gpu
+def test_nccl_pinned_host_slices(cuda_ok, exchange_mode):
+    """ley_sort_dist with pinned host slices: staged on the device (H2D, the device path, D2H of the
+    rank's range), with the exchange phases on; a budget below slice + capacity is refused (all ranks
+    agree first, so none is left waiting in a collective)."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    ley.ley_set_option("dist_exchange_g1", 1)
+    comm = ley.ley_comm_init(1, 0, ley.ley_comm_get_unique_id(), 0)
+    try:
+        n = 70_001
+        recs = gen.records(n, seed=63, dist="skewed")
+        x = torch.from_numpy(recs).pin_memory()
+        out = torch.empty_like(x).pin_memory()
+        n_out, off = ley.ley_sort_dist(comm, x, n, out, n)
+        assert (n_out, off) == (n, 0)
+        assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
+        with pytest.raises(ley.LeyendaError) as ei:
+            ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=n * 100)
+        assert ei.value.status == ley.LEY_ERR_UNSUPPORTED
+        # the communicator is still usable afterwards
+        out.zero_()
+        assert ley.ley_sort_dist(comm, x, n, out, n) == (n, 0)
+        assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
+    finally:
+        ley.ley_comm_destroy(comm)
+        ley.ley_set_option("dist_exchange_g1", 0)
+
+
 # ----------------------------------------------------------------------------------------- CPU (gloo)
 def _free_port():
     s = socket.socket()
