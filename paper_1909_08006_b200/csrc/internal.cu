@@ -11,6 +11,7 @@
 // All work is on the caller's stream. The only host synchronisations are one 4-byte read of the
 // big-bucket count per recursion level (usually exactly one per call) and the final completion wait.
 #include <algorithm>
+#include <vector>
 
 #include "kernels.cuh"
 #include "runtime.h"
@@ -200,8 +201,32 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 
 uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm) {
   if (key_bytes <= kKeyBytes) return 0;
-  return a256(n * kRecordBytes) + (perm ? 2 * a256(4 * n) : 0);
+  // the other record buffer of the window passes; with perm two permutation arrays, else the tie-group
+  // lists of the hybrid form (first/last positions, <= n/2 groups each, and the (first, len) array)
+  return a256(n * kRecordBytes) + (perm ? 2 * a256(4 * n) : 2 * a256(4 * (n / 2 + 1)) + a256(8 * (n / 2 + 1)) + 256);
 }
+
+namespace {
+constexpr uint32_t kSmallGroup = 32;       // tie groups up to this size: one warp, comparison sort
+constexpr size_t kMaxLargeGroups = 64;     // more larger groups than this: plain LSD window passes
+
+// LSD passes over windows W-1 .. first_window of records [0, n) of `data` (in place, via tmp), ordinals =
+// current positions.
+ley_status window_passes(DeviceContext& ctx, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t key_bytes,
+                         uint32_t first_window, cudaStream_t s, Profiler& prof, void* work, size_t work_bytes) {
+  const uint32_t W = (key_bytes + kKeyBytes - 1) / kKeyBytes;
+  const uint8_t* src = data;
+  uint8_t* dst = tmp;
+  for (uint32_t w = W; w-- > first_window;) {
+    const KeySpec ks{kKeyBytes * w, std::min<uint32_t>(kKeyBytes, key_bytes - kKeyBytes * w)};
+    if (ley_status st = sort_pass(ctx, src, dst, nullptr, n, s, prof, work, work_bytes, ks)) return st;
+    src = dst;
+    dst = dst == tmp ? data : tmp;
+  }
+  if (src != data) LEY_CUDA("tie groups", cudaMemcpyAsync(data, src, n * kRecordBytes, cudaMemcpyDeviceToDevice, s));
+  return LEY_OK;
+}
+}  // namespace
 
 // Keys of up to 10 bytes: one pass. Longer keys (§5, flexible key sizes): LSD over the
 // 10-byte windows, the last (possibly partial) window first. Each pass is stable with respect to its own
@@ -223,6 +248,59 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
   ley_status st = ensure_buffer(ctx.keypass, keypass_bytes(n, key_bytes, perm_out != nullptr), "key passes", s);
   if (st) return st;
   uint8_t* tmp = static_cast<uint8_t*>(ctx.keypass.ptr);
+  if (!perm_out && options_snapshot().key_hybrid) {
+    // Hybrid ("hybrid between prefix sorting and comparison-based record sorting"): sort by the first
+    // 10 key bytes, then only the runs of equal 10-byte prefixes need the rest of the key — tiny ones by a
+    // warp comparison sort, a few large ones by the window passes on their slice. Random keys: no ties,
+    // one pass + one read of the output.
+    if ((st = sort_pass(ctx, in, out, nullptr, n, s, prof, work, work_bytes, KeySpec{0, kKeyBytes}))) return st;
+    const uint32_t cap = (uint32_t)(n / 2 + 1);
+    uint32_t* firsts = reinterpret_cast<uint32_t*>(tmp + a256(n * kRecordBytes));
+    uint32_t* lasts = firsts + a256(4ull * cap) / 4;
+    uint2* groups = reinterpret_cast<uint2*>(lasts + a256(4ull * cap) / 4);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(groups) + a256(8ull * cap));
+    if ((st = prof.begin("tie groups"))) return st;
+    LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 8, s));
+    LEY_CUDA("tie groups", launch_tie_groups(out, n, firsts, lasts, cap, counts, ctx.sms, s));
+    ++prof.launches;
+    uint32_t hc[2] = {0, 0};
+    LEY_CUDA("tie groups", cudaMemcpyAsync(hc, counts, 8, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("tie groups", cudaStreamSynchronize(s));
+    bool fallback = hc[0] != hc[1] || hc[0] > cap;
+    if (!fallback && hc[0]) {
+      std::vector<uint32_t> f(hc[0]), l(hc[0]);
+      LEY_CUDA("tie groups", cudaMemcpyAsync(f.data(), firsts, 4ull * hc[0], cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("tie groups", cudaMemcpyAsync(l.data(), lasts, 4ull * hc[0], cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("tie groups", cudaStreamSynchronize(s));
+      std::sort(f.begin(), f.end());
+      std::sort(l.begin(), l.end());
+      std::vector<uint2> small, large;
+      for (size_t g = 0; g < f.size(); ++g) {
+        const uint2 gr{f[g], l[g] - f[g] + 1};
+        (gr.y <= kSmallGroup ? small : large).push_back(gr);
+      }
+      fallback = large.size() > kMaxLargeGroups;
+      if (!fallback) {
+        if (!small.empty()) {
+          LEY_CUDA("tie groups", cudaMemcpyAsync(groups, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
+          LEY_CUDA("tie groups", launch_fix_small_groups(out, groups, (uint32_t)small.size(), key_bytes, ctx.sms, s));
+          ++prof.launches;
+        }
+        for (const uint2& gr : large) {
+          // the passes need a 16-byte-aligned slice: start at the record index rounded down to a multiple
+          // of 4 and sort by the whole key (window 0 too), so the up to 3 records before the group — already
+          // in their final order, all with a smaller or equal-and-earlier full key — stay where they are
+          const uint64_t x0 = gr.x & ~3u, len = gr.x + gr.y - x0;
+          if ((st = window_passes(ctx, out + x0 * kRecordBytes, tmp, len, key_bytes, 0, s, prof, work, work_bytes)))
+            return st;
+        }
+        LEY_CUDA("tie groups", cudaStreamSynchronize(s));  // the host vectors above are in flight until here
+      }
+    }
+    if ((st = prof.end())) return st;
+    if (!fallback) return LEY_OK;
+    // many large tie groups: the plain LSD window passes from the input (below)
+  }
   uint32_t* pa = perm_out ? reinterpret_cast<uint32_t*>(tmp + a256(n * kRecordBytes)) : nullptr;
   uint32_t* pb = perm_out ? pa + a256(4 * n) / 4 : nullptr;
   const uint8_t* src = in;

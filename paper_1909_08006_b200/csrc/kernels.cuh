@@ -59,6 +59,13 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
 // K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
                              cudaStream_t s);
+// keys > 10 bytes, hybrid form (k_ties.cu): runs of equal 10-byte prefixes in sorted records -> unordered
+// (first, last) lists (counts[0], counts[1]; entries past cap dropped); in-place comparison sort of
+// groups (first, len <= 32) by key bytes [10, key_bytes) then position
+cudaError_t launch_tie_groups(const uint8_t* recs, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
+                              uint32_t* counts, int sms, cudaStream_t s);
+cudaError_t launch_fix_small_groups(uint8_t* recs, const uint2* groups, uint32_t ngroups, uint32_t key_bytes, int sms,
+                                    cudaStream_t s);
 // multi-pass keys: cur[j] = prev[cur[j]] (the permutation of the passes so far, k_gather.cu)
 cudaError_t launch_compose_perm(const uint32_t* prev, uint32_t* cur, uint64_t n, int sms, cudaStream_t s);
 

@@ -36,6 +36,7 @@ const OptDesc kOpts[] = {
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"kd_ws", &Options::kd_ws, 0, 1},
     {"ka_stream", &Options::ka_stream, 0, 1},
+    {"key_hybrid", &Options::key_hybrid, 0, 1},
     {"resident_path", &Options::resident_path, 0, 1},
     {"resident_chunk_records", &Options::resident_chunk_records, 0, (int64_t)0xFFFFFFFEll},
     {"dist_fused", &Options::dist_fused, 0, 1},

@@ -45,6 +45,7 @@ struct Options {
   int64_t kd_insert_max = 16;
   int64_t kd_ws = 1;
   int64_t ka_stream = 1;
+  int64_t key_hybrid = 1;         // keys > 10 bytes: 10-byte sort + tie-group fix-up (0: LSD windows always)
   int64_t resident_path = 1;        // host pointers: allow path 2 (resident input, streamed output)
   int64_t resident_chunk_records = 0;  // path 2 output window (records; 0 = 2^21)
   int64_t dist_fused = 1;        // K-p stores into peers' NCCL symmetric windows (0: send buffer + all-to-all)

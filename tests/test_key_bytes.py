@@ -46,6 +46,41 @@ def test_device_path(cuda_ok, k, dist):
     assert torch.equal(out, out2)
 
 
+@pytest.mark.parametrize("groups", [0, 40, 3000, 1])
+@pytest.mark.parametrize("hybrid", [1, 0])
+def test_long_keys_tie_groups(cuda_ok, groups, hybrid):
+    """Keys of 24 bytes whose 10-byte prefixes tie in controlled ways: none (uniform), 40 large groups
+    (window passes on each slice), 3000 groups of ~67 (more large groups than the hybrid handles: the
+    plain window passes), one group holding every record; plus small groups of 2..32 around them. The
+    hybrid (key_hybrid=1) and the plain LSD passes (0) must both equal the oracle."""
+    import paper_1909_08006_b200 as ley
+
+    n = 200_001
+    r = gen.records(n, seed=33 + groups, dist="uniform").reshape(n, 100)
+    rng = np.random.default_rng(groups)
+    if groups:  # prefix = group id (big-endian in bytes 6..9), bytes 0..5 zero
+        g = rng.integers(0, groups, size=n).astype(np.uint32)
+        r[:, :10] = 0
+        for b in range(4):
+            r[:, 9 - b] = (g >> (8 * b)) & 0xFF
+    # small groups: every 10th record joins a pair (or a few) sharing a fresh prefix 0xFF ++ (i // 20)
+    idx = np.arange(0, n, 10)
+    pid = (idx // 20).astype(np.uint64)
+    r[idx, 0], r[idx, 1] = 0xFF, 0
+    for b in range(8):
+        r[idx, 9 - b] = (pid >> np.uint64(8 * b)) & np.uint64(0xFF)
+    r[:, 10:24] = rng.integers(0, 3, size=(n, 14))  # the rest of the key: low entropy -> deep ties
+    recs = np.ascontiguousarray(r.reshape(-1))
+    x = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x)
+    ley.ley_set_option("key_hybrid", hybrid)
+    try:
+        ley.ley_sort(x, out, n, key_bytes=24)
+    finally:
+        ley.ley_set_option("key_hybrid", 1)
+    assert np.array_equal(out.cpu().numpy(), _expect(recs, 24)[0])
+
+
 @pytest.mark.parametrize("k", [1, 4, 12])
 def test_large_and_skewed(cuda_ok, k):
     """Skewed C3-style keys at 2M records (recursion below the key prefix) with short and long keys."""
