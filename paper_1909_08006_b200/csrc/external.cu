@@ -239,79 +239,78 @@ unsigned grid_for(uint64_t work, int sms, int per_sm = 8) {
   return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------------------------------- driver
-ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                              uint64_t budget, uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
-  ley_status st;
-  if (key_bytes > kKeyBytes) {  // the merge compares 10-byte composites (K-m)
-    set_error("external: keys longer than 10 bytes are not supported on the external path (raise the budget "
-              "to the staged path's ley_plan_query().staged_bytes)");
-    return LEY_ERR_UNSUPPORTED;
-  }
-  const uint64_t C = external_run_records(n, budget);
-  if (C < 1024 && C < n) {
-    set_error("external: device_budget_bytes " + std::to_string(budget) +
-              " is below the minimum working set (runs of >= 1024 records)");
-    return LEY_ERR_BUDGET;
-  }
-  const uint32_t R = (uint32_t)((n + C - 1) / C);
-  const int sms = ctx.sms;
-  // ---------------------------------------------------------------- device buffer plan (within budget)
-  // run generation: run in (100 C) + run out (100 C) + internal workspace(C) + samples
-  const InternalLayout LC = plan_internal(C);
-  const uint64_t S = external_sample_stride(n, C, budget);  // sample stride (bounds every partition)
-  uint64_t nsamp = 0;
-  std::vector<uint64_t> run_off(R), run_len(R), samp_base(R);
-  for (uint32_t r = 0; r < R; ++r) {
-    run_off[r] = (uint64_t)r * C;
-    run_len[r] = std::min<uint64_t>(C, n - run_off[r]);
-    samp_base[r] = nsamp;
-    nsamp += (run_len[r] + S - 1) / S;
-  }
-  const size_t sz_run = a256(C * kRecordBytes);
-  const size_t sz_samples = a256(nsamp * kRecordBytes);
-  const size_t phase1 = 4 * sz_run + a256(LC.bytes) + 2 * sz_samples + a256(4 * nsamp) + 2 * a256(4 * C) +
-                        a256(plan_internal(nsamp).bytes);
-  if ((st = ensure_buffer(ctx.ext, phase1, "external buffers", s))) return st;
-  uint8_t* eb = static_cast<uint8_t*>(ctx.ext.ptr);
-  uint8_t* d_in[2] = {eb, eb + sz_run};
-  uint8_t* d_out[2] = {eb + 2 * sz_run, eb + 3 * sz_run};
-  uint8_t* d_work = eb + 4 * sz_run;
-  uint8_t* d_samp = d_work + a256(LC.bytes);
-  uint8_t* d_samp_sorted = d_samp + sz_samples;
-  uint32_t* d_samp_perm = reinterpret_cast<uint32_t*>(d_samp_sorted + sz_samples);
-  uint32_t* d_run_perm[2];
-  d_run_perm[0] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_samp_perm) + a256(4 * nsamp));
-  d_run_perm[1] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_run_perm[0]) + a256(4 * C));
-  uint8_t* d_work2 = reinterpret_cast<uint8_t*>(d_run_perm[1]) + a256(4 * C);
-
-  // pinned host run scratch (records, and global ordinals when perm is requested)
-  const size_t scratch_bytes = (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0);
-  if (ctx.host_scratch_cap < scratch_bytes) {
-    if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
-    ctx.host_scratch = nullptr;
-    ctx.host_scratch_cap = 0;
-    LEY_CUDA("external scratch", cudaHostAlloc(&ctx.host_scratch, scratch_bytes, cudaHostAllocMapped));
-    ctx.host_scratch_cap = scratch_bytes;
-  }
-  uint8_t* h_runs = static_cast<uint8_t*>(ctx.host_scratch);
-  uint32_t* h_perm = perm_out ? reinterpret_cast<uint32_t*>(h_runs + (size_t)n * kRecordBytes) : nullptr;
+// ---------------------------------------------------------------------------------------- phases
+// Sorted runs in a pinned (mapped) host scratch. Record j of the global layout sits at h_runs + 100 j; run
+// k covers [off[k], off[k] + len[k]) and was sampled every S[k]-th record (its first sample is sample
+// number samp_base[k] of the run-ordered sample set). With one GPU the layout is the input's; with G ranks
+// the runs of rank r sit at its global offset (ranks' runs in rank order = global input order).
+struct RunSet {
+  uint8_t* h_runs = nullptr;
   uint8_t* h_runs_dev = nullptr;
-  LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&h_runs_dev, h_runs, 0));
+  uint32_t* h_perm = nullptr;  // global ordinals of the run records (perm requested)
+  std::vector<uint64_t> off, len, S, samp_base;
+  uint64_t nsamp = 0;
+};
 
-  if (ley_status est = ensure_copy_streams(ctx)) return est;
+// Phase-1 device buffers: two run slots (in | out), the inner sort's workspace, two run perms, and the
+// sample area (samples, sorted samples, sample perm, sample-sort workspace) for up to `nsamp_cap` samples.
+struct Phase1 {
+  uint8_t* d_in[2];
+  uint8_t* d_out[2];
+  uint8_t* d_work;
+  uint32_t* d_run_perm[2];
+  uint8_t* d_samp;
+  uint8_t* d_samp_sorted;
+  uint32_t* d_samp_perm;
+  uint8_t* d_work2;
+  size_t work_bytes, work2_bytes;
+};
+
+size_t phase1_bytes(uint64_t C, uint64_t nsamp_cap) {
+  return 4 * a256(C * kRecordBytes) + a256(plan_internal(C).bytes) + 2 * a256(nsamp_cap * kRecordBytes) +
+         a256(4 * nsamp_cap) + 2 * a256(4 * C) + a256(plan_internal(nsamp_cap).bytes);
+}
+
+Phase1 phase1_layout(uint8_t* eb, uint64_t C, uint64_t nsamp_cap) {
+  Phase1 b;
+  const size_t sz_run = a256(C * kRecordBytes), sz_samples = a256(nsamp_cap * kRecordBytes);
+  b.d_in[0] = eb;
+  b.d_in[1] = eb + sz_run;
+  b.d_out[0] = eb + 2 * sz_run;
+  b.d_out[1] = eb + 3 * sz_run;
+  b.d_work = eb + 4 * sz_run;
+  b.work_bytes = plan_internal(C).bytes;
+  b.d_samp = b.d_work + a256(b.work_bytes);
+  b.d_samp_sorted = b.d_samp + sz_samples;
+  b.d_samp_perm = reinterpret_cast<uint32_t*>(b.d_samp_sorted + sz_samples);
+  b.d_run_perm[0] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(b.d_samp_perm) + a256(4 * nsamp_cap));
+  b.d_run_perm[1] = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(b.d_run_perm[0]) + a256(4 * C));
+  b.d_work2 = reinterpret_cast<uint8_t*>(b.d_run_perm[1]) + a256(4 * C);
+  b.work2_bytes = plan_internal(nsamp_cap).bytes;
+  return b;
+}
+
+// a10: input records [0, n) of `in` (global records [gbase, gbase + n)) -> sorted runs of C records in
+// rs.h_runs at their global offsets; samples appended to b.d_samp at rs.nsamp.
+ley_status ext_generate(DeviceContext& ctx, const uint8_t* in, uint64_t n, uint64_t gbase, uint64_t C, uint64_t S,
+                        RunSet& rs, const Phase1& b, bool want_perm, uint32_t key_bytes, cudaStream_t s,
+                        Profiler& prof, ExtTrace& tr) {
+  ley_status st;
+  const int sms = ctx.sms;
+  const size_t first = rs.off.size();
+  for (uint64_t at = 0; at < n; at += C) {
+    rs.off.push_back(gbase + at);
+    rs.len.push_back(std::min<uint64_t>(C, n - at));
+    rs.S.push_back(S);
+    rs.samp_base.push_back(rs.nsamp);
+    rs.nsamp += (rs.len.back() + S - 1) / S;
+  }
+  const uint32_t R = (uint32_t)(rs.off.size() - first);
   cudaStream_t h2d = ctx.copy_stream[0], d2h = ctx.copy_stream[1];
   // per slot: input landed, slot sorted (input free, output ready), output copied out (output free)
   cudaEvent_t ev_start = ctx.ev[0];
   cudaEvent_t ev_in[2] = {ctx.ev[1], ctx.ev[2]}, ev_sorted[2] = {ctx.ev[3], ctx.ev[4]},
               ev_out[2] = {ctx.ev[5], ctx.ev[6]};
-
-  // ---------------------------------------------------------------- a10: run generation
-  if ((st = prof.begin("ext run generation"))) return st;
-  ExtTrace tr;
-  tr.start(s);
   LEY_CUDA("ext runs", cudaEventRecord(ev_start, s));
   LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_start, 0));
   LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_start, 0));
@@ -323,119 +322,133 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
     const int sl = r & 1;
     if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(h2d, ev_sorted[sl], 0));
     const size_t t_h = tr.begin("run H2D", h2d);
-    LEY_CUDA("ext H2D", cudaMemcpyAsync(d_in[sl], in + run_off[r] * kRecordBytes, run_len[r] * kRecordBytes,
-                                        cudaMemcpyHostToDevice, h2d));
+    LEY_CUDA("ext H2D", cudaMemcpyAsync(b.d_in[sl], in + (rs.off[first + r] - gbase) * kRecordBytes,
+                                        rs.len[first + r] * kRecordBytes, cudaMemcpyHostToDevice, h2d));
     tr.end(t_h, h2d);
     LEY_CUDA("ext runs", cudaEventRecord(ev_in[sl], h2d));
     return LEY_OK;
   };
-  if ((st = issue_run_h2d(0))) return st;
+  if (R && (st = issue_run_h2d(0))) return st;
   for (uint32_t r = 0; r < R; ++r) {
-    const uint64_t len = run_len[r];
+    const size_t k = first + r;
+    const uint64_t len = rs.len[k];
     const int sl = r & 1;
     // queue the next run's input before this run's sort blocks the host on its own stream
     if (r + 1 < R && (st = issue_run_h2d(r + 1))) return st;
     LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_in[sl], 0));
     if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_out[sl] copied out
     const size_t t_s = tr.begin("run sort", s);
-    st = sort_internal_device(ctx, d_in[sl], d_out[sl], perm_out ? d_run_perm[sl] : nullptr, len, s, quiet, d_work,
-                              LC.bytes, key_bytes);
+    st = sort_internal_device(ctx, b.d_in[sl], b.d_out[sl], want_perm ? b.d_run_perm[sl] : nullptr, len, s, quiet,
+                              b.d_work, b.work_bytes, key_bytes);
     if (st) return st;
     tr.end(t_s, s);
     prof.launches += quiet.launches;
     quiet.launches = 0;
     ext_take_samples<<<grid_for((len + S - 1) / S * kRecordWords, sms), 256, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(d_out[sl]), len, (uint32_t)S, reinterpret_cast<uint32_t*>(d_samp),
-        samp_base[r]);
+        reinterpret_cast<const uint32_t*>(b.d_out[sl]), len, (uint32_t)S, reinterpret_cast<uint32_t*>(b.d_samp),
+        rs.samp_base[k]);
     LEY_CUDA("ext samples", cudaGetLastError());
     prof.launches += 1;
-    if (perm_out) {
-      ext_add_base<<<grid_for(len, sms), 256, 0, s>>>(d_run_perm[sl], len, (uint32_t)run_off[r]);
+    if (want_perm) {
+      ext_add_base<<<grid_for(len, sms), 256, 0, s>>>(b.d_run_perm[sl], len, (uint32_t)rs.off[k]);
       LEY_CUDA("ext perm", cudaGetLastError());
       prof.launches += 1;
     }
     LEY_CUDA("ext runs", cudaEventRecord(ev_sorted[sl], s));
     LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
     const size_t t_d = tr.begin("run D2H", d2h);
-    LEY_CUDA("ext D2H", cudaMemcpyAsync(h_runs + run_off[r] * kRecordBytes, d_out[sl], len * kRecordBytes,
+    LEY_CUDA("ext D2H", cudaMemcpyAsync(rs.h_runs + rs.off[k] * kRecordBytes, b.d_out[sl], len * kRecordBytes,
                                         cudaMemcpyDeviceToHost, d2h));
     tr.end(t_d, d2h);
-    if (perm_out)
-      LEY_CUDA("ext D2H", cudaMemcpyAsync(h_perm + run_off[r], d_run_perm[sl], len * 4, cudaMemcpyDeviceToHost, d2h));
+    if (want_perm)
+      LEY_CUDA("ext D2H", cudaMemcpyAsync(rs.h_perm + rs.off[k], b.d_run_perm[sl], len * 4, cudaMemcpyDeviceToHost, d2h));
     LEY_CUDA("ext runs", cudaEventRecord(ev_out[sl], d2h));
   }
   LEY_CUDA("ext runs", cudaEventRecord(ev_start, d2h));  // every run copied out
   LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_start, 0));
-  if ((st = prof.end())) return st;
+  return LEY_OK;
+}
 
-  // ---------------------------------------------------------------- a11: splitters and slice bounds
-  if ((st = prof.begin("ext partition"))) return st;
-  // merge-phase device plan: a partition of m records needs two slots of slice (100 m) + out (100 m)
-  // (partition p+1 streams in and p-1 streams out while p merges) + 2 x 16 m composites (+ 16 m perm);
-  // keep it inside the same budget as phase 1.
-  const uint64_t m_target = external_merge_target(C, budget);
-  uint64_t q = m_target / S > 2ull * R ? m_target / S - R : std::max<uint64_t>(1, m_target / (2 * S));
-  if (q == 0) q = 1;
-  const uint32_t P = (uint32_t)std::max<uint64_t>(1, (nsamp + q - 1) / q);
+// a11: splitters from the run-ordered samples b.d_samp[0, rs.nsamp) (sorted: order = (key, run, pos)),
+// every q-th one a splitter; exact slice bounds split[p * R + k] of every run by K-loc. part_off[p] =
+// first global output position of partition p.
+ley_status ext_partition(DeviceContext& ctx, const RunSet& rs, const Phase1& b, uint64_t q, uint32_t key_bytes,
+                         cudaStream_t s, Profiler& prof, uint32_t* P_out, std::vector<uint64_t>& split,
+                         std::vector<uint64_t>& part_off) {
+  const uint32_t R = (uint32_t)rs.off.size();
+  const uint32_t P = (uint32_t)std::max<uint64_t>(1, (rs.nsamp + q - 1) / q);
   std::vector<Splitter> spl(P > 1 ? P - 1 : 0);
-  std::vector<uint64_t> split((size_t)(P + 1) * R);
-  for (uint32_t r = 0; r < R; ++r) {
-    split[r] = 0;
-    split[(size_t)P * R + r] = run_len[r];
-  }
+  split.assign((size_t)(P + 1) * R, 0);
+  for (uint32_t r = 0; r < R; ++r) split[(size_t)P * R + r] = rs.len[r];
   if (P > 1) {
-    st = sort_internal_device(ctx, d_samp, d_samp_sorted, d_samp_perm, nsamp, s, quiet, d_work2,
-                              plan_internal(nsamp).bytes, key_bytes);
+    Profiler quiet;
+    quiet.ctx = &ctx;
+    quiet.stream = s;
+    ley_status st = sort_internal_device(ctx, b.d_samp, b.d_samp_sorted, b.d_samp_perm, rs.nsamp, s, quiet, b.d_work2,
+                                         b.work2_bytes, key_bytes);
     if (st) return st;
     prof.launches += quiet.launches;
-    quiet.launches = 0;
-    std::vector<uint32_t> sp_idx(P - 1);
-    std::vector<uint8_t> sp_key(10);
+    std::vector<uint32_t> sidx(P - 1);
     for (uint32_t p = 1; p < P; ++p) {
       const uint64_t at = (uint64_t)p * q;
-      uint32_t sidx = 0;
-      LEY_CUDA("ext splitters", cudaMemcpyAsync(&sidx, d_samp_perm + at, 4, cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("ext splitters", cudaMemcpyAsync(spl[p - 1].key, d_samp_sorted + at * kRecordBytes, 10,
+      LEY_CUDA("ext splitters", cudaMemcpyAsync(&sidx[p - 1], b.d_samp_perm + at, 4, cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("ext splitters", cudaMemcpyAsync(spl[p - 1].key, b.d_samp_sorted + at * kRecordBytes, 10,
                                                 cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("ext splitters", cudaStreamSynchronize(s));
-      const uint32_t r = (uint32_t)(std::upper_bound(samp_base.begin(), samp_base.end(), (uint64_t)sidx) -
-                                    samp_base.begin() - 1);
-      spl[p - 1].run = r;
-      spl[p - 1].pos = (sidx - samp_base[r]) * S;
     }
-    Splitter* d_spl = reinterpret_cast<Splitter*>(d_work);
-    uint64_t* d_runoff = reinterpret_cast<uint64_t*>(d_work + a256(sizeof(Splitter) * spl.size()));
+    LEY_CUDA("ext splitters", cudaStreamSynchronize(s));
+    for (uint32_t p = 1; p < P; ++p) {
+      const uint32_t r = (uint32_t)(std::upper_bound(rs.samp_base.begin(), rs.samp_base.end(), (uint64_t)sidx[p - 1]) -
+                                    rs.samp_base.begin() - 1);
+      spl[p - 1].run = r;
+      spl[p - 1].pos = (sidx[p - 1] - rs.samp_base[r]) * rs.S[r];
+    }
+    // the run offsets relative to the scratch base: ext_locate reads run r at h_runs_dev + 100 off[r]
+    Splitter* d_spl = reinterpret_cast<Splitter*>(b.d_work);
+    uint64_t* d_runoff = reinterpret_cast<uint64_t*>(b.d_work + a256(sizeof(Splitter) * spl.size()));
     uint64_t* d_runlen = d_runoff + R;
     uint64_t* d_split = d_runlen + R;
     LEY_CUDA("ext locate", cudaMemcpyAsync(d_spl, spl.data(), sizeof(Splitter) * spl.size(), cudaMemcpyHostToDevice, s));
-    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runoff, run_off.data(), 8 * R, cudaMemcpyHostToDevice, s));
-    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runlen, run_len.data(), 8 * R, cudaMemcpyHostToDevice, s));
+    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runoff, rs.off.data(), 8 * R, cudaMemcpyHostToDevice, s));
+    LEY_CUDA("ext locate", cudaMemcpyAsync(d_runlen, rs.len.data(), 8 * R, cudaMemcpyHostToDevice, s));
     const uint64_t nthreads = (uint64_t)(P - 1) * R;
-    ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
+    ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(rs.h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
                                                                   key_bytes, d_split);
     LEY_CUDA("ext locate", cudaGetLastError());
     prof.launches += 1;
     LEY_CUDA("ext locate", cudaMemcpyAsync(split.data() + R, d_split, 8 * nthreads, cudaMemcpyDeviceToHost, s));
     LEY_CUDA("ext locate", cudaStreamSynchronize(s));
   }
-  uint64_t m_max = 0;
-  std::vector<uint64_t> part_off(P + 1, 0);
+  part_off.assign(P + 1, 0);
   for (uint32_t p = 0; p < P; ++p) {
     uint64_t m = 0;
     for (uint32_t r = 0; r < R; ++r) m += split[(size_t)(p + 1) * R + r] - split[(size_t)p * R + r];
     part_off[p + 1] = part_off[p] + m;
-    m_max = std::max(m_max, m);
   }
-  if ((st = prof.end())) return st;
+  *P_out = P;
+  return LEY_OK;
+}
 
-  // ---------------------------------------------------------------- a12: K-way merge per partition
-  if ((st = prof.begin("ext merge"))) return st;
+// a12: K-way merge of partitions [p_begin, p_end); partition p lands at out + 100 (part_off[p] -
+// part_off[p_begin]) (perm_out likewise).
+ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uint64_t>& split,
+                     const std::vector<uint64_t>& part_off, uint32_t p_begin, uint32_t p_end, uint8_t* out,
+                     uint32_t* perm_out, uint32_t key_bytes, cudaStream_t s, Profiler& prof, ExtTrace& tr) {
+  ley_status st;
+  const uint32_t R = (uint32_t)rs.off.size();
+  const int sms = ctx.sms;
+  cudaStream_t h2d = ctx.copy_stream[0], d2h = ctx.copy_stream[1];
+  cudaEvent_t ev_start = ctx.ev[0];
+  cudaEvent_t ev_in[2] = {ctx.ev[1], ctx.ev[2]}, ev_sorted[2] = {ctx.ev[3], ctx.ev[4]},
+              ev_out[2] = {ctx.ev[5], ctx.ev[6]};
+  uint64_t m_max = 0;
+  std::vector<uint32_t> parts;  // non-empty partitions, merged in order
+  for (uint32_t p = p_begin; p < p_end; ++p) {
+    m_max = std::max(m_max, part_off[p + 1] - part_off[p]);
+    if (part_off[p + 1] > part_off[p]) parts.push_back(p);
+  }
   const size_t sz_slice = a256(m_max * kRecordBytes);
   const size_t sz_comp = a256(m_max * 8);
   const size_t sz_p = perm_out ? a256(m_max * 4) : 0;
-  std::vector<uint32_t> parts;  // non-empty partitions, merged in order
-  for (uint32_t p = 0; p < P; ++p)
-    if (part_off[p + 1] > part_off[p]) parts.push_back(p);
   // merge-tree boundaries of every level of every partition, computed once on the host and copied to the
   // device in one transfer (no host round trip between levels): level 0 = the R slice starts in the
   // concatenation; level l+1 keeps every other boundary of level l (adjacent pairs merged)
@@ -467,7 +480,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   if (phase2 > ctx.ext.cap) {
     if ((st = ensure_buffer(ctx.ext, phase2, "external merge buffers", s))) return st;
   }
-  eb = static_cast<uint8_t*>(ctx.ext.ptr);
+  uint8_t* eb = static_cast<uint8_t*>(ctx.ext.ptr);
   uint8_t* d_slice[2] = {eb, eb + sz_slice};
   uint8_t* d_mout[2] = {eb + 2 * sz_slice, eb + 3 * sz_slice};
   uint8_t* cb = eb + 4 * sz_slice;
@@ -497,10 +510,10 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
       const uint64_t at = off0[r];
       if (hi > lo) {
         LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice[sl] + at * kRecordBytes,
-                                                  h_runs + (run_off[r] + lo) * kRecordBytes, (hi - lo) * kRecordBytes,
+                                                  rs.h_runs + (rs.off[r] + lo) * kRecordBytes, (hi - lo) * kRecordBytes,
                                                   cudaMemcpyHostToDevice, h2d));
         if (perm_out)
-          LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice[sl] + at, h_perm + run_off[r] + lo, (hi - lo) * 4,
+          LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice[sl] + at, rs.h_perm + rs.off[r] + lo, (hi - lo) * 4,
                                                     cudaMemcpyHostToDevice, h2d));
       }
     }
@@ -511,6 +524,7 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   // the slices are read from the host run scratch: every run's D2H (which s has waited for) comes first
   LEY_CUDA("ext merge", cudaEventRecord(ctx.ev[7], s));
   LEY_CUDA("ext merge", cudaStreamWaitEvent(h2d, ctx.ev[7], 0));
+  LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ctx.ev[7], 0));
   if (!parts.empty() && (st = issue_slices(0))) return st;
   for (size_t i = 0; i < parts.size(); ++i) {
     const uint32_t p = parts[i];
@@ -541,19 +555,86 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
     LEY_CUDA("ext merge", cudaEventRecord(ev_sorted[sl], s));
     LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
     tr.end(t_mm, s);
+    const uint64_t o = part_off[p] - part_off[p_begin];
     const size_t t_md = tr.begin("merge D2H", d2h);
-    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + part_off[p] * kRecordBytes, d_mout[sl], m * kRecordBytes,
+    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + o * kRecordBytes, d_mout[sl], m * kRecordBytes,
                                               cudaMemcpyDeviceToHost, d2h));
     tr.end(t_md, d2h);
     if (perm_out)
-      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + part_off[p], d_pout[sl], m * 4, cudaMemcpyDeviceToHost, d2h));
+      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + o, d_pout[sl], m * 4, cudaMemcpyDeviceToHost, d2h));
     LEY_CUDA("ext merge", cudaEventRecord(ev_out[sl], d2h));
   }
   LEY_CUDA("ext merge", cudaEventRecord(ev_start, d2h));
   LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_start, 0));
-  tr.report();
-  if ((st = prof.end())) return st;
   return LEY_OK;
+}
+
+// partitions of about m_target records: every q-th sample (a partition holds at most (q + R) S records)
+uint64_t ext_sample_q(uint64_t m_target, uint64_t S, uint64_t R) {
+  uint64_t q = m_target / S > 2ull * R ? m_target / S - R : std::max<uint64_t>(1, m_target / (2 * S));
+  return q ? q : 1;
+}
+
+ley_status ensure_host_scratch(DeviceContext& ctx, size_t bytes) {
+  if (ctx.host_scratch_cap >= bytes) return LEY_OK;
+  if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
+  ctx.host_scratch = nullptr;
+  ctx.host_scratch_cap = 0;
+  LEY_CUDA("external scratch", cudaHostAlloc(&ctx.host_scratch, bytes, cudaHostAllocMapped));
+  ctx.host_scratch_cap = bytes;
+  return LEY_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------- driver
+ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
+                              uint64_t budget, uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
+  ley_status st;
+  if (key_bytes > kKeyBytes) {  // the merge compares 10-byte composites (K-m)
+    set_error("external: keys longer than 10 bytes are not supported on the external path (raise the budget "
+              "to the staged path's ley_plan_query().staged_bytes)");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  const uint64_t C = external_run_records(n, budget);
+  if (C < 1024 && C < n) {
+    set_error("external: device_budget_bytes " + std::to_string(budget) +
+              " is below the minimum working set (runs of >= 1024 records)");
+    return LEY_ERR_BUDGET;
+  }
+  const uint64_t R = (n + C - 1) / C;
+  const uint64_t S = external_sample_stride(n, C, budget);  // sample stride (bounds every partition)
+  const uint64_t nsamp_cap = R * ((C + S - 1) / S);
+  if ((st = ensure_buffer(ctx.ext, phase1_bytes(C, nsamp_cap), "external buffers", s))) return st;
+  const Phase1 b = phase1_layout(static_cast<uint8_t*>(ctx.ext.ptr), C, nsamp_cap);
+  // pinned host run scratch (records, and global ordinals when perm is requested)
+  if ((st = ensure_host_scratch(ctx, (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0)))) return st;
+  RunSet rs;
+  rs.h_runs = static_cast<uint8_t*>(ctx.host_scratch);
+  rs.h_perm = perm_out ? reinterpret_cast<uint32_t*>(rs.h_runs + (size_t)n * kRecordBytes) : nullptr;
+  LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&rs.h_runs_dev, rs.h_runs, 0));
+  if ((st = ensure_copy_streams(ctx))) return st;
+  ExtTrace tr;
+  tr.start(s);
+
+  if ((st = prof.begin("ext run generation"))) return st;
+  if ((st = ext_generate(ctx, in, n, 0, C, S, rs, b, perm_out != nullptr, key_bytes, s, prof, tr))) return st;
+  if ((st = prof.end())) return st;
+
+  if ((st = prof.begin("ext partition"))) return st;
+  // merge-phase device plan: a partition of m records needs two slots of slice (100 m) + out (100 m)
+  // (partition p+1 streams in and p-1 streams out while p merges) + 2 x 16 m composites (+ 16 m perm);
+  // keep it inside the same budget as phase 1.
+  const uint64_t q = ext_sample_q(external_merge_target(C, budget), S, R);
+  uint32_t P = 1;
+  std::vector<uint64_t> split, part_off;
+  if ((st = ext_partition(ctx, rs, b, q, key_bytes, s, prof, &P, split, part_off))) return st;
+  if ((st = prof.end())) return st;
+
+  if ((st = prof.begin("ext merge"))) return st;
+  if ((st = ext_merge(ctx, rs, split, part_off, 0, P, out, perm_out, key_bytes, s, prof, tr))) return st;
+  tr.report();
+  return prof.end();
 }
 
 }  // namespace ley
