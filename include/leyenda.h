@@ -117,8 +117,11 @@ const char* ley_last_error(void);
  * the concatenated input. key_bytes: 1..10 (shorter keys compare as their prefix).
  * in_local/out_local: device memory on the comm's device, or pinned host memory on EVERY rank — then each
  * rank's slice and output capacity are staged on its device (H2D, the device path, D2H of its range) if
- * they fit device_budget_bytes on every rank, else all ranks return LEY_ERR_UNSUPPORTED (the
- * multi-GPU external path, is not built). */
+ * they fit device_budget_bytes on every rank, else the multi-GPU EXTERNAL path runs: every
+ * rank writes sorted runs of its slice into a host run scratch shared by all ranks (POSIX shared memory
+ * under /dev/shm, N x 100 bytes; LEY_ERR_UNSUPPORTED if it cannot be created), all ranks derive the same
+ * splitters from the shared samples, and rank r merges global sorted positions
+ * [floor(r N/G), floor((r+1) N/G)) into out_local (key_bytes <= 10). */
 typedef struct ley_comm ley_comm;
 ley_status ley_comm_get_unique_id(uint8_t id_out[128]);  /* rank 0; broadcast it (e.g. torch PG)  */
 ley_status ley_comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);
@@ -129,13 +132,16 @@ ley_status ley_sort_dist(ley_comm* comm, const void* in_local, uint64_t n_local,
 ley_status ley_comm_destroy(ley_comm* comm);
 
 /* Loopback verification hook: the same G-rank algorithm (kernels K-s0/K-s1/
- * K-s2/K-p, plans, local sort) with all G ranks' slices on the CURRENT device and device copies standing
- * in for the NCCL collectives. Arrays have nranks entries; in_local[r]/out_local[r] are device pointers.
- * Same results as ley_sort_dist on G GPUs. Not a performance path. */
+ * K-s2/K-p, plans, local sort) with all G ranks' slices on the CURRENT device; K-p stores into every
+ * receiver's buffer (dist_fused) or device copies stand in for the all-to-all. Arrays have nranks
+ * entries. in_local[r]/out_local[r]: device pointers, or pinned host pointers — then the multi-GPU
+ * EXTERNAL algorithm runs (every rank's runs, one shared partition, each rank's merge of its exact share;
+ * device_budget_bytes as in ley_sort_dist). Same results as ley_sort_dist on G GPUs. Not a performance
+ * path. */
 ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const uint64_t* n_local,
                                   void* const* out_local, const uint64_t* out_capacity_records,
                                   uint64_t* n_out_local, uint64_t* out_global_offset, uint32_t record_bytes,
-                                  uint32_t key_bytes, void* stream);
+                                  uint32_t key_bytes, uint64_t device_budget_bytes, void* stream);
 
 /* Host-only planning steps of the distributed sort (pure functions, no CUDA; exposed so the multi-rank
  * logic is testable on CPU with any transport):
@@ -155,6 +161,12 @@ void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins
 void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
                             uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset);
 void ley_dist_dest_offsets(const uint64_t* send_counts, int nranks, int rank, uint64_t* dst_offsets);
+
+/* Test hooks of the multi-GPU external path's shared host run scratch (host logic only, no CUDA): create
+ * (create=1: checks /dev/shm free space, replaces a stale segment) or open a POSIX shared memory segment
+ * of `bytes` and map it (*ptr); close unmaps it and, if unlink_name is non-NULL, removes the name. */
+ley_status ley_test_shared_scratch(const char* name, uint64_t bytes, int create, void** ptr);
+void ley_test_shared_scratch_close(void* ptr, uint64_t bytes, const char* unlink_name);
 
 /* ---------------------------------------------------------------- introspection and tuning */
 

@@ -41,7 +41,7 @@ MAX_RECORDS = 0xFFFFFFFE
 EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get_unique_id", "ley_comm_init",
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
                     "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
-                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange", "ley_dist_dest_offsets",
+                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange", "ley_dist_dest_offsets", "ley_test_shared_scratch", "ley_test_shared_scratch_close",
                     "ley_sort_submit", "ley_sort_drain", "ley_test_scan_excl", "ley_test_tile_sort", "ley_device_bytes")
 
 
@@ -93,7 +93,7 @@ _lib.ley_version.argtypes = []
 _lib.ley_version.restype = _u32
 _pu64 = ctypes.POINTER(_u64)
 _lib.ley_sort_dist_loopback.argtypes = [_i32, ctypes.POINTER(_vp), _pu64, ctypes.POINTER(_vp), _pu64, _pu64, _pu64,
-                                        _u32, _u32, _vp]
+                                        _u32, _u32, _u64, _vp]
 _lib.ley_sort_dist_loopback.restype = _i32
 _lib.ley_dist_plan_splitters.argtypes = [_pu64, _u64, _i32, ctypes.POINTER(_u32), _pu64, _pu64]
 _lib.ley_dist_plan_splitters.restype = _i32
@@ -103,6 +103,10 @@ _lib.ley_dist_plan_exchange.argtypes = [_pu64, _i32, _i32, _pu64, _pu64, _pu64, 
 _lib.ley_dist_plan_exchange.restype = None
 _lib.ley_dist_dest_offsets.argtypes = [_pu64, _i32, _i32, _pu64]
 _lib.ley_dist_dest_offsets.restype = None
+_lib.ley_test_shared_scratch.argtypes = [ctypes.c_char_p, _u64, _i32, ctypes.POINTER(_vp)]
+_lib.ley_test_shared_scratch.restype = _i32
+_lib.ley_test_shared_scratch_close.argtypes = [_vp, _u64, ctypes.c_char_p]
+_lib.ley_test_shared_scratch_close.restype = None
 
 
 class LeyendaError(RuntimeError):
@@ -239,7 +243,7 @@ def ley_comm_destroy(comm: int) -> None:
 
 
 def ley_sort_dist_loopback(ins, n_locals, outs, caps, record_bytes: int = RECORD_BYTES, key_bytes: int = KEY_BYTES,
-                           stream=None):
+                           device_budget_bytes: int = 0, stream=None):
     """G logical ranks on the current device (test hook). Returns [(n_out, out_global_offset)] per rank."""
     G = len(ins)
     a_in = (_vp * G)(*[_addr(x) for x in ins])
@@ -248,7 +252,8 @@ def ley_sort_dist_loopback(ins, n_locals, outs, caps, record_bytes: int = RECORD
     a_cap = (_u64 * G)(*caps)
     n_out = (_u64 * G)()
     off = (_u64 * G)()
-    st = _lib.ley_sort_dist_loopback(G, a_in, a_n, a_out, a_cap, n_out, off, record_bytes, key_bytes, _stream(stream))
+    st = _lib.ley_sort_dist_loopback(G, a_in, a_n, a_out, a_cap, n_out, off, record_bytes, key_bytes,
+                                     device_budget_bytes, _stream(stream))
     _check(st, "ley_sort_dist_loopback", True)
     return [(n_out[i], off[i]) for i in range(G)]
 
@@ -290,6 +295,18 @@ def ley_dist_dest_offsets(send_counts, nranks: int, rank: int):
     d = (_u64 * nranks)()
     _lib.ley_dist_dest_offsets(m, nranks, rank, d)
     return list(d)
+
+
+def ley_test_shared_scratch(name: str, nbytes: int, create: bool) -> int:
+    """Create/open + map the shared run scratch segment (host logic only); returns its address."""
+    p = _vp()
+    _check(_lib.ley_test_shared_scratch(name.encode(), nbytes, int(create), ctypes.byref(p)), "ley_test_shared_scratch",
+           True)
+    return p.value
+
+
+def ley_test_shared_scratch_close(addr: int, nbytes: int, unlink_name: str | None = None) -> None:
+    _lib.ley_test_shared_scratch_close(addr, nbytes, unlink_name.encode() if unlink_name else None)
 
 
 def library_path() -> str:

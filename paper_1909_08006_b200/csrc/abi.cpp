@@ -21,9 +21,11 @@ ley_status comm_get_unique_id(uint8_t id_out[128]);
 ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128], int device);
 ley_status comm_destroy(ley_comm* comm);
 ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
-                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint32_t key_bytes,
-                              cudaStream_t s);
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint64_t budget,
+                              uint32_t key_bytes, cudaStream_t s);
 int dist_plan_splitters(const uint64_t* hist, uint64_t N, int G, uint32_t* bins, uint64_t* rho, uint64_t* first);
+ley_status test_shared_scratch(const char* name, uint64_t bytes, int create, void** ptr);
+void test_shared_scratch_close(void* p, uint64_t bytes, const char* unlink_name);
 void dist_bin_dest_counts(const uint64_t* local_hist, const uint32_t* bins, int nspl, uint64_t* counts);
 void dist_plan_exchange(const uint64_t* send_counts, int G, int rank, uint64_t* recv_counts, uint64_t* recv_off,
                         uint64_t* send_off, uint64_t* n_out, uint64_t* out_off);
@@ -309,7 +311,8 @@ ley_status ley_comm_destroy(ley_comm* comm) {
 
 ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const uint64_t* n_local,
                                   void* const* out_local, const uint64_t* out_capacity_records, uint64_t* n_out_local,
-                                  uint64_t* out_global_offset, uint32_t record_bytes, uint32_t key_bytes, void* stream) {
+                                  uint64_t* out_global_offset, uint32_t record_bytes, uint32_t key_bytes,
+                                  uint64_t device_budget_bytes, void* stream) {
   clear_error();
   if (ley_status st = check_record_key(record_bytes, key_bytes, kKeyBytes)) return st;
   if (!in_local || !n_local || !out_local || !out_capacity_records || !n_out_local || !out_global_offset) {
@@ -317,7 +320,7 @@ ley_status ley_sort_dist_loopback(int nranks, const void* const* in_local, const
     return LEY_ERR_INVALID_ARGUMENT;
   }
   return dist_sort_loopback(nranks, in_local, n_local, out_local, out_capacity_records, n_out_local,
-                            out_global_offset, key_bytes, static_cast<cudaStream_t>(stream));
+                            out_global_offset, device_budget_bytes, key_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int ley_dist_plan_splitters(const uint64_t* global_hist16, uint64_t n_total, int nranks, uint32_t* bins,
@@ -333,6 +336,19 @@ void ley_dist_bin_dest_counts(const uint64_t* local_hist16, const uint32_t* bins
 void ley_dist_plan_exchange(const uint64_t* send_counts, int nranks, int rank, uint64_t* recv_counts,
                             uint64_t* recv_offsets, uint64_t* send_offsets, uint64_t* n_out, uint64_t* out_offset) {
   dist_plan_exchange(send_counts, nranks, rank, recv_counts, recv_offsets, send_offsets, n_out, out_offset);
+}
+
+ley_status ley_test_shared_scratch(const char* name, uint64_t bytes, int create, void** ptr) {
+  clear_error();
+  if (!name || !ptr) {
+    set_error("ley_test_shared_scratch: NULL");
+    return LEY_ERR_INVALID_ARGUMENT;
+  }
+  return test_shared_scratch(name, bytes, create, ptr);
+}
+
+void ley_test_shared_scratch_close(void* ptr, uint64_t bytes, const char* unlink_name) {
+  test_shared_scratch_close(ptr, bytes, unlink_name);
 }
 
 void ley_dist_dest_offsets(const uint64_t* send_counts, int nranks, int rank, uint64_t* dst_offsets) {

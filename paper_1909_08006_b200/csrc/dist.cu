@@ -18,8 +18,12 @@
 //                                                                  C4 all-to-all-v (grouped send/recv)
 //   P6  internal sort of the received records (K-a..K-e); receive order = global ordinal order.
 // With exact splitters rank r ends up with global sorted positions [floor(r N/G), floor((r+1) N/G)).
+#include <fcntl.h>
 #include <nccl.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <sys/statvfs.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <memory>
@@ -371,6 +375,8 @@ struct ley_comm {
   ncclWindow_t win = nullptr;
   uint8_t** d_peers = nullptr;
   ley::DeviceBuffer stage;  // pinned host slices: the device copy of this rank's input and output
+  uint64_t uid_hash = 0;    // names this communicator's shared host run scratch (external path)
+  uint64_t ext_calls = 0;   // (the same count on every rank: calls are collective)
 };
 
 namespace ley {
@@ -438,6 +444,9 @@ ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128
   c->rank = rank;
   c->device = device;
   LEY_NCCL("comm", ncclCommInitRank(&c->nccl, nranks, uid, rank));
+  uint64_t h = 1469598103934665603ull;  // FNV-1a of the unique id
+  for (int i = 0; i < 128; ++i) h = (h ^ id[i]) * 1099511628211ull;
+  c->uid_hash = h;
   *comm = c.release();
   return LEY_OK;
 }
@@ -654,6 +663,166 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
 
 }  // namespace
 
+// ------------------------------------------------------------------------- multi-GPU external path
+// Host run scratch every rank can read: POSIX shared memory (rank 0 creates it, every rank maps it and
+// registers it with CUDA as mapped pinned memory); with one rank the library's own pinned scratch.
+struct SharedScratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  bool registered = false;
+};
+
+void shared_scratch_close(SharedScratch& sh) {
+  if (sh.registered) cudaHostUnregister(sh.p);
+  if (sh.p) munmap(sh.p, sh.bytes);
+  sh = SharedScratch{};
+}
+
+// 0 on success; else an error message (the caller turns every rank's outcome into one agreement)
+std::string shared_scratch_open(const std::string& name, size_t bytes, bool create, SharedScratch& sh,
+                                bool cuda_register = true) {
+  if (create) {
+    struct statvfs v{};
+    if (statvfs("/dev/shm", &v) == 0 && (uint64_t)v.f_bavail * v.f_frsize < bytes)
+      return "dist external: /dev/shm has " + std::to_string((uint64_t)v.f_bavail * v.f_frsize) +
+             " bytes free, the shared run scratch needs " + std::to_string(bytes);
+    shm_unlink(name.c_str());  // a stale segment of a crashed run
+  }
+  const int fd = shm_open(name.c_str(), create ? (O_CREAT | O_RDWR | O_EXCL) : O_RDWR, 0600);
+  if (fd < 0) return "dist external: shm_open(" + name + ") failed: " + strerror(errno);
+  if (create && ftruncate(fd, (off_t)bytes) != 0) {
+    const std::string e = strerror(errno);
+    close(fd);
+    return "dist external: ftruncate of the shared run scratch failed: " + e;
+  }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return std::string("dist external: mmap failed: ") + strerror(errno);
+  sh.p = p;
+  sh.bytes = bytes;
+  if (!cuda_register) return "";
+  if (cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return "dist external: cudaHostRegister of the shared run scratch failed";
+  }
+  sh.registered = true;
+  return "";
+}
+
+// All ranks' outcomes summed (NCCL, on s): 0 iff every rank succeeded.
+ley_status agree(ley_comm* comm, bool ok, cudaStream_t s, uint64_t* any) {
+  uint64_t* flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
+  const uint64_t bad = ok ? 0 : 1;
+  LEY_CUDA("dist agree", cudaMemcpyAsync(flag, &bad, 8, cudaMemcpyHostToDevice, s));
+  LEY_NCCL("dist agree", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
+  LEY_CUDA("dist agree", cudaMemcpyAsync(any, flag, 8, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("dist agree", cudaStreamSynchronize(s));
+  return LEY_OK;
+}
+
+// SURVEY §8e "External at 8 GPUs": runs of every rank's pinned host slice into the shared scratch (global
+// layout), samples broadcast to every rank, identical splitters and slice bounds everywhere, and rank r
+// merging global sorted positions [floor(r N/G), floor((r+1) N/G)) into its out_local (external.cu).
+ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_local, uint8_t* out, uint64_t cap,
+                              uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
+                              cudaStream_t s) {
+  const int G = comm->nranks, rank = comm->rank;
+  if (key_bytes > kKeyBytes) {
+    set_error("dist external: keys longer than 10 bytes are not supported on the external path");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  DeviceContext& ctx = device_context(comm->device);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  if (!ctx.host_pinned) LEY_CUDA("dist", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
+  // slice sizes -> the plan every rank derives alike
+  std::vector<uint64_t> nl(G);
+  {
+    uint64_t* d = reinterpret_cast<uint64_t*>(comm->state.d_status);
+    LEY_CUDA("dist external", cudaMemcpyAsync(d + G, &n_local, 8, cudaMemcpyHostToDevice, s));
+    LEY_NCCL("dist external", ncclAllGather(d + G, d, 1, ncclUint64, comm->nccl, s));
+    LEY_CUDA("dist external", cudaMemcpyAsync(nl.data(), d, 8 * G, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("dist external", cudaStreamSynchronize(s));
+  }
+  const ExtDistPlan P = ext_dist_plan(nl, budget);
+  if (P.N > LEY_MAX_RECORDS) {
+    set_error("dist external: total records > 2^32-2");
+    return LEY_ERR_TOO_LARGE;
+  }
+  const bool dev_ok = !budget || ext_dist_device_bytes(P) <= budget;
+  // shared host run scratch
+  const size_t bytes = std::max<size_t>((size_t)P.N * kRecordBytes, 4096);
+  SharedScratch sh;
+  std::string err;
+  const std::string name = "/ley-" + std::to_string(comm->uid_hash) + "-" + std::to_string(comm->ext_calls++);
+  uint8_t* h_runs = nullptr;
+  if (G == 1) {
+    if (ctx.host_scratch_cap < bytes) {
+      if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
+      ctx.host_scratch = nullptr;
+      ctx.host_scratch_cap = 0;
+      LEY_CUDA("dist external", cudaHostAlloc(&ctx.host_scratch, bytes, cudaHostAllocMapped));
+      ctx.host_scratch_cap = bytes;
+    }
+    h_runs = static_cast<uint8_t*>(ctx.host_scratch);
+  } else if (rank == 0) {
+    err = shared_scratch_open(name, bytes, true, sh);
+  }
+  uint64_t any = 0;
+  ley_status st = agree(comm, err.empty() && dev_ok, s, &any);
+  if (!st && !any && G > 1 && rank != 0) err = shared_scratch_open(name, bytes, false, sh);
+  if (!st && !any && G > 1) st = agree(comm, err.empty(), s, &any);
+  if (G > 1 && rank == 0 && !st) shm_unlink(name.c_str());  // every rank has it mapped (or gave up)
+  auto fail = [&](ley_status code) {
+    shared_scratch_close(sh);
+    return code;
+  };
+  if (st) return fail(st);
+  if (any) {
+    set_error(!err.empty() ? err : !dev_ok ? "dist external: device_budget_bytes below the external working set ("
+                                                 + std::to_string(ext_dist_device_bytes(P)) + " bytes)"
+                                           : "dist external: another rank could not set up the shared run scratch");
+    return fail(dev_ok ? LEY_ERR_UNSUPPORTED : LEY_ERR_BUDGET);
+  }
+  if (G > 1) h_runs = static_cast<uint8_t*>(sh.p);
+  Profiler quiet;
+  quiet.ctx = &ctx;
+  quiet.stream = s;
+  // a10: this rank's runs; then every rank's runs must be in the scratch before anyone reads them
+  if ((st = ext_dist_runs(ctx, P, rank, in, h_runs, key_bytes, s, quiet))) return fail(st);
+  LEY_CUDA("dist external", cudaStreamSynchronize(s));
+  // samples: rank r's block of the run-ordered sample set broadcast from rank r (the all-reduce inside
+  // the group also orders every rank's run D2H before the partition phase reads the scratch)
+  uint8_t* samp = ext_dist_samples(ctx, P);
+  LEY_NCCL("dist external", ncclGroupStart());
+  for (int r = 0; r < G; ++r) {
+    const uint64_t c = (P.samp_off[r + 1] - P.samp_off[r]) * kRecordBytes;
+    if (c) {
+      uint8_t* blk = samp + P.samp_off[r] * kRecordBytes;
+      LEY_NCCL("dist external", ncclBroadcast(blk, blk, c, ncclUint8, r, comm->nccl, s));
+    }
+  }
+  LEY_NCCL("dist external", ncclGroupEnd());
+  if ((st = agree(comm, true, s, &any))) return fail(st);
+  // a11 (identical on every rank) and a12 (this rank's range); every rank checks its capacity first
+  const uint64_t lo = (uint64_t)((unsigned __int128)rank * P.N / (unsigned)G);
+  const uint64_t hi = (uint64_t)((unsigned __int128)(rank + 1) * P.N / (unsigned)G);
+  if ((st = agree(comm, hi - lo <= cap, s, &any))) return fail(st);
+  if (any) {
+    set_error("dist external: out_capacity_records below the rank's share floor((r+1) N/G) - floor(r N/G) on some rank");
+    return fail(LEY_ERR_CAPACITY);
+  }
+  ExtDistParts parts;
+  if ((st = ext_dist_partition(ctx, P, h_runs, key_bytes, s, quiet, parts))) return fail(st);
+  if ((st = ext_dist_merge(ctx, P, parts, rank, h_runs, out, cap, n_out_local, out_global_offset, key_bytes, s, quiet)))
+    return fail(st);
+  LEY_CUDA("dist external", cudaStreamSynchronize(s));
+  // nobody may unmap a scratch another rank still reads: one last agreement
+  if ((st = agree(comm, true, s, &any))) return fail(st);
+  record_launches(quiet.launches);
+  shared_scratch_close(sh);
+  return LEY_OK;
+}
+
 // Pointer kinds: both device pointers (the NCCL path proper), or both pinned host pointers — staged: this
 // rank's slice is copied into a comm-owned device buffer, sorted by the device path, and its output range
 // copied back. Every rank first agrees (one all-reduce) that its staging fits its budget, so a rank that
@@ -684,6 +853,8 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
                             key_bytes, s);
   const size_t a_in = a256(n_local * kRecordBytes), a_out = a256(out_capacity * kRecordBytes);
   const bool fits = !budget || a_in + a_out <= budget;
+  bool external = false;
+  ley_status st_ = LEY_OK;
   {
     DeviceContext& ctx = device_context(comm->device);
     std::lock_guard<std::mutex> guard(ctx.mu);
@@ -698,13 +869,12 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     uint64_t any = 0;
     LEY_CUDA("dist staging", cudaMemcpyAsync(&any, flag, 8, cudaMemcpyDeviceToHost, s));
     LEY_CUDA("dist staging", cudaStreamSynchronize(s));
-    if (any) {
-      set_error("dist: pinned host slices are staged on the device, and a rank's slice + output capacity exceed "
-                "its device_budget_bytes (the multi-GPU external path is not built)");
-      return LEY_ERR_UNSUPPORTED;
-    }
-    if (ley_status st = ensure_buffer(comm->stage, std::max<size_t>(a_in + a_out, 256), "dist staging", s)) return st;
+    if (!any && (st_ = ensure_buffer(comm->stage, std::max<size_t>(a_in + a_out, 256), "dist staging", s))) return st_;
+    if (any) external = true;
   }
+  if (external)
+    return dist_sort_external(comm, static_cast<const uint8_t*>(in_local), n_local, static_cast<uint8_t*>(out_local),
+                              out_capacity, n_out_local, out_global_offset, budget, key_bytes, s);
   uint8_t* din = static_cast<uint8_t*>(comm->stage.ptr);
   uint8_t* dout = din + a_in;
   if (n_local)
@@ -720,12 +890,68 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
 // ------------------------------------------------------------------------------ loopback transport
 // All G ranks on the current device in one process; collectives are host-side reductions and device
 // copies. Exercises exactly the kernels and plans of dist_sort (test hook).
+// Loopback of the multi-GPU external path: the G ranks' phases run one after another on this device
+// (run generation of every rank, one partition, each rank's merge); the library's pinned scratch stands in
+// for the shared memory segment.
+ley_status dist_external_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
+                                  const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint64_t budget,
+                                  uint32_t key_bytes, cudaStream_t s) {
+  if (key_bytes > kKeyBytes) {
+    set_error("dist external: keys longer than 10 bytes are not supported on the external path");
+    return LEY_ERR_UNSUPPORTED;
+  }
+  int dev = 0;
+  LEY_CUDA("loopback", cudaGetDevice(&dev));
+  DeviceContext& ctx = device_context(dev);
+  std::lock_guard<std::mutex> guard(ctx.mu);
+  if (!ctx.host_pinned) LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
+  const ExtDistPlan P = ext_dist_plan(std::vector<uint64_t>(n_local, n_local + G), budget);
+  if (budget && ext_dist_device_bytes(P) > budget) {
+    set_error("dist external: device_budget_bytes below the external working set");
+    return LEY_ERR_BUDGET;
+  }
+  const size_t bytes = std::max<size_t>((size_t)P.N * kRecordBytes, 4096);
+  if (ctx.host_scratch_cap < bytes) {
+    if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
+    ctx.host_scratch = nullptr;
+    ctx.host_scratch_cap = 0;
+    LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_scratch, bytes, cudaHostAllocMapped));
+    ctx.host_scratch_cap = bytes;
+  }
+  uint8_t* h_runs = static_cast<uint8_t*>(ctx.host_scratch);
+  Profiler quiet;
+  quiet.ctx = &ctx;
+  quiet.stream = s;
+  ley_status st;
+  for (int r = 0; r < G; ++r)
+    if ((st = ext_dist_runs(ctx, P, r, static_cast<const uint8_t*>(in[r]), h_runs, key_bytes, s, quiet))) return st;
+  LEY_CUDA("loopback", cudaStreamSynchronize(s));
+  ExtDistParts parts;
+  if ((st = ext_dist_partition(ctx, P, h_runs, key_bytes, s, quiet, parts))) return st;
+  for (int r = 0; r < G; ++r)
+    if ((st = ext_dist_merge(ctx, P, parts, r, h_runs, static_cast<uint8_t*>(out[r]), caps[r], &n_out[r], &out_off[r],
+                             key_bytes, s, quiet)))
+      return st;
+  LEY_CUDA("loopback", cudaStreamSynchronize(s));
+  record_launches(quiet.launches);
+  return LEY_OK;
+}
+
 ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_local, void* const* out,
-                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint32_t key_bytes,
-                              cudaStream_t s) {
+                              const uint64_t* caps, uint64_t* n_out, uint64_t* out_off, uint64_t budget,
+                              uint32_t key_bytes, cudaStream_t s) {
   if (G < 1 || G > kMaxRanks) {
     set_error("loopback: 1 <= G <= 8");
     return LEY_ERR_INVALID_ARGUMENT;
+  }
+  {  // pinned host slices: the multi-GPU external path
+    cudaPointerAttributes a{};
+    const void* probe = nullptr;
+    for (int i = 0; i < G && !probe; ++i)
+      if (n_local[i]) probe = in[i];
+    if (probe && cudaPointerGetAttributes(&a, probe) == cudaSuccess && a.type == cudaMemoryTypeHost)
+      return dist_external_loopback(G, in, n_local, out, caps, n_out, out_off, budget, key_bytes, s);
+    cudaGetLastError();
   }
   int dev = 0;
   LEY_CUDA("loopback", cudaGetDevice(&dev));
@@ -842,6 +1068,24 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
     out_off[i] = r.out_off;
   }
   return LEY_OK;
+}
+
+// Test hooks of the shared host run scratch (host logic only: no CUDA registration), so two CPU
+// processes can check creation, opening, sizing and unlinking (tests/test_dist.py, gloo).
+ley_status test_shared_scratch(const char* name, uint64_t bytes, int create, void** ptr) {
+  SharedScratch sh;
+  const std::string err = shared_scratch_open(name, bytes, create != 0, sh, false);
+  if (!err.empty()) {
+    set_error(err);
+    shared_scratch_close(sh);
+    return LEY_ERR_UNSUPPORTED;
+  }
+  *ptr = sh.p;
+  return LEY_OK;
+}
+void test_shared_scratch_close(void* p, uint64_t bytes, const char* unlink_name) {
+  if (p) munmap(p, bytes);
+  if (unlink_name) shm_unlink(unlink_name);
 }
 
 }  // namespace ley

@@ -432,7 +432,11 @@ ley_status ext_partition(DeviceContext& ctx, const RunSet& rs, const Phase1& b, 
 // part_off[p_begin]) (perm_out likewise).
 ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uint64_t>& split,
                      const std::vector<uint64_t>& part_off, uint32_t p_begin, uint32_t p_end, uint8_t* out,
-                     uint32_t* perm_out, uint32_t key_bytes, cudaStream_t s, Profiler& prof, ExtTrace& tr) {
+                     uint32_t* perm_out, uint32_t key_bytes, cudaStream_t s, Profiler& prof, ExtTrace& tr,
+                     uint64_t clip_lo = 0, uint64_t clip_hi = ~0ull) {
+  // only global output positions [clip_lo, clip_hi) are written, at out + 100 (pos - max(clip_lo,
+  // part_off[p_begin])) — a rank of the multi-GPU external sort keeps its exact share of the boundary
+  // partitions it merges
   ley_status st;
   const uint32_t R = (uint32_t)rs.off.size();
   const int sms = ctx.sms;
@@ -555,13 +559,17 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
     LEY_CUDA("ext merge", cudaEventRecord(ev_sorted[sl], s));
     LEY_CUDA("ext merge", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
     tr.end(t_mm, s);
-    const uint64_t o = part_off[p] - part_off[p_begin];
+    const uint64_t base = std::max(clip_lo, part_off[p_begin]);
+    const uint64_t w0 = std::max(part_off[p], clip_lo), w1 = std::min(part_off[p + 1], clip_hi);
     const size_t t_md = tr.begin("merge D2H", d2h);
-    LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + o * kRecordBytes, d_mout[sl], m * kRecordBytes,
-                                              cudaMemcpyDeviceToHost, d2h));
+    if (w1 > w0) {
+      const uint64_t o = w0 - base, from = w0 - part_off[p], cnt = w1 - w0;
+      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(out + o * kRecordBytes, d_mout[sl] + from * kRecordBytes,
+                                                cnt * kRecordBytes, cudaMemcpyDeviceToHost, d2h));
+      if (perm_out)
+        LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + o, d_pout[sl] + from, cnt * 4, cudaMemcpyDeviceToHost, d2h));
+    }
     tr.end(t_md, d2h);
-    if (perm_out)
-      LEY_CUDA("ext merge D2H", cudaMemcpyAsync(perm_out + o, d_pout[sl], m * 4, cudaMemcpyDeviceToHost, d2h));
     LEY_CUDA("ext merge", cudaEventRecord(ev_out[sl], d2h));
   }
   LEY_CUDA("ext merge", cudaEventRecord(ev_start, d2h));
@@ -635,6 +643,108 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   if ((st = ext_merge(ctx, rs, split, part_off, 0, P, out, perm_out, key_bytes, s, prof, tr))) return st;
   tr.report();
   return prof.end();
+}
+
+// ------------------------------------------------------------------------------- multi-GPU external
+// SURVEY.md §8e "External at 8 GPUs" (BASELINE.json configs[4] at 8 GPUs): every rank generates sorted runs
+// of its pinned host slice into a host run scratch that every rank can read (global record layout), the
+// samples of all runs are shared, every rank derives the same splitters and slice bounds, and rank r merges
+// the partitions that cover global sorted positions [floor(r N / G), floor((r+1) N / G)) — the boundary
+// partitions by both neighbours, each keeping its exact share — into its own output. No NVLink traffic:
+// the host link (and host DRAM) is the bound.
+ExtDistPlan ext_dist_plan(const std::vector<uint64_t>& n_local, uint64_t budget) {
+  ExtDistPlan P;
+  const int G = (int)n_local.size();
+  P.N = 0;
+  for (uint64_t v : n_local) P.N += v;
+  P.C = std::max<uint64_t>(1, external_run_records(P.N, budget));
+  P.S = external_sample_stride(P.N, P.C, budget);
+  P.gbase.assign(G, 0);
+  P.samp_off.assign(G + 1, 0);
+  uint64_t runs = 0;
+  for (int r = 0; r < G; ++r) {
+    P.gbase[r] = r ? P.gbase[r - 1] + n_local[r - 1] : 0;
+    uint64_t ns = 0;
+    for (uint64_t at = 0; at < n_local[r]; at += P.C) {
+      ns += (std::min<uint64_t>(P.C, n_local[r] - at) + P.S - 1) / P.S;
+      ++runs;
+    }
+    P.samp_off[r + 1] = P.samp_off[r] + ns;
+  }
+  P.n_local = n_local;
+  P.runs = runs;
+  P.q = ext_sample_q(external_merge_target(P.C, budget), P.S, std::max<uint64_t>(1, runs));
+  return P;
+}
+
+size_t ext_dist_device_bytes(const ExtDistPlan& P) { return phase1_bytes(P.C, std::max<uint64_t>(1, P.samp_off.back())); }
+
+namespace {
+RunSet ext_dist_runset(const ExtDistPlan& P, uint8_t* h_runs) {
+  RunSet rs;
+  rs.h_runs = h_runs;
+  for (size_t r = 0; r < P.n_local.size(); ++r)
+    for (uint64_t at = 0; at < P.n_local[r]; at += P.C) {
+      rs.off.push_back(P.gbase[r] + at);
+      rs.len.push_back(std::min<uint64_t>(P.C, P.n_local[r] - at));
+      rs.S.push_back(P.S);
+      rs.samp_base.push_back(rs.nsamp);
+      rs.nsamp += (rs.len.back() + P.S - 1) / P.S;
+    }
+  return rs;
+}
+}  // namespace
+
+uint8_t* ext_dist_samples(DeviceContext& ctx, const ExtDistPlan& P) {
+  return phase1_layout(static_cast<uint8_t*>(ctx.ext.ptr), P.C, std::max<uint64_t>(1, P.samp_off.back())).d_samp;
+}
+
+ley_status ext_dist_runs(DeviceContext& ctx, const ExtDistPlan& P, int rank, const uint8_t* in, uint8_t* h_runs,
+                         uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
+  ley_status st;
+  const uint64_t cap = std::max<uint64_t>(1, P.samp_off.back());
+  if ((st = ensure_buffer(ctx.ext, phase1_bytes(P.C, cap), "external buffers", s))) return st;
+  if ((st = ensure_copy_streams(ctx))) return st;
+  const Phase1 b = phase1_layout(static_cast<uint8_t*>(ctx.ext.ptr), P.C, cap);
+  RunSet rs;
+  rs.h_runs = h_runs;
+  rs.nsamp = P.samp_off[rank];  // this rank's samples land at their place in the run-ordered sample set
+  ExtTrace tr;
+  return ext_generate(ctx, in, P.n_local[rank], P.gbase[rank], P.C, P.S, rs, b, false, key_bytes, s, prof, tr);
+}
+
+ley_status ext_dist_partition(DeviceContext& ctx, const ExtDistPlan& P, uint8_t* h_runs, uint32_t key_bytes,
+                              cudaStream_t s, Profiler& prof, ExtDistParts& parts) {
+  RunSet rs = ext_dist_runset(P, h_runs);
+  LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&rs.h_runs_dev, h_runs, 0));
+  const Phase1 b = phase1_layout(static_cast<uint8_t*>(ctx.ext.ptr), P.C, std::max<uint64_t>(1, P.samp_off.back()));
+  return ext_partition(ctx, rs, b, P.q, key_bytes, s, prof, &parts.P, parts.split, parts.part_off);
+}
+
+ley_status ext_dist_merge(DeviceContext& ctx, const ExtDistPlan& P, const ExtDistParts& parts, int rank,
+                          uint8_t* h_runs, uint8_t* out, uint64_t cap, uint64_t* n_out, uint64_t* out_off,
+                          uint32_t key_bytes, cudaStream_t s, Profiler& prof) {
+  const int G = (int)P.n_local.size();
+  const uint64_t lo = (uint64_t)((unsigned __int128)rank * P.N / (unsigned)G);
+  const uint64_t hi = (uint64_t)((unsigned __int128)(rank + 1) * P.N / (unsigned)G);
+  *n_out = hi - lo;
+  *out_off = lo;
+  if (hi - lo > cap) {
+    set_error("dist external: rank " + std::to_string(rank) + " must hold " + std::to_string(hi - lo) +
+              " records but out_capacity_records is " + std::to_string(cap));
+    return LEY_ERR_CAPACITY;
+  }
+  if (hi == lo) return LEY_OK;
+  // partitions overlapping [lo, hi)
+  const auto& po = parts.part_off;
+  const uint32_t pb = (uint32_t)(std::upper_bound(po.begin(), po.end(), lo) - po.begin() - 1);
+  const uint32_t pe = (uint32_t)(std::lower_bound(po.begin(), po.end(), hi) - po.begin());
+  RunSet rs = ext_dist_runset(P, h_runs);
+  ley_status st = ensure_copy_streams(ctx);
+  if (st) return st;
+  ExtTrace tr;
+  return ext_merge(ctx, rs, parts.split, po, pb, std::min<uint32_t>(pe, parts.P), out, nullptr, key_bytes, s, prof, tr,
+                   lo, hi);
 }
 
 }  // namespace ley

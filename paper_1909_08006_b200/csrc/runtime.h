@@ -180,6 +180,31 @@ uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm);
 ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                               uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status ensure_copy_streams(DeviceContext& ctx);  // ctx.copy_stream[2] + ctx.ev (external / resident)
+
+// Multi-GPU external sort (external.cu): the plan every rank derives alike from the ranks'
+// slice sizes and the budget, the phases, and the partition set they share.
+struct ExtDistPlan {
+  uint64_t N = 0, C = 0, S = 1, q = 1, runs = 0;
+  std::vector<uint64_t> n_local, gbase, samp_off;  // samp_off[r]: rank r's first sample (run order)
+};
+struct ExtDistParts {
+  uint32_t P = 1;
+  std::vector<uint64_t> split, part_off;
+};
+ExtDistPlan ext_dist_plan(const std::vector<uint64_t>& n_local, uint64_t budget);
+size_t ext_dist_device_bytes(const ExtDistPlan& P);
+// a10 for one rank: its runs into h_runs (global layout, pinned + mapped), its samples into the ctx.ext
+// sample area at samp_off[rank]
+ley_status ext_dist_runs(DeviceContext& ctx, const ExtDistPlan& P, int rank, const uint8_t* in, uint8_t* h_runs,
+                         uint32_t key_bytes, cudaStream_t s, Profiler& prof);
+uint8_t* ext_dist_samples(DeviceContext& ctx, const ExtDistPlan& P);  // the sample area (all ranks' samples)
+// a11 once all runs are in h_runs and all samples in the sample area (identical on every rank)
+ley_status ext_dist_partition(DeviceContext& ctx, const ExtDistPlan& P, uint8_t* h_runs, uint32_t key_bytes,
+                              cudaStream_t s, Profiler& prof, ExtDistParts& parts);
+// a12 for one rank: global sorted positions [floor(r N/G), floor((r+1) N/G)) into out
+ley_status ext_dist_merge(DeviceContext& ctx, const ExtDistPlan& P, const ExtDistParts& parts, int rank,
+                          uint8_t* h_runs, uint8_t* out, uint64_t cap, uint64_t* n_out, uint64_t* out_off,
+                          uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint64_t n, uint32_t key_bytes,
                        cudaStream_t user);
 ley_status sort_drain(DeviceContext& ctx);

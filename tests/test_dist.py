@@ -130,8 +130,8 @@ def test_nccl_world_size_one(cuda_ok, exchange_mode, exchange_g1):
 @pytest.mark.gpu
 def test_nccl_pinned_host_slices(cuda_ok, exchange_mode):
     """ley_sort_dist with pinned host slices: staged on the device (H2D, the device path, D2H of the
-    rank's range), with the exchange phases on; a budget below slice + capacity is refused (all ranks
-    agree first, so none is left waiting in a collective)."""
+    rank's range), with the exchange phases on; under a budget below slice + capacity (all ranks agree
+    first) the external path runs instead and gives the same bytes."""
     import torch
 
     import paper_1909_08006_b200 as ley
@@ -146,16 +146,74 @@ def test_nccl_pinned_host_slices(cuda_ok, exchange_mode):
         n_out, off = ley.ley_sort_dist(comm, x, n, out, n)
         assert (n_out, off) == (n, 0)
         assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
-        with pytest.raises(ley.LeyendaError) as ei:
-            ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=n * 100)
-        assert ei.value.status == ley.LEY_ERR_UNSUPPORTED
-        # the communicator is still usable afterwards
+        # a budget below slice + capacity: the external path instead (same bytes)
         out.zero_()
-        assert ley.ley_sort_dist(comm, x, n, out, n) == (n, 0)
+        assert ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=n * 100) == (n, 0)
         assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
     finally:
         ley.ley_comm_destroy(comm)
         ley.ley_set_option("dist_exchange_g1", 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("dist", ["uniform", "skewed", "all_equal", "reverse"])
+def test_external_loopback(cuda_ok, G, dist):
+    """The multi-GPU EXTERNAL algorithm through the loopback: pinned host slices, a budget
+    that forces many runs per rank, every rank's runs in one shared scratch, one partition, and each rank
+    merging exactly floor((r+1)N/G) - floor(rN/G) records (boundary partitions merged by both neighbours,
+    clipped); the concatenation is the oracle's output."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    N = 300_007
+    recs = gen.records(N, seed=81 + G, dist=dist)
+    rng = np.random.default_rng(G)
+    cuts = np.sort(rng.integers(0, N, size=G - 1))
+    n_local = np.diff(np.concatenate([[0], cuts, [N]])).tolist()
+    if G > 2:
+        n_local[0] += n_local[1]  # an empty rank
+        n_local[1] = 0
+    ins, outs, at = [], [], 0
+    for r in range(G):
+        ins.append(torch.from_numpy(recs[at * 100:(at + n_local[r]) * 100].copy()).pin_memory()
+                   if n_local[r] else torch.empty(100, dtype=torch.uint8).pin_memory())
+        at += n_local[r]
+        outs.append(torch.empty((N // G + 2) * 100, dtype=torch.uint8).pin_memory())
+    res = ley.ley_sort_dist_loopback(ins, n_local, outs, [N // G + 2] * G, device_budget_bytes=12 << 20)
+    sizes, offs = _closed_form(N, G)
+    assert [x[0] for x in res] == sizes and [x[1] for x in res] == offs
+    got = np.concatenate([outs[r][: res[r][0] * 100].numpy() for r in range(G)])
+    assert np.array_equal(got, oracle.sort(recs)[0])
+
+
+@pytest.mark.gpu
+def test_nccl_external_world_one(cuda_ok):
+    """ley_sort_dist with pinned host slices whose staging exceeds the budget: the multi-GPU external path
+    at world size 1 (runs, sample broadcast, partition, the rank's merge), equal to the oracle; a budget
+    below its working set is refused (LEY_ERR_BUDGET) and the communicator stays usable."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    comm = ley.ley_comm_init(1, 0, ley.ley_comm_get_unique_id(), 0)
+    try:
+        n = 400_001
+        recs = gen.records(n, seed=85, dist="skewed")
+        x = torch.from_numpy(recs).pin_memory()
+        out = torch.empty_like(x).pin_memory()
+        n_out, off = ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=16 << 20)
+        assert (n_out, off) == (n, 0)
+        assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
+        with pytest.raises(ley.LeyendaError) as ei:
+            ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=1 << 20)
+        assert ei.value.status == ley.LEY_ERR_BUDGET
+        out.zero_()
+        assert ley.ley_sort_dist(comm, x, n, out, n, device_budget_bytes=24 << 20) == (n, 0)
+        assert np.array_equal(out.numpy(), oracle.sort(recs)[0])
+    finally:
+        ley.ley_comm_destroy(comm)
 
 
 # ----------------------------------------------------------------------------------------- CPU (gloo)
@@ -261,3 +319,55 @@ def test_gloo_two_ranks_host_logic(dist):
         p.join(timeout=240)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+def _shm_worker(rank, world, port, name, nbytes, q):
+    import ctypes
+
+    import torch.distributed as tdist
+
+    import paper_1909_08006_b200 as ley
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        if rank == 0:
+            addr = ley.ley_test_shared_scratch(name, nbytes, True)
+            buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+            for i in range(0, nbytes, 4099):  # rank 0's "runs"
+                buf[i] = (i * 7) & 0xFF
+        tdist.barrier()
+        if rank == 1:
+            addr = ley.ley_test_shared_scratch(name, nbytes, False)
+            buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+            ok = all(buf[i] == (i * 7) & 0xFF for i in range(0, nbytes, 4099))
+            buf[1] = 0xAB  # written by rank 1, seen by rank 0
+        tdist.barrier()
+        if rank == 0:
+            ok = buf[1] == 0xAB
+        ley.ley_test_shared_scratch_close(addr, nbytes, name if rank == 0 else None)
+        q.put((rank, ok))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_shared_run_scratch():
+    """The multi-GPU external path's shared host run scratch between two processes (host logic, CPU): rank 0
+    creates and fills it, rank 1 opens the same name and sees the bytes, writes of either are seen by the
+    other, and the name is removed afterwards."""
+    import torch.multiprocessing as mp
+
+    import paper_1909_08006_b200 as ley
+
+    name, nbytes = f"/ley-test-{os.getpid()}", 1 << 20
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shm_worker, args=(r, 2, port, name, nbytes, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sorted(q.get(timeout=10) for _ in range(2)) == [(0, True), (1, True)]
+    with pytest.raises(ley.LeyendaError):  # unlinked: opening it again fails
+        ley.ley_test_shared_scratch(name, nbytes, False)
