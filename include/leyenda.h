@@ -8,9 +8,10 @@
  *   "ley_sort(in, out, n_records, record_bytes=100, key_bytes=10, device_budget_bytes, stream)".
  *
  * RESULT (all entry points): the unique stable ascending arrangement out[j] = in[pi(j)] where pi orders
- * record ordinals by (key bytes 0..9 compared as unsigned bytes, most significant first; then ordinal).
+ * record ordinals by (key bytes [0, key_bytes) compared as unsigned bytes, most significant first; then
+ * ordinal). key_bytes = 10 is the paper's record format; 1..100 are its "flexible key sizes".
  * Ties keep input order (BJ north_star "stable tie order"). Output is bit-identical
- * across runs, budgets, thresholds/options and GPU counts.
+ * across runs, budgets, paths, thresholds/options and GPU counts.
  *
  * THREADING: calls on different devices may run concurrently; calls on the same device are serialised
  * by a per-device mutex. ley_last_error() is thread-local.
@@ -207,6 +208,8 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    SURVEY §8f NEXT 1), 0 = K-p into a local send buffer, then an NCCL all-to-all-v
  *   "dist_exchange_g1" 1 = run the splitter, partition and exchange phases even with one rank (tests the
  *                    exchange path on a single GPU), 0 = one rank sorts locally
+ *   "key_hybrid"     keys > 10 bytes: 1 = one 10-byte sort + comparison sort of the tie groups (P:164's
+ *                    hybrid), 0 = LSD passes over every 10-byte window
  *   "profile"        1 = record CUDA events around every stage (ley_stage_times)
  *   "ext_run_records" external path: force the run size (records; 0 = from the budget)
  *   "resident_path"  1 = host pointers may take path 2 (resident input, streamed output) when in + out
