@@ -131,6 +131,46 @@ def _oracle_step(recs, threads, key_bytes):
     return None
 
 
+def host_link_gbs(nbytes: int = 1 << 30, reps: int = 3):
+    """Pinned-memory copy-engine bandwidth of this GPU's host link (GB/s): H2D alone, D2H alone, and each
+    direction while both run (two streams) — the denominators of the host-path rooflines."""
+    import torch
+
+    h = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    d = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(reps):
+            e0.record()
+            fn()
+            torch.cuda.synchronize()  # (both side streams joined)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return nbytes / (best / 1e3) / 1e9
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d[0].copy_(h[0], non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            h[1].copy_(d[1], non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    out = {"h2d": round(timed(h2d), 1), "d2h": round(timed(d2h), 1), "bidir_each": round(timed(both), 1)}
+    del h, d
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline(cfg, sample_n: int, key_bytes: int = 10):
     """The oracle as it stands (oracle/), timed on this host's cores on a bounded sample."""
     import gen
@@ -308,6 +348,21 @@ def main():
                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dominant,
                     "alg_bytes_per_record": STAGE_ALG_BYTES[dominant], "peak_source": peak_src}
     step_roof_ms = 200 * n / (peak * 1e9) * 1e3
+    host_roofline = None
+    if external and rank == 0:
+        # host-link roofline (SURVEY §8d HOST_alg): the external path crosses the link twice in each direction
+        # (200 B/record per direction, the directions overlap); the resident path once each way, serially
+        link = host_link_gbs()
+        plan = ley.ley_plan_query(n, budget)
+        if plan["host_path"] == 2:
+            t_roof = 100 * n / (link["h2d"] * 1e9) + 100 * n / (link["d2h"] * 1e9)
+            model = "resident path: 100 B/record H2D then 100 B/record D2H (serial: the sort needs all input)"
+        else:
+            t_roof = 200 * n / (link["bidir_each"] * 1e9)
+            model = "external path: 200 B/record per direction, both directions at once"
+        host_roofline = {"bound": "host-link", "t_roof_ms": round(t_roof * 1e3, 1),
+                         "frac": round(t_roof * 1e3 / ms, 4), "link_gbs": link, "model": model,
+                         "note": "measured pinned copy-engine bandwidth of this box (host_link_gbs)"}
     step_roofline = {"alg_bytes_per_record": 200, "t_roof_ms": round(step_roof_ms, 3),
                      "frac": round(step_roof_ms / ms, 4), "peak": peak, "unit": "GB/s",
                      "note": "HBM term only" + (" (external: host-link bound, see DESIGN.md)" if external else "")}
@@ -402,7 +457,7 @@ def main():
                                        ("all-to-all-v" if args.alltoall else "fused partition+exchange") +
                                        (", exchange at G=1" if args.exchange else "") + ")")
                        if comm is not None else "1 GPU"},
-            "roofline": roofline, "step_roofline": step_roofline,
+            "roofline": roofline, "step_roofline": step_roofline, "host_roofline": host_roofline,
             "stages_ms": {k: round(v, 4) for k, v in avg.items()},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches,

@@ -1,12 +1,14 @@
-# Round measurement: GPU tests, bench lines C1-C5, ncu launch lists (C1-C4) and one --set full capture of
-# the dominant kernel at C2. Everything lands in gpurun_out/ (copied to profiles/ by hand).
+# Round measurement: GPU tests, bench lines C1-C7 (+ C2 with 20-byte keys), ncu launch lists (C1-C4) and
+# one --set full capture of the dominant kernels at C2. Everything lands in gpurun_out/ (copied to profiles/
+# by hand).
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > gpurun_out/smi.log
 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; echo "tests exit $?" >> gpurun_out/t.log
-for c in c2 c1 c3 c4 c5; do
-  extra=""; [ $c != c2 ] && extra="--no-e2e"; [ $c = c5 ] && extra="--no-e2e --steps 3"
+for c in c2 c1 c3 c4 c5 c6 c7; do
+  extra=""; [ $c != c2 ] && extra="--no-e2e"; [ $c = c5 ] || [ $c = c7 ] && extra="--steps 3"
   timeout 1200 python bench.py --config $c --warmup 3 $extra > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err
 done
+timeout 900 python bench.py --key-bytes 20 --no-e2e --warmup 3 > gpurun_out/b_c2_kb20.json 2> gpurun_out/b_c2_kb20.err
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
 for spec in "c1 1e6 uniform 0" "c2 1e8 uniform 1" "c3 2e8 skewed 2" "c4 6e8 uniform 3"; do
   set -- $spec
