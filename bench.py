@@ -333,7 +333,7 @@ def main():
     avg = {k: statistics.mean(v) for k, v in stage_ms.items()}
     roofline = None
     kern = [k for k in avg if k in STAGE_ALG_BYTES]
-    if kern:
+    if kern and not external:  # (host paths: the host link is the bound, host_roofline below)
         dominant = max(kern, key=lambda k: avg[k])
         alg = STAGE_ALG_BYTES[dominant] * n
         achieved = alg / (avg[dominant] / 1e3) / 1e9
