@@ -375,6 +375,7 @@ struct ley_comm {
   ncclWindow_t win = nullptr;
   uint8_t** d_peers = nullptr;
   ley::DeviceBuffer stage;  // pinned host slices: the device copy of this rank's input and output
+  int fused_ok = -1;        // fused exchange usable on this communicator (-1: not checked yet)
   uint64_t uid_hash = 0;    // names this communicator's shared host run scratch (external path)
   uint64_t ext_calls = 0;   // (the same count on every rank: calls are collective)
 };
@@ -614,9 +615,8 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   if ((st = prof.end()) || (st = prof.begin("D4 partition"))) return st;
   if ((st = phase5_plan(r, P))) return st;
   const uint8_t* recv = nullptr;
-  if (opts.dist_fused) {
-    // fused (SURVEY §8f NEXT 1): K-p stores each destination run straight into its owner's symmetric
-    // window over NVLink; one tiny all-reduce afterwards orders every rank's stores before any local sort
+  bool fused = opts.dist_fused && comm->fused_ok != 0;
+  if (fused) {
     uint64_t most = 0;
     for (int d = 0; d < G; ++d) {
       uint64_t in_d = 0;
@@ -624,6 +624,24 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       most = std::max(most, in_d);
     }
     if ((st = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s))) return st;
+    if (comm->fused_ok < 0) {
+      // every peer must be reachable through the window (one NVLink/NVSwitch domain); if any rank sees a
+      // null peer pointer, all ranks agree to use the all-to-all transport on this communicator
+      uint8_t* hp[kMaxRanks] = {};
+      LEY_CUDA("dist window", cudaMemcpy(hp, comm->d_peers, 8 * G, cudaMemcpyDeviceToHost));
+      uint64_t bad = 0;
+      for (int d = 0; d < G; ++d) bad += hp[d] == nullptr;
+      LEY_CUDA("dist window", cudaMemcpyAsync(d_tmp, &bad, 8, cudaMemcpyHostToDevice, s));
+      LEY_NCCL("dist window", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
+      LEY_CUDA("dist window", cudaMemcpyAsync(&bad, d_tmp, 8, cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("dist window", cudaStreamSynchronize(s));
+      comm->fused_ok = bad ? 0 : 1;
+      fused = comm->fused_ok == 1;
+    }
+  }
+  if (fused) {
+    // fused (SURVEY §8f NEXT 1): K-p stores each destination run straight into its owner's symmetric
+    // window over NVLink; one tiny all-reduce afterwards orders every rank's stores before any local sort
     uint64_t dst_off[kMaxRanks];
     dist_dest_offsets(P.send_matrix.data(), G, r.rank, dst_off);
     if (r.n && (st = phase5_partition(r, P, nullptr, comm->d_peers, dst_off, G > 1))) return st;
