@@ -774,13 +774,7 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
   const std::string name = "/ley-" + std::to_string(comm->uid_hash) + "-" + std::to_string(comm->ext_calls++);
   uint8_t* h_runs = nullptr;
   if (G == 1) {
-    if (ctx.host_scratch_cap < bytes) {
-      if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
-      ctx.host_scratch = nullptr;
-      ctx.host_scratch_cap = 0;
-      LEY_CUDA("dist external", cudaHostAlloc(&ctx.host_scratch, bytes, cudaHostAllocMapped));
-      ctx.host_scratch_cap = bytes;
-    }
+    if (ley_status hs = ensure_host_scratch(ctx, bytes)) return hs;
     h_runs = static_cast<uint8_t*>(ctx.host_scratch);
   } else if (rank == 0) {
     err = shared_scratch_open(name, bytes, true, sh);
@@ -929,18 +923,12 @@ ley_status dist_external_loopback(int G, const void* const* in, const uint64_t* 
     return LEY_ERR_BUDGET;
   }
   const size_t bytes = std::max<size_t>((size_t)P.N * kRecordBytes, 4096);
-  if (ctx.host_scratch_cap < bytes) {
-    if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
-    ctx.host_scratch = nullptr;
-    ctx.host_scratch_cap = 0;
-    LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_scratch, bytes, cudaHostAllocMapped));
-    ctx.host_scratch_cap = bytes;
-  }
+  ley_status st = ensure_host_scratch(ctx, bytes);
+  if (st) return st;
   uint8_t* h_runs = static_cast<uint8_t*>(ctx.host_scratch);
   Profiler quiet;
   quiet.ctx = &ctx;
   quiet.stream = s;
-  ley_status st;
   for (int r = 0; r < G; ++r)
     if ((st = ext_dist_runs(ctx, P, r, static_cast<const uint8_t*>(in[r]), h_runs, key_bytes, s, quiet))) return st;
   LEY_CUDA("loopback", cudaStreamSynchronize(s));

@@ -583,6 +583,9 @@ uint64_t ext_sample_q(uint64_t m_target, uint64_t S, uint64_t R) {
   return q ? q : 1;
 }
 
+}  // namespace
+
+// Pinned, mapped host run scratch of the external paths (grow-only; freed by ley_release_cache).
 ley_status ensure_host_scratch(DeviceContext& ctx, size_t bytes) {
   if (ctx.host_scratch_cap >= bytes) return LEY_OK;
   if (ctx.host_scratch) cudaFreeHost(ctx.host_scratch);
@@ -592,8 +595,6 @@ ley_status ensure_host_scratch(DeviceContext& ctx, size_t bytes) {
   ctx.host_scratch_cap = bytes;
   return LEY_OK;
 }
-
-}  // namespace
 
 // ---------------------------------------------------------------------------------------- driver
 ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,

@@ -180,6 +180,7 @@ uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm);
 ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                               uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status ensure_copy_streams(DeviceContext& ctx);  // ctx.copy_stream[2] + ctx.ev (external / resident)
+ley_status ensure_host_scratch(DeviceContext& ctx, size_t bytes);  // ctx.host_scratch (external.cu)
 
 // Multi-GPU external sort (external.cu): the plan every rank derives alike from the ranks'
 // slice sizes and the budget, the phases, and the partition set they share.
