@@ -39,6 +39,7 @@ const OptDesc kOpts[] = {
     {"key_hybrid", &Options::key_hybrid, 0, 1},
     {"resident_path", &Options::resident_path, 0, 1},
     {"resident_chunk_records", &Options::resident_chunk_records, 0, (int64_t)0xFFFFFFFEll},
+    {"pipe_split", &Options::pipe_split, 1, DeviceContext::Pipe::kParts},
     {"dist_fused", &Options::dist_fused, 0, 1},
     {"dist_exchange_g1", &Options::dist_exchange_g1, 0, 1},
     {"profile", &Options::profile, 0, 1},

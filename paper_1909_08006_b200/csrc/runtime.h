@@ -48,6 +48,7 @@ struct Options {
   int64_t key_hybrid = 1;         // keys > 10 bytes: 10-byte sort + tie-group fix-up (0: LSD windows always)
   int64_t resident_path = 1;        // host pointers: allow path 2 (resident input, streamed output)
   int64_t resident_chunk_records = 0;  // path 2 output window (records; 0 = 2^21)
+  int64_t pipe_split = 2;          // ley_sort_submit: each copy in this many pieces on their own streams
   int64_t dist_fused = 1;        // K-p stores into peers' NCCL symmetric windows (0: send buffer + all-to-all)
   int64_t dist_exchange_g1 = 0;  // run splitters/partition/exchange even when G == 1 (test hook)
   int64_t profile = 0;
@@ -114,9 +115,13 @@ struct DeviceContext {
       uint8_t* out;
       uint64_t n;
       uint32_t key_bytes;
+      int parts;
     };
     bool init = false;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    static constexpr int kParts = 4;  // copies split into up to kParts pieces on their own streams
+    cudaStream_t h2d_x[kParts - 1] = {}, d2h_x[kParts - 1] = {};
+    cudaEvent_t part_in[kParts - 1] = {}, part_out[kParts - 1] = {};
     DeviceBuffer slot[2];
     cudaEvent_t user = nullptr;
     cudaEvent_t copied_in[2] = {nullptr, nullptr}, sorted[2] = {nullptr, nullptr}, copied_out[2] = {nullptr, nullptr};

@@ -100,9 +100,20 @@ void worker_main(DeviceContext* ctx) {
       if (!st && (e = cudaEventRecord(P.sorted[s], P.comp)) != cudaSuccess) fail("submit sort", e);
       if (!st && (e = cudaStreamWaitEvent(P.d2h, P.sorted[s], 0)) != cudaSuccess) fail("submit D2H", e);
       g_trace.mark((uint64_t)(6 * job.k + 4), P.d2h);
-      if (!st && (e = cudaMemcpyAsync(job.out, job.dout, job.n * kRecordBytes, cudaMemcpyDeviceToHost, P.d2h)) !=
-                     cudaSuccess)
+      // the output in job.parts pieces, piece q > 0 on its own stream, all joined back into d2h
+      const size_t bytes = job.n * kRecordBytes;
+      const size_t piece = job.parts > 1 ? (bytes / job.parts) & ~size_t(255) : bytes;
+      for (int q = 1; q < job.parts && !st; ++q) {
+        const size_t o = q * piece, len = q + 1 < job.parts ? piece : bytes - o;
+        if ((e = cudaStreamWaitEvent(P.d2h_x[q - 1], P.sorted[s], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(job.out + o, job.dout + o, len, cudaMemcpyDeviceToHost, P.d2h_x[q - 1])) != cudaSuccess ||
+            (e = cudaEventRecord(P.part_out[q - 1], P.d2h_x[q - 1])) != cudaSuccess)
+          fail("submit D2H", e);
+      }
+      if (!st && (e = cudaMemcpyAsync(job.out, job.dout, piece, cudaMemcpyDeviceToHost, P.d2h)) != cudaSuccess)
         fail("submit D2H", e);
+      for (int q = 1; q < job.parts && !st; ++q)
+        if ((e = cudaStreamWaitEvent(P.d2h, P.part_out[q - 1], 0)) != cudaSuccess) fail("submit D2H", e);
       g_trace.mark((uint64_t)(6 * job.k + 5), P.d2h);
       if (!st && (e = cudaEventRecord(P.copied_out[s], P.d2h)) != cudaSuccess) fail("submit D2H", e);
     }
@@ -141,6 +152,9 @@ void pipe_release(DeviceContext& c) {
   if (P.worker.joinable()) P.worker.join();
   for (cudaStream_t st : {P.h2d, P.comp, P.d2h})
     if (st) cudaStreamSynchronize(st);
+  for (int q = 0; q < DeviceContext::Pipe::kParts - 1; ++q)
+    for (cudaStream_t st : {P.h2d_x[q], P.d2h_x[q]})
+      if (st) cudaStreamSynchronize(st);
   for (int i = 0; i < 2; ++i) {
     if (P.slot[i].ptr) {
       cudaFree(P.slot[i].ptr);
@@ -153,11 +167,21 @@ void pipe_release(DeviceContext& c) {
     }
   }
   if (P.user) cudaEventDestroy(P.user);
+  P.user = nullptr;
   for (cudaStream_t* st : {&P.h2d, &P.comp, &P.d2h}) {
     if (*st) cudaStreamDestroy(*st);
     *st = nullptr;
   }
-  P.user = nullptr;
+  for (int q = 0; q < DeviceContext::Pipe::kParts - 1; ++q) {
+    for (cudaStream_t* st : {&P.h2d_x[q], &P.d2h_x[q]}) {
+      if (*st) cudaStreamDestroy(*st);
+      *st = nullptr;
+    }
+    for (cudaEvent_t* e : {&P.part_in[q], &P.part_out[q]}) {
+      if (*e) cudaEventDestroy(*e);
+      *e = nullptr;
+    }
+  }
   P.submitted = P.sort_done = 0;
   P.q.clear();
   P.stop = P.busy = false;
@@ -174,6 +198,12 @@ ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint
   if (!P.init) {
     for (cudaStream_t* st : {&P.h2d, &P.comp, &P.d2h})
       LEY_CUDA("submit", cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (int q = 0; q < DeviceContext::Pipe::kParts - 1; ++q) {
+      LEY_CUDA("submit", cudaStreamCreateWithFlags(&P.h2d_x[q], cudaStreamNonBlocking));
+      LEY_CUDA("submit", cudaStreamCreateWithFlags(&P.d2h_x[q], cudaStreamNonBlocking));
+      LEY_CUDA("submit", cudaEventCreateWithFlags(&P.part_in[q], cudaEventDisableTiming));
+      LEY_CUDA("submit", cudaEventCreateWithFlags(&P.part_out[q], cudaEventDisableTiming));
+    }
     LEY_CUDA("submit", cudaEventCreateWithFlags(&P.user, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i)
       for (cudaEvent_t* e : {&P.copied_in[i], &P.sorted[i], &P.copied_out[i]})
@@ -202,10 +232,21 @@ ley_status sort_submit(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint
   if (k >= 2) LEY_CUDA("submit H2D", cudaStreamWaitEvent(P.h2d, P.sorted[s], 0));
   g_trace.reserve(k);
   g_trace.mark((uint64_t)(6 * k + 0), P.h2d);
-  LEY_CUDA("submit H2D", cudaMemcpyAsync(din, in, bytes, cudaMemcpyHostToDevice, P.h2d));
+  // the input in `parts` pieces, piece q > 0 on its own stream, all joined back into h2d
+  const int parts = (int)options_snapshot().pipe_split;
+  const size_t piece = parts > 1 ? (bytes / parts) & ~size_t(255) : bytes;
+  for (int q = 1; q < parts; ++q) {
+    const size_t o = q * piece, len = q + 1 < parts ? piece : bytes - o;
+    LEY_CUDA("submit H2D", cudaStreamWaitEvent(P.h2d_x[q - 1], P.user, 0));
+    if (k >= 2) LEY_CUDA("submit H2D", cudaStreamWaitEvent(P.h2d_x[q - 1], P.sorted[s], 0));
+    LEY_CUDA("submit H2D", cudaMemcpyAsync(din + o, in + o, len, cudaMemcpyHostToDevice, P.h2d_x[q - 1]));
+    LEY_CUDA("submit H2D", cudaEventRecord(P.part_in[q - 1], P.h2d_x[q - 1]));
+  }
+  LEY_CUDA("submit H2D", cudaMemcpyAsync(din, in, piece, cudaMemcpyHostToDevice, P.h2d));
+  for (int q = 1; q < parts; ++q) LEY_CUDA("submit H2D", cudaStreamWaitEvent(P.h2d, P.part_in[q - 1], 0));
   g_trace.mark((uint64_t)(6 * k + 1), P.h2d);
   LEY_CUDA("submit H2D", cudaEventRecord(P.copied_in[s], P.h2d));
-  P.q.push_back(DeviceContext::Pipe::Job{k, din, dout, out, n, key_bytes});
+  P.q.push_back(DeviceContext::Pipe::Job{k, din, dout, out, n, key_bytes, parts});
   P.submitted = k + 1;
   lk.unlock();
   P.cv.notify_all();
@@ -218,6 +259,10 @@ ley_status sort_drain(DeviceContext& ctx) {
   if (!P.init) return LEY_OK;
   P.cv.wait(lk, [&] { return P.q.empty() && !P.busy; });
   for (cudaStream_t st : {P.h2d, P.comp, P.d2h}) LEY_CUDA("drain", cudaStreamSynchronize(st));
+  for (int q = 0; q < DeviceContext::Pipe::kParts - 1; ++q) {
+    LEY_CUDA("drain", cudaStreamSynchronize(P.h2d_x[q]));
+    LEY_CUDA("drain", cudaStreamSynchronize(P.d2h_x[q]));
+  }
   LEY_CUDA("drain", cudaGetLastError());
   g_trace.dump();
   return take_error(P);
