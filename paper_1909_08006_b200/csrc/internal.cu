@@ -142,7 +142,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     size_t r_nch = 0, r_cst = a256(4ull * (nbig + 1)), r_hist = r_cst + a256(4ull * (nbig + 1));
     size_t r_excl = r_hist + a256(4ull * nbig * kRadix), r_nos = r_excl + a256(4ull * nbig * kRadix);
     size_t r_scan = r_nos + a256(nbig);
-    size_t r_tick = r_scan + a256(8 * scan_words), r_end = r_tick + 256;
+    size_t r_tick = r_scan + a256(8 * scan_words), r_map = r_tick + 256, r_end = r_map + a256(8 * chunks_ub);
     if ((st = ensure_buffer(ctx.rec, r_end, "recursion arrays", s))) return st;
     if (child_cap > kd.cap) {
       if ((st = ensure_buffer(ctx.lists, (size_t)kNumKdLists * a256(child_cap * sizeof(Seg)), "K-d lists", s)))
@@ -160,6 +160,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     uint8_t* noscatter = rb + r_nos;
     uint64_t* rscan = reinterpret_cast<uint64_t*>(rb + r_scan);
     uint32_t* rtick = reinterpret_cast<uint32_t*>(rb + r_tick);
+    uint2* cmap = reinterpret_cast<uint2*>(rb + r_map);
     const Seg* segs = static_cast<const Seg*>(ctx.big[cur].ptr);
     Seg* next_big = static_cast<Seg*>(ctx.big[cur ^ 1].ptr);
 
@@ -172,12 +173,13 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     LEY_CUDA("K-c' recursion", launch_kr_nchunks(segs, nbig, nch, s));
     LEY_CUDA("K-c' recursion", launch_scan_excl(nch, cst, nbig, rscan, rtick + 0, cst + nbig, s));
     uint32_t hist_grid = (uint32_t)std::min<uint64_t>(chunks_ub, (uint64_t)sms * 8);
-    LEY_CUDA("K-c' recursion", launch_kr_hist(segs, nbig, cst, hist_grid, At, Ai, Bt, Bi, seg_hist, s));
+    LEY_CUDA("K-c' recursion", launch_kr_chunk_map(cst, nbig, (uint32_t)chunks_ub, cmap, s));
+    LEY_CUDA("K-c' recursion", launch_kr_hist(segs, nbig, cst, hist_grid, At, Ai, Bt, Bi, seg_hist, cmap, s));
     LEY_CUDA("K-c' recursion",
              launch_kr_plan(segs, nbig, seg_hist, seg_excl, noscatter, tu, kd, next_big, big_count, s));
-    LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rtick + 1,
+    LEY_CUDA("K-c' recursion", launch_kr_split(segs, nbig, cst, seg_excl, noscatter, At, Ai, Bt, Bi, rtick + 1, cmap,
                                               (uint32_t)chunks_ub, s));
-    launches += 5;
+    launches += 6;
     if ((st = prof.end())) return st;
     if ((st = prof.begin("K-de sort+gather"))) return st;
     LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));

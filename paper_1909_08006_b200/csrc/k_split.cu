@@ -125,32 +125,50 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
   const uint32_t total = cstart[256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // persistent: thread 0 claims a ticket (= chunk id, handed out in order) whenever the CTA is free, so
-  // every chunk a chunk waits on in its look-back is already owned by a running CTA.
-  while (true) {
-    if (threadIdx.x == 0) {
-      const uint32_t k = atomicAdd(ticket, 1u);
-      s_misc[32] = k;
-      if (k < total) {
-        const uint32_t kk = order ? order[k] : k;
-        uint4 pa = plan_a[kk];
-        uint2 pb = plan_b[kk];
-        s_misc[33] = pa.x;
-        s_misc[34] = pa.y;
-        s_misc[35] = pa.z;
-        s_misc[38] = pa.w;
-        s_misc[36] = pb.x;
-        s_misc[37] = pb.y;
-      }
+  // persistent: chunks are claimed by ticket (thread 0), one chunk ahead — the next ticket and its plan are
+  // fetched while the current chunk is processed, and every thread prefetches its entry of the next chunk's
+  // run table during the write-out, so neither latency sits between chunks (no look-back: any order works).
+  if (threadIdx.x == 0) {  // the first chunk
+    const uint32_t k = atomicAdd(ticket, 1u);
+    s_misc[40] = k;
+    if (k < total) {
+      const uint32_t kk = order ? order[k] : k;
+      const uint4 pa = plan_a[kk];
+      const uint2 pb = plan_b[kk];
+      s_misc[41] = pa.x;
+      s_misc[42] = pa.y;
+      s_misc[43] = pa.z;
+      s_misc[46] = pa.w;
+      s_misc[44] = pb.x;
+      s_misc[45] = pb.y;
     }
-    __syncthreads();
-    const uint32_t k = s_misc[32];
+  }
+  __syncthreads();
+  uint32_t pf_vs = 0, pf_lo = 0;  // this thread's run-table entry of the current chunk, if prefetched
+  bool pf = false;
+  while (true) {
+    const uint32_t k = s_misc[40];
     if (k >= total) return;
-    const uint32_t b = s_misc[33], v0 = s_misc[34], cnt = s_misc[35], t0 = s_misc[36], t1 = s_misc[37];
-    const uint32_t k0 = s_misc[38];
+    const uint32_t b = s_misc[41], v0 = s_misc[42], cnt = s_misc[43], t0 = s_misc[44], t1 = s_misc[45];
     const uint32_t R = t1 - t0 + 1;
     const uint32_t* off_b = off + (uint64_t)b * tiles;
     const bool table = R <= kMaxRuns / 2;
+    __syncthreads();  // everyone has the plan: thread 0 may fetch the next one into s_misc[40..46]
+    uint32_t nxt[7];
+    if (threadIdx.x == 0) {  // issued now, stored to shared memory once the chunk's run table is dead
+      nxt[0] = atomicAdd(ticket, 1u);
+      if (nxt[0] < total) {
+        const uint32_t kk = order ? order[nxt[0]] : nxt[0];
+        const uint4 pa = plan_a[kk];
+        const uint2 pb = plan_b[kk];
+        nxt[1] = pa.x;
+        nxt[2] = pa.y;
+        nxt[3] = pa.z;
+        nxt[6] = pa.w;
+        nxt[4] = pb.x;
+        nxt[5] = pb.y;
+      }
+    }
     uint32_t src[kItems];  // position of each element in K-a's output
     if (table) {
       // run table (virtual start, source base: src = base + v) and run-start marks; an inclusive
@@ -158,9 +176,16 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       uint16_t* s_mark = reinterpret_cast<uint16_t*>(s_off + kMaxRuns / 2);
       for (uint32_t e = threadIdx.x; e < cnt; e += kThreads) s_mark[e] = 0;
       for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
-        const uint32_t vs = off_b[t0 + i];
+        uint32_t vs, lv;
+        if (pf && i == threadIdx.x) {
+          vs = pf_vs;
+          lv = pf_lo;
+        } else {
+          vs = off_b[t0 + i];
+          lv = lo[(uint64_t)(t0 + i) * kRadix + b];
+        }
         s_off[i] = vs;
-        s_lo[i] = ((t0 + i) << kTileLog2) + lo[(uint64_t)(t0 + i) * kRadix + b] - vs;
+        s_lo[i] = ((t0 + i) << kTileLog2) + lv - vs;
       }
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < R; i += kThreads) {
@@ -217,6 +242,11 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       dig[j] = (uint32_t)(k1[j] >> 56);
     }
     __syncthreads();  // run tables dead from here on
+    if (threadIdx.x == 0) {
+      s_misc[40] = nxt[0];
+      if (nxt[0] < total)
+        for (int q = 1; q < 7; ++q) s_misc[40 + q] = nxt[q];
+    }
 
     uint32_t pos[kItems], total_d, excl_d;
         block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
@@ -236,12 +266,25 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       }
     }
     __syncthreads();
+    // the next chunk's plan is in s_misc[40..46]: prefetch this thread's run-table entry while writing
+    pf = false;
+    {
+      const uint32_t kn = s_misc[40];
+      if (kn < total) {
+        const uint32_t bn = s_misc[41], tn0 = s_misc[44], Rn = s_misc[45] - tn0 + 1;
+        if (Rn <= kMaxRuns / 2 && threadIdx.x < Rn) {
+          pf_vs = off[(uint64_t)bn * tiles + tn0 + threadIdx.x];
+          pf_lo = lo[(uint64_t)(tn0 + threadIdx.x) * kRadix + bn];
+          pf = true;
+        }
+      }
+    }
     for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
       uint32_t g = s_dst[s_dig[i]] + i;
       tail_out[g] = s_tail[i];
       idx_out[g] = s_idx[i];
     }
-    __syncthreads();  // staging and s_misc reused by the next chunk
+    __syncthreads();  // staging reused by the next chunk
   }
 }
 
@@ -267,18 +310,27 @@ __global__ void kr_nchunks(const Seg* __restrict__ segs, uint32_t nseg, uint32_t
   if (s < nseg) nch[s] = (segs[s].len + kChunk - 1) / kChunk;
 }
 
+// chunk -> (segment, chunk inside it), one thread per chunk: the binary searches run in parallel here
+// instead of one dependent chain of global loads per chunk inside kr_hist / kr_split
+__global__ void kr_chunk_map(const uint32_t* __restrict__ cstart, uint32_t nseg, uint32_t ub, uint2* __restrict__ map) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= ub || k >= cstart[nseg]) return;
+  const uint32_t s = chunk_segment(cstart, nseg, k);
+  map[k] = make_uint2(s, k - cstart[s]);
+}
+
 __global__ void __launch_bounds__(256)
     kr_hist(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart, uint32_t nchunks_total_ub,
             const uint64_t* __restrict__ tails0, const uint32_t* __restrict__ idx0, const uint64_t* __restrict__ tails1,
-            const uint32_t* __restrict__ idx1, uint32_t* __restrict__ seg_hist) {
+            const uint32_t* __restrict__ idx1, uint32_t* __restrict__ seg_hist, const uint2* __restrict__ map) {
   __shared__ uint32_t h[kRadix];
   const uint32_t total = cstart[nseg];
   for (uint32_t k = blockIdx.x; k < total; k += gridDim.x) {
     h[threadIdx.x] = 0;
     __syncthreads();
-    uint32_t s = chunk_segment(cstart, nseg, k);
+    const uint2 m = map[k];
+    const uint32_t s = m.x, c = m.y;
     Seg sg = segs[s];
-    uint32_t c = k - cstart[s];
     uint32_t beg = c * kChunk, end = min(sg.len, beg + kChunk);
     if (sg.depth < 10) {
       const uint64_t* t = (sg.parity ? tails1 : tails0) + sg.start;
@@ -322,7 +374,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
     kr_split(const Seg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ cstart,
              uint32_t* __restrict__ cursor, const uint8_t* __restrict__ noscatter, uint64_t* tails0, uint32_t* idx0,
-             uint64_t* tails1, uint32_t* idx1, uint32_t* __restrict__ ticket) {
+             uint64_t* tails1, uint32_t* idx1, uint32_t* __restrict__ ticket, const uint2* __restrict__ map) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_tail + kChunk);
@@ -332,21 +384,38 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
   uint32_t* s_misc = s_dst + 256;
   const uint32_t total = cstart[nseg];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  while (true) {
-    if (threadIdx.x == 0) {
-      uint32_t k = atomicAdd(ticket, 1u);
-      s_misc[32] = k;
-      if (k < total) {
-        uint32_t s = chunk_segment(cstart, nseg, k);
-        s_misc[33] = s;
-        s_misc[34] = k - cstart[s];
-      }
+  // chunks claimed one ahead (as in kc_split_level1): thread 0 fetches the next ticket and its map entry
+  // while this chunk is processed
+  if (threadIdx.x == 0) {
+    const uint32_t k = atomicAdd(ticket, 1u);
+    s_misc[40] = k;
+    if (k < total) {
+      const uint2 m = map[k];
+      s_misc[41] = m.x;
+      s_misc[42] = m.y;
     }
-    __syncthreads();
-    const uint32_t k = s_misc[32];
+  }
+  __syncthreads();
+  while (true) {
+    const uint32_t k = s_misc[40];
     if (k >= total) return;
-    const uint32_t s = s_misc[33], c = s_misc[34];
+    const uint32_t s = s_misc[41], c = s_misc[42];
+    __syncthreads();  // everyone has the chunk: thread 0 may claim the next
+    uint32_t nk = 0;
+    uint2 nm = make_uint2(0, 0);
+    if (threadIdx.x == 0) {
+      nk = atomicAdd(ticket, 1u);
+      if (nk < total) nm = map[nk];
+    }
+    auto publish_next = [&]() {
+      if (threadIdx.x == 0) {
+        s_misc[40] = nk;
+        s_misc[41] = nm.x;
+        s_misc[42] = nm.y;
+      }
+    };
     if (noscatter[s]) {
+      publish_next();
       __syncthreads();
       continue;
     }
@@ -374,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
     }
     uint32_t pos[kItems], total_d, excl_d;
         block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+    publish_next();  // (read after the barrier below, at the top of the next iteration)
     if (threadIdx.x < kRadix) {
       const int d = threadIdx.x;
       const uint32_t base = total_d ? atomicAdd(&cursor[(uint64_t)s * kRadix + d], total_d) : 0u;
@@ -440,10 +510,15 @@ cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cud
   return cudaGetLastError();
 }
 
+cudaError_t launch_kr_chunk_map(const uint32_t* cstart, uint32_t nseg, uint32_t ub, uint2* map, cudaStream_t s) {
+  kr_chunk_map<<<(ub + 255) / 256, 256, 0, s>>>(cstart, nseg, ub, map);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
                            const uint64_t* tails0, const uint32_t* idx0, const uint64_t* tails1, const uint32_t* idx1,
-                           uint32_t* seg_hist, cudaStream_t s) {
-  kr_hist<<<grid, 256, 0, s>>>(segs, nseg, cstart, grid, tails0, idx0, tails1, idx1, seg_hist);
+                           uint32_t* seg_hist, const uint2* map, cudaStream_t s) {
+  kr_hist<<<grid, 256, 0, s>>>(segs, nseg, cstart, grid, tails0, idx0, tails1, idx1, seg_hist, map);
   return cudaGetLastError();
 }
 
@@ -456,7 +531,7 @@ cudaError_t launch_kr_plan(const Seg* segs, uint32_t nseg, const uint32_t* seg_h
 
 cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t* cursor,
                             const uint8_t* noscatter, uint64_t* tails0, uint32_t* idx0, uint64_t* tails1,
-                            uint32_t* idx1, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s) {
+                            uint32_t* idx1, uint32_t* ticket, const uint2* map, uint32_t grid_ub, cudaStream_t s) {
   size_t smem = SplitSmem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kr_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -467,7 +542,8 @@ cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* csta
   if (e != cudaSuccess) return e;
   uint32_t grid = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
   if (grid > grid_ub) grid = grid_ub;
-  kr_split<<<grid, kThreads, smem, s>>>(segs, nseg, cstart, cursor, noscatter, tails0, idx0, tails1, idx1, ticket);
+  kr_split<<<grid, kThreads, smem, s>>>(segs, nseg, cstart, cursor, noscatter, tails0, idx0, tails1, idx1, ticket,
+                                        map);
   return cudaGetLastError();
 }
 

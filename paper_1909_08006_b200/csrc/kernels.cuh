@@ -37,15 +37,16 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s);
 cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
+cudaError_t launch_kr_chunk_map(const uint32_t* cstart, uint32_t nseg, uint32_t ub, uint2* map, cudaStream_t s);
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
                            const uint64_t* tails0, const uint32_t* idx0, const uint64_t* tails1, const uint32_t* idx1,
-                           uint32_t* seg_hist, cudaStream_t s);
+                           uint32_t* seg_hist, const uint2* map, cudaStream_t s);
 cudaError_t launch_kr_plan(const Seg* segs, uint32_t nseg, const uint32_t* seg_hist, uint32_t* seg_excl,
                            uint8_t* noscatter, const Tunables& tu, const ListSet& kd, Seg* big_out,
                            uint32_t* big_count, cudaStream_t s);
 cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t* cursor,
                             const uint8_t* noscatter, uint64_t* tails0, uint32_t* idx0, uint64_t* tails1,
-                            uint32_t* idx1, uint32_t* ticket, uint32_t grid_ub, cudaStream_t s);
+                            uint32_t* idx1, uint32_t* ticket, const uint2* map, uint32_t grid_ub, cudaStream_t s);
 
 // K-d (k_bucket.cu)
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,

@@ -174,11 +174,12 @@ uint64_t external_run_records(uint64_t n, uint64_t budget) {
 
 // Device bytes the internal path holds outside its workspace: the K-d work lists (6 tiers of 16-byte
 // bucket descriptors, level 1: one per 16-bit bucket; deeper levels: at most 256 children of each of the
-// <= n / 16385 big buckets), the big-bucket lists and the recursion arrays (each at least 1 MB).
+// <= n / 16385 big buckets), the big-bucket lists and the recursion arrays (each at least 1 MB): per big
+// bucket 2 x 256 u32 histograms/cursors (<= n / 8 bytes) plus per-chunk and per-bucket words (<= n / 256).
 uint64_t internal_aux_bytes(uint64_t n) {
   const uint64_t buckets = std::max<uint64_t>(std::min<uint64_t>(65536, n), n / 64 + 1);
   return (uint64_t)kNumKdListsHost * align256(16 * buckets) + 2 * std::max<uint64_t>(1 << 20, 16 * (n / 16385 + 1)) +
-         std::max<uint64_t>(1 << 20, n / 8 + (64 << 10));
+         std::max<uint64_t>(1 << 20, n / 8 + n / 256 + (64 << 10));
 }
 
 ley_status ensure_copy_streams(DeviceContext& ctx) {
