@@ -27,13 +27,27 @@ __global__ void __launch_bounds__(kScanThreads)
   const uint32_t blk = s_blk;
   const uint64_t base = (uint64_t)blk * kScanTile + (uint64_t)threadIdx.x * kScanItems;
 
+  // each thread's kScanItems consecutive words as 16-byte vectors (base is a multiple of 16 words)
+  static_assert(kScanItems % 4 == 0, "vector loads");
   uint32_t v[kScanItems];
   uint32_t sum = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+                   base + kScanItems <= m;
+  if (vec) {
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = (base + i < m) ? in[base + i] : 0u;
-    sum += v[i];
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(in + base) + q);
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < m) ? in[base + i] : 0u;
   }
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) sum += v[i];
   uint32_t agg;
   uint32_t texcl = block_excl_scan<kScanThreads>(sum, s_tmp, &agg);
 
@@ -59,10 +73,26 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   __syncthreads();
   uint32_t run = s_prefix + texcl;
+  if (vec) {
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < m) out[base + i] = run;
-    run += v[i];
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      uint4 x;
+      x.x = run;
+      run += v[4 * q];
+      x.y = run;
+      run += v[4 * q + 1];
+      x.z = run;
+      run += v[4 * q + 2];
+      x.w = run;
+      run += v[4 * q + 3];
+      reinterpret_cast<uint4*>(out + base)[q] = x;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      if (base + i < m) out[base + i] = run;
+      run += v[i];
+    }
   }
 }
 
