@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kPartThreads)
                  uint64_t* __restrict__ status, uint32_t* __restrict__ ticket, int remote, DistKeyMask km) {
   extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* s_rec = s_dyn;                                 // tile in input order
-  uint32_t* s_out = s_dyn + kPartTile * kRecordWords;      // tile in destination order
+  __shared__ uint16_t s_inv[kPartTile];                    // destination-ordered slot p holds record s_inv[p]
+  __shared__ uint8_t s_slot_d[kPartTile];                  // and goes to destination s_slot_d[p]
   __shared__ DistSplitter s_spl[kMaxRanks - 1];
   __shared__ uint32_t s_wc[kPartThreads / 32][kMaxRanks];
   __shared__ uint32_t s_dcnt[kMaxRanks], s_dex[kMaxRanks];
@@ -265,22 +266,19 @@ __global__ void __launch_bounds__(kPartThreads)
     s_dst[k] = dst_off[k] + pre;
     s_dptr[k] = dst_base[k];
   }
-  // stage in destination order
+  // destination order as a slot map (no second copy of the tile: half the shared memory, twice the CTAs
+  // per SM), then every destination run written as a coalesced word stream straight from the input tile
   if (valid) {
     const uint32_t p = s_dex[d] + s_wc[warp][d] + before;
-    const uint32_t* srcr = s_rec + i * kRecordWords;
-    uint32_t* dstr = s_out + p * kRecordWords;
-#pragma unroll
-    for (int w = 0; w < (int)kRecordWords; ++w) dstr[w] = srcr[w];
+    s_inv[p] = (uint16_t)i;
+    s_slot_d[p] = (uint8_t)d;
   }
   __syncthreads();
-  // write every destination run as a coalesced word stream
-  for (int k = 0; k <= nspl; ++k) {
-    const uint32_t c = s_dcnt[k];
-    if (!c) continue;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_dptr[k] + s_dst[k] * kRecordBytes);
-    const uint32_t* src = s_out + s_dex[k] * kRecordWords;
-    for (uint32_t w = threadIdx.x; w < c * kRecordWords; w += kPartThreads) dst[w] = src[w];
+  for (uint32_t w = threadIdx.x; w < cnt * kRecordWords; w += kPartThreads) {
+    const uint32_t p = w / kRecordWords, c = w - p * kRecordWords;
+    const uint32_t k = s_slot_d[p];
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_dptr[k] + (s_dst[k] + p - s_dex[k]) * kRecordBytes);
+    dst[c] = s_rec[(uint32_t)s_inv[p] * kRecordWords + c];
   }
   // fused exchange: the stores above went to peers' receive windows over NVLink. One system-scope fence
   // per CTA, after the barrier that orders every thread's stores before it (fences are cumulative), so
@@ -335,7 +333,7 @@ cudaError_t launch_kp_partition(const uint8_t* in, uint64_t n, uint32_t gbase, c
                                 uint8_t* const* dst_base, const uint64_t* dst_off, uint64_t* status, uint32_t* ticket,
                                 bool remote, DistKeyMask km, cudaStream_t s) {
   if (!n) return cudaSuccess;
-  const size_t smem = 2ull * kPartTile * kRecordBytes;
+  const size_t smem = (size_t)kPartTile * kRecordBytes;
   cudaError_t e = cudaFuncSetAttribute(kp_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kp_partition<<<(unsigned)kp_tiles(n), kPartThreads, smem, s>>>(in, n, gbase, spl, nspl, dst_base, dst_off, status,
