@@ -151,7 +151,9 @@ struct RankState {
   int launches = 0;  // kernels this rank launched in the current sort (reported by ley_stage_times)
   // grow-only caches, so repeated sorts allocate nothing on the hot path
   DeviceBuffer cand_buf, split_buf, recv_buf, send_buf;
+  uint32_t* h_hist = nullptr;  // pinned: [0, 65536) local hist16, [65536, 131072) the global one
   ~RankState() {
+    if (h_hist) cudaFreeHost(h_hist);
     for (DeviceBuffer* b : {&buf, &cand_buf, &split_buf, &recv_buf, &send_buf})
       if (b->ptr) {
         cudaFree(b->ptr);
@@ -288,6 +290,20 @@ ley_status phase3_splitters(DeviceContext& ctx, cudaStream_t s, const uint8_t* a
   return LEY_OK;
 }
 
+// K-s2 on the device, accumulated onto the whole-bin counts in r.d_dcount (left there for the all-gather;
+// nothing is read back here).
+ley_status phase4_counts_device(RankState& r, const Plan& P) {
+  const int nspl = P.G - 1;
+  dist_bin_dest_counts(r.hist.data(), P.bins, nspl, r.send_counts);
+  LEY_CUDA("K-s2 counts", cudaMemcpyAsync(r.d_dcount, r.send_counts, 8 * P.G, cudaMemcpyHostToDevice, r.s));
+  if (nspl == 0) return LEY_OK;
+  LEY_CUDA("K-s2 counts", cudaMemcpyAsync(r.d_spl, P.spl, sizeof(DistSplitter) * nspl, cudaMemcpyHostToDevice, r.s));
+  r.launches += 1;
+  LEY_CUDA("K-s2 counts", launch_ks_dest_counts(r.d_cand, r.d_cand_gidx, r.ncand, r.d_spl, nspl, r.d_dcount,
+                                                r.km, r.ctx->sms, r.s));
+  return LEY_OK;
+}
+
 ley_status phase4_counts(RankState& r, const Plan& P) {
   const int nspl = P.G - 1;
   dist_bin_dest_counts(r.hist.data(), P.bins, nspl, r.send_counts);
@@ -353,11 +369,14 @@ ley_status phase6_local_sort(RankState& r, const uint8_t* recv) {
   return st;
 }
 
-void host_hist(RankState& r) {
-  r.hist.assign(65536, 0);
-  std::vector<uint32_t> h(65536);
-  cudaMemcpy(h.data(), r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost);
-  for (int b = 0; b < 65536; ++b) r.hist[b] = h[b];
+// The local histogram into pinned host memory on the rank's stream (queued; read after the next sync).
+ley_status host_hist_async(RankState& r) {
+  if (!r.h_hist) LEY_CUDA("dist hist", cudaHostAlloc(&r.h_hist, 2 * 4 * 65536, cudaHostAllocDefault));
+  LEY_CUDA("dist hist", cudaMemcpyAsync(r.h_hist, r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, r.s));
+  return LEY_OK;
+}
+void host_hist_take(RankState& r) {
+  r.hist.assign(r.h_hist, r.h_hist + 65536);
 }
 
 }  // namespace
@@ -540,14 +559,13 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
     return LEY_OK;
   }
   if ((st = prof.begin("D1 hist16+allreduce"))) return st;
-  if ((st = phase1_hist(r))) return st;
-  host_hist(r);
-  // global histogram (u32 sums: N < 2^32), in place: the local one is already on the host
-  std::vector<uint32_t> gh(65536);
+  if ((st = phase1_hist(r)) || (st = host_hist_async(r))) return st;
+  // global histogram (u32 sums: N < 2^32), in place once the local copy is queued; one host sync for both
   LEY_NCCL("dist allreduce hist16", ncclAllReduce(r.d_hist, r.d_hist, 65536, ncclUint32, ncclSum, comm->nccl, s));
-  LEY_CUDA("dist", cudaMemcpyAsync(gh.data(), r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, s));
+  LEY_CUDA("dist", cudaMemcpyAsync(r.h_hist + 65536, r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, s));
   LEY_CUDA("dist", cudaStreamSynchronize(s));
-  P.ghist.assign(gh.begin(), gh.end());
+  host_hist_take(r);
+  P.ghist.assign(r.h_hist + 65536, r.h_hist + 2 * 65536);
   if ((st = prof.end()) || (st = prof.begin("D2 splitters"))) return st;
   if (P.N && dist_plan_splitters(P.ghist.data(), P.N, G, P.bins, P.rho, P.first)) {
     set_error("dist: splitter planning failed");
@@ -602,14 +620,14 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   }
   // P4 + C3: send counts
   if ((st = prof.end()) || (st = prof.begin("D3 send counts"))) return st;
-  if ((st = phase4_counts(r, P))) return st;
+  if ((st = phase4_counts_device(r, P))) return st;
   P.send_matrix.assign((size_t)G * G, 0);
-  {
+  {  // the counts stay on the device: all-gathered from d_dcount, one host sync for the matrix
     uint64_t* d_m = d_tmp;
-    LEY_CUDA("dist", cudaMemcpyAsync(d_m + (size_t)G * G, r.send_counts, 8 * G, cudaMemcpyHostToDevice, s));
-    LEY_NCCL("dist allgather counts", ncclAllGather(d_m + (size_t)G * G, d_m, G, ncclUint64, comm->nccl, s));
+    LEY_NCCL("dist allgather counts", ncclAllGather(r.d_dcount, d_m, G, ncclUint64, comm->nccl, s));
     LEY_CUDA("dist", cudaMemcpyAsync(P.send_matrix.data(), d_m, 8ull * G * G, cudaMemcpyDeviceToHost, s));
     LEY_CUDA("dist", cudaStreamSynchronize(s));
+    for (int d = 0; d < G; ++d) r.send_counts[d] = P.send_matrix[(size_t)r.rank * G + d];
   }
   // P5 + C4: partition and exchange
   if ((st = prof.end()) || (st = prof.begin("D4 partition"))) return st;
@@ -995,9 +1013,9 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
   // P1 + C1
   P.ghist.assign(65536, 0);
   for (int i = 0; i < G; ++i) {
-    if ((st = phase1_hist(*R[i]))) return st;
+    if ((st = phase1_hist(*R[i])) || (st = host_hist_async(*R[i]))) return st;
     LEY_CUDA("loopback", cudaStreamSynchronize(s));
-    host_hist(*R[i]);
+    host_hist_take(*R[i]);
     for (int b = 0; b < 65536; ++b) P.ghist[b] += R[i]->hist[b];
   }
   if (P.N && dist_plan_splitters(P.ghist.data(), P.N, G, P.bins, P.rho, P.first)) {
