@@ -707,7 +707,12 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
                           uint8_t* out, cudaStream_t s, int* launches) {
   cudaError_t e;
-  kd_warp_sort<<<sms * 4, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in, out);
+  static int warp_per_sm = 0;  // resident CTAs per SM (registers bound it: 5 at 46 registers)
+  if (!warp_per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&warp_per_sm, kd_warp_sort, 256, 0) != cudaSuccess ||
+                       warp_per_sm < 1))
+    warp_per_sm = 4;
+  kd_warp_sort<<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in,
+                                                  out);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
   // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
