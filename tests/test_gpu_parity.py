@@ -212,6 +212,25 @@ def test_streaming_submit_pipeline():
     ley.ley_sort_drain()
 
 
+@pytest.mark.parametrize("parts", [1, 2, 3, 4])
+def test_streaming_copy_pieces(parts):
+    """ley_sort_submit with its copies in 1..4 pieces on their own streams (option pipe_split): ragged sizes
+    (pieces rounded to 256 bytes, the last one takes the rest) and interleaved calls land byte-exact."""
+    import paper_1909_08006_b200 as ley
+
+    with Options(pipe_split=parts):
+        bufs = []
+        for i, n in enumerate((1, 4097, 333_333, 77_777)):
+            recs = gen.records(n, seed=120 + i + parts, dist="skewed")
+            x, out = _pinned(recs)
+            out.fill_(0x5A)
+            ley.ley_sort_submit(x, out, n)
+            bufs.append((recs, out))
+        ley.ley_sort_drain()
+        for recs, out in bufs:
+            assert_parity(recs, out.numpy())
+
+
 def test_pageable_rejected():
     import paper_1909_08006_b200 as ley
 

@@ -157,6 +157,25 @@ def test_dist_loopback(cuda_ok, fused, k):
         ley.ley_set_option("dist_fused", 1)
 
 
+@pytest.mark.parametrize("k", [2, 7])
+def test_dist_external_loopback(cuda_ok, k):
+    """The multi-GPU external algorithm (loopback, G = 3, pinned host slices, many runs) with short keys:
+    merge composites and slice searches compare the k-byte prefix, ties by global input order."""
+    import paper_1909_08006_b200 as ley
+
+    G, N = 3, 150_001
+    recs = _records(N, 30 + k, "tiny_alphabet")
+    n_local = [60_000, 40_000, N - 100_000]
+    ins, outs, at = [], [], 0
+    for r in range(G):
+        ins.append(torch.from_numpy(recs[at * 100:(at + n_local[r]) * 100].copy()).pin_memory())
+        at += n_local[r]
+        outs.append(torch.empty((N // G + 2) * 100, dtype=torch.uint8).pin_memory())
+    res = ley.ley_sort_dist_loopback(ins, n_local, outs, [N // G + 2] * G, key_bytes=k, device_budget_bytes=12 << 20)
+    got = np.concatenate([outs[r][: res[r][0] * 100].numpy() for r in range(G)])
+    assert np.array_equal(got, _expect(recs, k)[0])
+
+
 def test_nccl_world_one_exchange(cuda_ok):
     import paper_1909_08006_b200 as ley
 
