@@ -15,16 +15,19 @@ constexpr uint32_t kTileRecords = kTileThreads * kTileItems;  // 4096, power of 
 constexpr uint32_t kTileLog2 = 12;
 static_assert((1u << kTileLog2) == kTileRecords, "tile must be a power of two");
 
-// K-c / K-c' chunk: THREADS x ITEMS (key-tail, index) pairs.
+// K-c / K-c' chunk: THREADS x ITEMS (key-tail, index) pairs. 2048-pair chunks with four 256-thread CTAs
+// per SM measured faster than 4096 with two 512-thread CTAs (more independent barrier domains per SM):
+// K-c C2 0.89 -> 0.83 ms, C4 5.98 -> 5.72 ms; THREADS must be >= 256 (one thread per digit).
 #ifndef LEY_SPLIT_THREADS
-#define LEY_SPLIT_THREADS 512
+#define LEY_SPLIT_THREADS 256
 #define LEY_SPLIT_ITEMS 8
-#define LEY_SPLIT_MINB 2
+#define LEY_SPLIT_MINB 4
 #endif
 constexpr int kSplitThreads = LEY_SPLIT_THREADS;
 constexpr int kSplitItems = LEY_SPLIT_ITEMS;
 constexpr int kSplitMinBlocks = LEY_SPLIT_MINB;
-constexpr uint32_t kChunk = kSplitThreads * kSplitItems;  // 4096
+constexpr uint32_t kChunk = kSplitThreads * kSplitItems;  // 2048
+static_assert(kSplitThreads >= 256, "K-c ranks 256 digits with one thread each");
 
 constexpr int kRadix = 256;
 

@@ -2,7 +2,7 @@
 
 Integer/byte work, so the bar is bit-exact (BASELINE.json north_star "output bit-exact
 against the oracle on the same seeded inputs, including stable tie order"). Sizes span several K-a tiles
-(4096 records), K-c chunks (4096 pairs) and ragged tails; distributions cover the configs and the edge
+(4096 records), K-c chunks (2048 pairs) and ragged tails; distributions cover the configs and the edge
 cases of SURVEY.md §4 item 4.
 """
 import numpy as np
