@@ -727,7 +727,7 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
                                              sms, in, out, s))) {
     return e;
   }
-  if ((e = launch_cta_sort<8192, 512>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
+  if ((e = launch_cta_sort<8192, 1024>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
                                       out, s)))
     return e;
   if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
