@@ -178,6 +178,7 @@ struct KdLayout {
   static constexpr uint32_t BINS = kd_bins<CAP>();
   static constexpr int WARPS = THREADS / 32;
   static constexpr bool REGS = CAP / THREADS <= 16;  // bucket held in registers (else re-read from L2)
+  static_assert(!REGS || CAP % THREADS == 0, "the register form holds exactly CAP / THREADS items per thread");
   // [s_idx CAP x 4][s_perm CAP x 4 (REGS only)][reusable: s_tail CAP x 8 | s_cnt | s_bigl | s_tmp][stage]
   static constexpr size_t kIdx = 0;
   static constexpr size_t kPerm = kIdx + (size_t)CAP * 4;
@@ -733,7 +734,7 @@ cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t*
   if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
                                         in, out, s)))
     return e;
-  if ((e = launch_cta_sort<16384, 512>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
+  if ((e = launch_cta_sort<16384, 768>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
                                        in, out, s)))
     return e;
   if (launches) *launches += 6;
