@@ -15,6 +15,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+# LEY_LIBRARY_OVERRIDE: load a variant build of the same library (tools/build_variant.sh, A/B timing only)
 _LIB_PATH = os.environ.get("LEY_LIBRARY_OVERRIDE") or os.path.join(_HERE, "libleyenda.so")
 
 if not os.path.exists(_LIB_PATH):
@@ -41,7 +42,8 @@ MAX_RECORDS = 0xFFFFFFFE
 EXPORTED_SYMBOLS = ("ley_sort", "ley_sort_perm", "ley_last_error", "ley_comm_get_unique_id", "ley_comm_init",
                     "ley_sort_dist", "ley_comm_destroy", "ley_plan_query", "ley_set_option", "ley_get_option",
                     "ley_stage_times", "ley_release_cache", "ley_version", "ley_sort_dist_loopback",
-                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange", "ley_dist_dest_offsets", "ley_test_shared_scratch", "ley_test_shared_scratch_close",
+                    "ley_dist_plan_splitters", "ley_dist_bin_dest_counts", "ley_dist_plan_exchange",
+                    "ley_dist_dest_offsets", "ley_test_shared_scratch", "ley_test_shared_scratch_close",
                     "ley_sort_submit", "ley_sort_drain", "ley_test_scan_excl", "ley_test_tile_sort", "ley_device_bytes")
 
 
