@@ -30,13 +30,16 @@ __device__ __forceinline__ uint32_t warp_peers8(uint32_t d, bool valid) {
 // inside its digit group, a block scan of the 256 counts gives the group starts. The order inside a
 // group is whatever the atomics produce — the sort's result does not depend on it, because every later
 // comparison is on the composite (key, ordinal). s_hist: [256] u32; s_tmp: [32] u32.
-template <int THREADS, int ITEMS>
+// ZEROED = true: the caller zeroed s_hist before its last barrier (saves one barrier).
+template <int THREADS, int ITEMS, bool ZEROED = false>
 __device__ __forceinline__ void block_rank_atomic(const uint32_t (&dig)[ITEMS], uint32_t count, uint32_t (&pos)[ITEMS],
                                                   uint32_t* s_hist, uint32_t* s_tmp, uint32_t& total_d,
                                                   uint32_t& excl_d) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kRadix; i += THREADS) s_hist[i] = 0;
-  __syncthreads();
+  if (!ZEROED) {
+    for (int i = threadIdx.x; i < kRadix; i += THREADS) s_hist[i] = 0;
+    __syncthreads();
+  }
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const uint32_t e = warp * (32 * ITEMS) + j * 32 + lane;
@@ -44,7 +47,7 @@ __device__ __forceinline__ void block_rank_atomic(const uint32_t (&dig)[ITEMS], 
   }
   __syncthreads();
   const uint32_t total = threadIdx.x < kRadix ? s_hist[threadIdx.x] : 0u;
-  const uint32_t excl = block_excl_scan<THREADS>(total, s_tmp, nullptr);
+  const uint32_t excl = block_excl_scan<THREADS, false>(total, s_tmp, nullptr);  // (barrier below)
   if (threadIdx.x < kRadix) s_hist[threadIdx.x] = excl;
   __syncthreads();
 #pragma unroll

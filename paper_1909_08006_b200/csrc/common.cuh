@@ -79,7 +79,8 @@ constexpr uint64_t kFlagPrefix = 2ull << 32;
 __device__ __forceinline__ uint32_t status_flag(uint64_t s) { return (uint32_t)(s >> 32); }
 
 // Block-wide exclusive scan of one u32 per thread (THREADS <= 1024). `tmp` holds >= 32 words.
-template <int THREADS>
+// SYNC_AFTER = false: the caller guarantees a barrier before `tmp` is written again (saves one barrier).
+template <int THREADS, bool SYNC_AFTER = true>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {
   constexpr int WARPS = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -104,12 +105,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, u
   uint32_t warp_excl = warp ? tmp[warp - 1] : 0;
   if (total) *total = tmp[WARPS - 1];
   uint32_t r = warp_excl + x - v;
-  __syncthreads();  // tmp reusable after return
+  if (SYNC_AFTER) __syncthreads();  // tmp reusable after return
   return r;
 }
 
 // Block-wide exclusive max-scan of one u32 per thread (identity 0). `tmp` holds >= 32 words.
-template <int THREADS>
+template <int THREADS, bool SYNC_AFTER = true>
 __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* tmp) {
   constexpr int WARPS = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -134,7 +135,7 @@ __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* tmp) {
   uint32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
   uint32_t r = lane ? prev : 0u;
   if (warp) r = max(r, tmp[warp - 1]);
-  __syncthreads();
+  if (SYNC_AFTER) __syncthreads();
   return r;
 }
 

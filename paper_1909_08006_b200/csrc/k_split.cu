@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
   // persistent: chunks are claimed by ticket (thread 0), one chunk ahead — the next ticket and its plan are
   // fetched while the current chunk is processed, and every thread prefetches its entry of the next chunk's
   // run table during the write-out, so neither latency sits between chunks (no look-back: any order works).
+  for (int q = threadIdx.x; q < kRadix; q += kThreads) s_wh[q] = 0;  // (block_rank_atomic: pre-zeroed)
   if (threadIdx.x == 0) {  // the first chunk
     const uint32_t k = atomicAdd(ticket, 1u);
     s_misc[40] = k;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
           run = max(run, m[q]);
           m[q] = run;
         }
-        const uint32_t pre = block_excl_max<kThreads>(run, s_misc);
+        const uint32_t pre = block_excl_max<kThreads, false>(run, s_misc);  // (barrier below)
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (e0 + q < cnt) s_mark[e0 + q] = (uint16_t)max(pre, m[q]);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
     }
 
     uint32_t pos[kItems], total_d, excl_d;
-        block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+        block_rank_atomic<kThreads, kItems, true>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
     if (threadIdx.x < kRadix) {
       const int d = threadIdx.x;
       const uint32_t base = total_d ? atomicAdd(&cursor[b * 256 + d], total_d) : 0u;
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       tail_out[g] = s_tail[i];
       idx_out[g] = s_idx[i];
     }
+    for (int q = threadIdx.x; q < kRadix; q += kThreads) s_wh[q] = 0;  // the next chunk's rank histogram
     __syncthreads();  // staging reused by the next chunk
   }
 }
