@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // chunks claimed one ahead (as in kc_split_level1): thread 0 fetches the next ticket and its map entry
   // while this chunk is processed
+  for (int q = threadIdx.x; q < kRadix; q += kThreads) s_wh[q] = 0;  // (block_rank_atomic: pre-zeroed)
   if (threadIdx.x == 0) {
     const uint32_t k = atomicAdd(ticket, 1u);
     s_misc[40] = k;
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       dig[j] = digit_at(tv[j], iv[j], sg.depth);
     }
     uint32_t pos[kItems], total_d, excl_d;
-        block_rank_atomic<kThreads, kItems>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
+        block_rank_atomic<kThreads, kItems, true>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
     publish_next();  // (read after the barrier below, at the top of the next iteration)
     if (threadIdx.x < kRadix) {
       const int d = threadIdx.x;
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       tout[g] = s_tail[i];
       iout[g] = s_idx[i];
     }
+    for (int q = threadIdx.x; q < kRadix; q += kThreads) s_wh[q] = 0;  // the next chunk's rank histogram
     __syncthreads();
   }
 }
