@@ -81,6 +81,21 @@ def test_medium_buckets_both_kd_forms(ws):
     assert_parity(recs, out, perm)
 
 
+@pytest.mark.parametrize("size", [32, 33, 512, 513, 2048, 2049, 8192, 8193, 10240, 10241, 16384, 16385])
+@pytest.mark.parametrize("ws", [1, 0])
+def test_kd_tier_boundaries(size, ws):
+    """One level-1 bucket of exactly `size` records (a constant 2-byte prefix, prefix2) among a few
+    thousand others, at every K-d tier boundary (warp 32, 512/128, 2048 warp-specialised or not,
+    8192/1024, 10240/1024, 16384/768, and 16385 -> the byte-2 recursion): byte-exact with the oracle."""
+    big = gen.records(size, seed=size, dist="prefix2").reshape(size, 100)
+    rest = gen.records(3001, seed=size + 1, dist="uniform").reshape(3001, 100)
+    rest[rest[:, 0] == 0xAB, 0] = 0xAC  # keep the big bucket exactly `size` records
+    recs = np.ascontiguousarray(np.concatenate([rest[:1500], big, rest[1500:]]).reshape(-1))
+    with Options(kd_ws=ws):
+        out, perm = gpu_sort(recs)
+    assert_parity(recs, out, perm)
+
+
 def test_zero_records():
     import paper_1909_08006_b200 as ley
 
