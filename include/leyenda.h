@@ -215,6 +215,10 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *   "resident_path"  1 = host pointers may take path 2 (resident input, streamed output) when in + out
  *                    do not both fit the budget but the input does; 0 = such sorts go external
  *   "resident_chunk_records" path 2 output window (records; 0 = 2^21; never above ceil(n / 4))
+ *   "pipe_split"     ley_sort_submit: each H2D / D2H copy in this many pieces on their own streams
+ *                    (1..4, default 2: more of the host link busy in each direction)
+ *   "l2_fetch_bytes" cudaLimitMaxL2FetchGranularity set before each call (0 = leave the device default;
+ *                    32/64/128 accepted; measured without effect on this part, kept for experiments)
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
 ley_status ley_set_option(const char* name, int64_t value);
 ley_status ley_get_option(const char* name, int64_t* value);
