@@ -99,3 +99,19 @@ def test_options(ley):
         ley.ley_set_option("warp_tier_max", 33)
     with pytest.raises(ley.LeyendaError):
         ley.ley_set_option("no_such_option", 1)
+
+
+def test_documented_options_exist(ley):
+    """Every option the header documents can be read (and only real names can): the header's option list
+    and the library's registry agree."""
+    import re
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "leyenda.h")).read()
+    block = hdr[hdr.index("Integer options"):hdr.index("ley_status ley_set_option")]
+    names = re.findall(r'^ \*   "([a-z_0-9]+)"', block, flags=re.M)
+    assert len(names) >= 15
+    for nm in names:
+        ley.ley_get_option(nm)  # raises on an unknown name
+    with pytest.raises(ley.LeyendaError):
+        ley.ley_get_option("no_such_option")
