@@ -1,6 +1,8 @@
 // runtime.cpp — errors, options, planning, device arena and profiling for libleyenda (host C++).
 #include "runtime.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -345,7 +347,11 @@ struct StageRecord {
 thread_local StageRecord g_stages;
 }  // namespace
 
+// Every stage is also an NVTX range (header-only NVTX3: a no-op unless a tool such as Nsight Systems
+// is attached), so the sort's stages show up on a profiler timeline without the "profile" option.
 ley_status Profiler::begin(const char* name) {
+  nvtxRangePushA(name);
+  ++nvtx_depth;
   if (!on) return LEY_OK;
   int need = next_event + 2;
   while ((int)ctx->events.size() < need) {
@@ -360,10 +366,18 @@ ley_status Profiler::begin(const char* name) {
 }
 
 ley_status Profiler::end() {
+  if (nvtx_depth > 0) {
+    nvtxRangePop();
+    --nvtx_depth;
+  }
   if (!on) return LEY_OK;
   ev_end.push_back(next_event);
   LEY_CUDA("profiler", cudaEventRecord(ctx->events[next_event++], stream));
   return LEY_OK;
+}
+
+Profiler::~Profiler() {
+  while (nvtx_depth-- > 0) nvtxRangePop();
 }
 
 void Profiler::finish() {

@@ -163,6 +163,8 @@ struct Profiler {
   std::vector<int> ev_begin, ev_end;
   int next_event = 0;
   int launches = 0;
+  int nvtx_depth = 0;  // open NVTX ranges (closed by end(); an early error return leaves them to ~Profiler)
+  ~Profiler();
   ley_status begin(const char* name);
   ley_status end();
   void finish();  // after stream sync: compute times into the thread-local record
