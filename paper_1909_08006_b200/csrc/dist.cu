@@ -641,14 +641,20 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       for (int src = 0; src < G; ++src) in_d += P.send_matrix[(size_t)src * G + d];
       most = std::max(most, in_d);
     }
-    if ((st = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s))) return st;
+    const ley_status wst = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s);
+    if (wst && comm->fused_ok > 0) return wst;  // a window that worked failed to grow: a real error
     if (comm->fused_ok < 0) {
-      // every peer must be reachable through the window (one NVLink/NVSwitch domain); if any rank sees a
-      // null peer pointer, all ranks agree to use the all-to-all transport on this communicator
-      uint8_t* hp[kMaxRanks] = {};
-      LEY_CUDA("dist window", cudaMemcpy(hp, comm->d_peers, 8 * G, cudaMemcpyDeviceToHost));
-      uint64_t bad = 0;
-      for (int d = 0; d < G; ++d) bad += hp[d] == nullptr;
+      // every peer must be reachable through the window (one NVLink/NVSwitch domain); if any rank failed
+      // to allocate/register the window or sees a null peer pointer, all ranks agree to use the all-to-all
+      // transport on this communicator
+      uint64_t bad = wst ? 1 : 0;
+      if (wst) {
+        window_release(comm);
+      } else {
+        uint8_t* hp[kMaxRanks] = {};
+        LEY_CUDA("dist window", cudaMemcpy(hp, comm->d_peers, 8 * G, cudaMemcpyDeviceToHost));
+        for (int d = 0; d < G; ++d) bad += hp[d] == nullptr;
+      }
       LEY_CUDA("dist window", cudaMemcpyAsync(d_tmp, &bad, 8, cudaMemcpyHostToDevice, s));
       LEY_NCCL("dist window", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
       LEY_CUDA("dist window", cudaMemcpyAsync(&bad, d_tmp, 8, cudaMemcpyDeviceToHost, s));
