@@ -25,7 +25,8 @@ inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 namespace {
 // One pass of the internal sort (K-a .. K-e) ordered by the key window `key`.
 ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                     cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, KeySpec key) {
+                     cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, KeySpec key,
+                     uint64_t* digest = nullptr) {
   const InternalLayout L = plan_internal(n);
   ley_status st;
   if (!out && !perm_out) {  // out == nullptr is the perm-only mode (K-d without the fused gather)
@@ -125,7 +126,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   bind_lists(kd_cap);
   LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
   ++launches;
-  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
+  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, digest, s, &launches));
   LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
   LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
   uint32_t nbig = host_cnt[0];
@@ -182,7 +183,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     launches += 6;
     if ((st = prof.end())) return st;
     if ((st = prof.begin("K-de sort+gather"))) return st;
-    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, s, &launches));
+    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, digest, s, &launches));
     LEY_CUDA("K-c' recursion", launch_publish_u32(big_count, host_cnt_dev, s));
     LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
     nbig = host_cnt[0];
@@ -255,7 +256,10 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     // 10 key bytes, then only the runs of equal 10-byte prefixes need the rest of the key — tiny ones by a
     // warp comparison sort, a few large ones by the window passes on their slice. Random keys: no ties,
     // one pass + one read of the output.
-    if ((st = sort_pass(ctx, in, out, nullptr, n, s, prof, work, work_bytes, KeySpec{0, kKeyBytes}))) return st;
+    // K-e writes each output record's prefix digest into the (not yet used) scratch record buffer, so the
+    // tie-group scan reads 8 B per record instead of the records' lines
+    uint64_t* digest = reinterpret_cast<uint64_t*>(tmp);
+    if ((st = sort_pass(ctx, in, out, nullptr, n, s, prof, work, work_bytes, KeySpec{0, kKeyBytes}, digest))) return st;
     const uint32_t cap = (uint32_t)(n / 2 + 1);
     uint32_t* firsts = reinterpret_cast<uint32_t*>(tmp + a256(n * kRecordBytes));
     uint32_t* lasts = firsts + a256(4ull * cap) / 4;
@@ -263,7 +267,7 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     uint32_t* counts = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(groups) + a256(8ull * cap));
     if ((st = prof.begin("tie groups"))) return st;
     LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 8, s));
-    LEY_CUDA("tie groups", launch_tie_groups(out, n, firsts, lasts, cap, counts, ctx.sms, s));
+    LEY_CUDA("tie groups", launch_tie_groups(out, digest, n, firsts, lasts, cap, counts, ctx.sms, s));
     ++prof.launches;
     uint32_t hc[2] = {0, 0};
     LEY_CUDA("tie groups", cudaMemcpyAsync(hc, counts, 8, cudaMemcpyDeviceToHost, s));

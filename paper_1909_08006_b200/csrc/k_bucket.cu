@@ -42,11 +42,19 @@ __device__ __forceinline__ void stg_cs_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Digest of a record's 10-byte key prefix (words 0, 1 and the low half of word 2): equal prefixes give
+// equal digests, so the tie-group scan of the hybrid long-key form (k_ties.cu) reads 8 B per record
+// instead of the records' lines and verifies only the candidates against the records.
+__device__ __forceinline__ uint64_t prefix_digest(const uint32_t* w) {
+  return ((uint64_t)w[1] << 32 | w[0]) ^ ((uint64_t)(w[2] & 0xFFFFu) * 0x9E3779B97F4A7C15ull);
+}
+
 // Records in[perm[i]] -> out_base[i] for i in [0, s) by one warp, groups g0 = first, first + stride, ...
-// of 32 records, through `stage` (kStageBytes, 16-byte aligned). perm lives in shared memory.
+// of 32 records, through `stage` (kStageBytes, 16-byte aligned). perm lives in shared memory. With
+// dg_base, also dg_base[i] = prefix_digest(record).
 __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
                                             const uint8_t* __restrict__ in, uint8_t* __restrict__ out_base,
-                                            uint8_t* stage) {
+                                            uint8_t* stage, uint64_t* __restrict__ dg_base) {
   const int lane = threadIdx.x & 31;
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
   for (uint32_t g0 = first; g0 < s; g0 += stride) {
@@ -70,6 +78,9 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
       const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
       stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
     }
+    if (dg_base && lane < (int)cnt)
+      dg_base[g0 + lane] =
+          prefix_digest(reinterpret_cast<const uint32_t*>(stage + lane * kWindow + ((p * 4u) & 15u)));
     __syncwarp();
   }
 }
@@ -85,10 +96,13 @@ __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const ui
 }
 
 // ---------------------------------------------------------------------------- warp tier (len <= 32)
+// (DG: write prefix digests too — a separate instantiation, so the plain form keeps its 46 registers)
+template <bool DG>
 __global__ void __launch_bounds__(256)
     kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                  const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                 uint64_t* __restrict__ dg) {
   __shared__ __align__(16) uint8_t s_stage[8][kStageBytes];
   __shared__ uint32_t s_perm[8][32];
   const uint32_t nitems = *count;
@@ -125,7 +139,8 @@ __global__ void __launch_bounds__(256)
     }
     __syncwarp();
     if (out)  // (perm-only mode: the resident host path gathers later, chunk by chunk)
-      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib]);
+      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib],
+                  DG ? dg + sg.start : nullptr);
   }
 }
 
@@ -208,11 +223,12 @@ struct KdLayout {
 //   3. exact rank inside every tiny sub-bucket (count of smaller composites; <= kd_insert_max), a warp
 //      bitonic network for larger ones — Alg. 1's ComparisonSort below tinyBucketThreshold,
 //   4. the bucket's records gathered into out[start, start+len) by the CTA's warps (see file header).
-template <uint32_t CAP, int THREADS>
+template <uint32_t CAP, int THREADS, bool DG>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 8)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+                uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                uint64_t* __restrict__ dg) {
   using L = KdLayout<CAP, THREADS>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int WARPS = L::WARPS;
@@ -403,16 +419,17 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
     if (out && warp < L::GWARPS)
       warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in,
-                  out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes);
+                  out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
+                  DG ? dg + sg.start : nullptr);
     __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
 }
 
-template <uint32_t CAP, int THREADS>
+template <uint32_t CAP, int THREADS, bool DG>
 cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                             const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                            const uint8_t* in, uint8_t* out, cudaStream_t s) {
-  auto kern = kd_cta_sort<CAP, THREADS>;
+                            const uint8_t* in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+  auto kern = kd_cta_sort<CAP, THREADS, DG>;
   const size_t smem = KdLayout<CAP, THREADS>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -420,7 +437,7 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out);
+  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out, dg);
   if (getenv("LEY_DEBUG_SYNC")) {
     fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
     cudaError_t e2 = cudaStreamSynchronize(s);
@@ -500,11 +517,12 @@ struct WsLayout {
   static constexpr size_t kBytes = kStage + (size_t)GW * 2 * kStageBytes;
 };
 
-template <uint32_t CAP, int ST, int GW>
+template <uint32_t CAP, int ST, int GW, bool DG>
 __global__ void __launch_bounds__(ST + 32 * GW, 2)
     kd_ws_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-               uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+               uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+               uint64_t* __restrict__ dg) {
   using L = WsLayout<CAP, ST, GW>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int ITEMS = CAP / ST;
@@ -670,6 +688,9 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
           const uint32_t off = (pr[g0 + r] * 4u) & 15u;
           stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWindow + off + 4 * o));
         }
+        if (DG && lane < (int)cnt)
+          dg[d.x + g0 + lane] =
+              prefix_digest(reinterpret_cast<const uint32_t*>(sb + lane * kWindow + ((pr[g0 + lane] * 4u) & 15u)));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         st ^= 1;
@@ -679,11 +700,11 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
   }
 }
 
-template <uint32_t CAP, int ST, int GW>
+template <uint32_t CAP, int ST, int GW, bool DG>
 cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                            const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                           const uint8_t* in, uint8_t* out, cudaStream_t s) {
-  auto kern = kd_ws_sort<CAP, ST, GW>;
+                           const uint8_t* in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+  auto kern = kd_ws_sort<CAP, ST, GW, DG>;
   const size_t smem = WsLayout<CAP, ST, GW>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -691,7 +712,7 @@ cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST + 32 * GW, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out);
+  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out, dg);
   return cudaGetLastError();
 }
 
@@ -703,42 +724,52 @@ cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B1
   return cudaGetLastError();
 }
 
+namespace {
 // All K-d/K-e tiers for the lists of one level (counts are read on the device; no host sync).
-cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
-                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint8_t* out, cudaStream_t s, int* launches) {
+template <bool DG>
+cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1, const uint32_t* i1,
+                   uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in, uint8_t* out, uint64_t* dg,
+                   cudaStream_t s, int* launches) {
   cudaError_t e;
   static int warp_per_sm = 0;  // resident CTAs per SM (registers bound it: 5 at 46 registers)
-  if (!warp_per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&warp_per_sm, kd_warp_sort, 256, 0) != cudaSuccess ||
+  if (!warp_per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&warp_per_sm, kd_warp_sort<DG>, 256, 0) != cudaSuccess ||
                        warp_per_sm < 1))
     warp_per_sm = 4;
-  kd_warp_sort<<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in,
-                                                  out);
+  kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in,
+                                                  out, dg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
   // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
-  if ((e = launch_cta_sort<512, 128>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
-                                     out, s)))
+  if ((e = launch_cta_sort<512, 128, DG>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
+                                     out, dg, s)))
     return e;
   if (tu.kd_ws && out) {  // (no gather warps to feed in perm-only mode)
-    if ((e = launch_ws_sort<2048, 256, 8>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
-                                          out, s)))
+    if ((e = launch_ws_sort<2048, 256, 8, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
+                                          out, dg, s)))
       return e;
-  } else if ((e = launch_cta_sort<2048, 256>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu,
-                                             sms, in, out, s))) {
+  } else if ((e = launch_cta_sort<2048, 256, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu,
+                                             sms, in, out, dg, s))) {
     return e;
   }
-  if ((e = launch_cta_sort<8192, 1024>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
-                                      out, s)))
+  if ((e = launch_cta_sort<8192, 1024, DG>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
+                                      out, dg, s)))
     return e;
-  if ((e = launch_cta_sort<10240, 1024>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
-                                        in, out, s)))
+  if ((e = launch_cta_sort<10240, 1024, DG>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
+                                        in, out, dg, s)))
     return e;
-  if ((e = launch_cta_sort<16384, 768>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
-                                       in, out, s)))
+  if ((e = launch_cta_sort<16384, 768, DG>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
+                                       in, out, dg, s)))
     return e;
   if (launches) *launches += 6;
   return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
+                          const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
+                          uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches) {
+  return dg && out ? kd_all<true>(kd, t0, i0, t1, i1, perm, tu, sms, in, out, dg, s, launches)
+                   : kd_all<false>(kd, t0, i0, t1, i1, perm, tu, sms, in, out, nullptr, s, launches);
 }
 
 }  // namespace ley

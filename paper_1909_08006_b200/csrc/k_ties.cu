@@ -21,12 +21,21 @@ __device__ __forceinline__ bool prefix10_equal(const uint8_t* a, const uint8_t* 
   return x[0] == y[0] && x[1] == y[1] && ((x[2] ^ y[2]) & 0xFFFFu) == 0;
 }
 
-__global__ void kt_tie_groups(const uint8_t* __restrict__ recs, uint64_t n, uint32_t* __restrict__ firsts,
-                              uint32_t* __restrict__ lasts, uint32_t cap, uint32_t* __restrict__ counts) {
+// dg (nullable): the prefix digests K-e wrote beside the records (k_bucket.cu prefix_digest); equal
+// prefixes have equal digests, so only adjacent records with equal digests are compared on the records.
+__global__ void kt_tie_groups(const uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
+                              uint32_t* __restrict__ firsts, uint32_t* __restrict__ lasts, uint32_t cap,
+                              uint32_t* __restrict__ counts) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint8_t* r = recs + j * kRecordBytes;
-    const bool tie_prev = j > 0 && prefix10_equal(r - kRecordBytes, r);
-    const bool tie_next = j + 1 < n && prefix10_equal(r, r + kRecordBytes);
+    bool cand_prev = j > 0, cand_next = j + 1 < n;
+    if (dg) {
+      const uint64_t d = dg[j];
+      cand_prev = cand_prev && dg[j - 1] == d;
+      cand_next = cand_next && dg[j + 1] == d;
+    }
+    const bool tie_prev = cand_prev && prefix10_equal(r - kRecordBytes, r);
+    const bool tie_next = cand_next && prefix10_equal(r, r + kRecordBytes);
     if (tie_next && !tie_prev) {
       const uint32_t at = atomicAdd(&counts[0], 1u);
       if (at < cap) firsts[at] = (uint32_t)j;
@@ -77,12 +86,12 @@ __global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint2* __restrict
 
 }  // namespace
 
-cudaError_t launch_tie_groups(const uint8_t* recs, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
+cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
                               uint32_t* counts, int sms, cudaStream_t s) {
   if (n < 2) return cudaSuccess;
   uint64_t blocks = (n + 255) / 256;
   if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
-  kt_tie_groups<<<(unsigned)blocks, 256, 0, s>>>(recs, n, firsts, lasts, cap, counts);
+  kt_tie_groups<<<(unsigned)blocks, 256, 0, s>>>(recs, dg, n, firsts, lasts, cap, counts);
   return cudaGetLastError();
 }
 

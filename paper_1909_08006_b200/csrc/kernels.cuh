@@ -52,18 +52,19 @@ cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* csta
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
                                       const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
 // K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
-// out == nullptr: perm-only, no gather).
+// out == nullptr: perm-only, no gather; dg non-null: dg[j] = digest of output record j's 10-byte prefix).
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint8_t* out, cudaStream_t s, int* launches);
+                          uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches);
 
 // K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
                              cudaStream_t s);
 // keys > 10 bytes, hybrid form (k_ties.cu): runs of equal 10-byte prefixes in sorted records -> unordered
-// (first, last) lists (counts[0], counts[1]; entries past cap dropped); in-place comparison sort of
+// (first, last) lists (counts[0], counts[1]; entries past cap dropped; dg: the K-e prefix digests of the
+// records, or null to compare every adjacent pair on the records); in-place comparison sort of
 // groups (first, len <= 32) by key bytes [10, key_bytes) then position
-cudaError_t launch_tie_groups(const uint8_t* recs, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
+cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
                               uint32_t* counts, int sms, cudaStream_t s);
 cudaError_t launch_fix_small_groups(uint8_t* recs, const uint2* groups, uint32_t ngroups, uint32_t key_bytes, int sms,
                                     cudaStream_t s);

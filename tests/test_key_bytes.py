@@ -81,6 +81,38 @@ def test_long_keys_tie_groups(cuda_ok, groups, hybrid):
     assert np.array_equal(out.cpu().numpy(), _expect(recs, 24)[0])
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tie_scan_digest_collision(cuda_ok, seed):
+    """The tie-group scan reads the prefix digests K-e writes (k_bucket.cu prefix_digest) and verifies
+    equal-digest neighbours on the records. Two different 10-byte prefixes A, B built to share a digest,
+    adjacent in sorted order (fillers sort before/after them), 12 records each: treating them as one tie
+    group of 24 would reorder A's and B's records together by bytes 10.. — the result must equal the oracle."""
+    import paper_1909_08006_b200 as ley
+
+    C = 0x9E3779B97F4A7C15  # white-box: the digest's multiplier (words 0-1 XOR (bytes 8-9) * C, mod 2^64)
+    rng = np.random.default_rng(seed)
+    while True:
+        x = int(rng.integers(0, 2**63)) | (int(rng.integers(0, 2)) << 63)
+        a, b = (int(v) for v in rng.integers(0, 1 << 16, size=2))
+        y = x ^ ((a * C) & (2**64 - 1)) ^ ((b * C) & (2**64 - 1))
+        if a != b and all(0 < (v & 0xFF) < 0xFF for v in (x, y)):
+            break
+    n = 100_000
+    r = gen.records(n, seed=70 + seed, dist="uniform").reshape(n, 100)
+    r[: n // 2, 0], r[n // 2:, 0] = 0x00, 0xFF
+    at = rng.permutation(n)[:24]
+    for j, pos in enumerate(at):
+        lo, hi = (x, a) if j < 12 else (y, b)
+        r[pos, 0:8] = np.frombuffer(lo.to_bytes(8, "little"), dtype=np.uint8)
+        r[pos, 8:10] = np.frombuffer(hi.to_bytes(2, "little"), dtype=np.uint8)
+    r[:, 10:20] = rng.integers(0, 3, size=(n, 10))
+    recs = np.ascontiguousarray(r.reshape(-1))
+    x_t = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x_t)
+    ley.ley_sort(x_t, out, n, key_bytes=20)
+    assert np.array_equal(out.cpu().numpy(), _expect(recs, 20)[0])
+
+
 @pytest.mark.parametrize("k", [1, 4, 12])
 def test_large_and_skewed(cuda_ok, k):
     """Skewed C3-style keys at 2M records (recursion below the key prefix) with short and long keys."""
