@@ -205,13 +205,16 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm) {
   if (key_bytes <= kKeyBytes) return 0;
   // the other record buffer of the window passes; with perm two permutation arrays, else the tie-group
-  // lists of the hybrid form (first/last positions, <= n/2 groups each, and the (first, len) array)
-  return a256(n * kRecordBytes) + (perm ? 2 * a256(4 * n) : 2 * a256(4 * (n / 2 + 1)) + a256(8 * (n / 2 + 1)) + 256);
+  // lists of the hybrid form (first/last positions, <= n/2 groups each, the two large-group lists and
+  // the counts)
+  return a256(n * kRecordBytes) + (perm ? 2 * a256(4 * n) : 2 * a256(4 * (n / 2 + 1)) + 1024);
 }
 
 namespace {
-constexpr uint32_t kSmallGroup = 32;       // tie groups up to this size: one warp, comparison sort
-constexpr size_t kMaxLargeGroups = 64;     // more larger groups than this: plain LSD window passes
+// tie groups of <= 32 records: one warp each, comparison sort (k_ties.cu); larger ones: window passes on
+// their slice, unless there are more than this many
+constexpr size_t kMaxLargeGroups = 64;
+constexpr uint32_t kLargeCap = kMaxLargeGroups + 1;  // large-group list entries read back
 
 // LSD passes over windows W-1 .. first_window of records [0, n) of `data` (in place, via tmp), ordinals =
 // current positions.
@@ -263,45 +266,33 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     const uint32_t cap = (uint32_t)(n / 2 + 1);
     uint32_t* firsts = reinterpret_cast<uint32_t*>(tmp + a256(n * kRecordBytes));
     uint32_t* lasts = firsts + a256(4ull * cap) / 4;
-    uint2* groups = reinterpret_cast<uint2*>(lasts + a256(4ull * cap) / 4);
-    uint32_t* counts = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(groups) + a256(8ull * cap));
+    uint32_t* large_f = lasts + a256(4ull * cap) / 4;  // [kLargeCap] each, then the 4 counts
+    uint32_t* large_l = large_f + kLargeCap;
+    uint32_t* counts = large_l + kLargeCap;
     if ((st = prof.begin("tie groups"))) return st;
-    LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 8, s));
+    LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 16, s));
     LEY_CUDA("tie groups", launch_tie_groups(out, digest, n, firsts, lasts, cap, counts, ctx.sms, s));
-    ++prof.launches;
-    uint32_t hc[2] = {0, 0};
-    LEY_CUDA("tie groups", cudaMemcpyAsync(hc, counts, 8, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("tie groups", launch_fix_small_groups(out, digest, n, firsts, lasts, counts, key_bytes, large_f, large_l,
+                                                   kLargeCap, ctx.sms, s));
+    prof.launches += 3;
+    // one read-back: the four counts and the two short large-group lists
+    uint32_t h[2 * kLargeCap + 4];
+    LEY_CUDA("tie groups", cudaMemcpyAsync(h, large_f, sizeof(h), cudaMemcpyDeviceToHost, s));
     LEY_CUDA("tie groups", cudaStreamSynchronize(s));
-    bool fallback = hc[0] != hc[1] || hc[0] > cap;
-    if (!fallback && hc[0]) {
-      std::vector<uint32_t> f(hc[0]), l(hc[0]);
-      LEY_CUDA("tie groups", cudaMemcpyAsync(f.data(), firsts, 4ull * hc[0], cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("tie groups", cudaMemcpyAsync(l.data(), lasts, 4ull * hc[0], cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("tie groups", cudaStreamSynchronize(s));
+    const uint32_t* hc = h + 2 * kLargeCap;
+    bool fallback = hc[0] != hc[1] || hc[0] > cap || hc[2] != hc[3] || hc[2] > kMaxLargeGroups;
+    if (!fallback && hc[2]) {
+      std::vector<uint32_t> f(h, h + hc[2]), l(h + kLargeCap, h + kLargeCap + hc[3]);
       std::sort(f.begin(), f.end());
       std::sort(l.begin(), l.end());
-      std::vector<uint2> small, large;
-      for (size_t g = 0; g < f.size(); ++g) {
-        const uint2 gr{f[g], l[g] - f[g] + 1};
-        (gr.y <= kSmallGroup ? small : large).push_back(gr);
+      for (size_t g = 0; g < f.size() && !st; ++g) {
+        // the passes need a 16-byte-aligned slice: start at the record index rounded down to a multiple
+        // of 4 and sort by the whole key (window 0 too), so the up to 3 records before the group — already
+        // in their final order, all with a smaller or equal-and-earlier full key — stay where they are
+        const uint64_t x0 = f[g] & ~3u, len = l[g] + 1 - x0;
+        st = window_passes(ctx, out + x0 * kRecordBytes, tmp, len, key_bytes, 0, s, prof, work, work_bytes);
       }
-      fallback = large.size() > kMaxLargeGroups;
-      if (!fallback) {
-        if (!small.empty()) {
-          LEY_CUDA("tie groups", cudaMemcpyAsync(groups, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
-          LEY_CUDA("tie groups", launch_fix_small_groups(out, groups, (uint32_t)small.size(), key_bytes, ctx.sms, s));
-          ++prof.launches;
-        }
-        for (const uint2& gr : large) {
-          // the passes need a 16-byte-aligned slice: start at the record index rounded down to a multiple
-          // of 4 and sort by the whole key (window 0 too), so the up to 3 records before the group — already
-          // in their final order, all with a smaller or equal-and-earlier full key — stay where they are
-          const uint64_t x0 = gr.x & ~3u, len = gr.x + gr.y - x0;
-          if ((st = window_passes(ctx, out + x0 * kRecordBytes, tmp, len, key_bytes, 0, s, prof, work, work_bytes)))
-            return st;
-        }
-        LEY_CUDA("tie groups", cudaStreamSynchronize(s));  // the host vectors above are in flight until here
-      }
+      if (st) return st;
     }
     if ((st = prof.end())) return st;
     if (!fallback) return LEY_OK;

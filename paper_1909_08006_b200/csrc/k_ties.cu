@@ -2,12 +2,15 @@
 // sorting and comparison-based record sorting"). The radix sort orders the records by their first 10 key
 // bytes (ties by input index); only records whose 10-byte prefixes tie need the rest of the key:
 //   kt_tie_groups  one pass over the sorted records: maximal runs of equal 10-byte prefixes ("tie groups",
-//                  >= 2 records) are reported as (first, last) positions (unordered lists; the host pairs
-//                  them after sorting both, as groups never overlap)
-//   kt_fix_small   one warp per tie group of <= 32 records: each lane ranks its record against the others
-//                  by (key bytes [10, key_bytes), position) — a comparison sort on the records themselves —
-//                  and the group is rewritten in place in that order
-// Larger groups are sorted by the LSD window passes restricted to their slice (internal.cu).
+//                  >= 2 records) are reported as first and last positions (two unordered lists)
+//   kt_fix_small   one warp per group first: the warp finds the group's length itself (a ballot of prefix
+//                  equality over the next 32 records — the run is contiguous and maximal); a group of <= 32
+//                  records is ranked lane by lane by (key bytes [10, key_bytes), position) — a comparison
+//                  sort on the records themselves — and rewritten in place in that order; a longer one is
+//                  appended to the short "large firsts" list instead
+//   kt_large_lasts the matching "large lasts" list (a group is large iff the record 32 before its last ties)
+// No list is ever sorted or shipped to the host except the two large lists (<= 65 entries read); large
+// groups are sorted by the LSD window passes restricted to their slice (internal.cu).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -21,29 +24,43 @@ __device__ __forceinline__ bool prefix10_equal(const uint8_t* a, const uint8_t* 
   return x[0] == y[0] && x[1] == y[1] && ((x[2] ^ y[2]) & 0xFFFFu) == 0;
 }
 
+// Appends v to list[counts[c]++] for the lanes with `take` (one atomic per warp; all 32 lanes call it).
+__device__ __forceinline__ void warp_append(bool take, uint32_t v, uint32_t* list, uint32_t* counter, uint32_t cap) {
+  const uint32_t m = __ballot_sync(0xffffffffu, take);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(counter, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (take) {
+    const uint32_t at = base + __popc(m & ((1u << lane) - 1u));
+    if (at < cap) list[at] = v;
+  }
+}
+
 // dg (nullable): the prefix digests K-e wrote beside the records (k_bucket.cu prefix_digest); equal
 // prefixes have equal digests, so only adjacent records with equal digests are compared on the records.
 __global__ void kt_tie_groups(const uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
                               uint32_t* __restrict__ firsts, uint32_t* __restrict__ lasts, uint32_t cap,
                               uint32_t* __restrict__ counts) {
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint8_t* r = recs + j * kRecordBytes;
-    bool cand_prev = j > 0, cand_next = j + 1 < n;
-    if (dg) {
-      const uint64_t d = dg[j];
-      cand_prev = cand_prev && dg[j - 1] == d;
-      cand_next = cand_next && dg[j + 1] == d;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count: every lane takes part in the appends' ballots
+  for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n; j0 += stride) {
+    const uint64_t j = j0 + (threadIdx.x & 31);
+    bool tie_prev = false, tie_next = false;
+    if (j < n) {
+      const uint8_t* r = recs + j * kRecordBytes;
+      bool cand_prev = j > 0, cand_next = j + 1 < n;
+      if (dg) {
+        const uint64_t d = dg[j];
+        cand_prev = cand_prev && dg[j - 1] == d;
+        cand_next = cand_next && dg[j + 1] == d;
+      }
+      tie_prev = cand_prev && prefix10_equal(r - kRecordBytes, r);
+      tie_next = cand_next && prefix10_equal(r, r + kRecordBytes);
     }
-    const bool tie_prev = cand_prev && prefix10_equal(r - kRecordBytes, r);
-    const bool tie_next = cand_next && prefix10_equal(r, r + kRecordBytes);
-    if (tie_next && !tie_prev) {
-      const uint32_t at = atomicAdd(&counts[0], 1u);
-      if (at < cap) firsts[at] = (uint32_t)j;
-    }
-    if (tie_prev && !tie_next) {
-      const uint32_t at = atomicAdd(&counts[1], 1u);
-      if (at < cap) lasts[at] = (uint32_t)j;
-    }
+    warp_append(tie_next && !tie_prev, (uint32_t)j, firsts, &counts[0], cap);
+    warp_append(tie_prev && !tie_next, (uint32_t)j, lasts, &counts[1], cap);
   }
 }
 
@@ -58,29 +75,58 @@ __device__ __forceinline__ bool tail_less(const uint8_t* recs, uint32_t a, uint3
   return a < b;
 }
 
-__global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint2* __restrict__ groups, uint32_t ngroups,
-                             uint32_t kb) {
+// (prefix comparisons go to the records only where the digests dg already match)
+__device__ __forceinline__ bool same_prefix(const uint8_t* recs, const uint64_t* dg, uint64_t a, uint64_t b) {
+  return dg[a] == dg[b] && prefix10_equal(recs + a * kRecordBytes, recs + b * kRecordBytes);
+}
+
+__global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
+                             const uint32_t* __restrict__ firsts, uint32_t* __restrict__ counts, uint32_t kb,
+                             uint32_t* __restrict__ large_f, uint32_t large_cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t ngroups = counts[0];
   for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups; g += warps) {
-    const uint2 grp = groups[g];  // (first, len), len in [2, 32]
-    const bool active = (uint32_t)lane < grp.y;
-    const uint32_t me = grp.x + lane;
+    const uint32_t f = firsts[g];
+    const bool eq = (uint64_t)f + lane < n && same_prefix(recs, dg, f, (uint64_t)f + lane);
+    const uint32_t len = __popc(__ballot_sync(0xffffffffu, eq));  // the run from f is contiguous
+    if (len == 32 && (uint64_t)f + 32 < n && same_prefix(recs, dg, f, (uint64_t)f + 32)) {
+      if (lane == 0) {
+        const uint32_t at = atomicAdd(&counts[2], 1u);
+        if (at < large_cap) large_f[at] = f;
+      }
+      continue;
+    }
+    const bool active = (uint32_t)lane < len;
+    const uint32_t me = f + lane;
     uint32_t rank = 0;
     if (active)
-      for (uint32_t m = 0; m < grp.y; ++m)
-        if (m != (uint32_t)lane && tail_less(recs, grp.x + m, me, kb)) ++rank;
+      for (uint32_t m = 0; m < len; ++m)
+        if (m != (uint32_t)lane && tail_less(recs, f + m, me, kb)) ++rank;
     uint32_t w[kRecordWords];
     const uint32_t* src = reinterpret_cast<const uint32_t*>(recs + (uint64_t)me * kRecordBytes);
 #pragma unroll
     for (int q = 0; q < (int)kRecordWords; ++q) w[q] = active ? src[q] : 0u;
     __syncwarp();  // every lane holds its record before any is overwritten
     if (active) {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(recs + (uint64_t)(grp.x + rank) * kRecordBytes);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(recs + (uint64_t)(f + rank) * kRecordBytes);
 #pragma unroll
       for (int q = 0; q < (int)kRecordWords; ++q) dst[q] = w[q];
     }
     __syncwarp();
+  }
+}
+
+__global__ void kt_large_lasts(const uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg,
+                               const uint32_t* __restrict__ lasts, uint32_t* __restrict__ counts,
+                               uint32_t* __restrict__ large_l, uint32_t large_cap) {
+  const uint32_t nl = counts[1];
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nl; g += gridDim.x * blockDim.x) {
+    const uint32_t l = lasts[g];
+    if (l >= 32 && same_prefix(recs, dg, l - 32, l)) {
+      const uint32_t at = atomicAdd(&counts[3], 1u);  // (rare: at most a few large groups)
+      if (at < large_cap) large_l[at] = l;
+    }
   }
 }
 
@@ -95,12 +141,15 @@ cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_fix_small_groups(uint8_t* recs, const uint2* groups, uint32_t ngroups, uint32_t key_bytes, int sms,
-                                    cudaStream_t s) {
-  if (!ngroups) return cudaSuccess;
-  uint64_t blocks = (ngroups + 7) / 8;
-  if (blocks > (uint64_t)sms * 16) blocks = (uint64_t)sms * 16;
-  kt_fix_small<<<(unsigned)blocks, 256, 0, s>>>(recs, groups, ngroups, key_bytes);
+cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, const uint32_t* firsts,
+                                    const uint32_t* lasts, uint32_t* counts, uint32_t key_bytes, uint32_t* large_f,
+                                    uint32_t* large_l, uint32_t large_cap, int sms, cudaStream_t s) {
+  if (n < 2) return cudaSuccess;
+  // group counts live on the device: persistent grids, grid-stride over counts[0] / counts[1]
+  kt_fix_small<<<sms * 8, 256, 0, s>>>(recs, dg, n, firsts, counts, key_bytes, large_f, large_cap);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  kt_large_lasts<<<sms * 4, 256, 0, s>>>(recs, dg, lasts, counts, large_l, large_cap);
   return cudaGetLastError();
 }
 

@@ -81,6 +81,34 @@ def test_long_keys_tie_groups(cuda_ok, groups, hybrid):
     assert np.array_equal(out.cpu().numpy(), _expect(recs, 24)[0])
 
 
+def _grouped(n, sizes, seed):
+    """n records whose 10-byte prefixes come in runs of the given sizes (cycled; distinct prefixes, shuffled
+    positions), key bytes 10..23 low-entropy."""
+    rng = np.random.default_rng(seed)
+    r = gen.records(n, seed=seed, dist="uniform").reshape(n, 100)
+    gid = np.repeat(np.arange(n, dtype=np.uint64), np.resize(np.asarray(sizes), n))[:n]
+    gid = gid[rng.permutation(n)] * np.uint64(2654435761) + np.uint64(12345)  # distinct, scattered prefixes
+    r[:, 0:2] = 7
+    for b in range(8):
+        r[:, 9 - b] = (gid >> np.uint64(8 * b)) & np.uint64(0xFF)
+    r[:, 10:24] = rng.integers(0, 3, size=(n, 14))
+    return np.ascontiguousarray(r.reshape(-1))
+
+
+@pytest.mark.parametrize("sizes", [[32, 33], [31, 32, 33, 34, 2], [2, 3, 5], [64, 1, 1]])
+def test_tie_group_sizes(cuda_ok, sizes):
+    """Groups at the warp-sort boundary (32 small, 33 large) and many tiny groups (about 120K), all found
+    and fixed on the device; the few large ones go through the window passes on their slices."""
+    import paper_1909_08006_b200 as ley
+
+    n = 300_000 if max(sizes) <= 5 else 30 * sum(sizes)  # <= 64 large groups when they exist
+    recs = _grouped(n, sizes, 5 + len(sizes))
+    x = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x)
+    ley.ley_sort(x, out, n, key_bytes=24)
+    assert np.array_equal(out.cpu().numpy(), _expect(recs, 24)[0])
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_tie_scan_digest_collision(cuda_ok, seed):
     """The tie-group scan reads the prefix digests K-e writes (k_bucket.cu prefix_digest) and verifies
