@@ -268,13 +268,13 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     uint32_t* lasts = firsts + a256(4ull * cap) / 4;
     uint32_t* large_f = lasts + a256(4ull * cap) / 4;  // [kLargeCap] each, then the 4 counts
     uint32_t* large_l = large_f + kLargeCap;
-    uint32_t* counts = large_l + kLargeCap;
+    uint32_t* counts = large_l + kLargeCap;  // [8]
     if ((st = prof.begin("tie groups"))) return st;
-    LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 16, s));
+    LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 32, s));
     LEY_CUDA("tie groups", launch_tie_groups(out, digest, n, firsts, lasts, cap, counts, ctx.sms, s));
     LEY_CUDA("tie groups", launch_fix_small_groups(out, digest, n, firsts, lasts, counts, key_bytes, large_f, large_l,
                                                    kLargeCap, ctx.sms, s));
-    prof.launches += 3;
+    prof.launches += 4;
     // one read-back: the four counts and the two short large-group lists
     uint32_t h[2 * kLargeCap + 4];
     LEY_CUDA("tie groups", cudaMemcpyAsync(h, large_f, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -3,12 +3,15 @@
 // bytes (ties by input index); only records whose 10-byte prefixes tie need the rest of the key:
 //   kt_tie_groups  one pass over the sorted records: maximal runs of equal 10-byte prefixes ("tie groups",
 //                  >= 2 records) are reported as first and last positions (two unordered lists)
-//   kt_fix_small   one warp per group first: the warp finds the group's length itself (a ballot of prefix
-//                  equality over the next 32 records — the run is contiguous and maximal); a group of <= 32
-//                  records is ranked lane by lane by (key bytes [10, key_bytes), position) — a comparison
-//                  sort on the records themselves — and rewritten in place in that order; a longer one is
+//   kt_large_lasts the "large lasts" list (a group is large, > 32 records, iff the record 32 before its
+//                  last ties)
+//   kt_fix_tiny    eight lanes per group first: the lanes find the group's length themselves (a ballot of
+//                  prefix equality over the next 8 records — the run is contiguous and maximal); a group of
+//                  <= 7 records is ranked lane by lane by (key bytes [10, key_bytes), position) — a
+//                  comparison sort on the records themselves — and rewritten in place in that order; a
+//                  longer one goes to the "mid" list (written over the lasts, no longer needed)
+//   kt_fix_small   the same with a whole warp per mid group for groups of <= 32 records; a longer one is
 //                  appended to the short "large firsts" list instead
-//   kt_large_lasts the matching "large lasts" list (a group is large iff the record 32 before its last ties)
 // No list is ever sorted or shipped to the host except the two large lists (<= 65 entries read); large
 // groups are sorted by the LSD window passes restricted to their slice (internal.cu).
 #include "common.cuh"
@@ -80,12 +83,52 @@ __device__ __forceinline__ bool same_prefix(const uint8_t* recs, const uint64_t*
   return dg[a] == dg[b] && prefix10_equal(recs + a * kRecordBytes, recs + b * kRecordBytes);
 }
 
+// Lanes [0, len) of a group of len records starting at f (all lanes of the warp call it): rank by
+// (key bytes [10, kb), position), then rewrite the group in place in that order.
+__device__ __forceinline__ void rank_and_rewrite(uint8_t* recs, uint32_t f, uint32_t len, bool active, uint32_t idx,
+                                                 uint32_t kb) {
+  const uint32_t me = f + idx;
+  uint32_t rank = 0;
+  if (active)
+    for (uint32_t m = 0; m < len; ++m)
+      if (m != idx && tail_less(recs, f + m, me, kb)) ++rank;
+  uint32_t w[kRecordWords];
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(recs + (uint64_t)me * kRecordBytes);
+#pragma unroll
+  for (int q = 0; q < (int)kRecordWords; ++q) w[q] = active ? src[q] : 0u;
+  __syncwarp();  // every lane holds its record before any is overwritten
+  if (active) {
+    uint32_t* dst = reinterpret_cast<uint32_t*>(recs + (uint64_t)(f + rank) * kRecordBytes);
+#pragma unroll
+    for (int q = 0; q < (int)kRecordWords; ++q) dst[q] = w[q];
+  }
+  __syncwarp();
+}
+
+__global__ void kt_fix_tiny(uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
+                            const uint32_t* __restrict__ firsts, uint32_t* __restrict__ counts, uint32_t kb,
+                            uint32_t* __restrict__ mid, uint32_t cap) {
+  const int lane = threadIdx.x & 31, sub = lane >> 3, sl = lane & 7;
+  const uint32_t step = gridDim.x * (blockDim.x >> 3);  // four groups per warp per iteration
+  const uint32_t ngroups = counts[0];
+  for (uint32_t g0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; g0 < ngroups; g0 += step) {
+    const uint32_t g = g0 + sub;
+    const bool valid = g < ngroups;
+    const uint32_t f = valid ? firsts[g] : 0u;
+    const bool eq = valid && (uint64_t)f + sl < n && same_prefix(recs, dg, f, (uint64_t)f + sl);
+    const uint32_t len = __popc((__ballot_sync(0xffffffffu, eq) >> (sub * 8)) & 0xFFu);
+    const bool tiny = valid && len < 8;  // the record after the run was seen (or is past n)
+    warp_append(valid && !tiny && sl == 0, f, mid, &counts[4], cap);
+    rank_and_rewrite(recs, f, len, tiny && (uint32_t)sl < len, (uint32_t)sl, kb);
+  }
+}
+
 __global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
-                             const uint32_t* __restrict__ firsts, uint32_t* __restrict__ counts, uint32_t kb,
-                             uint32_t* __restrict__ large_f, uint32_t large_cap) {
+                             const uint32_t* __restrict__ firsts, const uint32_t* __restrict__ count, uint32_t kb,
+                             uint32_t* __restrict__ counts, uint32_t* __restrict__ large_f, uint32_t large_cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  const uint32_t ngroups = counts[0];
+  const uint32_t ngroups = *count;
   for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups; g += warps) {
     const uint32_t f = firsts[g];
     const bool eq = (uint64_t)f + lane < n && same_prefix(recs, dg, f, (uint64_t)f + lane);
@@ -97,23 +140,7 @@ __global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint64_t* __restr
       }
       continue;
     }
-    const bool active = (uint32_t)lane < len;
-    const uint32_t me = f + lane;
-    uint32_t rank = 0;
-    if (active)
-      for (uint32_t m = 0; m < len; ++m)
-        if (m != (uint32_t)lane && tail_less(recs, f + m, me, kb)) ++rank;
-    uint32_t w[kRecordWords];
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(recs + (uint64_t)me * kRecordBytes);
-#pragma unroll
-    for (int q = 0; q < (int)kRecordWords; ++q) w[q] = active ? src[q] : 0u;
-    __syncwarp();  // every lane holds its record before any is overwritten
-    if (active) {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(recs + (uint64_t)(f + rank) * kRecordBytes);
-#pragma unroll
-      for (int q = 0; q < (int)kRecordWords; ++q) dst[q] = w[q];
-    }
-    __syncwarp();
+    rank_and_rewrite(recs, f, len, (uint32_t)lane < len, (uint32_t)lane, kb);
   }
 }
 
@@ -142,14 +169,18 @@ cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t 
 }
 
 cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, const uint32_t* firsts,
-                                    const uint32_t* lasts, uint32_t* counts, uint32_t key_bytes, uint32_t* large_f,
+                                    uint32_t* lasts, uint32_t* counts, uint32_t key_bytes, uint32_t* large_f,
                                     uint32_t* large_l, uint32_t large_cap, int sms, cudaStream_t s) {
   if (n < 2) return cudaSuccess;
-  // group counts live on the device: persistent grids, grid-stride over counts[0] / counts[1]
-  kt_fix_small<<<sms * 8, 256, 0, s>>>(recs, dg, n, firsts, counts, key_bytes, large_f, large_cap);
+  // group counts live on the device: persistent grids, grid-stride over the counts. The large lasts first:
+  // the tiny pass then reuses the lasts array for its mid list (counts[4]).
+  kt_large_lasts<<<sms * 4, 256, 0, s>>>(recs, dg, lasts, counts, large_l, large_cap);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  kt_large_lasts<<<sms * 4, 256, 0, s>>>(recs, dg, lasts, counts, large_l, large_cap);
+  uint32_t* mid = lasts;
+  kt_fix_tiny<<<sms * 8, 256, 0, s>>>(recs, dg, n, firsts, counts, key_bytes, mid, (uint32_t)(n / 2 + 1));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  kt_fix_small<<<sms * 8, 256, 0, s>>>(recs, dg, n, mid, counts + 4, key_bytes, counts, large_f, large_cap);
   return cudaGetLastError();
 }
 

@@ -95,13 +95,14 @@ def _grouped(n, sizes, seed):
     return np.ascontiguousarray(r.reshape(-1))
 
 
-@pytest.mark.parametrize("sizes", [[32, 33], [31, 32, 33, 34, 2], [2, 3, 5], [64, 1, 1]])
+@pytest.mark.parametrize("sizes", [[32, 33], [31, 32, 33, 34, 2], [2, 3, 5], [7, 8, 9, 1], [64, 1, 1]])
 def test_tie_group_sizes(cuda_ok, sizes):
-    """Groups at the warp-sort boundary (32 small, 33 large) and many tiny groups (about 120K), all found
-    and fixed on the device; the few large ones go through the window passes on their slices."""
+    """Groups at the eight-lane boundary (7 tiny, 8 and 9 to the warp pass), at the warp-sort boundary (32
+    small, 33 large) and many tiny groups (about 10^5), all found and fixed on the device; the few large
+    ones go through the window passes on their slices."""
     import paper_1909_08006_b200 as ley
 
-    n = 300_000 if max(sizes) <= 5 else 30 * sum(sizes)  # <= 64 large groups when they exist
+    n = 300_000 if max(sizes) <= 9 else 30 * sum(sizes)  # <= 64 large groups when they exist
     recs = _grouped(n, sizes, 5 + len(sizes))
     x = torch.from_numpy(recs).cuda()
     out = torch.empty_like(x)
