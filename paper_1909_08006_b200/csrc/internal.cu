@@ -274,8 +274,8 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     LEY_CUDA("tie groups", launch_tie_groups(out, digest, n, firsts, lasts, cap, counts, ctx.sms, s));
     LEY_CUDA("tie groups", launch_fix_small_groups(out, digest, n, firsts, lasts, counts, key_bytes, large_f, large_l,
                                                    kLargeCap, ctx.sms, s));
-    prof.launches += 4;
-    // one read-back: the four counts and the two short large-group lists
+    prof.launches += 6;
+    // one read-back: the counts and the two short large-group lists
     uint32_t h[2 * kLargeCap + 4];
     LEY_CUDA("tie groups", cudaMemcpyAsync(h, large_f, sizeof(h), cudaMemcpyDeviceToHost, s));
     LEY_CUDA("tie groups", cudaStreamSynchronize(s));

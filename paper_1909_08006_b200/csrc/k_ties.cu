@@ -3,15 +3,18 @@
 // bytes (ties by input index); only records whose 10-byte prefixes tie need the rest of the key:
 //   kt_tie_groups  one pass over the sorted records: maximal runs of equal 10-byte prefixes ("tie groups",
 //                  >= 2 records) are reported as first and last positions (two unordered lists)
-//   kt_large_lasts the "large lasts" list (a group is large, > 32 records, iff the record 32 before its
-//                  last ties)
+//   kt_large_lasts the "large lasts" list (a group is large, > kCtaGroup records, iff the record kCtaGroup
+//                  before its last ties)
 //   kt_fix_tiny    eight lanes per group first: the lanes find the group's length themselves (a ballot of
 //                  prefix equality over the next 8 records — the run is contiguous and maximal); a group of
 //                  <= 7 records is ranked lane by lane by (key bytes [10, key_bytes), position) — a
 //                  comparison sort on the records themselves — and rewritten in place in that order; a
 //                  longer one goes to the "mid" list (written over the lasts, no longer needed)
-//   kt_fix_small   the same with a whole warp per mid group for groups of <= 32 records; a longer one is
-//                  appended to the short "large firsts" list instead
+//   kt_fix_small   the same with a whole warp per mid group for groups of <= 32 records; a longer one goes
+//                  to the "big" list (written over the firsts)
+//   kt_fix_cta     one CTA per big group, staged in shared memory and ordered there: groups of <= 128
+//                  records by small CTAs (many per SM), longer ones passed on to CTAs with 100 KB staging for
+//                  <= kCtaGroup records; longer still: appended to the short "large firsts" list
 // No list is ever sorted or shipped to the host except the two large lists (<= 65 entries read); large
 // groups are sorted by the LSD window passes restricted to their slice (internal.cu).
 #include "common.cuh"
@@ -19,6 +22,8 @@
 
 namespace ley {
 namespace {
+
+constexpr uint32_t kCtaGroup = 1024;  // largest group kt_fix_cta sorts (100 KB of shared memory staging)
 
 __device__ __forceinline__ bool prefix10_equal(const uint8_t* a, const uint8_t* b) {
   // records are 4-byte aligned: words 0, 1 and the low half of word 2
@@ -125,7 +130,7 @@ __global__ void kt_fix_tiny(uint8_t* __restrict__ recs, const uint64_t* __restri
 
 __global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
                              const uint32_t* __restrict__ firsts, const uint32_t* __restrict__ count, uint32_t kb,
-                             uint32_t* __restrict__ counts, uint32_t* __restrict__ large_f, uint32_t large_cap) {
+                             uint32_t* __restrict__ counts, uint32_t* __restrict__ big) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint32_t ngroups = *count;
@@ -134,13 +139,100 @@ __global__ void kt_fix_small(uint8_t* __restrict__ recs, const uint64_t* __restr
     const bool eq = (uint64_t)f + lane < n && same_prefix(recs, dg, f, (uint64_t)f + lane);
     const uint32_t len = __popc(__ballot_sync(0xffffffffu, eq));  // the run from f is contiguous
     if (len == 32 && (uint64_t)f + 32 < n && same_prefix(recs, dg, f, (uint64_t)f + 32)) {
-      if (lane == 0) {
-        const uint32_t at = atomicAdd(&counts[2], 1u);
-        if (at < large_cap) large_f[at] = f;
-      }
+      if (lane == 0) big[atomicAdd(&counts[5], 1u)] = f;  // (one per warp-group: no aggregation needed)
       continue;
     }
     rank_and_rewrite(recs, f, len, (uint32_t)lane < len, (uint32_t)lane, kb);
+  }
+}
+
+// One CTA per listed group known to be longer than LO records: a group of <= CAPG records is staged in
+// shared memory, ordered there (rank by pairs up to 128 records, else a bitonic network) and written back
+// in place; a longer one goes to `next` (entries past next_cap dropped). Two tiers: <= 128 records with
+// 12.8 KB of staging (many CTAs per SM), <= 1024 with 100 KB.
+template <uint32_t LO, uint32_t CAPG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    kt_fix_cta(uint8_t* __restrict__ recs, const uint64_t* __restrict__ dg, uint64_t n,
+               const uint32_t* __restrict__ big, const uint32_t* __restrict__ count, uint32_t kb,
+               uint32_t* __restrict__ next, uint32_t* __restrict__ next_count, uint32_t next_cap) {
+  constexpr int kCtaThreads = THREADS;
+  extern __shared__ __align__(16) uint32_t s_rec[];  // [CAPG * kRecordWords]
+  __shared__ uint32_t s_len;
+  __shared__ uint32_t s_rank[CAPG];
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(s_rec);
+  const uint32_t nbig = *count;
+  for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
+    const uint32_t f = big[g];
+    if (threadIdx.x == 0) s_len = CAPG + 1;
+    __syncthreads();
+    // the run from f is contiguous: its length is the first position that does not tie with f (scanned
+    // THREADS positions at a time, stopping at the first window that holds it)
+    for (uint32_t t0 = LO + 1; t0 <= CAPG; t0 += kCtaThreads) {
+      const uint32_t t = t0 + threadIdx.x;
+      if (t <= CAPG && ((uint64_t)f + t >= n || !same_prefix(recs, dg, f, (uint64_t)f + t))) atomicMin(&s_len, t);
+      __syncthreads();
+      if (s_len <= CAPG) break;
+    }
+    const uint32_t len = s_len;
+    if (len > CAPG) {
+      if (threadIdx.x == 0) {
+        const uint32_t at = atomicAdd(next_count, 1u);
+        if (at < next_cap) next[at] = f;
+      }
+      __syncthreads();  // s_len is rewritten by the next group
+      continue;
+    }
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(recs + (uint64_t)f * kRecordBytes);
+    for (uint32_t w = threadIdx.x; w < len * kRecordWords; w += kCtaThreads) s_rec[w] = src[w];
+    // (group records y before x by (key bytes [10, kb), position); indices >= len are +infinity)
+    auto before = [&](uint32_t y, uint32_t x) -> bool {
+      if (y >= len) return false;
+      if (x >= len) return true;
+      const uint8_t* px = sb + (size_t)x * kRecordBytes;
+      const uint8_t* py = sb + (size_t)y * kRecordBytes;
+      uint32_t b = kKeyBytes;
+      while (b < kb && px[b] == py[b]) ++b;
+      return b < kb ? py[b] < px[b] : y < x;
+    };
+    uint32_t* dst = reinterpret_cast<uint32_t*>(recs + (uint64_t)f * kRecordBytes);
+    if (CAPG <= 128 || len <= 128) {
+      // small: rank of record i = how many records precede it; every ordered pair (i, m) with m before i
+      // adds one (a warp: 32 different i, one m)
+      for (uint32_t i = threadIdx.x; i < len; i += kCtaThreads) s_rank[i] = 0;
+      __syncthreads();
+      for (uint32_t p = threadIdx.x; p < len * len; p += kCtaThreads) {
+        const uint32_t m = p / len, i = p - m * len;
+        if (m != i && before(m, i)) atomicAdd(&s_rank[i], 1u);
+      }
+      __syncthreads();
+      for (uint32_t w = threadIdx.x; w < len * kRecordWords; w += kCtaThreads) {
+        const uint32_t i = w / kRecordWords, q = w - i * kRecordWords;
+        dst[(size_t)s_rank[i] * kRecordWords + q] = s_rec[w];
+      }
+    } else {
+      // larger: bitonic network over the record indices, padded to a power of two with +infinity
+      uint32_t P = 256;
+      while (P < len) P <<= 1;
+      for (uint32_t i = threadIdx.x; i < P; i += kCtaThreads) s_rank[i] = i;
+      __syncthreads();
+      for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t t = threadIdx.x; t < P / 2; t += kCtaThreads) {
+            const uint32_t i = (t / j) * 2 * j + (t % j), l = i + j;
+            const uint32_t a = s_rank[i], b = s_rank[l];
+            if (((i & k) == 0) ? before(b, a) : before(a, b)) {
+              s_rank[i] = b;
+              s_rank[l] = a;
+            }
+          }
+          __syncthreads();
+        }
+      for (uint32_t w = threadIdx.x; w < len * kRecordWords; w += kCtaThreads) {
+        const uint32_t r = w / kRecordWords, q = w - r * kRecordWords;
+        dst[w] = s_rec[(size_t)s_rank[r] * kRecordWords + q];
+      }
+    }
+    __syncthreads();  // staging reused by the next group
   }
 }
 
@@ -150,7 +242,7 @@ __global__ void kt_large_lasts(const uint8_t* __restrict__ recs, const uint64_t*
   const uint32_t nl = counts[1];
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nl; g += gridDim.x * blockDim.x) {
     const uint32_t l = lasts[g];
-    if (l >= 32 && same_prefix(recs, dg, l - 32, l)) {
+    if (l >= kCtaGroup && same_prefix(recs, dg, l - kCtaGroup, l)) {
       const uint32_t at = atomicAdd(&counts[3], 1u);  // (rare: at most a few large groups)
       if (at < large_cap) large_l[at] = l;
     }
@@ -168,7 +260,7 @@ cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, const uint32_t* firsts,
+cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts,
                                     uint32_t* lasts, uint32_t* counts, uint32_t key_bytes, uint32_t* large_f,
                                     uint32_t* large_l, uint32_t large_cap, int sms, cudaStream_t s) {
   if (n < 2) return cudaSuccess;
@@ -180,7 +272,17 @@ cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t 
   uint32_t* mid = lasts;
   kt_fix_tiny<<<sms * 8, 256, 0, s>>>(recs, dg, n, firsts, counts, key_bytes, mid, (uint32_t)(n / 2 + 1));
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  kt_fix_small<<<sms * 8, 256, 0, s>>>(recs, dg, n, mid, counts + 4, key_bytes, counts, large_f, large_cap);
+  // the firsts are no longer needed once kt_fix_tiny is done: the big list goes there (counts[5]); the
+  // mid list is free again after kt_fix_small: groups over 128 records go there (counts[6])
+  kt_fix_small<<<sms * 8, 256, 0, s>>>(recs, dg, n, mid, counts + 4, key_bytes, counts, firsts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  kt_fix_cta<32, 128, 128><<<sms * 16, 128, 128 * kRecordBytes, s>>>(recs, dg, n, firsts, counts + 5, key_bytes, mid,
+                                                                      counts + 6, (uint32_t)(n / 2 + 1));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t smem = (size_t)kCtaGroup * kRecordBytes;
+  auto k2 = kt_fix_cta<128, kCtaGroup, 512>;
+  if ((e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+  k2<<<sms * 2, 512, smem, s>>>(recs, dg, n, mid, counts + 6, key_bytes, large_f, counts + 2, large_cap);
   return cudaGetLastError();
 }
 

@@ -63,13 +63,14 @@ cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t c
 // keys > 10 bytes, hybrid form (k_ties.cu): runs of equal 10-byte prefixes in sorted records -> unordered
 // (first, last) lists (counts[0], counts[1]; entries past cap dropped; dg: the K-e prefix digests of the
 // records, or null to compare every adjacent pair on the records); then, driven by those device lists:
-// in-place comparison sort of every group of <= 32 records by key bytes [10, key_bytes) then position,
+// in-place comparison sort of every group of <= 1024 records by key bytes [10, key_bytes) then position,
 // and the firsts / lasts of the longer groups appended to large_f / large_l (counts[2], counts[3]; entries
-// past large_cap dropped; the lasts array is overwritten, counts[4] used)
+// past large_cap dropped; "large" = more than 1024 records, smaller groups sorted on the device; the
+// firsts and lasts arrays are overwritten, counts[4..5] used)
 cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
                               uint32_t* counts, int sms, cudaStream_t s);
 // (dg required here)
-cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, const uint32_t* firsts,
+cudaError_t launch_fix_small_groups(uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts,
                                     uint32_t* lasts, uint32_t* counts, uint32_t key_bytes, uint32_t* large_f,
                                     uint32_t* large_l, uint32_t large_cap, int sms, cudaStream_t s);
 // multi-pass keys: cur[j] = prev[cur[j]] (the permutation of the passes so far, k_gather.cu)

@@ -46,13 +46,14 @@ def test_device_path(cuda_ok, k, dist):
     assert torch.equal(out, out2)
 
 
-@pytest.mark.parametrize("groups", [0, 40, 3000, 1])
+@pytest.mark.parametrize("groups", [0, 40, 3000, 100, 1])
 @pytest.mark.parametrize("hybrid", [1, 0])
 def test_long_keys_tie_groups(cuda_ok, groups, hybrid):
-    """Keys of 24 bytes whose 10-byte prefixes tie in controlled ways: none (uniform), 40 large groups
-    (window passes on each slice), 3000 groups of ~67 (more large groups than the hybrid handles: the
-    plain window passes), one group holding every record; plus small groups of 2..32 around them. The
-    hybrid (key_hybrid=1) and the plain LSD passes (0) must both equal the oracle."""
+    """Keys of 24 bytes whose 10-byte prefixes tie in controlled ways: none (uniform), 40 large groups of
+    ~5000 (window passes on each slice), 3000 groups of ~67 (a CTA per group), 100 groups of ~2000 (more
+    large groups than the hybrid handles: the plain window passes), one group holding every record; plus
+    small groups of 2..32 around them. The hybrid (key_hybrid=1) and the plain LSD passes (0) must both
+    equal the oracle."""
     import paper_1909_08006_b200 as ley
 
     n = 200_001
@@ -95,11 +96,12 @@ def _grouped(n, sizes, seed):
     return np.ascontiguousarray(r.reshape(-1))
 
 
-@pytest.mark.parametrize("sizes", [[32, 33], [31, 32, 33, 34, 2], [2, 3, 5], [7, 8, 9, 1], [64, 1, 1]])
+@pytest.mark.parametrize("sizes", [[32, 33], [31, 32, 33, 34, 2], [2, 3, 5], [7, 8, 9, 1], [64, 1, 1],
+                                   [1024, 1025], [500, 67, 2]])
 def test_tie_group_sizes(cuda_ok, sizes):
-    """Groups at the eight-lane boundary (7 tiny, 8 and 9 to the warp pass), at the warp-sort boundary (32
-    small, 33 large) and many tiny groups (about 10^5), all found and fixed on the device; the few large
-    ones go through the window passes on their slices."""
+    """Groups at the eight-lane boundary (7 tiny, 8 and 9 to the warp pass), the warp boundary (32 warp,
+    33 CTA), the CTA boundary (1024 CTA, 1025 large) and many tiny groups (about 10^5), all found and fixed
+    on the device; the few large ones go through the window passes on their slices."""
     import paper_1909_08006_b200 as ley
 
     n = 300_000 if max(sizes) <= 9 else 30 * sum(sizes)  # <= 64 large groups when they exist

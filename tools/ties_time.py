@@ -10,7 +10,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1909_08006_b200 as ley  # noqa: E402
 
-for n, sizes in ((20_000_000, [2]), (20_000_000, [2, 3, 5, 8]), (20_000_000, [1])):
+for n, sizes in ((20_000_000, [2]), (20_000_000, [2, 3, 5, 8]), (20_000_000, [67]), (20_000_000, [500]),
+                 (20_000_000, [1])):
     rng = np.random.default_rng(1)
     r = rng.integers(0, 256, size=(n, 100), dtype=np.uint8)
     gid = np.repeat(np.arange(n, dtype=np.uint64), np.resize(np.asarray(sizes), n))[:n]
@@ -35,6 +36,17 @@ for n, sizes in ((20_000_000, [2]), (20_000_000, [2, 3, 5, 8]), (20_000_000, [1]
     e1.record()
     torch.cuda.synchronize()
     ley.ley_set_option("profile", 0)
-    groups = len(np.unique(gid[: min(n, 10**6)])) if sizes != [1] else 0
-    print(f"n {n:,} group sizes {sizes}: {e0.elapsed_time(e1) / reps:.2f} ms per sort; "
+    hybrid = e0.elapsed_time(e1) / reps
+    ley.ley_set_option("key_hybrid", 0)
+    ley.ley_sort(x, out, n, key_bytes=20)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        ley.ley_sort(x, out, n, key_bytes=20)
+    e1.record()
+    torch.cuda.synchronize()
+    ley.ley_set_option("key_hybrid", 1)
+    lsd = e0.elapsed_time(e1) / reps
+    print(f"n {n:,} group sizes {sizes}: {hybrid:.2f} ms per sort; "
           f"tie groups {stages.get('tie groups', 0):.2f} ms; K-de {stages.get('K-de sort+gather', 0):.2f} ms", flush=True)
+    print(f"   (LSD window passes instead of the hybrid: {lsd:.2f} ms)")
