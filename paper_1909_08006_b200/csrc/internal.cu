@@ -272,14 +272,20 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
     if ((st = prof.begin("tie groups"))) return st;
     LEY_CUDA("tie groups", cudaMemsetAsync(counts, 0, 32, s));
     LEY_CUDA("tie groups", launch_tie_groups(out, digest, n, firsts, lasts, cap, counts, ctx.sms, s));
-    LEY_CUDA("tie groups", launch_fix_small_groups(out, digest, n, firsts, lasts, counts, key_bytes, large_f, large_l,
-                                                   kLargeCap, ctx.sms, s));
-    prof.launches += 6;
-    // one read-back: the counts and the two short large-group lists
+    ++prof.launches;
+    // no tie groups (random keys): done after one small read-back, without the fixers' launches
     uint32_t h[2 * kLargeCap + 4];
-    LEY_CUDA("tie groups", cudaMemcpyAsync(h, large_f, sizeof(h), cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("tie groups", cudaStreamSynchronize(s));
     const uint32_t* hc = h + 2 * kLargeCap;
+    LEY_CUDA("tie groups", cudaMemcpyAsync(h + 2 * kLargeCap, counts, 16, cudaMemcpyDeviceToHost, s));
+    LEY_CUDA("tie groups", cudaStreamSynchronize(s));
+    if (hc[0] || hc[1]) {
+      LEY_CUDA("tie groups", launch_fix_small_groups(out, digest, n, firsts, lasts, counts, key_bytes, large_f,
+                                                     large_l, kLargeCap, ctx.sms, s));
+      prof.launches += 5;
+      // one read-back: the counts and the two short large-group lists
+      LEY_CUDA("tie groups", cudaMemcpyAsync(h, large_f, sizeof(h), cudaMemcpyDeviceToHost, s));
+      LEY_CUDA("tie groups", cudaStreamSynchronize(s));
+    }
     bool fallback = hc[0] != hc[1] || hc[0] > cap || hc[2] != hc[3] || hc[2] > kMaxLargeGroups;
     if (!fallback && hc[2]) {
       std::vector<uint32_t> f(h, h + hc[2]), l(h + kLargeCap, h + kLargeCap + hc[3]);
