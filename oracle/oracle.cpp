@@ -24,7 +24,10 @@
  * Pins (tests/test_oracle.py, -m "not gpu"): brute force over all n! orders for n <= 7, an insertion
  * sort written in Python, Python's stable sorted() on the key alone, closed forms (all-equal ->
  * identity, sorted -> identity, strictly decreasing -> reversal, single-byte-position keys), the §2.2
- * worked example (tests/golden/paper_s2_2_example.json) and the multiset-hash invariants.
+ * worked example (tests/golden/paper_s2_2_example.json) and the multiset-hash invariants; the
+ * __gnu_parallel branch (n >= 2e5) and the stage-timed form against numpy's lexsort at 2e5..5e6 records
+ * (uniform, tiny-alphabet, three-key inputs); oracle_is_sorted by accept/reject cases at every key byte.
+ * Parity unpinned: none of the functions in this file.
  *
  * Helpers: a permutation-invariant multiset hash (SPEC-style: per-record 128-bit hash summed mod
  * 2^128), an order-dependent digest (for configs whose sorted output is too big to keep on the host),
@@ -83,64 +86,57 @@ inline void add128(uint64_t* lo, uint64_t* hi, uint64_t a_lo, uint64_t a_hi) {
 
 }  // namespace
 
-extern "C" {
-
-/* Returns 0 on success, 1 if n is out of the ordinal range (n > 2^32 - 2). perm may be NULL. */
-int oracle_sort(const uint8_t* in, uint8_t* out, uint32_t* perm, uint64_t n, int threads) {
+/* The one sort body behind oracle_sort and oracle_sort_timed: extraction of the (key, pointer) tuples
+ * (P:102), the library comparison sort on (key, index), and the record scatter. When
+ * secs != NULL the three stages are timed (Table 3's stage breakdown). The comparison sort is
+ * std::sort below 2e5 tuples or with one thread, else __gnu_parallel::sort (OpenMP, `threads`); both
+ * are pinned by tests/test_oracle.py (the parallel branch against numpy's lexsort at n >= 2e5). */
+static int sort_body(const uint8_t* in, uint8_t* out, uint32_t* perm, uint64_t n, int threads, double* secs) {
   if (n > 0xFFFFFFFEULL) return 1;
+  if (secs) secs[0] = secs[1] = secs[2] = 0.0;
   if (n == 0) return 0;
   if (threads <= 0) threads = omp_get_max_threads();
+  const double t0 = omp_get_wtime();
   std::vector<Tuple> e(n);
 #pragma omp parallel for num_threads(threads) schedule(static)
   for (int64_t i = 0; i < (int64_t)n; ++i) {
     memcpy(e[i].key, in + 100 * (uint64_t)i, 10);
     e[i].idx = (uint32_t)i;
   }
+  const double t1 = omp_get_wtime();
   if (n < 200000 || threads == 1) {
     std::sort(e.begin(), e.end(), tuple_less);
   } else {
     omp_set_num_threads(threads);
     __gnu_parallel::sort(e.begin(), e.end(), tuple_less);
   }
+  const double t2 = omp_get_wtime();
 #pragma omp parallel for num_threads(threads) schedule(static)
   for (int64_t j = 0; j < (int64_t)n; ++j) {
     uint32_t p = e[j].idx;
     if (perm) perm[j] = p;
     if (out) memcpy(out + 100 * (uint64_t)j, in + 100 * (uint64_t)p, 100);
   }
+  const double t3 = omp_get_wtime();
+  if (secs) {
+    secs[0] = t1 - t0;
+    secs[1] = t2 - t1;
+    secs[2] = t3 - t2;
+  }
   return 0;
 }
 
-/* Stage-timed variant for the CPU baseline (mirrors Table 3's stage breakdown):
- * secs[0] = tuple extraction, secs[1] = sort, secs[2] = record gather. */
+extern "C" {
+
+/* Returns 0 on success, 1 if n is out of the ordinal range (n > 2^32 - 2). perm may be NULL. */
+int oracle_sort(const uint8_t* in, uint8_t* out, uint32_t* perm, uint64_t n, int threads) {
+  return sort_body(in, out, perm, n, threads, nullptr);
+}
+
+/* Stage-timed form for the CPU baseline (the same sort body; mirrors Table 3's stage breakdown,
+ * P:141-144): secs[0] = tuple extraction, secs[1] = sort, secs[2] = record gather. */
 int oracle_sort_timed(const uint8_t* in, uint8_t* out, uint64_t n, int threads, double secs[3]) {
-  if (n > 0xFFFFFFFEULL) return 1;
-  secs[0] = secs[1] = secs[2] = 0.0;
-  if (n == 0) return 0;
-  if (threads <= 0) threads = omp_get_max_threads();
-  double t0 = omp_get_wtime();
-  std::vector<Tuple> e(n);
-#pragma omp parallel for num_threads(threads) schedule(static)
-  for (int64_t i = 0; i < (int64_t)n; ++i) {
-    memcpy(e[i].key, in + 100 * (uint64_t)i, 10);
-    e[i].idx = (uint32_t)i;
-  }
-  double t1 = omp_get_wtime();
-  if (n < 200000 || threads == 1) {
-    std::sort(e.begin(), e.end(), tuple_less);
-  } else {
-    omp_set_num_threads(threads);
-    __gnu_parallel::sort(e.begin(), e.end(), tuple_less);
-  }
-  double t2 = omp_get_wtime();
-#pragma omp parallel for num_threads(threads) schedule(static)
-  for (int64_t j = 0; j < (int64_t)n; ++j)
-    memcpy(out + 100 * (uint64_t)j, in + 100 * (uint64_t)e[j].idx, 100);
-  double t3 = omp_get_wtime();
-  secs[0] = t1 - t0;
-  secs[1] = t2 - t1;
-  secs[2] = t3 - t2;
-  return 0;
+  return sort_body(in, out, nullptr, n, threads, secs);
 }
 
 /* Permutation-invariant digest: sum over records of a 128-bit record hash, mod 2^128. */
