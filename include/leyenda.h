@@ -201,8 +201,10 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    warp bitonic network (tinyBucketThreshold)       (1..64, default 16)
  *   "kd_ws"          1 = warp-specialised K-d+K-e for 513..2048-record buckets (sort warps feed gather
  *                    warps through a ring; TMA bulk record copies), 0 = alternating sort/gather CTAs
- *   "ka_stream"      1 = K-a streams records through a TMA bulk-copy ring (one persistent CTA per SM),
- *                    0 = one CTA per tile with direct key loads
+ *   "ka_stream"      K-a form: 1 (default) = one persistent CTA per SM streaming only the key rows of the
+ *                    records through a ring of TMA tensor copies (64-B L2 fetches: 72 instead of 100
+ *                    DRAM bytes per record); 2 = the same ring carrying whole records (TMA bulk
+ *                    copies); 0 = one CTA per tile with direct key loads
  *   "dist_fused"     ley_sort_dist / loopback: 1 = fused partition + exchange — K-p stores every record
  *                    straight into its owner's receive window (NCCL symmetric memory over NVLink;
  *                    SURVEY §8f NEXT 1), 0 = K-p into a local send buffer, then an NCCL all-to-all-v
@@ -218,7 +220,15 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *   "pipe_split"     ley_sort_submit: each H2D / D2H copy in this many pieces on their own streams
  *                    (1..4, default 2: more of the host link busy in each direction)
  *   "l2_fetch_bytes" cudaLimitMaxL2FetchGranularity set before each call (0 = leave the device default;
- *                    32/64/128 accepted; measured without effect on this part, kept for experiments)
+ *                    32/64/128 accepted; kept for experiments, see profiles/r02_fetch_granularity.txt)
+ *   "nccl_timeout_ms" multi-GPU fault handling ("any stage failure aborts the pipeline, reports
+ *                    the stage"): every wait on a collective polls ncclCommGetAsyncError; an NCCL error,
+ *                    or a collective still incomplete after this many ms (a peer that failed or never
+ *                    arrived), aborts the communicator (ncclCommAbort) and returns LEY_ERR_NCCL with the
+ *                    stage in ley_last_error(). An aborted communicator refuses further sorts
+ *                    (LEY_ERR_NCCL); ley_comm_destroy still releases it. Default 120000, 50..3600000.
+ *   "dist_fault_stall" test hook: after the k-th collective of a ley_sort_dist call the stream is held as
+ *                    if a peer never completed it (0 = off), exercising the timeout + abort path on one GPU.
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
 ley_status ley_set_option(const char* name, int64_t value);
 ley_status ley_get_option(const char* name, int64_t* value);
@@ -247,8 +257,9 @@ uint32_t ley_version(void); /* (major << 16) | minor */
  *   tiles t = 0..T-1, T = ceil(n / 4096): k1/w = u64[n] / u32[n] (each tile's pairs in byte-0 order:
  *   k1 = key bytes 1..8 big-endian, w = key byte 9 << 24 | index inside the tile), cnt = u32[256 * T]
  *   (cnt[b * T + t] = records of tile t with byte 0 = b), lo = u32[T * 256] (tile-local exclusive offsets),
- *   hist16 = u32[65536] (zeroed, then the count of every 2-byte prefix). stream_form: 1 = the streaming
- *   form (TMA ring), 0 = one CTA per tile. */
+ *   hist16 = u32[65536] (zeroed, then the count of every 2-byte prefix). stream_form: the K-a form of the
+ *   "ka_stream" option (1 = key rows by TMA tensor copies, 2 = whole records by TMA bulk copies, 0 = one
+ *   CTA per tile). */
 ley_status ley_test_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, void* stream);
 ley_status ley_test_tile_sort(const void* in, uint64_t n, uint64_t* k1, uint32_t* w, uint32_t* cnt, uint32_t* lo,
                               uint32_t* hist16, int stream_form, void* stream);

@@ -26,7 +26,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -397,16 +399,137 @@ struct ley_comm {
   int fused_ok = -1;        // fused exchange usable on this communicator (-1: not checked yet)
   uint64_t uid_hash = 0;    // names this communicator's shared host run scratch (external path)
   uint64_t ext_calls = 0;   // (the same count on every rank: calls are collective)
+  // fault handling ("any stage failure aborts the pipeline, reports the stage")
+  bool aborted = false;                      // ncclCommAbort ran: the communicator refuses further work
+  volatile uint32_t* stall_flag = nullptr;  // mapped pinned word releasing the fault-injection stall
+  int colls = 0;                             // collectives enqueued by the current call (test hook)
 };
 
 namespace ley {
 
 cudaError_t launch_peer_pointers(ncclWindow_t win, int G, uint8_t** out, cudaStream_t s);  // k_exchange.cu
+cudaError_t launch_stall(const volatile uint32_t* release, cudaStream_t s);                // k_exchange.cu
 
 namespace {
 
-void window_release(ley_comm* c) {
-  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+// ------------------------------------------------------------------ NCCL fault handling
+// Every NCCL call goes through comm_wait (an error aborts; ncclInProgress, which only a nonblocking
+// communicator returns, is polled through ncclCommGetAsyncError with the timeout), and every host wait on
+// a stream that carries a collective goes through comm_sync, which polls the stream and the
+// communicator's asynchronous error instead of blocking in cudaStreamSynchronize. An NCCL error, or a
+// collective still incomplete after the "nccl_timeout_ms" option (a peer that failed before it, or died),
+// aborts the communicator (ncclCommAbort: in-flight NCCL kernels exit) and returns LEY_ERR_NCCL naming the
+// stage. Communicator creation and window registration are blocking NCCL calls; the library reaches the
+// registration only after an all-rank agreement, so every rank is alive when it starts.
+using Clock = std::chrono::steady_clock;
+
+int64_t elapsed_ms(Clock::time_point t0) {
+  return std::chrono::duration_cast<std::chrono::milliseconds>(Clock::now() - t0).count();
+}
+
+void comm_abort(ley_comm* c, cudaStream_t s) {
+  if (c->stall_flag) *c->stall_flag = 1u;
+  if (c->nccl && !c->aborted) ncclCommAbort(c->nccl);
+  c->aborted = true;
+  if (!s) return;
+  // let what the aborted kernels leave on the stream drain (bounded), so no buffer is still in use
+  const auto t0 = Clock::now();
+  while (cudaStreamQuery(s) == cudaErrorNotReady && elapsed_ms(t0) < 10000)
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  cudaGetLastError();
+}
+
+ley_status comm_fail(ley_comm* c, cudaStream_t s, const std::string& stage, const std::string& why) {
+  comm_abort(c, s);
+  set_error(stage + ": " + why + " (rank " + std::to_string(c->rank) + " of " + std::to_string(c->nranks) +
+            "; communicator aborted)");
+  return LEY_ERR_NCCL;
+}
+
+// Completes one NCCL call on the communicator.
+ley_status comm_wait(ley_comm* c, cudaStream_t s, ncclResult_t r, const char* stage, const char* what) {
+  if (r == ncclSuccess) return LEY_OK;
+  if (r != ncclInProgress) return comm_fail(c, s, stage, std::string(ncclGetErrorString(r)) + " at " + what);
+  const auto t0 = Clock::now();
+  const int64_t to = options_snapshot().nccl_timeout_ms;
+  for (;;) {
+    ncclResult_t a = ncclInProgress;
+    const ncclResult_t q = ncclCommGetAsyncError(c->nccl, &a);
+    if (q != ncclSuccess) a = q;
+    if (a == ncclSuccess) return LEY_OK;
+    if (a != ncclInProgress) return comm_fail(c, s, stage, std::string(ncclGetErrorString(a)) + " at " + what);
+    if (elapsed_ms(t0) > to)
+      return comm_fail(c, s, stage, std::string("no completion after ") + std::to_string(to) + " ms at " + what);
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// Host wait for stream s, which carries collectives of c.
+ley_status comm_sync(ley_comm* c, cudaStream_t s, const char* stage) {
+  const auto t0 = Clock::now();
+  const int64_t to = options_snapshot().nccl_timeout_ms;
+  for (uint32_t spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return LEY_OK;
+    if (e != cudaErrorNotReady) {
+      set_error(std::string(stage) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") while waiting on the stream");
+      return LEY_ERR_CUDA;
+    }
+    ncclResult_t a = ncclSuccess;
+    if (ncclCommGetAsyncError(c->nccl, &a) == ncclSuccess && a != ncclSuccess && a != ncclInProgress)
+      return comm_fail(c, s, stage, std::string("NCCL asynchronous error: ") + ncclGetErrorString(a));
+    if (spin >= 64 && elapsed_ms(t0) > to)
+      return comm_fail(c, s, stage, "collective not complete after " + std::to_string(to) +
+                                        " ms (a peer failed before it or died)");
+    if (spin < 64) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// After each collective: the fault-injection hook (option dist_fault_stall = k holds the stream after the
+// k-th collective of the call, as a peer that never completes it would).
+ley_status comm_after_collective(ley_comm* c, cudaStream_t s) {
+  const int64_t k = options_snapshot().dist_fault_stall;
+  if (++c->colls != k) return LEY_OK;
+  if (!c->stall_flag) {
+    void* p = nullptr;
+    LEY_CUDA("dist fault hook", cudaHostAlloc(&p, 64, cudaHostAllocMapped));
+    c->stall_flag = static_cast<volatile uint32_t*>(p);
+  }
+  *c->stall_flag = 0u;
+  LEY_CUDA("dist fault hook", launch_stall(c->stall_flag, s));
+  return LEY_OK;
+}
+
+#define LEY_NCCLC(c, s, stage, expr)                                                   \
+  do {                                                                                  \
+    if (ley_status _st = ::ley::comm_wait((c), (s), (expr), (stage), #expr)) return _st; \
+  } while (0)
+#define LEY_COLL(c, s, stage, expr)                                                     \
+  do {                                                                                  \
+    LEY_NCCLC(c, s, stage, expr);                                                       \
+    if (ley_status _st = ::ley::comm_after_collective((c), (s))) return _st;            \
+  } while (0)
+#define LEY_CSYNC(c, s, stage)                                                          \
+  do {                                                                                  \
+    if (ley_status _st = ::ley::comm_sync((c), (s), (stage))) return _st;               \
+  } while (0)
+
+// All ranks' outcomes summed (NCCL, on s): *any = number of ranks that reported !ok.
+ley_status agree(ley_comm* comm, bool ok, cudaStream_t s, uint64_t* any) {
+  uint64_t* flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
+  const uint64_t bad = ok ? 0 : 1;
+  LEY_CUDA("dist agree", cudaMemcpyAsync(flag, &bad, 8, cudaMemcpyHostToDevice, s));
+  LEY_COLL(comm, s, "dist agree", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
+  LEY_CSYNC(comm, s, "dist agree");  // (a D2H into pageable memory would block in the copy)
+  LEY_CUDA("dist agree", cudaMemcpyAsync(any, flag, 8, cudaMemcpyDeviceToHost, s));
+  LEY_CSYNC(comm, s, "dist agree");
+  return LEY_OK;
+}
+
+ley_status window_release(ley_comm* c, cudaStream_t s) {
+  ley_status st = LEY_OK;
+  if (c->win && !c->aborted) st = comm_wait(c, s, ncclCommWindowDeregister(c->nccl, c->win), "dist window", "deregister");
   if (c->win_buf) {
     ncclMemFree(c->win_buf);
     track_device_bytes(-(int64_t)c->win_cap);
@@ -414,26 +537,60 @@ void window_release(ley_comm* c) {
   c->win = nullptr;
   c->win_buf = nullptr;
   c->win_cap = 0;
+  return st;
 }
 
 // Collective: every rank calls it with the same `bytes` (derived from the replicated send matrix), so
-// they all (re)register together. Grow-only with 25% headroom, so repeated sorts register once.
+// they all (re)register together. Grow-only with 25% headroom, so repeated sorts register once. The steps
+// a rank could fail alone (the allocation, the peer mapping) are each agreed before the next collective
+// step, so either every rank ends with a usable window (fused_ok = 1) or every rank falls back to the
+// all-to-all transport (fused_ok = 0) together; a failing collective registration is an NCCL error
+// (timeout + abort on the ranks left waiting).
 ley_status window_ensure(ley_comm* c, size_t bytes, cudaStream_t s) {
   if (c->win && c->win_cap >= bytes) return LEY_OK;
-  LEY_CUDA("dist window", cudaStreamSynchronize(s));  // nothing may still use the old window
-  window_release(c);
+  LEY_CSYNC(c, s, "dist window");  // nothing may still use the old window
+  if (ley_status st = window_release(c, s)) return st;
   size_t cap = bytes + bytes / 4;
   cap = (cap + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
-  LEY_NCCL("dist window", ncclMemAlloc(&c->win_buf, cap));
-  c->win_cap = cap;
-  track_device_bytes((int64_t)cap);
-  LEY_NCCL("dist window", ncclCommWindowRegister(c->nccl, c->win_buf, cap, &c->win, NCCL_WIN_COLL_SYMMETRIC));
-  if (!c->d_peers) LEY_CUDA("dist window", cudaMalloc(&c->d_peers, 8 * kMaxRanks));
-  LEY_CUDA("dist window", launch_peer_pointers(c->win, c->nranks, c->d_peers, s));
-  // this rank's own run goes through its local mapping: stores through the window's flat (LSA) mapping
-  // of local memory measured slower (C2 at G=1: K-p 9.0 vs 7.3 ms)
-  LEY_CUDA("dist window", cudaMemcpyAsync(c->d_peers + c->rank, &c->win_buf, 8, cudaMemcpyHostToDevice, s));
-  LEY_CUDA("dist window", cudaStreamSynchronize(s));
+  const bool alloc_ok = ncclMemAlloc(&c->win_buf, cap) == ncclSuccess && c->win_buf;
+  if (alloc_ok) {
+    c->win_cap = cap;
+    track_device_bytes((int64_t)cap);
+  } else {
+    c->win_buf = nullptr;
+  }
+  uint64_t any = 0;
+  if (ley_status st = agree(c, alloc_ok, s, &any)) return st;
+  if (any) {  // some rank could not allocate: nobody registers, everybody uses the all-to-all
+    window_release(c, s);
+    c->fused_ok = 0;
+    return LEY_OK;
+  }
+  LEY_NCCLC(c, s, "dist window", ncclCommWindowRegister(c->nccl, c->win_buf, cap, &c->win, NCCL_WIN_COLL_SYMMETRIC));
+  // every peer must be reachable through the window (one NVLink/NVSwitch domain)
+  bool peers_ok = true;
+  if (!c->d_peers && cudaMalloc(&c->d_peers, 8 * kMaxRanks) != cudaSuccess) {
+    cudaGetLastError();
+    c->d_peers = nullptr;
+    peers_ok = false;
+  }
+  if (peers_ok) {
+    LEY_CUDA("dist window", launch_peer_pointers(c->win, c->nranks, c->d_peers, s));
+    uint8_t* hp[kMaxRanks] = {};
+    LEY_CUDA("dist window", cudaMemcpyAsync(hp, c->d_peers, 8 * c->nranks, cudaMemcpyDeviceToHost, s));
+    LEY_CSYNC(c, s, "dist window");
+    for (int d = 0; d < c->nranks; ++d) peers_ok = peers_ok && hp[d] != nullptr;
+    // this rank's own run goes through its local mapping: stores through the window's flat (LSA) mapping
+    // of local memory measured slower (C2 at G=1: K-p 9.0 vs 7.3 ms)
+    LEY_CUDA("dist window", cudaMemcpyAsync(c->d_peers + c->rank, &c->win_buf, 8, cudaMemcpyHostToDevice, s));
+  }
+  if (ley_status st = agree(c, peers_ok, s, &any)) return st;
+  if (any) {
+    if (ley_status st = window_release(c, s)) return st;
+    c->fused_ok = 0;
+    return LEY_OK;
+  }
+  c->fused_ok = 1;
   return LEY_OK;
 }
 
@@ -463,7 +620,17 @@ ley_status comm_init(ley_comm** comm, int nranks, int rank, const uint8_t id[128
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
-  LEY_NCCL("comm", ncclCommInitRank(&c->nccl, nranks, uid, rank));
+  // blocking communicator (a nonblocking one sets up symmetric windows asynchronously: the peer-pointer
+  // kernel then read an unfinished window, measured); the waits that can hang on a dead peer are the stream
+  // waits after collectives, and those go through comm_sync's timeout
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 1;
+  const ncclResult_t ir = ncclCommInitRankConfig(&c->nccl, nranks, uid, rank, &cfg);
+  if (ir != ncclSuccess && ir != ncclInProgress) {
+    set_error(std::string("comm: ") + ncclGetErrorString(ir) + " at ncclCommInitRankConfig");
+    return LEY_ERR_NCCL;
+  }
+  if (ley_status st = comm_wait(c.get(), nullptr, ir, "comm", "ncclCommInitRankConfig")) return st;  // aborted
   uint64_t h = 1469598103934665603ull;  // FNV-1a of the unique id
   for (int i = 0; i < 128; ++i) h = (h ^ id[i]) * 1099511628211ull;
   c->uid_hash = h;
@@ -475,15 +642,21 @@ ley_status comm_destroy(ley_comm* comm) {
   if (!comm) return LEY_OK;
   cudaSetDevice(comm->device);
   cudaDeviceSynchronize();
-  window_release(comm);
+  ley_status st = window_release(comm, nullptr);
   if (comm->d_peers) cudaFree(comm->d_peers);
   if (comm->stage.ptr) {
     cudaFree(comm->stage.ptr);
     track_device_bytes(-(int64_t)comm->stage.cap);
   }
-  if (comm->nccl) ncclCommDestroy(comm->nccl);
+  if (comm->nccl && !comm->aborted) {
+    // finalize (collective; bounded by the timeout, which aborts instead), then free
+    const ley_status fst = comm_wait(comm, nullptr, ncclCommFinalize(comm->nccl), "comm destroy", "ncclCommFinalize");
+    if (!st) st = fst;
+    if (!comm->aborted) ncclCommDestroy(comm->nccl);
+  }
+  if (comm->stall_flag) cudaFreeHost(const_cast<uint32_t*>(comm->stall_flag));
   delete comm;
-  return LEY_OK;
+  return st;
 }
 
 namespace {
@@ -527,10 +700,11 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   {
     uint64_t* d_nl = d_tmp;
     LEY_CUDA("dist", cudaMemcpyAsync(d_nl + G, &n_local, 8, cudaMemcpyHostToDevice, s));
-    LEY_NCCL("dist allgather n", ncclAllGather(d_nl + G, d_nl, 1, ncclUint64, comm->nccl, s));
+    LEY_COLL(comm, s, "dist allgather n", ncclAllGather(d_nl + G, d_nl, 1, ncclUint64, comm->nccl, s));
     P.n_local.resize(G);
+    LEY_CSYNC(comm, s, "dist");  // (a D2H into pageable memory would block in the copy)
     LEY_CUDA("dist", cudaMemcpyAsync(P.n_local.data(), d_nl, 8 * G, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("dist", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist");
   }
   P.N = 0;
   r.gbase = 0;
@@ -551,7 +725,7 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       return LEY_ERR_CAPACITY;
     }
     if ((st = prof.begin("D5 local sort")) || (st = phase6_local_sort(r, r.in)) || (st = prof.end())) return st;
-    LEY_CUDA("dist", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist");
     *n_out_local = r.n_out;
     *out_global_offset = 0;
     prof.launches = r.launches;
@@ -561,9 +735,9 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   if ((st = prof.begin("D1 hist16+allreduce"))) return st;
   if ((st = phase1_hist(r)) || (st = host_hist_async(r))) return st;
   // global histogram (u32 sums: N < 2^32), in place once the local copy is queued; one host sync for both
-  LEY_NCCL("dist allreduce hist16", ncclAllReduce(r.d_hist, r.d_hist, 65536, ncclUint32, ncclSum, comm->nccl, s));
+  LEY_COLL(comm, s, "dist allreduce hist16", ncclAllReduce(r.d_hist, r.d_hist, 65536, ncclUint32, ncclSum, comm->nccl, s));
   LEY_CUDA("dist", cudaMemcpyAsync(r.h_hist + 65536, r.d_hist, 4 * 65536, cudaMemcpyDeviceToHost, s));
-  LEY_CUDA("dist", cudaStreamSynchronize(s));
+  LEY_CSYNC(comm, s, "dist");
   host_hist_take(r);
   P.ghist.assign(r.h_hist + 65536, r.h_hist + 2 * 65536);
   if ((st = prof.end()) || (st = prof.begin("D2 splitters"))) return st;
@@ -579,9 +753,10 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       uint64_t* d_c = d_tmp;
       uint64_t mine = r.ncand;
       LEY_CUDA("dist", cudaMemcpyAsync(d_c + G, &mine, 8, cudaMemcpyHostToDevice, s));
-      LEY_NCCL("dist allgather cand", ncclAllGather(d_c + G, d_c, 1, ncclUint64, comm->nccl, s));
+      LEY_COLL(comm, s, "dist allgather cand", ncclAllGather(d_c + G, d_c, 1, ncclUint64, comm->nccl, s));
+      LEY_CSYNC(comm, s, "dist");  // (a D2H into pageable memory would block in the copy)
       LEY_CUDA("dist", cudaMemcpyAsync(counts.data(), d_c, 8 * G, cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("dist", cudaStreamSynchronize(s));
+      LEY_CSYNC(comm, s, "dist");
     }
     uint64_t maxc = 0, total = 0;
     for (int i = 0; i < G; ++i) {
@@ -603,8 +778,8 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       LEY_CUDA("dist cand", cudaMemcpyAsync(my_rec, r.d_cand, r.ncand * kRecordBytes, cudaMemcpyDeviceToDevice, s));
       LEY_CUDA("dist cand", cudaMemcpyAsync(my_gid, r.d_cand_gidx, 4ull * r.ncand, cudaMemcpyDeviceToDevice, s));
     }
-    LEY_NCCL("dist allgather cand", ncclAllGather(my_rec, all_rec, rec_b, ncclUint8, comm->nccl, s));
-    LEY_NCCL("dist allgather cand", ncclAllGather(my_gid, all_gid, gid_b, ncclUint8, comm->nccl, s));
+    LEY_COLL(comm, s, "dist allgather cand", ncclAllGather(my_rec, all_rec, rec_b, ncclUint8, comm->nccl, s));
+    LEY_COLL(comm, s, "dist allgather cand", ncclAllGather(my_gid, all_gid, gid_b, ncclUint8, comm->nccl, s));
     uint64_t at = 0;
     for (int i = 0; i < G; ++i) {
       if (counts[i]) {
@@ -615,8 +790,9 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       }
       at += counts[i];
     }
+    LEY_CSYNC(comm, s, "dist allgather cand");  // the candidate sort below waits on the host
     if ((st = phase3_splitters(ctx, s, cat_rec, cat_gid, total, P, r.split_buf, key_bytes))) return st;
-    LEY_CUDA("dist cand", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist cand");
   }
   // P4 + C3: send counts
   if ((st = prof.end()) || (st = prof.begin("D3 send counts"))) return st;
@@ -624,9 +800,10 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   P.send_matrix.assign((size_t)G * G, 0);
   {  // the counts stay on the device: all-gathered from d_dcount, one host sync for the matrix
     uint64_t* d_m = d_tmp;
-    LEY_NCCL("dist allgather counts", ncclAllGather(r.d_dcount, d_m, G, ncclUint64, comm->nccl, s));
+    LEY_COLL(comm, s, "dist allgather counts", ncclAllGather(r.d_dcount, d_m, G, ncclUint64, comm->nccl, s));
+    LEY_CSYNC(comm, s, "dist");  // (a D2H into pageable memory would block in the copy)
     LEY_CUDA("dist", cudaMemcpyAsync(P.send_matrix.data(), d_m, 8ull * G * G, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("dist", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist");
     for (int d = 0; d < G; ++d) r.send_counts[d] = P.send_matrix[(size_t)r.rank * G + d];
   }
   // P5 + C4: partition and exchange
@@ -641,27 +818,10 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
       for (int src = 0; src < G; ++src) in_d += P.send_matrix[(size_t)src * G + d];
       most = std::max(most, in_d);
     }
-    const ley_status wst = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s);
-    if (wst && comm->fused_ok > 0) return wst;  // a window that worked failed to grow: a real error
-    if (comm->fused_ok < 0) {
-      // every peer must be reachable through the window (one NVLink/NVSwitch domain); if any rank failed
-      // to allocate/register the window or sees a null peer pointer, all ranks agree to use the all-to-all
-      // transport on this communicator
-      uint64_t bad = wst ? 1 : 0;
-      if (wst) {
-        window_release(comm);
-      } else {
-        uint8_t* hp[kMaxRanks] = {};
-        LEY_CUDA("dist window", cudaMemcpy(hp, comm->d_peers, 8 * G, cudaMemcpyDeviceToHost));
-        for (int d = 0; d < G; ++d) bad += hp[d] == nullptr;
-      }
-      LEY_CUDA("dist window", cudaMemcpyAsync(d_tmp, &bad, 8, cudaMemcpyHostToDevice, s));
-      LEY_NCCL("dist window", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
-      LEY_CUDA("dist window", cudaMemcpyAsync(&bad, d_tmp, 8, cudaMemcpyDeviceToHost, s));
-      LEY_CUDA("dist window", cudaStreamSynchronize(s));
-      comm->fused_ok = bad ? 0 : 1;
-      fused = comm->fused_ok == 1;
-    }
+    // every rank computes the same size from the replicated matrix, so all ranks (re)register together
+    // and all reach the same fused_ok
+    if ((st = window_ensure(comm, std::max<size_t>(most * kRecordBytes, 4096), s))) return st;
+    fused = comm->fused_ok == 1;
   }
   if (fused) {
     // fused: K-p stores each destination run straight into its owner's symmetric
@@ -670,7 +830,8 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
     dist_dest_offsets(P.send_matrix.data(), G, r.rank, dst_off);
     if (r.n && (st = phase5_partition(r, P, nullptr, comm->d_peers, dst_off, G > 1))) return st;
     if ((st = prof.end()) || (st = prof.begin("D4b exchange"))) return st;
-    LEY_NCCL("dist exchange", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
+    LEY_COLL(comm, s, "dist exchange", ncclAllReduce(d_tmp, d_tmp, 1, ncclUint64, ncclSum, comm->nccl, s));
+    LEY_CSYNC(comm, s, "dist exchange");  // the local sort below waits on the host
     recv = static_cast<const uint8_t*>(comm->win_buf);
   } else {
     if ((st = phase5_partition_send(r, P))) return st;
@@ -678,24 +839,25 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
     if ((st = ensure_buffer(r.recv_buf, std::max<size_t>(r.n_out * kRecordBytes, 256), "dist exchange", s))) return st;
     DeviceBuffer& rb = r.recv_buf;
     const uint8_t* send = static_cast<const uint8_t*>(r.send_buf.ptr);
-    LEY_NCCL("dist exchange", ncclGroupStart());
+    LEY_NCCLC(comm, s, "dist exchange", ncclGroupStart());
     for (int peer = 0; peer < G; ++peer) {
       const uint64_t sc = P.send_matrix[(size_t)r.rank * G + peer];
       if (sc)
-        LEY_NCCL("dist exchange", ncclSend(send + r.send_off[peer] * kRecordBytes, sc * kRecordBytes, ncclUint8,
+        LEY_NCCLC(comm, s, "dist exchange", ncclSend(send + r.send_off[peer] * kRecordBytes, sc * kRecordBytes, ncclUint8,
                                            peer, comm->nccl, s));
       if (r.recv_counts[peer])
-        LEY_NCCL("dist exchange", ncclRecv(static_cast<uint8_t*>(rb.ptr) + r.recv_off[peer] * kRecordBytes,
+        LEY_NCCLC(comm, s, "dist exchange", ncclRecv(static_cast<uint8_t*>(rb.ptr) + r.recv_off[peer] * kRecordBytes,
                                            r.recv_counts[peer] * kRecordBytes, ncclUint8, peer, comm->nccl, s));
     }
-    LEY_NCCL("dist exchange", ncclGroupEnd());
+    LEY_COLL(comm, s, "dist exchange", ncclGroupEnd());
+    LEY_CSYNC(comm, s, "dist exchange");
     recv = static_cast<uint8_t*>(rb.ptr);
   }
   // P6: local sort of the received range
   if ((st = prof.end()) || (st = prof.begin("D5 local sort"))) return st;
   if ((st = phase6_local_sort(r, recv))) return st;
   if ((st = prof.end())) return st;
-  LEY_CUDA("dist", cudaStreamSynchronize(s));
+  LEY_CSYNC(comm, s, "dist");
   *n_out_local = r.n_out;
   *out_global_offset = r.out_off;
   prof.launches = r.launches + P.launches;
@@ -751,17 +913,6 @@ std::string shared_scratch_open(const std::string& name, size_t bytes, bool crea
   return "";
 }
 
-// All ranks' outcomes summed (NCCL, on s): 0 iff every rank succeeded.
-ley_status agree(ley_comm* comm, bool ok, cudaStream_t s, uint64_t* any) {
-  uint64_t* flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
-  const uint64_t bad = ok ? 0 : 1;
-  LEY_CUDA("dist agree", cudaMemcpyAsync(flag, &bad, 8, cudaMemcpyHostToDevice, s));
-  LEY_NCCL("dist agree", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
-  LEY_CUDA("dist agree", cudaMemcpyAsync(any, flag, 8, cudaMemcpyDeviceToHost, s));
-  LEY_CUDA("dist agree", cudaStreamSynchronize(s));
-  return LEY_OK;
-}
-
 // SURVEY §8e "External at 8 GPUs": runs of every rank's pinned host slice into the shared scratch (global
 // layout), samples broadcast to every rank, identical splitters and slice bounds everywhere, and rank r
 // merging global sorted positions [floor(r N/G), floor((r+1) N/G)) into its out_local (external.cu).
@@ -781,9 +932,10 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
   {
     uint64_t* d = reinterpret_cast<uint64_t*>(comm->state.d_status);
     LEY_CUDA("dist external", cudaMemcpyAsync(d + G, &n_local, 8, cudaMemcpyHostToDevice, s));
-    LEY_NCCL("dist external", ncclAllGather(d + G, d, 1, ncclUint64, comm->nccl, s));
+    LEY_COLL(comm, s, "dist external", ncclAllGather(d + G, d, 1, ncclUint64, comm->nccl, s));
+    LEY_CSYNC(comm, s, "dist external");  // (a D2H into pageable memory would block in the copy)
     LEY_CUDA("dist external", cudaMemcpyAsync(nl.data(), d, 8 * G, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("dist external", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist external");
   }
   const ExtDistPlan P = ext_dist_plan(nl, budget);
   if (P.N > LEY_MAX_RECORDS) {
@@ -824,20 +976,28 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
   quiet.ctx = &ctx;
   quiet.stream = s;
   // a10: this rank's runs; then every rank's runs must be in the scratch before anyone reads them
-  if ((st = ext_dist_runs(ctx, P, rank, in, h_runs, key_bytes, s, quiet))) return fail(st);
-  LEY_CUDA("dist external", cudaStreamSynchronize(s));
+  // (agreed: a rank whose run generation failed must not leave the others in the broadcasts below)
+  ley_status rst = ext_dist_runs(ctx, P, rank, in, h_runs, key_bytes, s, quiet);
+  if (!rst) rst = comm_sync(comm, s, "dist external runs");
+  if (comm->aborted) return fail(rst);
+  if ((st = agree(comm, rst == LEY_OK, s, &any))) return fail(st);
+  if (rst) return fail(rst);
+  if (any) {
+    set_error("dist external: another rank failed its run generation");
+    return fail(LEY_ERR_NCCL);
+  }
   // samples: rank r's block of the run-ordered sample set broadcast from rank r (the all-reduce inside
   // the group also orders every rank's run D2H before the partition phase reads the scratch)
   uint8_t* samp = ext_dist_samples(ctx, P);
-  LEY_NCCL("dist external", ncclGroupStart());
+  LEY_NCCLC(comm, s, "dist external", ncclGroupStart());
   for (int r = 0; r < G; ++r) {
     const uint64_t c = (P.samp_off[r + 1] - P.samp_off[r]) * kRecordBytes;
     if (c) {
       uint8_t* blk = samp + P.samp_off[r] * kRecordBytes;
-      LEY_NCCL("dist external", ncclBroadcast(blk, blk, c, ncclUint8, r, comm->nccl, s));
+      LEY_COLL(comm, s, "dist external", ncclBroadcast(blk, blk, c, ncclUint8, r, comm->nccl, s));
     }
   }
-  LEY_NCCL("dist external", ncclGroupEnd());
+  LEY_COLL(comm, s, "dist external", ncclGroupEnd());
   if ((st = agree(comm, true, s, &any))) return fail(st);
   // a11 (identical on every rank) and a12 (this rank's range); every rank checks its capacity first
   const uint64_t lo = (uint64_t)((unsigned __int128)rank * P.N / (unsigned)G);
@@ -851,7 +1011,7 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
   if ((st = ext_dist_partition(ctx, P, h_runs, key_bytes, s, quiet, parts))) return fail(st);
   if ((st = ext_dist_merge(ctx, P, parts, rank, h_runs, out, cap, n_out_local, out_global_offset, key_bytes, s, quiet)))
     return fail(st);
-  LEY_CUDA("dist external", cudaStreamSynchronize(s));
+  LEY_CSYNC(comm, s, "dist external");
   // nobody may unmap a scratch another rank still reads: one last agreement
   if ((st = agree(comm, true, s, &any))) return fail(st);
   record_launches(quiet.launches);
@@ -866,6 +1026,11 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
 ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, void* out_local, uint64_t out_capacity,
                      uint64_t* n_out_local, uint64_t* out_global_offset, uint64_t budget, uint32_t key_bytes,
                      cudaStream_t s) {
+  if (comm->aborted) {
+    set_error("dist: the communicator was aborted by an earlier failure (destroy it and create a new one)");
+    return LEY_ERR_NCCL;
+  }
+  comm->colls = 0;
   LEY_CUDA("dist", cudaSetDevice(comm->device));
   int kind = -1;  // 0 device, 1 pinned host
   const void* ptrs[2] = {n_local ? in_local : nullptr, out_capacity ? out_local : nullptr};
@@ -901,10 +1066,11 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
     }
     const uint64_t bad = fits ? 0 : 1;
     LEY_CUDA("dist staging", cudaMemcpyAsync(flag, &bad, 8, cudaMemcpyHostToDevice, s));
-    LEY_NCCL("dist staging", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
+    LEY_COLL(comm, s, "dist staging", ncclAllReduce(flag, flag, 1, ncclUint64, ncclSum, comm->nccl, s));
     uint64_t any = 0;
+    LEY_CSYNC(comm, s, "dist staging");  // (a D2H into pageable memory would block in the copy)
     LEY_CUDA("dist staging", cudaMemcpyAsync(&any, flag, 8, cudaMemcpyDeviceToHost, s));
-    LEY_CUDA("dist staging", cudaStreamSynchronize(s));
+    LEY_CSYNC(comm, s, "dist staging");
     if (!any && (st_ = ensure_buffer(comm->stage, std::max<size_t>(a_in + a_out, 256), "dist staging", s))) return st_;
     if (any) external = true;
   }
@@ -919,7 +1085,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   if (st) return st;
   if (*n_out_local)
     LEY_CUDA("dist D2H", cudaMemcpyAsync(out_local, dout, *n_out_local * kRecordBytes, cudaMemcpyDeviceToHost, s));
-  LEY_CUDA("dist D2H", cudaStreamSynchronize(s));
+  LEY_CSYNC(comm, s, "dist D2H");
   return LEY_OK;
 }
 
@@ -1077,7 +1243,8 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
     if (opts.dist_fused) {
       uint64_t dst_off[kMaxRanks];
       dist_dest_offsets(P.send_matrix.data(), G, i, dst_off);
-      if ((st = phase5_partition(r, P, rbuf.data(), nullptr, dst_off, false))) return st;
+      // remote = G > 1, exactly as the NCCL path launches it: the per-CTA system-scope fence form runs
+      if ((st = phase5_partition(r, P, rbuf.data(), nullptr, dst_off, G > 1))) return st;
     } else {
       if ((st = phase5_partition_send(r, P))) return st;
       for (int d = 0; d < G; ++d) {

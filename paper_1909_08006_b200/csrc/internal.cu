@@ -70,6 +70,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   tu.kd_digit_bits = (int)o.kd_digit_bits;
   tu.kd_insert_max = (int)o.kd_insert_max;
   tu.kd_ws = (int)o.kd_ws;
+  tu.ws_tma = (int)o.ws_gather_tma;
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;
@@ -83,7 +84,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 
   // ---------------------------------------------------------------- K-a
   if ((st = prof.begin("K-a tile sort"))) return st;
-  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, o.ka_stream != 0,
+  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, (int)o.ka_stream,
                                                 key, s));
   ++launches;
   if ((st = prof.end())) return st;
@@ -126,7 +127,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   bind_lists(kd_cap);
   LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
   ++launches;
-  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, digest, s, &launches));
+  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, n, out, digest, s, &launches));
   LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
   LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
   uint32_t nbig = host_cnt[0];
@@ -183,7 +184,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     launches += 6;
     if ((st = prof.end())) return st;
     if ((st = prof.begin("K-de sort+gather"))) return st;
-    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, out, digest, s, &launches));
+    LEY_CUDA("K-c' recursion", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, n, out, digest, s, &launches));
     LEY_CUDA("K-c' recursion", launch_publish_u32(big_count, host_cnt_dev, s));
     LEY_CUDA("K-c' recursion", cudaStreamSynchronize(s));
     nbig = host_cnt[0];
@@ -211,8 +212,9 @@ uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm) {
 }
 
 namespace {
-// tie groups of <= 32 records: one warp each, comparison sort (k_ties.cu); larger ones: window passes on
-// their slice, unless there are more than this many
+// tie groups of <= 1024 records are sorted on the device (k_ties.cu: eight lanes for <= 7 records, a warp
+// for <= 32, one CTA for <= 128 / <= 1024); only longer ones get window passes on their slice, unless
+// there are more than this many
 constexpr size_t kMaxLargeGroups = 64;
 constexpr uint32_t kLargeCap = kMaxLargeGroups + 1;  // large-group list entries read back
 
@@ -291,6 +293,8 @@ ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* 
       std::vector<uint32_t> f(h, h + hc[2]), l(h + kLargeCap, h + kLargeCap + hc[3]);
       std::sort(f.begin(), f.end());
       std::sort(l.begin(), l.end());
+      // the passes open their own profiler ranges: close "tie groups" first (ranges do not nest)
+      if ((st = prof.end()) || (st = prof.begin("tie group passes"))) return st;
       for (size_t g = 0; g < f.size() && !st; ++g) {
         // the passes need a 16-byte-aligned slice: start at the record index rounded down to a multiple
         // of 4 and sort by the whole key (window 0 too), so the up to 3 records before the group — already

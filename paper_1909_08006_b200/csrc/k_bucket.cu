@@ -34,8 +34,12 @@ constexpr int kGroup = 32;                     // records per warp gather group
 constexpr int kWindow = 112;                   // 7 x 16-byte chunks hold any 4-byte-aligned 100-byte record
 constexpr int kStageBytes = kGroup * kWindow;  // 3584 B per gathering warp
 
-__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+// 16-byte chunk of a record window. .L2::64B caps the L2's DRAM fetch for the miss at 64 B: a plain miss
+// is promoted to the whole 128-B line, so a random 100-B record cost 224 DRAM bytes instead of 162
+// (profiles/r02_fetch_granularity.txt). src_bytes < 16 zero-fills the rest (the input's last chunk).
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem_addr), "l"(gptr), "r"(src_bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void stg_cs_u32(uint32_t* p, uint32_t v) {
@@ -53,8 +57,9 @@ __device__ __forceinline__ uint64_t prefix_digest(const uint32_t* w) {
 // of 32 records, through `stage` (kStageBytes, 16-byte aligned). perm lives in shared memory. With
 // dg_base, also dg_base[i] = prefix_digest(record).
 __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
-                                            const uint8_t* __restrict__ in, uint8_t* __restrict__ out_base,
-                                            uint8_t* stage, uint64_t* __restrict__ dg_base) {
+                                            const uint8_t* __restrict__ in, uint64_t in_bytes,
+                                            uint8_t* __restrict__ out_base, uint8_t* stage,
+                                            uint64_t* __restrict__ dg_base) {
   const int lane = threadIdx.x & 31;
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
   for (uint32_t g0 = first; g0 < s; g0 += stride) {
@@ -65,9 +70,9 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
       const int cidx = q * 32 + lane;
       const int r = cidx / 7, c = cidx - r * 7;
       const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
-      if (r < (int)cnt)
-        cp_async16(stage_s + r * kWindow + c * 16,
-                   in + ((((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16));
+      const uint64_t a = (((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16;
+      if (r < (int)cnt && a < in_bytes)  // (chunks past the input's end hold no record byte)
+        cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u);
     }
     cp_async_wait_all();
     __syncwarp();
@@ -101,8 +106,8 @@ template <bool DG>
 __global__ void __launch_bounds__(256)
     kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                  const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                 uint64_t* __restrict__ dg) {
+                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint64_t in_bytes,
+                 uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
   __shared__ __align__(16) uint8_t s_stage[8][kStageBytes];
   __shared__ uint32_t s_perm[8][32];
   const uint32_t nitems = *count;
@@ -139,8 +144,8 @@ __global__ void __launch_bounds__(256)
     }
     __syncwarp();
     if (out)  // (perm-only mode: the resident host path gathers later, chunk by chunk)
-      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, out + (uint64_t)sg.start * kRecordBytes, s_stage[wib],
-                  DG ? dg + sg.start : nullptr);
+      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, in_bytes, out + (uint64_t)sg.start * kRecordBytes,
+                  s_stage[wib], DG ? dg + sg.start : nullptr);
   }
 }
 
@@ -227,8 +232,8 @@ template <uint32_t CAP, int THREADS, bool DG>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 8)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                uint64_t* __restrict__ dg) {
+                uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint64_t in_bytes,
+                uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
   using L = KdLayout<CAP, THREADS>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int WARPS = L::WARPS;
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     if (perm)
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
     if (out && warp < L::GWARPS)
-      warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in,
+      warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in, in_bytes,
                   out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
                   DG ? dg + sg.start : nullptr);
     __syncthreads();  // staging (and s_perm) reused by the next bucket
@@ -428,7 +433,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
 template <uint32_t CAP, int THREADS, bool DG>
 cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                             const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                            const uint8_t* in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+                            const uint8_t* in, uint64_t in_bytes, uint8_t* out, uint64_t* dg, cudaStream_t s) {
   auto kern = kd_cta_sort<CAP, THREADS, DG>;
   const size_t smem = KdLayout<CAP, THREADS>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -437,7 +442,7 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out, dg);
+  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, in_bytes, out, dg);
   if (getenv("LEY_DEBUG_SYNC")) {
     fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
     cudaError_t e2 = cudaStreamSynchronize(s);
@@ -456,11 +461,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}"
                ::"r"(a), "r"(parity) : "memory");
 }
-// TMA bulk copy global -> shared, completion counted in bytes on an mbarrier
+// One record's 16-byte-aligned 112-byte window by a TMA tensor copy, completion counted in bytes on an
+// mbarrier. The tensor map views the records as [n/4 groups][25 rows][16 B] (group pitch 400 B): record
+// p = 4g + j starts in row floor(100 j / 16) = 0, 6, 12, 18 of group g and its window is the box of 7 rows
+// there (never past row 24). The map's L2 promotion is 64 B: a plain bulk copy's misses fetch whole 128-B
+// lines (224 DRAM bytes per random record instead of 162; profiles/r02_fetch_granularity.txt).
+__device__ __forceinline__ void tma_window(uint32_t dst, const CUtensorMap* map, uint32_t p, uint32_t mbar) {
+  const int row = (int)((100u * (p & 3u)) >> 4), grp = (int)(p >> 2);
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               ::"r"(dst), "l"((uint64_t)map), "r"(0), "r"(row), "r"(grp), "r"(mbar) : "memory");
+}
+// (A/B form: a plain bulk copy of the same window, whose misses fetch whole 128-B lines)
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
+constexpr int kWsSlot = 128;                     // tensor-copy destinations 128-byte aligned
+constexpr int kWsStageBytes = kGroup * kWsSlot;  // 4096 B per gathering warp and stage
 
 // ---------------------------------------------------------------------------- warp-specialised tier
 // The fused kernel above alternates: all warps sort a bucket, then all warps gather it, so a CTA issues no
@@ -513,22 +530,25 @@ struct WsLayout {
   static constexpr size_t kTmp = kBigl + (size_t)BINS * 4;            // u32[64]
   static constexpr size_t kRing = (kTmp + 64 * 4 + 15) & ~size_t(15);  // u32[2][CAP]
   static constexpr size_t kDesc = kRing + 2 * (size_t)CAP * 4;        // uint2[2]
-  static constexpr size_t kStage = (kDesc + 16 + 127) & ~size_t(127);  // [GW][2][kStageBytes]
-  static constexpr size_t kBytes = kStage + (size_t)GW * 2 * kStageBytes;
+  static constexpr size_t kMbar = kDesc + 16;                          // u64[GW][2] gather-stage mbarriers
+  static constexpr size_t kStage = (kMbar + (size_t)GW * 16 + 127) & ~size_t(127);  // [GW][2][kWsStageBytes]
+  static constexpr size_t kBytes = kStage + (size_t)GW * 2 * kWsStageBytes;
 };
 
 template <uint32_t CAP, int ST, int GW, bool DG>
 __global__ void __launch_bounds__(ST + 32 * GW, 2)
     kd_ws_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-               uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-               uint64_t* __restrict__ dg) {
+               uint32_t* __restrict__ perm, Tunables tu, const __grid_constant__ CUtensorMap in_map,
+               const uint8_t* __restrict__ in, uint64_t n4, uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
   using L = WsLayout<CAP, ST, GW>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int ITEMS = CAP / ST;
   constexpr int NT = ST + 32 * GW;
   constexpr int SW = ST / 32;
-  extern __shared__ __align__(16) uint8_t smem[];
+  // (no static shared memory: the dynamic block starts the CTA's window, so the 128-byte-aligned stage
+  // offsets are 128-byte-aligned addresses, as the tensor copies need)
+  extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + L::kIdx);
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem + L::kTail);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L::kCnt);
@@ -646,10 +666,9 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
   } else {
     // ================================================================ gather group
     const int gw = (tid - ST) >> 5, lane = tid & 31;
-    uint8_t* stage = smem + L::kStage + (size_t)gw * 2 * kStageBytes;
+    uint8_t* stage = smem + L::kStage + (size_t)gw * 2 * kWsStageBytes;
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
-    __shared__ __align__(8) uint64_t s_mb[GW][2];
-    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&s_mb[gw][0]);
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(smem + L::kMbar + (size_t)gw * 16);
     if (lane < 2) mbar_init(mb0 + 8 * lane, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
@@ -664,11 +683,22 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       uint8_t* ob = out + (uint64_t)d.x * kRecordBytes;
       auto issue = [&](uint32_t g0, int st) {
         const uint32_t cnt = min((uint32_t)kGroup, len - g0);
-        if (lane == 0) mbar_expect_tx(mb0 + 8 * st, cnt * kWindow);
+        const uint32_t p = lane < (int)cnt ? pr[g0 + lane] : 0u;
+        const bool tma = lane < (int)cnt && p < n4;
+        const uint32_t ntma = __popc(__ballot_sync(0xffffffffu, tma));
+        if (lane == 0) mbar_expect_tx(mb0 + 8 * st, ntma * kWindow);
         __syncwarp();
-        if (lane < (int)cnt)
-          bulk_g2s(stage_s + st * kStageBytes + lane * kWindow,
-                   in + (((uint64_t)pr[g0 + lane] * kRecordBytes) & ~uint64_t(15)), kWindow, mb0 + 8 * st);
+        if (tma && !tu.ws_tma) {
+          bulk_g2s(stage_s + st * kWsStageBytes + lane * kWsSlot, in + (((uint64_t)p * kRecordBytes) & ~uint64_t(15)),
+                   kWindow, mb0 + 8 * st);
+        } else if (tma) {
+          tma_window(stage_s + st * kWsStageBytes + lane * kWsSlot, &in_map, p, mb0 + 8 * st);
+        } else if (lane < (int)cnt) {  // one of the last n mod 4 records (outside the map): exact word loads
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(in + (uint64_t)p * kRecordBytes);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(stage + st * kWsStageBytes + lane * kWsSlot + ((p * 4u) & 15u));
+#pragma unroll 5
+          for (int o = 0; o < kRecordWords; ++o) dst[o] = src[o];
+        }
       };
       const uint32_t first = (uint32_t)gw * kGroup, stride = (uint32_t)GW * kGroup;
       int st = 0;
@@ -680,17 +710,17 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
         phases ^= 1u << st;
         __syncwarp();
         const uint32_t cnt = min((uint32_t)kGroup, len - g0);
-        const uint8_t* sb = stage + st * kStageBytes;
+        const uint8_t* sb = stage + st * kWsStageBytes;
         uint32_t* dst = reinterpret_cast<uint32_t*>(ob + (uint64_t)g0 * kRecordBytes);
         const uint32_t words = cnt * kRecordWords;
         for (uint32_t w = lane; w < words; w += 32) {
           const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
           const uint32_t off = (pr[g0 + r] * 4u) & 15u;
-          stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWindow + off + 4 * o));
+          stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWsSlot + off + 4 * o));
         }
         if (DG && lane < (int)cnt)
           dg[d.x + g0 + lane] =
-              prefix_digest(reinterpret_cast<const uint32_t*>(sb + lane * kWindow + ((pr[g0 + lane] * 4u) & 15u)));
+              prefix_digest(reinterpret_cast<const uint32_t*>(sb + lane * kWsSlot + ((pr[g0 + lane] * 4u) & 15u)));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         st ^= 1;
@@ -703,7 +733,10 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
 template <uint32_t CAP, int ST, int GW, bool DG>
 cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                            const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                           const uint8_t* in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+                           const uint8_t* in, uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+  CUtensorMap map;  // the record windows of tma_window: boxes of 7 rows x 1 group (tmap.cu)
+  cudaError_t me = record_group_map(&map, in, n_in, 7, 1);
+  if (me != cudaSuccess) return me;
   auto kern = kd_ws_sort<CAP, ST, GW, DG>;
   const size_t smem = WsLayout<CAP, ST, GW>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -712,7 +745,7 @@ cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST + 32 * GW, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, out, dg);
+  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, map, in, n_in & ~uint64_t(3), out, dg);
   return cudaGetLastError();
 }
 
@@ -728,37 +761,38 @@ namespace {
 // All K-d/K-e tiers for the lists of one level (counts are read on the device; no host sync).
 template <bool DG>
 cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1, const uint32_t* i1,
-                   uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in, uint8_t* out, uint64_t* dg,
-                   cudaStream_t s, int* launches) {
+                   uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in, uint64_t n_in, uint8_t* out,
+                   uint64_t* dg, cudaStream_t s, int* launches) {
+  const uint64_t in_bytes = n_in * kRecordBytes;
   cudaError_t e;
   static int warp_per_sm = 0;  // resident CTAs per SM (registers bound it: 5 at 46 registers)
   if (!warp_per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&warp_per_sm, kd_warp_sort<DG>, 256, 0) != cudaSuccess ||
                        warp_per_sm < 1))
     warp_per_sm = 4;
   kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in,
-                                                  out, dg);
+                                                  in_bytes, out, dg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
   // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
-  if ((e = launch_cta_sort<512, 128, DG>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
+  if ((e = launch_cta_sort<512, 128, DG>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in, in_bytes,
                                      out, dg, s)))
     return e;
   if (tu.kd_ws && out) {  // (no gather warps to feed in perm-only mode)
     if ((e = launch_ws_sort<2048, 256, 8, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
-                                          out, dg, s)))
+                                              n_in, out, dg, s)))
       return e;
   } else if ((e = launch_cta_sort<2048, 256, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu,
-                                             sms, in, out, dg, s))) {
+                                             sms, in, in_bytes, out, dg, s))) {
     return e;
   }
-  if ((e = launch_cta_sort<8192, 1024, DG>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
+  if ((e = launch_cta_sort<8192, 1024, DG>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in, in_bytes,
                                       out, dg, s)))
     return e;
   if ((e = launch_cta_sort<10240, 1024, DG>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
-                                        in, out, dg, s)))
+                                        in, in_bytes, out, dg, s)))
     return e;
   if ((e = launch_cta_sort<16384, 768, DG>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
-                                       in, out, dg, s)))
+                                       in, in_bytes, out, dg, s)))
     return e;
   if (launches) *launches += 6;
   return cudaSuccess;
@@ -767,9 +801,9 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
 
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches) {
-  return dg && out ? kd_all<true>(kd, t0, i0, t1, i1, perm, tu, sms, in, out, dg, s, launches)
-                   : kd_all<false>(kd, t0, i0, t1, i1, perm, tu, sms, in, out, nullptr, s, launches);
+                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches) {
+  return dg && out ? kd_all<true>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, dg, s, launches)
+                   : kd_all<false>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, nullptr, s, launches);
 }
 
 }  // namespace ley

@@ -166,12 +166,14 @@ __global__ void __launch_bounds__(THREADS)
     if (threadIdx.x == 0) s_len = CAPG + 1;
     __syncthreads();
     // the run from f is contiguous: its length is the first position that does not tie with f (scanned
-    // THREADS positions at a time, stopping at the first window that holds it)
+    // THREADS positions at a time, stopping at the first window that holds it). The stop decision is the
+    // barrier's own OR, so every warp leaves the loop at the same window (reading s_len after a plain
+    // barrier could see a faster warp's atomicMin from the next window and break one window early).
     for (uint32_t t0 = LO + 1; t0 <= CAPG; t0 += kCtaThreads) {
       const uint32_t t = t0 + threadIdx.x;
-      if (t <= CAPG && ((uint64_t)f + t >= n || !same_prefix(recs, dg, f, (uint64_t)f + t))) atomicMin(&s_len, t);
-      __syncthreads();
-      if (s_len <= CAPG) break;
+      const bool end = t <= CAPG && ((uint64_t)f + t >= n || !same_prefix(recs, dg, f, (uint64_t)f + t));
+      if (end) atomicMin(&s_len, t);
+      if (__syncthreads_or(end)) break;
     }
     const uint32_t len = s_len;
     if (len > CAPG) {

@@ -344,6 +344,189 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------- key-row K-a (form 1)
+// The streaming structure above, but the ring carries only the key rows, not whole records. A miss of
+// the whole-record bulk copies (or of any plain load) fetches full 128-B lines: 100 B/record of DRAM
+// reads for a 10-byte key. Here each 512-record piece arrives as four TMA tensor boxes over the record
+// array viewed as [groups of 4][25 rows][16 B] (tmap.cu): rows {0}, {6}, {12,13}, {18,19} of 128
+// consecutive groups hold the key bytes 0..11 of records 4g, 4g+1, 4g+2, 4g+3 at byte 0, 4, 8, 12 of
+// their first row; the map's 64-B L2 promotion fetches 72 B/record (measured) into a 12 KB slot, so a
+// deeper ring fits. The last n mod 4 records (outside the map) are read with plain loads.
+constexpr int kKeyRing = 6;
+constexpr int kKeyGroups = kPiece / 4;                   // 128 groups per piece
+constexpr uint32_t kKeySlotBytes = kKeyGroups * 16 * 6;  // rows 0, 6 (16 B each), 12-13, 18-19 (32 B each)
+static_assert(kPiece % 4 == 0, "pieces are whole 4-record groups");
+
+__device__ __forceinline__ void ka_tma3(uint32_t dst, const CUtensorMap* m, int row, int grp, uint32_t mbar,
+                                        uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(dst), "l"((uint64_t)m), "r"(0), "r"(row), "r"(grp), "r"(mbar), "l"(pol) : "memory");
+}
+
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS, 1)
+    ka_tile_keys(const __grid_constant__ CUtensorMap m1, const __grid_constant__ CUtensorMap m2,
+                 const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles, uint64_t* __restrict__ k1_out,
+                 uint32_t* __restrict__ w_out, uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
+                 uint32_t* __restrict__ hist16, uint32_t copies, uint32_t key_len) {
+  constexpr int T = THREADS * ITEMS;
+  constexpr int WARPS = THREADS / 32;
+  static_assert(THREADS == kPiece, "one record of every piece per thread");
+  // (no static shared memory: the dynamic block starts the CTA's window, so the tensor-copy slots are
+  // 128-byte aligned; the mbarriers live at its end)
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* s_ring = smem;                                                           // [kKeyRing][kKeySlotBytes]
+  uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem + kKeyRing * kKeySlotBytes);    // [T]
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                            // [T]
+  uint32_t* s_wh = s_w + T;                                                         // [WARPS][256]
+  uint32_t* s_tmp = s_wh + WARPS * kRadix;                                          // [32]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_tmp + 32);                       // [kKeyRing]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
+  uint64_t pol_ef, pol_el;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
+  const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(s_ring);
+  if (tid < kKeyRing) ka_mbar_init(full0 + 8 * tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const uint64_t n4 = n & ~uint64_t(3);  // records inside the map
+  const uint32_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t total_pieces = my_tiles * kPieces;
+  auto issue = [&](uint32_t P) {  // thread 0 only
+    const uint32_t t = blockIdx.x + (P / kPieces) * gridDim.x;
+    const uint64_t r0 = (uint64_t)t * T + (uint64_t)(P % kPieces) * kPiece;
+    const uint32_t slot = P % kKeyRing;
+    const uint32_t mb = full0 + 8 * slot;
+    if (r0 < n4) {
+      // boxes past the last group are zero-filled by the TMA and still count their full bytes
+      const uint32_t dst = ring0 + slot * kKeySlotBytes;
+      const int g0 = (int)(r0 >> 2);
+      ka_mbar_expect_tx(mb, kKeySlotBytes);
+      ka_tma3(dst, &m1, 0, g0, mb, pol_ef);
+      ka_tma3(dst + kKeyGroups * 16, &m1, 6, g0, mb, pol_ef);
+      ka_tma3(dst + kKeyGroups * 32, &m2, 12, g0, mb, pol_ef);
+      ka_tma3(dst + kKeyGroups * 64, &m2, 18, g0, mb, pol_ef);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
+    }
+  };
+  if (tid == 0)
+    for (uint32_t P = 0; P < (uint32_t)kKeyRing && P < total_pieces; ++P) issue(P);
+
+  // where this thread's key words sit in a slot: record 4g + jj at byte 4 jj of its first row
+  const uint32_t g = (uint32_t)tid >> 2, jj = (uint32_t)tid & 3u;
+  const uint32_t key_off = jj == 0 ? g * 16 : jj == 1 ? kKeyGroups * 16 + g * 16 + 4
+                         : jj == 2 ? kKeyGroups * 32 + g * 32 + 8 : kKeyGroups * 64 + g * 32 + 12;
+
+  for (uint32_t i = 0; i < my_tiles; ++i) {
+    const uint32_t t = blockIdx.x + i * gridDim.x;
+    const uint64_t base = (uint64_t)t * T;
+    const uint32_t cnt_t = (uint32_t)(n - base < (uint64_t)T ? n - base : (uint64_t)T);
+    for (int q = tid; q < WARPS * kRadix; q += THREADS) s_wh[q] = 0;
+    // ---- 1. keys of piece j -> item j (record r = j * THREADS + tid)
+    uint32_t a[ITEMS], b[ITEMS], c[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t P = i * kPieces + j;
+      const uint32_t slot = P % kKeyRing;
+      ka_mbar_wait(full0 + 8 * slot, (P / kKeyRing) & 1u);
+      const uint32_t r = j * THREADS + tid;
+      if (r < cnt_t) {
+        if (base + r < n4) {
+          const uint32_t* kw = reinterpret_cast<const uint32_t*>(s_ring + slot * kKeySlotBytes + key_off);
+          a[j] = kw[0];
+          b[j] = kw[1];
+          c[j] = kw[2];
+        } else {  // one of the last n mod 4 records
+          const uint32_t* kw = reinterpret_cast<const uint32_t*>(in + (base + r) * kRecordBytes);
+          a[j] = kw[0];
+          b[j] = kw[1];
+          c[j] = kw[2];
+        }
+        if (key_len < 10) ka_compose(a[j], b[j], c[j], key_len, (uint32_t)(base + r));
+      } else {
+        a[j] = b[j] = c[j] = 0;
+      }
+      __syncthreads();  // every thread has its key words: the slot may be refilled
+      if (tid == 0 && P + kKeyRing < total_pieces) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(P + kKeyRing);
+      }
+    }
+
+    // ---- 2. warp multi-split ranking on byte 0
+    uint32_t rank[ITEMS];
+    uint32_t* wh = s_wh + warp * kRadix;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t r = j * THREADS + tid;
+      const bool valid = r < cnt_t;
+      const uint32_t hi = bswap32(a[j]);
+      const uint32_t d = hi >> 24;
+      const uint32_t peers = warp_peers8(d, valid);
+      const uint32_t before = __popc(peers & lt);
+      const uint32_t cur = valid ? wh[d] : 0;
+      __syncwarp();
+      if (valid && before == 0) wh[d] = cur + __popc(peers);
+      __syncwarp();
+      rank[j] = cur + before;
+      const uint32_t p16 = hi >> 16;
+      const uint32_t peers16 = peers & warp_peers8((hi >> 16) & 0xFFu, valid);
+      if (valid && __popc(peers16 & lt) == 0)
+        asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(&hist_copy[p16]),
+                     "r"((uint32_t)__popc(peers16)), "l"(pol_el) : "memory");
+    }
+    __syncthreads();
+
+    // ---- 3. per-digit totals over warps, tile exclusive offsets
+    uint32_t total = 0;
+    if (tid < kRadix) {
+#pragma unroll 4
+      for (int w = 0; w < WARPS; ++w) {
+        const uint32_t v = s_wh[w * kRadix + tid];
+        s_wh[w * kRadix + tid] = total;
+        total += v;
+      }
+    }
+    const uint32_t excl = block_excl_scan<THREADS>(tid < kRadix ? total : 0, s_tmp, nullptr);
+    if (tid < kRadix) {
+#pragma unroll 4
+      for (int w = 0; w < WARPS; ++w) s_wh[w * kRadix + tid] += excl;
+      cnt[(uint64_t)tid * tiles + t] = total;
+      lo[(uint64_t)t * kRadix + tid] = excl;
+    }
+    __syncthreads();
+
+    // ---- 4. scatter into shared memory in byte-0 order
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t r = j * THREADS + tid;
+      if (r < cnt_t) {
+        const uint32_t hi = bswap32(a[j]);
+        const uint32_t d = hi >> 24;
+        const uint32_t pos = wh[d] + rank[j];
+        const uint64_t kk = ((uint64_t)hi << 32) | bswap32(b[j]);
+        s_k1[pos] = (kk << 8) | (c[j] & 0xFFu);
+        s_w[pos] = ((c[j] >> 8) & 0xFFu) << 24 | r;
+      }
+    }
+    __syncthreads();
+
+    // ---- 5. coalesced write-out
+    for (uint32_t q = tid; q < cnt_t; q += THREADS) {
+      k1_out[base + q] = s_k1[q];
+      w_out[base + q] = s_w[q];
+    }
+    __syncthreads();  // staging and per-warp counters reused by the next tile
+  }
+}
+
 }  // namespace
 
 size_t ka_smem_bytes() {
@@ -351,22 +534,33 @@ size_t ka_smem_bytes() {
 }
 
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
-                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, int form,
                                 KeySpec key, cudaStream_t s) {
   auto kern = ka_tile_sort<kTileThreads, kTileItems>;
   size_t smem = ka_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (stream_form && key.off == 0) {  // (the ring copies whole records but keys only from bytes 0..11)
-    auto sk = ka_tile_stream<kTileThreads, kTileItems>;
-    const size_t ssm = (size_t)kRing * kPieceBytes + (size_t)kTileRecords * 12 +
-                       (size_t)(kTileThreads / 32) * kRadix * 4 + 32 * 4;
-    e = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-    if (e != cudaSuccess) return e;
+  if (form != 0 && key.off == 0) {  // (the persistent forms read keys from record bytes 0..11 only)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
+    const size_t rest = (size_t)kTileRecords * 12 + (size_t)(kTileThreads / 32) * kRadix * 4 + 32 * 4;
+    if (form == 1) {
+      CUtensorMap m1, m2;  // boxes of 1 and 2 rows over kKeyGroups groups
+      if ((e = record_group_map(&m1, in, n, 1, kKeyGroups)) != cudaSuccess) return e;
+      if ((e = record_group_map(&m2, in, n, 2, kKeyGroups)) != cudaSuccess) return e;
+      auto kk = ka_tile_keys<kTileThreads, kTileItems>;
+      const size_t ksm = (size_t)kKeyRing * kKeySlotBytes + rest + 8 * kKeyRing;
+      e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);
+      if (e != cudaSuccess) return e;
+      kk<<<grid, kTileThreads, ksm, s>>>(m1, m2, in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key.len);
+      return cudaGetLastError();
+    }
+    auto sk = ka_tile_stream<kTileThreads, kTileItems>;
+    const size_t ssm = (size_t)kRing * kPieceBytes + rest;
+    e = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    if (e != cudaSuccess) return e;
     sk<<<grid, kTileThreads, ssm, s>>>(in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key.len);
     return cudaGetLastError();
   }

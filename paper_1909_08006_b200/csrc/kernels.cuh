@@ -1,5 +1,6 @@
 // kernels.cuh — launch wrappers of the sm_100a kernels (K-a .. K-e) used by the host drivers.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -15,10 +16,15 @@ struct KeySpec {
   uint32_t len = 10;
 };
 
-// K-a (k_tile.cu)
+// TMA tensor map over records [0, 4 floor(n/4)) of `in` viewed as [groups][25 rows][16 B] (400-B group
+// pitch), boxes of box_rows x box_groups, L2 promotion 64 B (tmap.cu)
+cudaError_t record_group_map(CUtensorMap* map, const uint8_t* in, uint64_t n, uint32_t box_rows, uint32_t box_groups);
+
+// K-a (k_tile.cu). form: 0 = one CTA per tile, direct key loads; 1 = persistent, key rows by TMA tensor
+// copies (64-B L2 fetches; keys at record offset 0 only); 2 = persistent, whole records by TMA bulk copies
 size_t ka_smem_bytes();
 cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, uint64_t* k1_out, uint32_t* w_out,
-                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, bool stream_form,
+                                uint32_t* cnt, uint32_t* lo, uint32_t* hist16, uint32_t copies, int form,
                                 KeySpec key, cudaStream_t s);
 
 // K-b (k_scan.cu)
@@ -53,9 +59,10 @@ cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B1
                                       const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
 // K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
 // out == nullptr: perm-only, no gather; dg non-null: dg[j] = digest of output record j's 10-byte prefix).
+// in holds n_in records; no gather reads outside them.
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches);
+                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches);
 
 // K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,
@@ -66,7 +73,8 @@ cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t c
 // in-place comparison sort of every group of <= 1024 records by key bytes [10, key_bytes) then position,
 // and the firsts / lasts of the longer groups appended to large_f / large_l (counts[2], counts[3]; entries
 // past large_cap dropped; "large" = more than 1024 records, smaller groups sorted on the device; the
-// firsts and lasts arrays are overwritten, counts[4..5] used)
+// firsts and lasts arrays are overwritten, counts[4..6] used as scratch counters: the caller's 32-byte
+// memset of counts covers them)
 cudaError_t launch_tie_groups(const uint8_t* recs, const uint64_t* dg, uint64_t n, uint32_t* firsts, uint32_t* lasts, uint32_t cap,
                               uint32_t* counts, int sms, cudaStream_t s);
 // (dg required here)

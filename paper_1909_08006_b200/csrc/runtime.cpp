@@ -37,7 +37,7 @@ const OptDesc kOpts[] = {
     {"kd_digit_bits", &Options::kd_digit_bits, 0, 12},
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"kd_ws", &Options::kd_ws, 0, 1},
-    {"ka_stream", &Options::ka_stream, 0, 1},
+    {"ka_stream", &Options::ka_stream, 0, 2},
     {"key_hybrid", &Options::key_hybrid, 0, 1},
     {"resident_path", &Options::resident_path, 0, 1},
     {"resident_chunk_records", &Options::resident_chunk_records, 0, (int64_t)0xFFFFFFFEll},
@@ -47,6 +47,10 @@ const OptDesc kOpts[] = {
     {"profile", &Options::profile, 0, 1},
     {"ext_run_records", &Options::ext_run_records, 0, (int64_t)0xFFFFFFFEll},
     {"l2_fetch_bytes", &Options::l2_fetch_bytes, 0, 128},
+    {"nccl_timeout_ms", &Options::nccl_timeout_ms, 50, 3600000},
+    {"dist_fault_stall", &Options::dist_fault_stall, 0, 1000},
+    {"tma_l2_promo", &Options::tma_l2_promo, 0, 256},
+    {"ws_gather_tma", &Options::ws_gather_tma, 0, 1},
 };
 }  // namespace
 

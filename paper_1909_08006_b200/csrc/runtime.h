@@ -54,6 +54,10 @@ struct Options {
   int64_t profile = 0;
   int64_t ext_run_records = 0;
   int64_t l2_fetch_bytes = 0;  // 0 = leave the device default; else cudaLimitMaxL2FetchGranularity
+  int64_t nccl_timeout_ms = 120000;  // multi-GPU: a collective not complete after this long aborts the comm
+  int64_t dist_fault_stall = 0;      // test hook: stall the stream after the k-th collective of a call
+  int64_t tma_l2_promo = 64;  // L2 promotion of the record tensor maps (0 = none, 64, 128, 256)
+  int64_t ws_gather_tma = 1;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
 };
 Options options_snapshot();
 ley_status option_set(const char* name, int64_t value);

@@ -46,7 +46,7 @@ ley_status ley_test_tile_sort(const void* in, uint64_t n, uint64_t* k1, uint32_t
   const uint32_t tiles = (uint32_t)((n + kTileRecords - 1) / kTileRecords);
   LEY_CUDA("test K-a", cudaMemsetAsync(hist16, 0, 4 * 65536, s));
   LEY_CUDA("test K-a", launch_ka_tile_sort(static_cast<const uint8_t*>(in), n, tiles, k1, w, cnt, lo, hist16, 1,
-                                           stream_form != 0, KeySpec{}, s));
+                                           stream_form, KeySpec{}, s));
   LEY_CUDA("test K-a", cudaStreamSynchronize(s));
   return LEY_OK;
 }

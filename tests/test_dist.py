@@ -128,6 +128,56 @@ def test_nccl_world_size_one(cuda_ok, exchange_mode, exchange_g1):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("stall_at", [1, 2, 4], ids=["first", "second", "fourth"])
+def test_nccl_fault_times_out_and_aborts(cuda_ok, exchange_mode, stall_at):
+    """NCCL fault handling ("any stage failure aborts the pipeline, reports the
+    stage"). The dist_fault_stall hook holds the stream after the k-th collective of the call, as a peer
+    that never completes it would. The library must not wait forever: within nccl_timeout_ms it aborts the
+    communicator (ncclCommAbort), returns LEY_ERR_NCCL with the stage named in ley_last_error(), refuses
+    further sorts on that communicator, lets ley_comm_destroy release it, and a new communicator works."""
+    import time
+
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    n = 40_000
+    recs = gen.records(n, seed=65, dist="uniform")
+    x = torch.from_numpy(recs).cuda()
+    out = torch.empty_like(x)
+    ley.ley_set_option("dist_exchange_g1", 1)
+    ley.ley_set_option("nccl_timeout_ms", 1500)
+    comm = ley.ley_comm_init(1, 0, ley.ley_comm_get_unique_id(), 0)
+    try:
+        ley.ley_set_option("dist_fault_stall", stall_at)
+        t0 = time.monotonic()
+        with pytest.raises(ley.LeyendaError) as ei:
+            ley.ley_sort_dist(comm, x, n, out, n)
+        took = time.monotonic() - t0
+        assert ei.value.status == ley.LEY_ERR_NCCL
+        msg = ley.ley_last_error()
+        assert "communicator aborted" in msg and "dist" in msg, msg
+        assert took < 1.5 + 10.0, took
+        ley.ley_set_option("dist_fault_stall", 0)
+        with pytest.raises(ley.LeyendaError) as ei:
+            ley.ley_sort_dist(comm, x, n, out, n)
+        assert ei.value.status == ley.LEY_ERR_NCCL and "aborted" in ley.ley_last_error()
+    finally:
+        ley.ley_set_option("dist_fault_stall", 0)
+        ley.ley_comm_destroy(comm)
+    torch.cuda.synchronize()
+    comm = ley.ley_comm_init(1, 0, ley.ley_comm_get_unique_id(), 0)
+    try:
+        assert ley.ley_sort_dist(comm, x, n, out, n) == (n, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), oracle.sort(recs)[0])
+    finally:
+        ley.ley_comm_destroy(comm)
+        ley.ley_set_option("dist_exchange_g1", 0)
+        ley.ley_set_option("nccl_timeout_ms", 120000)
+
+
+@pytest.mark.gpu
 def test_nccl_pinned_host_slices(cuda_ok, exchange_mode):
     """ley_sort_dist with pinned host slices: staged on the device (H2D, the device path, D2H of the
     rank's range), with the exchange phases on; under a budget below slice + capacity (all ranks agree

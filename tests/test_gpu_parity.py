@@ -44,12 +44,13 @@ def test_uniform_sizes(n):
     assert_parity(recs, out, perm)
 
 
-@pytest.mark.parametrize("n", [1, 511, 513, 4095, 4097, 600_001, 606_209])
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 511, 513, 4095, 4097, 4098, 600_001, 606_209, 606_210])
 def test_ka_forms_ragged(n):
-    """Both K-a forms on ragged sizes: partial 512-record pieces (bulk copies rounded down to 16 bytes),
-    partial tiles, and more tiles than SMs (several tiles per persistent CTA)."""
+    """All K-a forms on ragged sizes: partial 512-record pieces (bulk copies rounded down to 16 bytes; key-row
+    boxes past the last 4-record group zero-filled), the last n mod 4 records read outside the tensor map
+    (n = 1..3: every record), partial tiles, and more tiles than SMs (several tiles per persistent CTA)."""
     recs = gen.records(n, seed=n + 1, dist="skewed")
-    for ks in (1, 0):
+    for ks in (1, 2, 0):
         with Options(ka_stream=ks):
             out, perm = gpu_sort(recs)
         assert_parity(recs, out, perm)
@@ -111,6 +112,7 @@ def test_zero_records():
     dict(kd_ws=0),                                   # alternating sort/gather CTAs instead of warp-specialised
     dict(kd_ws=0, kd_digit_bits=0),
     dict(ka_stream=0),                               # K-a: one CTA per tile, direct key loads
+    dict(ka_stream=2),                               # K-a: whole records through the bulk-copy ring
 ])
 @pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "byte9"])
 def test_forced_thresholds(opts, dist):

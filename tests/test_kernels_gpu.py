@@ -50,9 +50,10 @@ def _ka_model(recs: np.ndarray, n: int):
     return cnt, lo, hist16
 
 
-@pytest.mark.parametrize("form", [1, 0])
-@pytest.mark.parametrize("n,dist", [(1, "uniform"), (4095, "uniform"), (4097, "skewed"), (70_001, "uniform"),
-                                    (300_007, "skewed"), (200_000, "all_equal")])
+@pytest.mark.parametrize("form", [1, 2, 0])
+@pytest.mark.parametrize("n,dist", [(1, "uniform"), (3, "skewed"), (4095, "uniform"), (4097, "skewed"),
+                                    (4098, "uniform"), (70_001, "uniform"), (300_007, "skewed"),
+                                    (200_000, "all_equal")])
 def test_ka_tile_sort_matches_model(form, n, dist):
     recs = gen.records(n, seed=n + form, dist=dist)
     T = -(-n // TILE)
