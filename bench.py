@@ -3,17 +3,18 @@
 
 A "step" is one pass of the whole hot path (K-a .. K-e: SURVEY.md §8a rows a1-a6) over one batch of
 synthetic records already resident in HBM: one ley_sort call through the C ABI. Default workload:
-BASELINE.json configs[1] (C2: 1e8 uniform records = 10 GB, seed 1) on 1 GPU. Inputs are 10 GB, far
-larger than the 126 MB L2, so no explicit flush is needed between steps.
+BASELINE.json configs[3] (C4: 6e8 uniform records = 60 GB, seed 3), the largest configuration that fits
+one GPU, with configs[1] (C2: 1e8 records = 10 GB, seed 1) measured in the same run into the line's
+`secondary` key. Inputs are >= 10 GB, far larger than the 126 MB L2, so no flush is needed between steps.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c1|c2|c3|c4] [--impl ours|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c1..c7] [--secondary c2|none] [--impl ours|reference]
 
 Keys beyond the base contract: `roofline` (dominant kernel, algorithmic bytes / CUDA-event time against
 MEASURED_PEAKS.json hbm_gbs), `step_roofline` (the whole step: 200 B/record / HBM peak),
 `cpu_baseline` (the oracle timed on this host on a bounded sample), `e2e` (same metric through the C
 ABI with pinned host buffers: H2D + sort + D2H inside the timed region), `clocks`, `gpu_launches`.
-Multi-GPU (N > 1, torchrun): every rank sorts its own C2-sized slice ("scaling": "weak"); the dist
-key-range path is reported separately once it lands.
+Multi-GPU (N > 1, torchrun): the config's records are split into rank slices and sorted by the key-range
+path (ley_sort_dist: splitters, fused partition + exchange over NVLink, local sort; "scaling": "strong").
 """
 from __future__ import annotations
 
@@ -216,60 +217,23 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample records (0 = min(n, 1e8))")
-    ap.add_argument("--e2e-steps", type=int, default=16)
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dist", action="store_true", help="use the NCCL key-range path even at one GPU (checks it)")
-    ap.add_argument("--exchange", action="store_true",
-                    help="with --dist at one GPU: also run the splitter/partition/exchange phases (dist_exchange_g1)")
-    ap.add_argument("--key-bytes", type=int, default=10,
-                    help="key = record bytes [0, k), 1..100 (P:164 flexible key sizes; default the paper's 10)")
-    ap.add_argument("--alltoall", action="store_true", help="dist: K-p into a send buffer + NCCL all-to-all-v "
-                                                            "instead of the fused exchange (dist_fused=0)")
-    args = ap.parse_args()
-    cfg = CONFIGS[args.config]
-    if not args.cpu_sample:
-        args.cpu_sample = min(cfg["n"], 100_000_000)
-    if args.impl == "reference":
-        run_reference(args, cfg)
-        return
-
+def measure(args, cfg_name, world, rank, local, comm, with_cpu=True):
+    """One config on this rank's GPU: the device-timed step (value, stages, roofline), e2e through the C ABI
+    with pinned host buffers, clocks, launches; the CPU baseline on rank 0. Returns the JSON fields."""
     import torch
     import torch.distributed as dist
 
     import gen
     import paper_1909_08006_b200 as ley
 
-    if args.exchange:
-        ley.ley_set_option("dist_exchange_g1", 1)
-    if args.alltoall:
-        ley.ley_set_option("dist_fused", 0)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[cfg_name]
     stream = torch.cuda.current_stream()
     n_total = cfg["n"]
     external = "budget" in cfg
-    comm = None
-    if world > 1 or args.dist:
+    if comm is not None:
         # strong scaling: the config's records split into contiguous rank slices (SURVEY §8e)
         lo, hi = rank * n_total // world, (rank + 1) * n_total // world
         n = hi - lo
-        obj = [ley.ley_comm_get_unique_id() if rank == 0 else None]
-        if world > 1:
-            dist.broadcast_object_list(obj, src=0)
-        comm = ley.ley_comm_init(world, rank, obj[0], local)
     else:
         lo, n = 0, n_total
     cap = n_total // world + 2 if comm is not None else n
@@ -341,7 +305,7 @@ def main():
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp) and world == 1:
             with open(tp) as f:
-                ent = json.load(f).get(args.config, {}).get(dominant)
+                ent = json.load(f).get(cfg_name, {}).get(dominant)
             if ent:  # DRAM bytes of the stage's launches in one call (ncu; tools/ncu_traffic.py)
                 traffic = ent.get("bytes_per_launch")
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -409,8 +373,9 @@ def main():
         hin = torch.empty(n * 100, dtype=torch.uint8).pin_memory()
         hin.copy_(x[: n * 100])
         hout = torch.empty_like(hin).pin_memory()
-        del x, out  # room for the two streaming slots
+        del x, out  # room for the library's staging of in + out
         torch.cuda.empty_cache()
+        ley.ley_release_cache(-1)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
         def timed(call, steps, finish=None):
@@ -423,47 +388,125 @@ def main():
             torch.cuda.synchronize()
             return f0.elapsed_time(f1) / steps
 
-        # (1) the public streaming call: H2D of step k+1 overlaps the D2H of step k (ley_sort_submit); the
-        #     timed region ends after ley_sort_drain(), i.e. after the last step's output is in host memory
-        ley.ley_sort_submit(hin, hout, n, key_bytes=args.key_bytes, stream=stream)  # warm: the two device slots
-        ley.ley_sort_drain()
-        ems = timed(ley.ley_sort_submit, args.e2e_steps, finish=ley.ley_sort_drain)
-        # (2) the blocking call, one sort at a time (H2D + sort + D2H serialised)
-        ley.ley_release_cache(-1)
-        ley.ley_sort(hin, hout, n, key_bytes=args.key_bytes, stream=stream)
-        bms = timed(ley.ley_sort, max(2, args.e2e_steps // 3))
-        e2e = {"value": round(n * 100 / (ems / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * 100,
-               "d2h_bytes_per_step": n * 100, "ms_per_step": round(ems, 3), "steps": args.e2e_steps,
-               "api": "ley_sort_submit (pinned host in/out; consecutive calls overlap H2D and D2H)",
-               "blocking": {"api": "ley_sort (pinned host)", "value": round(n * 100 / (bms / 1e3) / 1e9, 3),
-                            "ms_per_step": round(bms, 3)}}
+        # (1) the SURVEY §8(b) call itself, one blocking ley_sort per step: H2D of the step's input, the sort,
+        #     D2H of its output, all inside the timed region
+        ley.ley_sort(hin, hout, n, key_bytes=args.key_bytes, stream=stream)  # warm: the staging buffers
+        bsteps = max(2, args.e2e_steps // 3) if n <= 200_000_000 else 2
+        bms = timed(ley.ley_sort, bsteps)
+        e2e = {"value": round(n * 100 / (bms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * 100,
+               "d2h_bytes_per_step": n * 100, "ms_per_step": round(bms, 3), "steps": bsteps,
+               "api": "ley_sort (pinned host in/out, blocking: H2D + sort + D2H per step)"}
+        # (2) the streaming call, when two device slots of in + out fit: H2D of step k+1 overlaps the D2H of
+        #     step k (ley_sort_submit); the region ends after ley_sort_drain(), i.e. once the last output landed
+        if 4 * n * 100 < torch.cuda.get_device_properties(0).total_memory * 0.8:
+            ley.ley_release_cache(-1)
+            ley.ley_sort_submit(hin, hout, n, key_bytes=args.key_bytes, stream=stream)  # warm: the two slots
+            ley.ley_sort_drain()
+            ems = timed(ley.ley_sort_submit, args.e2e_steps, finish=ley.ley_sort_drain)
+            e2e["streaming"] = {"api": "ley_sort_submit / ley_sort_drain (consecutive calls overlap H2D and D2H)",
+                                "value": round(n * 100 / (ems / 1e3) / 1e9, 3), "ms_per_step": round(ems, 3),
+                                "steps": args.e2e_steps}
         del hin, hout
+        ley.ley_release_cache(-1)
 
     cpu = None
-    if not args.no_cpu and rank == 0:
-        cpu = cpu_baseline(cfg, args.cpu_sample, args.key_bytes)
+    if with_cpu and not args.no_cpu and rank == 0:
+        cpu = cpu_baseline(cfg, min(args.cpu_sample or cfg["n"], cfg["n"], 100_000_000), args.key_bytes)
+
+    return {
+        "value": round(value, 3), "ms_per_step": round(ms, 4), "n_gpus": world,
+        "config": {"workload": cfg["name"] + ("" if args.key_bytes == 10 else f", {args.key_bytes}-byte keys (P:164)"),
+                   "n_records": n_total, "record_bytes": 100, "key_bytes": args.key_bytes,
+                   "seed": cfg["seed"], "distribution": cfg["dist"],
+                   "device_budget_bytes": budget,
+                   "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7
+                   else "100 MB input: L2 flushed by the next step's 100 MB output + 29 MB scratch",
+                   "parallelism": (f"key-range dist x{world} (NCCL, " +
+                                   ("all-to-all-v" if args.alltoall else "fused partition+exchange") +
+                                   (", exchange at G=1" if args.exchange else "") + ")")
+                   if comm is not None else "1 GPU"},
+        "roofline": roofline, "step_roofline": step_roofline, "host_roofline": host_roofline,
+        "stages_ms": {k: round(v, 4) for k, v in avg.items()},
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
+                    help="default c4: BASELINE configs[3], the largest config that fits one GPU")
+    ap.add_argument("--secondary", default="c2",
+                    help="single GPU, default run: also measure this config into the line's `secondary` key "
+                         "('none' to skip)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample records (0 = min(n, 1e8))")
+    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="use the NCCL key-range path even at one GPU (checks it)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="with --dist at one GPU: also run the splitter/partition/exchange phases (dist_exchange_g1)")
+    ap.add_argument("--key-bytes", type=int, default=10,
+                    help="key = record bytes [0, k), 1..100 (P:164 flexible key sizes; default the paper's 10)")
+    ap.add_argument("--alltoall", action="store_true", help="dist: K-p into a send buffer + NCCL all-to-all-v "
+                                                            "instead of the fused exchange (dist_fused=0)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if not args.cpu_sample:
+        args.cpu_sample = min(cfg["n"], 100_000_000)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_08006_b200 as ley
+
+    if args.exchange:
+        ley.ley_set_option("dist_exchange_g1", 1)
+    if args.alltoall:
+        ley.ley_set_option("dist_fused", 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = None
+    if world > 1 or args.dist:
+        obj = [ley.ley_comm_get_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        comm = ley.ley_comm_init(world, rank, obj[0], local)
+
+    res = measure(args, args.config, world, rank, local, comm)
+    secondary = None
+    if (world == 1 and comm is None and args.secondary not in ("", "none") and args.secondary != args.config
+            and args.secondary in CONFIGS):
+        torch.cuda.empty_cache()
+        ley.ley_release_cache(-1)
+        sec = measure(args, args.secondary, world, rank, local, comm, with_cpu=False)
+        secondary = {k: sec[k] for k in ("value", "ms_per_step", "config", "roofline", "step_roofline", "stages_ms",
+                                         "e2e", "clocks", "gpu_launches")}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based generator, SURVEY App. A)",
-            "config": {"workload": cfg["name"] + ("" if args.key_bytes == 10 else f", {args.key_bytes}-byte keys (P:164)"),
-                       "n_records": n_total, "record_bytes": 100, "key_bytes": args.key_bytes,
-                       "seed": cfg["seed"], "distribution": cfg["dist"],
-                       "device_budget_bytes": budget,
-                       "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7
-                       else "100 MB input: L2 flushed by the next step's 100 MB output + 29 MB scratch",
-                       "parallelism": (f"key-range dist x{world} (NCCL, " +
-                                       ("all-to-all-v" if args.alltoall else "fused partition+exchange") +
-                                       (", exchange at G=1" if args.exchange else "") + ")")
-                       if comm is not None else "1 GPU"},
-            "roofline": roofline, "step_roofline": step_roofline, "host_roofline": host_roofline,
-            "stages_ms": {k: round(v, 4) for k, v in avg.items()},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "gpu_launches": launches,
+            "config": res["config"],
+            "roofline": res["roofline"], "step_roofline": res["step_roofline"], "host_roofline": res["host_roofline"],
+            "stages_ms": res["stages_ms"],
+            "cpu_baseline": res["cpu_baseline"], "e2e": res["e2e"], "clocks": res["clocks"],
+            "gpu_launches": res["gpu_launches"] + (secondary["gpu_launches"] if secondary else 0),
         }
+        if secondary:
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     if comm is not None:
         ley.ley_comm_destroy(comm)

@@ -42,7 +42,8 @@ struct Tunables {
   int kd_digit_bits = kKdMaxBits;
   int kd_insert_max = 16;
   int kd_ws = 1;  // warp-specialised sort/gather tiers (kd_ws_sort) instead of the alternating kd_cta_sort
-  int ws_tma = 1;  // kd_ws_sort: record windows by TMA tensor copies (64-B L2 fetches) or plain bulk copies
+  int ws_tma = 0;  // kd_ws_sort: record windows by TMA tensor copies (64-B L2 fetches) or plain bulk copies
+  int gather_l2_64 = 1;  // kd_cta_sort gathers: cp.async with .L2::64B (1) or without the hint (0)
 };
 
 // ------------------------------------------------------------------ device helpers

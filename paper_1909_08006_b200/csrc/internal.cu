@@ -71,6 +71,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   tu.kd_insert_max = (int)o.kd_insert_max;
   tu.kd_ws = (int)o.kd_ws;
   tu.ws_tma = (int)o.ws_gather_tma;
+  tu.gather_l2_64 = (int)o.gather_l2_64;
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;

@@ -37,9 +37,12 @@ constexpr int kStageBytes = kGroup * kWindow;  // 3584 B per gathering warp
 // 16-byte chunk of a record window. .L2::64B caps the L2's DRAM fetch for the miss at 64 B: a plain miss
 // is promoted to the whole 128-B line, so a random 100-B record cost 224 DRAM bytes instead of 162
 // (profiles/r02_fetch_granularity.txt). src_bytes < 16 zero-fills the rest (the input's last chunk).
-__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem_addr), "l"(gptr), "r"(src_bytes)
-               : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, uint32_t src_bytes, bool l2_64) {
+  if (l2_64)
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem_addr), "l"(gptr), "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr), "l"(gptr), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void stg_cs_u32(uint32_t* p, uint32_t v) {
@@ -59,7 +62,7 @@ __device__ __forceinline__ uint64_t prefix_digest(const uint32_t* w) {
 __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
                                             const uint8_t* __restrict__ in, uint64_t in_bytes,
                                             uint8_t* __restrict__ out_base, uint8_t* stage,
-                                            uint64_t* __restrict__ dg_base) {
+                                            uint64_t* __restrict__ dg_base, bool l2_64 = true) {
   const int lane = threadIdx.x & 31;
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
   for (uint32_t g0 = first; g0 < s; g0 += stride) {
@@ -72,7 +75,7 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
       const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
       const uint64_t a = (((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16;
       if (r < (int)cnt && a < in_bytes)  // (chunks past the input's end hold no record byte)
-        cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u);
+        cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u, l2_64);
     }
     cp_async_wait_all();
     __syncwarp();
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     if (out && warp < L::GWARPS)
       warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in, in_bytes,
                   out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
-                  DG ? dg + sg.start : nullptr);
+                  DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
     __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
 }

@@ -19,6 +19,7 @@
 #include "block_rank.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "runtime.h"
 
 namespace ley {
 namespace {
@@ -352,10 +353,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // consecutive groups hold the key bytes 0..11 of records 4g, 4g+1, 4g+2, 4g+3 at byte 0, 4, 8, 12 of
 // their first row; the map's 64-B L2 promotion fetches 72 B/record (measured) into a 12 KB slot, so a
 // deeper ring fits. The last n mod 4 records (outside the map) are read with plain loads.
-constexpr int kKeyRing = 6;
 constexpr int kKeyGroups = kPiece / 4;                   // 128 groups per piece
 constexpr uint32_t kKeySlotBytes = kKeyGroups * 16 * 6;  // rows 0, 6 (16 B each), 12-13, 18-19 (32 B each)
 static_assert(kPiece % 4 == 0, "pieces are whole 4-record groups");
+int ka_ring_slots() { return (int)options_snapshot().ka_ring; }
 
 __device__ __forceinline__ void ka_tma3(uint32_t dst, const CUtensorMap* m, int row, int grp, uint32_t mbar,
                                         uint64_t pol) {
@@ -364,60 +365,107 @@ __device__ __forceinline__ void ka_tma3(uint32_t dst, const CUtensorMap* m, int 
       ::"r"(dst), "l"((uint64_t)m), "r"(0), "r"(row), "r"(grp), "r"(mbar), "l"(pol) : "memory");
 }
 
-template <int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS, 1)
+// consumer-group barrier (named barrier 1: the THREADS consumer threads, not the producer warp)
+template <int THREADS>
+__device__ __forceinline__ void ka_csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
+
+template <int THREADS>
+__device__ __forceinline__ uint32_t ka_cscan(uint32_t v, uint32_t* tmp) {  // exclusive, consumers only
+  constexpr int WARPS = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  ka_csync<THREADS>();
+  if (warp == 0) {
+    uint32_t w = lane < WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < WARPS) tmp[lane] = w;
+  }
+  ka_csync<THREADS>();
+  const uint32_t r = (warp ? tmp[warp - 1] : 0u) + x - v;
+  ka_csync<THREADS>();
+  return r;
+}
+
+// THREADS consumer threads (one record of every piece each) + one producer warp that keeps the ring full:
+// it refills a slot as soon as every consumer warp has arrived on the slot's "empty" mbarrier, so the
+// consumers never stop at a block-wide barrier for the ring (only for the tile's rank/scan/scatter steps).
+template <int THREADS, int ITEMS, int RING>
+__global__ void __launch_bounds__(THREADS + 32, 1)
     ka_tile_keys(const __grid_constant__ CUtensorMap m1, const __grid_constant__ CUtensorMap m2,
                  const uint8_t* __restrict__ in, uint64_t n, uint32_t tiles, uint64_t* __restrict__ k1_out,
                  uint32_t* __restrict__ w_out, uint32_t* __restrict__ cnt, uint32_t* __restrict__ lo,
                  uint32_t* __restrict__ hist16, uint32_t copies, uint32_t key_len) {
   constexpr int T = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
-  static_assert(THREADS == kPiece, "one record of every piece per thread");
+  static_assert(THREADS == kPiece, "one record of every piece per consumer thread");
   // (no static shared memory: the dynamic block starts the CTA's window, so the tensor-copy slots are
   // 128-byte aligned; the mbarriers live at its end)
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* s_ring = smem;                                                           // [kKeyRing][kKeySlotBytes]
-  uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem + kKeyRing * kKeySlotBytes);    // [T]
-  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                            // [T]
-  uint32_t* s_wh = s_w + T;                                                         // [WARPS][256]
-  uint32_t* s_tmp = s_wh + WARPS * kRadix;                                          // [32]
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_tmp + 32);                       // [kKeyRing]
+  uint8_t* s_ring = smem;                                                       // [RING][kKeySlotBytes]
+  uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem + RING * kKeySlotBytes);    // [T]
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                        // [T]
+  uint32_t* s_wh = s_w + T;                                                     // [WARPS][256]
+  uint32_t* s_tmp = s_wh + WARPS * kRadix;                                      // [32]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_tmp + 32);                   // [RING]
+  uint64_t* s_empty = s_full + RING;                                            // [RING]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
-  uint64_t pol_ef, pol_el;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
+  const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
   const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(s_ring);
-  if (tid < kKeyRing) ka_mbar_init(full0 + 8 * tid, 1);
+  if (tid < RING) {
+    ka_mbar_init(full0 + 8 * tid, 1);
+    ka_mbar_init(empty0 + 8 * tid, WARPS);
+  }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
   const uint64_t n4 = n & ~uint64_t(3);  // records inside the map
   const uint32_t my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const uint32_t total_pieces = my_tiles * kPieces;
-  auto issue = [&](uint32_t P) {  // thread 0 only
-    const uint32_t t = blockIdx.x + (P / kPieces) * gridDim.x;
-    const uint64_t r0 = (uint64_t)t * T + (uint64_t)(P % kPieces) * kPiece;
-    const uint32_t slot = P % kKeyRing;
-    const uint32_t mb = full0 + 8 * slot;
-    if (r0 < n4) {
-      // boxes past the last group are zero-filled by the TMA and still count their full bytes
-      const uint32_t dst = ring0 + slot * kKeySlotBytes;
-      const int g0 = (int)(r0 >> 2);
-      ka_mbar_expect_tx(mb, kKeySlotBytes);
-      ka_tma3(dst, &m1, 0, g0, mb, pol_ef);
-      ka_tma3(dst + kKeyGroups * 16, &m1, 6, g0, mb, pol_ef);
-      ka_tma3(dst + kKeyGroups * 32, &m2, 12, g0, mb, pol_ef);
-      ka_tma3(dst + kKeyGroups * 64, &m2, 18, g0, mb, pol_ef);
-    } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
-    }
-  };
-  if (tid == 0)
-    for (uint32_t P = 0; P < (uint32_t)kKeyRing && P < total_pieces; ++P) issue(P);
 
+  if (tid >= THREADS) {
+    // ================================================================ producer warp
+    if (lane == 0) {
+      uint64_t pol_ef;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+      for (uint32_t P = 0; P < total_pieces; ++P) {
+        const uint32_t slot = P % RING;
+        if (P >= (uint32_t)RING) ka_mbar_wait(empty0 + 8 * slot, ((P / RING) - 1) & 1u);
+        const uint32_t t = blockIdx.x + (P / kPieces) * gridDim.x;
+        const uint64_t r0 = (uint64_t)t * T + (uint64_t)(P % kPieces) * kPiece;
+        const uint32_t mb = full0 + 8 * slot;
+        if (r0 < n4) {
+          // boxes past the last group are zero-filled by the TMA and still count their full bytes
+          const uint32_t dst = ring0 + slot * kKeySlotBytes;
+          const int g0 = (int)(r0 >> 2);
+          ka_mbar_expect_tx(mb, kKeySlotBytes);
+          ka_tma3(dst, &m1, 0, g0, mb, pol_ef);
+          ka_tma3(dst + kKeyGroups * 16, &m1, 6, g0, mb, pol_ef);
+          ka_tma3(dst + kKeyGroups * 32, &m2, 12, g0, mb, pol_ef);
+          ka_tma3(dst + kKeyGroups * 64, &m2, 18, g0, mb, pol_ef);
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================================================ consumers
+  uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
+  uint64_t pol_el;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
   // where this thread's key words sit in a slot: record 4g + jj at byte 4 jj of its first row
   const uint32_t g = (uint32_t)tid >> 2, jj = (uint32_t)tid & 3u;
   const uint32_t key_off = jj == 0 ? g * 16 : jj == 1 ? kKeyGroups * 16 + g * 16 + 4
@@ -433,8 +481,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
       const uint32_t P = i * kPieces + j;
-      const uint32_t slot = P % kKeyRing;
-      ka_mbar_wait(full0 + 8 * slot, (P / kKeyRing) & 1u);
+      const uint32_t slot = P % RING;
+      ka_mbar_wait(full0 + 8 * slot, (P / RING) & 1u);
       const uint32_t r = j * THREADS + tid;
       if (r < cnt_t) {
         if (base + r < n4) {
@@ -452,10 +500,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       } else {
         a[j] = b[j] = c[j] = 0;
       }
-      __syncthreads();  // every thread has its key words: the slot may be refilled
-      if (tid == 0 && P + kKeyRing < total_pieces) {
+      __syncwarp();
+      if (lane == 0) {  // this warp is done with the slot (generic reads before the async-proxy refill)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(P + kKeyRing);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
       }
     }
 
@@ -463,6 +511,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t rank[ITEMS];
     uint32_t* wh = s_wh + warp * kRadix;
     const uint32_t lt = lanemask_lt();
+    ka_csync<THREADS>();  // s_wh zeroed
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
       const uint32_t r = j * THREADS + tid;
@@ -482,7 +531,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(&hist_copy[p16]),
                      "r"((uint32_t)__popc(peers16)), "l"(pol_el) : "memory");
     }
-    __syncthreads();
+    ka_csync<THREADS>();
 
     // ---- 3. per-digit totals over warps, tile exclusive offsets
     uint32_t total = 0;
@@ -494,14 +543,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         total += v;
       }
     }
-    const uint32_t excl = block_excl_scan<THREADS>(tid < kRadix ? total : 0, s_tmp, nullptr);
+    const uint32_t excl = ka_cscan<THREADS>(tid < kRadix ? total : 0, s_tmp);
     if (tid < kRadix) {
 #pragma unroll 4
       for (int w = 0; w < WARPS; ++w) s_wh[w * kRadix + tid] += excl;
       cnt[(uint64_t)tid * tiles + t] = total;
       lo[(uint64_t)t * kRadix + tid] = excl;
     }
-    __syncthreads();
+    ka_csync<THREADS>();
 
     // ---- 4. scatter into shared memory in byte-0 order
 #pragma unroll
@@ -516,14 +565,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         s_w[pos] = ((c[j] >> 8) & 0xFFu) << 24 | r;
       }
     }
-    __syncthreads();
+    ka_csync<THREADS>();
 
     // ---- 5. coalesced write-out
     for (uint32_t q = tid; q < cnt_t; q += THREADS) {
       k1_out[base + q] = s_k1[q];
       w_out[base + q] = s_w[q];
     }
-    __syncthreads();  // staging and per-warp counters reused by the next tile
+    ka_csync<THREADS>();  // staging and per-warp counters reused by the next tile
   }
 }
 
@@ -550,12 +599,18 @@ cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, u
       CUtensorMap m1, m2;  // boxes of 1 and 2 rows over kKeyGroups groups
       if ((e = record_group_map(&m1, in, n, 1, kKeyGroups)) != cudaSuccess) return e;
       if ((e = record_group_map(&m2, in, n, 2, kKeyGroups)) != cudaSuccess) return e;
-      auto kk = ka_tile_keys<kTileThreads, kTileItems>;
-      const size_t ksm = (size_t)kKeyRing * kKeySlotBytes + rest + 8 * kKeyRing;
-      e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);
-      if (e != cudaSuccess) return e;
-      kk<<<grid, kTileThreads, ksm, s>>>(m1, m2, in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key.len);
-      return cudaGetLastError();
+      const int ring = ka_ring_slots();
+      auto launch = [&](auto kk, int slots) {
+        const size_t ksm = (size_t)slots * kKeySlotBytes + rest + 16 * slots;
+        cudaError_t e2 = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);
+        if (e2 != cudaSuccess) return e2;
+        kk<<<grid, kTileThreads + 32, ksm, s>>>(m1, m2, in, n, tiles, k1_out, w_out, cnt, lo, hist16, copies, key.len);
+        return cudaGetLastError();
+      };
+      if (ring <= 4) return launch(ka_tile_keys<kTileThreads, kTileItems, 4>, 4);
+      if (ring <= 6) return launch(ka_tile_keys<kTileThreads, kTileItems, 6>, 6);
+      if (ring <= 8) return launch(ka_tile_keys<kTileThreads, kTileItems, 8>, 8);
+      return launch(ka_tile_keys<kTileThreads, kTileItems, 11>, 11);
     }
     auto sk = ka_tile_stream<kTileThreads, kTileItems>;
     const size_t ssm = (size_t)kRing * kPieceBytes + rest;

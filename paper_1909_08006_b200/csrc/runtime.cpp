@@ -51,6 +51,8 @@ const OptDesc kOpts[] = {
     {"dist_fault_stall", &Options::dist_fault_stall, 0, 1000},
     {"tma_l2_promo", &Options::tma_l2_promo, 0, 256},
     {"ws_gather_tma", &Options::ws_gather_tma, 0, 1},
+    {"ka_ring", &Options::ka_ring, 1, 11},
+    {"gather_l2_64", &Options::gather_l2_64, 0, 1},
 };
 }  // namespace
 

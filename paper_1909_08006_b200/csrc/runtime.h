@@ -57,7 +57,9 @@ struct Options {
   int64_t nccl_timeout_ms = 120000;  // multi-GPU: a collective not complete after this long aborts the comm
   int64_t dist_fault_stall = 0;      // test hook: stall the stream after the k-th collective of a call
   int64_t tma_l2_promo = 64;  // L2 promotion of the record tensor maps (0 = none, 64, 128, 256)
-  int64_t ws_gather_tma = 1;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
+  int64_t ws_gather_tma = 0;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
+  int64_t gather_l2_64 = 1;   // K-d CTA-tier gathers with cp.async .L2::64B (1) or without the hint (0)
+  int64_t ka_ring = 6;        // K-a key-row form: ring slots (4, 6, 8 or 11 pieces in flight)
 };
 Options options_snapshot();
 ley_status option_set(const char* name, int64_t value);
