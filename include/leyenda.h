@@ -229,6 +229,15 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    (LEY_ERR_NCCL); ley_comm_destroy still releases it. Default 120000, 50..3600000.
  *   "dist_fault_stall" test hook: after the k-th collective of a ley_sort_dist call the stream is held as
  *                    if a peer never completed it (0 = off), exercising the timeout + abort path on one GPU.
+ *   "ka_ring"        K-a key-row form: pieces in flight (4, 6 (default), 8 or 11; deeper measured slower)
+ *   "tma_l2_promo"   L2 promotion of the record tensor maps: 64 (default), 128, 256 or 0 ("none", which
+ *                    behaves like 128 on B200); profiles/r02_fetch_granularity.txt
+ *   "ws_gather_tma"  warp-specialised K-d+K-e tier: 0 (default) = record windows by plain bulk copies,
+ *                    1 = by tensor copies with 64-B L2 fetches (fewer DRAM bytes, measured slower)
+ *   "gather_l2_64"   alternating K-d+K-e tiers: 1 (default) = cp.async with .L2::64B, 0 = without the hint
+ *   "kc_fuse"        level-1 K-c split inside the K-d+K-e kernel of one tier: 0 (default) = its own kernel,
+ *                    1 = the tier of the average 16-bit bucket, 2..5 = the 2048 / 8192 / 10240 / 16384
+ *                    tier (tests); same bytes, measured slower
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
 ley_status ley_set_option(const char* name, int64_t value);
 ley_status ley_get_option(const char* name, int64_t* value);

@@ -25,6 +25,7 @@
 
 #include "classify.cuh"
 #include "common.cuh"
+#include "kc_chunk.cuh"
 #include "kernels.cuh"
 
 namespace ley {
@@ -231,19 +232,22 @@ struct KdLayout {
 //   3. exact rank inside every tiny sub-bucket (count of smaller composites; <= kd_insert_max), a warp
 //      bitonic network for larger ones — Alg. 1's ComparisonSort below tinyBucketThreshold,
 //   4. the bucket's records gathered into out[start, start+len) by the CTA's warps (see file header).
-template <uint32_t CAP, int THREADS, bool DG>
+// FUSED (level 1 only, THREADS >= 256): the kernel also owns the level-1 split, as kd_ws_sort's fused form
+// (kc_chunk.cuh): its items are the 16-bit buckets of tier `tier` claimed in ascending order, each sorted
+// once its byte-0 bucket is split; the CTA runs split chunks while it waits and after its last bucket.
+template <uint32_t CAP, int THREADS, bool DG, bool FUSED = false>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) > 8) ? 1 : (CAP / THREADS) > 4 ? 4 : 8)
     kd_cta_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                 uint32_t* __restrict__ perm, Tunables tu, const uint8_t* __restrict__ in, uint64_t in_bytes,
-                uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
+                uint8_t* __restrict__ out, uint64_t* __restrict__ dg, KcArgs kc = KcArgs{}, int tier = -1) {
   using L = KdLayout<CAP, THREADS>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int WARPS = L::WARPS;
   constexpr int ITEMS = CAP / THREADS;
   constexpr bool REGS = L::REGS;
   constexpr int RITEMS = REGS ? ITEMS : 1;
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + L::kIdx);
   uint32_t* s_perm = REGS ? reinterpret_cast<uint32_t*>(smem + L::kPerm) : s_idx;  // sorted ordinals
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem + L::kTail);
@@ -253,12 +257,50 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
   uint32_t* s_nbig = s_tmp + 32;
   uint8_t* s_stage = smem + L::kStage;                               // gather staging (reuses the sort area)
 
-  const uint32_t nitems = *count;
+  const uint32_t nitems = FUSED ? 0u : *count;
   const int warp = threadIdx.x >> 5;
-  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+  constexpr int KC_ITEMS = (kChunk + THREADS - 1) / THREADS;
+  static_assert(!FUSED || (THREADS >= kRadix && L::kBytes >= kKcSmem), "fused split geometry");
+  __shared__ uint32_t s_claim[4];
+  const uint32_t kc_total = FUSED ? kc.cstart[256] : 0u;
+  auto claim_chunk = [&]() -> uint32_t {  // next split chunk (~0u: none left)
+    if (threadIdx.x == 0) {
+      const uint32_t c = atomicAdd(kc.ticket, 1u);
+      s_claim[2] = c < kc_total ? c : ~0u;
+    }
+    __syncthreads();
+    const uint32_t c = s_claim[2];
+    __syncthreads();
+    return c;
+  };
+  uint32_t it = blockIdx.x;
+  while (true) {
+    Seg sg;
+    if constexpr (FUSED) {
+      if (threadIdx.x == 0) s_claim[0] = kc_claim_bucket(kc, [&](uint32_t len) { return tier_of(len, tu) == tier; });
+      __syncthreads();
+      const uint32_t p = s_claim[0];
+      __syncthreads();
+      if (p >= 65536u) break;
+      const uint32_t b0 = p >> 8, need = kc.cstart[b0 + 1] - kc.cstart[b0];
+      while (true) {  // byte-0 bucket b0 must be split: run chunks while waiting
+        if (threadIdx.x == 0) s_claim[1] = ld_acquire_u32(&kc.done[b0]) >= need;
+        __syncthreads();
+        const bool ready = s_claim[1] != 0;
+        __syncthreads();
+        if (ready) break;
+        const uint32_t c = claim_chunk();
+        if (c != ~0u) kc_chunk<THREADS, KC_ITEMS, SyncCta>(kc, c, smem);
+        else __nanosleep(1000);  // the remaining chunks are being split by running CTAs
+      }
+      sg = Seg{kc.B16[p], kc.hist16[p], 2u, 1u};
+    } else {
+      if (it >= nitems) break;
+      sg = list[it];
+      it += gridDim.x;
+    }
     for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;  // was gather staging
     __syncthreads();
-    const Seg sg = list[it];
     const uint32_t s = sg.len;
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
     const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
@@ -284,8 +326,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          tr[j] = tp[i];
-          xr[j] = ip[i];
+          tr[j] = __ldcg(tp + i);  // (L2 loads: in the fused form other SMs wrote these pairs during this kernel)
+          xr[j] = __ldcg(ip + i);
         }
       }
 #pragma unroll
@@ -301,8 +343,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t i = i0b + u * THREADS;
-          tb[u] = i < s ? tp[i] : 0;
-          xb[u] = (i < s && on_idx) ? ip[i] : 0;
+          tb[u] = i < s ? __ldcg(tp + i) : 0;
+          xb[u] = (i < s && on_idx) ? __ldcg(ip + i) : 0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -378,8 +420,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
         for (int u = 0; u < 8; ++u) {
           const uint32_t i = i0b + u * THREADS;
           if (i < s) {
-            tb[u] = tp[i];
-            xb[u] = ip[i];
+            tb[u] = __ldcg(tp + i);
+            xb[u] = __ldcg(ip + i);
           }
         }
 #pragma unroll
@@ -431,13 +473,18 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
                   DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
     __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
+  if constexpr (FUSED)  // the split's remaining chunks: the other tiers' buckets (later kernels) need them
+    for (uint32_t c = claim_chunk(); c != ~0u; c = claim_chunk()) kc_chunk<THREADS, KC_ITEMS, SyncCta>(kc, c, smem);
 }
 
 template <uint32_t CAP, int THREADS, bool DG>
 cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                             const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                            const uint8_t* in, uint64_t in_bytes, uint8_t* out, uint64_t* dg, cudaStream_t s) {
-  auto kern = kd_cta_sort<CAP, THREADS, DG>;
+                            const uint8_t* in, uint64_t in_bytes, uint8_t* out, uint64_t* dg, cudaStream_t s,
+                            const KcArgs* kc = nullptr, int tier = -1) {
+  auto kern = kd_cta_sort<CAP, THREADS, DG, false>;
+  if constexpr (THREADS >= kRadix && KdLayout<CAP, THREADS>::kBytes >= kKcSmem)
+    if (kc) kern = kd_cta_sort<CAP, THREADS, DG, true>;
   const size_t smem = KdLayout<CAP, THREADS>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -445,7 +492,8 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, in_bytes, out, dg);
+  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, in_bytes, out, dg,
+                                           kc ? *kc : KcArgs{}, tier);
   if (getenv("LEY_DEBUG_SYNC")) {
     fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
     cudaError_t e2 = cudaStreamSynchronize(s);
@@ -538,12 +586,19 @@ struct WsLayout {
   static constexpr size_t kBytes = kStage + (size_t)GW * 2 * kWsStageBytes;
 };
 
-template <uint32_t CAP, int ST, int GW, bool DG>
+constexpr uint32_t kEndDesc = 0xFFFFFFFFu;  // ring descriptor length that ends the gather group's loop
+
+// FUSED (level 1 only): the kernel also owns the level-1 split K-c (kc_chunk.cuh). Its items are the 16-bit
+// buckets of this tier claimed in ascending order from kc.kd_ticket instead of a list; before sorting a
+// bucket of byte-0 bucket b the sort group waits for done[b], running split chunks itself meanwhile, and
+// when no bucket is left it runs the split's remaining chunks (the other tiers' buckets need them).
+template <uint32_t CAP, int ST, int GW, bool DG, bool FUSED>
 __global__ void __launch_bounds__(ST + 32 * GW, 2)
     kd_ws_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                uint32_t* __restrict__ perm, Tunables tu, const __grid_constant__ CUtensorMap in_map,
-               const uint8_t* __restrict__ in, uint64_t n4, uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
+               const uint8_t* __restrict__ in, uint64_t n4, uint8_t* __restrict__ out, uint64_t* __restrict__ dg,
+               KcArgs kc) {
   using L = WsLayout<CAP, ST, GW>;
   constexpr uint32_t BINS = L::BINS;
   constexpr int ITEMS = CAP / ST;
@@ -560,21 +615,61 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
   uint32_t* s_nbig = s_tmp + 32;
   uint32_t* s_ring = reinterpret_cast<uint32_t*>(smem + L::kRing);
   uint2* s_desc = reinterpret_cast<uint2*>(smem + L::kDesc);
-  const uint32_t nitems = *count;
+  const uint32_t nitems = FUSED ? 0u : *count;
   const int tid = threadIdx.x;
+  static_assert(!FUSED || kKcSmem <= L::kTmp, "the split's staging reuses the sort area");
 
   if (tid < ST) {
     // ================================================================ sort group
     const int warp = tid >> 5;
+    using Group = SyncGroup<kBarSort, ST>;
+    uint32_t* s_claim = s_tmp + 40;  // (past the scan words and s_nbig; outside the split's staging)
+    const uint32_t kc_total = FUSED ? kc.cstart[256] : 0u;
+    // the next split chunk to run (thread 0 claims, the group reads; ~0u: none left)
+    auto claim_chunk = [&]() -> uint32_t {
+      if (tid == 0) {
+        const uint32_t c = atomicAdd(kc.ticket, 1u);
+        s_claim[2] = c < kc_total ? c : ~0u;
+      }
+      nbar_sync(kBarSort, ST);
+      const uint32_t c = s_claim[2];
+      nbar_sync(kBarSort, ST);  // (read by all before thread 0 writes it again)
+      return c;
+    };
     uint32_t k = 0;
-    for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
+    uint32_t it = blockIdx.x;
+    for (;; ++k) {
+      Seg sg;
+      if constexpr (FUSED) {
+        if (tid == 0)
+          s_claim[0] = kc_claim_bucket(kc, [&](uint32_t len) { return tier_of(len, tu) == kListMed2; });
+        nbar_sync(kBarSort, ST);
+        const uint32_t p = s_claim[0];
+        nbar_sync(kBarSort, ST);
+        if (p >= 65536u) break;
+        const uint32_t b0 = p >> 8, need = kc.cstart[b0 + 1] - kc.cstart[b0];
+        while (true) {  // byte-0 bucket b0 must be split: run chunks while waiting
+          if (tid == 0) s_claim[1] = ld_acquire_u32(&kc.done[b0]) >= need;
+          nbar_sync(kBarSort, ST);
+          const bool ready = s_claim[1] != 0;
+          nbar_sync(kBarSort, ST);
+          if (ready) break;
+          const uint32_t c = claim_chunk();
+          if (c != ~0u) kc_chunk<ST, (kChunk + ST - 1) / ST, Group>(kc, c, smem);
+          else __nanosleep(1000);  // the remaining chunks are being split by running CTAs
+        }
+        sg = Seg{kc.B16[p], kc.hist16[p], 2u, 1u};
+      } else {
+        if (it >= nitems) break;
+        sg = list[it];
+        it += gridDim.x;
+      }
       const int q = k & 1;
       uint32_t* s_perm = s_ring + q * CAP;
       if (k >= 2) nbar_sync(kBarEmpty + q, NT);  // the gather warps released slot q (bucket k-2)
       for (uint32_t g = tid; g <= BINS; g += ST) s_cnt[g] = 0;
       if (tid == 0) *s_nbig = 0;
       nbar_sync(kBarSort, ST);
-      const Seg sg = list[it];
       const uint32_t s = sg.len;
       const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
       const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
@@ -595,9 +690,9 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         const uint32_t i = j * ST + tid;
-        if (i < s) {
-          tr[j] = tp[i];
-          xr[j] = ip[i];
+        if (i < s) {  // (L2 loads: in the fused form other SMs wrote these pairs during this kernel)
+          tr[j] = __ldcg(tp + i);
+          xr[j] = __ldcg(ip + i);
         }
       }
 #pragma unroll
@@ -664,8 +759,18 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       __threadfence_block();
       nbar_arrive(kBarFull + q, NT);  // bucket k is in slot q
     }
-    // consume the gather group's last releases so no barrier is left with pending arrivals
-    for (uint32_t kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) nbar_sync(kBarEmpty + (kk & 1), NT);
+    if constexpr (FUSED) {  // the split's remaining chunks: the other tiers' buckets (later kernels) need them
+      for (uint32_t c = claim_chunk(); c != ~0u; c = claim_chunk()) kc_chunk<ST, (kChunk + ST - 1) / ST, Group>(kc, c, smem);
+    }
+    // end marker for the gather group, then consume its last releases so no barrier keeps pending arrivals
+    {
+      const int q = k & 1;
+      if (k >= 2) nbar_sync(kBarEmpty + q, NT);
+      if (tid == 0) s_desc[q] = make_uint2(0u, kEndDesc);
+      __threadfence_block();
+      nbar_arrive(kBarFull + q, NT);
+      for (uint32_t kk = k >= 2 ? k - 1 : 0; kk < k; ++kk) nbar_sync(kBarEmpty + (kk & 1), NT);
+    }
   } else {
     // ================================================================ gather group
     const int gw = (tid - ST) >> 5, lane = tid & 31;
@@ -676,11 +781,11 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     uint32_t phases = 0;
-    uint32_t k = 0;
-    for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
+    for (uint32_t k = 0;; ++k) {
       const int q = k & 1;
       nbar_sync(kBarFull + q, NT);
       const uint2 d = s_desc[q];
+      if (d.y == kEndDesc) break;
       const uint32_t* pr = s_ring + q * CAP;
       const uint32_t len = d.y;
       uint8_t* ob = out + (uint64_t)d.x * kRecordBytes;
@@ -736,11 +841,12 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
 template <uint32_t CAP, int ST, int GW, bool DG>
 cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_t* t0, const uint32_t* i0,
                            const uint64_t* t1, const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms,
-                           const uint8_t* in, uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s) {
+                           const uint8_t* in, uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s,
+                           const KcArgs* kc = nullptr) {
   CUtensorMap map;  // the record windows of tma_window: boxes of 7 rows x 1 group (tmap.cu)
   cudaError_t me = record_group_map(&map, in, n_in, 7, 1);
   if (me != cudaSuccess) return me;
-  auto kern = kd_ws_sort<CAP, ST, GW, DG>;
+  auto kern = kc ? kd_ws_sort<CAP, ST, GW, DG, true> : kd_ws_sort<CAP, ST, GW, DG, false>;
   const size_t smem = WsLayout<CAP, ST, GW>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -748,7 +854,8 @@ cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST + 32 * GW, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, map, in, n_in & ~uint64_t(3), out, dg);
+  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, map, in, n_in & ~uint64_t(3), out, dg,
+                                               kc ? *kc : KcArgs{});
   return cudaGetLastError();
 }
 
@@ -765,38 +872,47 @@ namespace {
 template <bool DG>
 cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1, const uint32_t* i1,
                    uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in, uint64_t n_in, uint8_t* out,
-                   uint64_t* dg, cudaStream_t s, int* launches) {
+                   uint64_t* dg, cudaStream_t s, int* launches, const KcArgs* kc, int fused_tier) {
   const uint64_t in_bytes = n_in * kRecordBytes;
-  cudaError_t e;
   static int warp_per_sm = 0;  // resident CTAs per SM (registers bound it: 5 at 46 registers)
   if (!warp_per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&warp_per_sm, kd_warp_sort<DG>, 256, 0) != cudaSuccess ||
                        warp_per_sm < 1))
     warp_per_sm = 4;
-  kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1, perm, in,
-                                                  in_bytes, out, dg);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
-  // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
-  if ((e = launch_cta_sort<512, 128, DG>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in, in_bytes,
-                                     out, dg, s)))
-    return e;
-  if (tu.kd_ws && out) {  // (no gather warps to feed in perm-only mode)
-    if ((e = launch_ws_sort<2048, 256, 8, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
-                                              n_in, out, dg, s)))
-      return e;
-  } else if ((e = launch_cta_sort<2048, 256, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu,
-                                             sms, in, in_bytes, out, dg, s))) {
-    return e;
-  }
-  if ((e = launch_cta_sort<8192, 1024, DG>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in, in_bytes,
-                                      out, dg, s)))
-    return e;
-  if ((e = launch_cta_sort<10240, 1024, DG>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
-                                        in, in_bytes, out, dg, s)))
-    return e;
-  if ((e = launch_cta_sort<16384, 768, DG>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
-                                       in, in_bytes, out, dg, s)))
-    return e;
+  // tier t's kernel; with split != nullptr the fused form (it also runs the level-1 split, and claims its
+  // buckets itself instead of reading list t)
+  auto tier_launch = [&](int t, const KcArgs* split) -> cudaError_t {
+    switch (t) {
+      case kListWarp:
+        kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1,
+                                                          perm, in, in_bytes, out, dg);
+        return cudaGetLastError();
+      // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
+      // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
+      case kListMed1:
+        return launch_cta_sort<512, 128, DG>(kd.items[kListMed1], kd.counts + kListMed1, t0, i0, t1, i1, perm, tu, sms, in,
+                                             in_bytes, out, dg, s);
+      case kListMed2:
+        if (tu.kd_ws && out)  // (no gather warps to feed in perm-only mode)
+          return launch_ws_sort<2048, 256, 8, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms,
+                                                  in, n_in, out, dg, s, split);
+        return launch_cta_sort<2048, 256, DG>(kd.items[kListMed2], kd.counts + kListMed2, t0, i0, t1, i1, perm, tu, sms, in,
+                                              in_bytes, out, dg, s, split, kListMed2);
+      case kListMed3:
+        return launch_cta_sort<8192, 1024, DG>(kd.items[kListMed3], kd.counts + kListMed3, t0, i0, t1, i1, perm, tu, sms, in,
+                                               in_bytes, out, dg, s, split, kListMed3);
+      case kListMed4:
+        return launch_cta_sort<10240, 1024, DG>(kd.items[kListMed4], kd.counts + kListMed4, t0, i0, t1, i1, perm, tu, sms,
+                                                in, in_bytes, out, dg, s, split, kListMed4);
+      default:
+        return launch_cta_sort<16384, 768, DG>(kd.items[kListMed5], kd.counts + kListMed5, t0, i0, t1, i1, perm, tu, sms,
+                                               in, in_bytes, out, dg, s, split, kListMed5);
+    }
+  };
+  cudaError_t e;
+  const bool fused = kc && fused_tier >= kListMed2 && fused_tier < kNumKdLists;
+  if (fused && (e = tier_launch(fused_tier, kc)) != cudaSuccess) return e;  // first: the split is done when it ends
+  for (int t = 0; t < kNumKdLists; ++t)
+    if (!(fused && t == fused_tier) && (e = tier_launch(t, nullptr)) != cudaSuccess) return e;
   if (launches) *launches += 6;
   return cudaSuccess;
 }
@@ -804,9 +920,10 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
 
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches) {
-  return dg && out ? kd_all<true>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, dg, s, launches)
-                   : kd_all<false>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, nullptr, s, launches);
+                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches, const KcArgs* kc,
+                          int fused_tier) {
+  return dg && out ? kd_all<true>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, dg, s, launches, kc, fused_tier)
+                   : kd_all<false>(kd, t0, i0, t1, i1, perm, tu, sms, in, n_in, out, nullptr, s, launches, kc, fused_tier);
 }
 
 }  // namespace ley

@@ -480,7 +480,8 @@ size_t split_smem_bytes() { return SplitSmem::kBytes; }
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
-                                   uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s) {
+                                   uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
+                                   bool run_split, const uint32_t** order_used) {
   kc_plan_level1<<<(grid_ub + 255) / 256, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -494,6 +495,8 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
   }
   e = cudaMemcpyAsync(cursor, B16, 4 * 65536, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return e;
+  if (order_used) *order_used = order;
+  if (!run_split) return cudaSuccess;  // (the fused K-d+K-e kernel runs the chunks: kc_chunk.cuh)
   size_t smem = SplitSmem::kBytes;
   e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -41,7 +41,8 @@ size_t split_smem_bytes();
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
-                                   uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s);
+                                   uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
+                                   bool run_split = true, const uint32_t** order_used = nullptr);
 cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
 cudaError_t launch_kr_chunk_map(const uint32_t* cstart, uint32_t nseg, uint32_t ub, uint2* map, cudaStream_t s);
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
@@ -59,10 +60,14 @@ cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B1
                                       const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
 // K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
 // out == nullptr: perm-only, no gather; dg non-null: dg[j] = digest of output record j's 10-byte prefix).
-// in holds n_in records; no gather reads outside them.
+// in holds n_in records; no gather reads outside them. Level 1 only: with kc and a fused_tier in
+// [kListMed2, kNumKdLists) that tier's kernel runs first and also performs the level-1 split K-c
+// (kc_chunk.cuh), claiming its own buckets from kc->kd_ticket (its list is ignored).
+struct KcArgs;
 cudaError_t launch_kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1,
                           const uint32_t* i1, uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in,
-                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches);
+                          uint64_t n_in, uint8_t* out, uint64_t* dg, cudaStream_t s, int* launches,
+                          const KcArgs* kc = nullptr, int fused_tier = -1);
 
 // K-e over one window of the sorted order (k_gather.cu): out[j] = in[perm[j]], j < cnt
 cudaError_t launch_ke_gather(const uint8_t* in, const uint32_t* perm, uint64_t cnt, uint8_t* out, int sms,

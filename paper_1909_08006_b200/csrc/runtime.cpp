@@ -53,6 +53,7 @@ const OptDesc kOpts[] = {
     {"ws_gather_tma", &Options::ws_gather_tma, 0, 1},
     {"ka_ring", &Options::ka_ring, 1, 11},
     {"gather_l2_64", &Options::gather_l2_64, 0, 1},
+    {"kc_fuse", &Options::kc_fuse, 0, 5},
 };
 }  // namespace
 
@@ -128,7 +129,7 @@ InternalLayout plan_internal(uint64_t n) {
   L.off_cstart = take(4 * 260);
   L.off_scan_status = take(8 * 2 * L.scan_status_words);
   L.off_cursor = take(4 * 65536);
-  L.off_small = take(4 * 64);  // tickets + list counters
+  L.off_small = take(4 * kSmallWords);  // tickets, list counters, the fused split's done[256] + K-d ticket
   L.off_plan_a = take(16 * L.split_chunks_ub);
   L.off_plan_b = take(8 * L.split_chunks_ub);
   L.off_order = take(4 * L.split_chunks_ub);  // K-c chunk processing order

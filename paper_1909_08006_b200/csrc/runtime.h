@@ -59,6 +59,8 @@ struct Options {
   int64_t tma_l2_promo = 64;  // L2 promotion of the record tensor maps (0 = none, 64, 128, 256)
   int64_t ws_gather_tma = 0;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
   int64_t gather_l2_64 = 1;   // K-d CTA-tier gathers with cp.async .L2::64B (1) or without the hint (0)
+  int64_t kc_fuse = 0;  // level-1 split fused into a K-d+K-e tier (0 off, 1 auto, 2..5 force tier 2048..16384):
+                        // measured slower (C2 K-c+K-de 7.49 vs 6.40 ms, C4 54.5 vs 38.8 ms)
   int64_t ka_ring = 6;        // K-a key-row form: ring slots (4, 6, 8 or 11 pieces in flight)
 };
 Options options_snapshot();
@@ -66,6 +68,9 @@ ley_status option_set(const char* name, int64_t value);
 ley_status option_get(const char* name, int64_t* value);
 
 // ------------------------------------------------------------------ plan (host-only arithmetic)
+// small counters of one sort (zeroed per call): [0, 16) tickets, [16, 16 + kNumKdLists) K-d list counts,
+// [32] big-bucket count, [64, 320) done chunks per byte-0 bucket (fused split), [320] fused K-d ticket
+constexpr uint32_t kSmallWords = 64 + 256 + 16;
 struct InternalLayout {
   uint64_t n = 0, tiles = 0, m = 0;  // m = 256 * tiles
   uint64_t split_chunks_ub = 0;      // level-1 chunk upper bound
