@@ -76,61 +76,6 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;
-
-  // ---------------------------------------------------------------- zero counters / look-back state
-  if ((st = prof.begin("init"))) return st;
-  LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4ull * 65536 * L.hist_copies, s));
-  LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * kSmallWords, s));
-  LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
-  if ((st = prof.end())) return st;
-
-  // ---------------------------------------------------------------- K-a
-  if ((st = prof.begin("K-a tile sort"))) return st;
-  LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, (int)o.ka_stream,
-                                                key, s));
-  ++launches;
-  if ((st = prof.end())) return st;
-
-  // ---------------------------------------------------------------- K-b
-  if ((st = prof.begin("K-b scan"))) return st;
-  LEY_CUDA("K-b scan", launch_hist_reduce(hist16, L.hist_copies, s));
-  LEY_CUDA("K-b scan", launch_scan_excl(cnt, off, L.m, scan_status, tickets + 0, off + L.m, s));
-  LEY_CUDA("K-b scan", launch_scan_excl(hist16, B16, 65536, scan_status + L.scan_status_words, tickets + 1,
-                                        B16 + 65536, s));
-  LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
-  launches += 4;
-  if ((st = prof.end())) return st;
-
-  // ---------------------------------------------------------------- K-c (byte 1)
-  // Fused form (option kc_fuse, off by default: measured slower): the split runs inside the
-  // level-1 K-d+K-e kernel of the tier the average 16-bit bucket falls in (kc_chunk.cuh), meant for the idle
-  // issue slots of its DRAM-bound record gather; the tier is a guess (n / 65536), any choice gives the same
-  // bytes. Not for tiers of small buckets (warp /
-  // 128-thread kernels) unless forced (kc_fuse = 2..5: the 2048 / 8192 / 10240 / 16384 tier; tests), nor in
-  // perm-only mode.
-  int fused_tier = -1;
-  if (o.kc_fuse >= 2 && out) {
-    fused_tier = kListMed2 + (int)(o.kc_fuse - 2);
-  } else if (o.kc_fuse && out) {
-    const uint64_t avg = n / 65536;
-    const int t = avg <= tu.warp_tier_max ? kListWarp : avg > tu.smem_tier_max ? kNumKdLists
-                : avg <= 512 ? kListMed1 : avg <= 2048 ? kListMed2 : avg <= 8192 ? kListMed3 : avg <= 10240 ? kListMed4
-                                                                                                   : kListMed5;
-    if (t >= kListMed2 && t < kNumKdLists) fused_tier = t;
-  }
-  const uint32_t* order_used = nullptr;
-  if ((st = prof.begin(fused_tier >= 0 ? "K-c plan" : "K-c split"))) return st;
-  LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
-                                               reinterpret_cast<uint4*>(base + L.off_plan_a),
-                                               reinterpret_cast<uint2*>(base + L.off_plan_b),
-                                               reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
-                                               tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, fused_tier < 0,
-                                               &order_used));
-  launches += fused_tier < 0 ? 2 : 1;
-  if ((st = prof.end())) return st;
-
-  // ---------------------------------------------------------------- classify level 1, K-d
-  if ((st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
   uint64_t tier = std::max<uint64_t>(tu.smem_tier_max, tu.warp_tier_max);
   uint64_t big_cap = std::min<uint64_t>(65536, n / (tier + 1) + 1);
   uint32_t kd_cap = (uint32_t)std::min<uint64_t>(65536, n);  // level-1 buckets: at most min(2^16, n) non-empty
@@ -145,31 +90,106 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     kd.cap = cap;
   };
   bind_lists(kd_cap);
-  LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
-  ++launches;
-  KcArgs kc;
-  if (fused_tier >= 0) {
-    kc.k1_in = At;
-    kc.w_in = Ai;
-    kc.tiles = tiles;
-    kc.off = off;
-    kc.lo = lo;
-    kc.cstart = cstart;
-    kc.plan_a = reinterpret_cast<const uint4*>(base + L.off_plan_a);
-    kc.plan_b = reinterpret_cast<const uint2*>(base + L.off_plan_b);
-    kc.order = order_used;
-    kc.cursor = cursor;
-    kc.ticket = tickets + 2;
-    kc.done = small + 64;
-    kc.kd_ticket = small + 320;
-    kc.tail_out = Bt;
-    kc.idx_out = Bi;
-    kc.hist16 = hist16;
-    kc.B16 = B16;
+
+  // Level 1 (init .. K-a .. K-b .. K-c .. classify .. K-d+K-e of every tier .. publish of the big-bucket
+  // count) is a fixed sequence for a given (buffers, n, options): ~16 launches whose launch overhead
+  // dominates small sorts (C1). It is captured once into a CUDA graph and replayed (option "graphs"), on
+  // the library's own stream joined to the caller's by events (the caller's stream may be the legacy
+  // default stream, which cannot be captured). With stage profiling on it runs directly.
+  auto level1 = [&](cudaStream_t s) -> ley_status {
+    ley_status st;
+
+    // ---------------------------------------------------------------- zero counters / look-back state
+    if ((st = prof.begin("init"))) return st;
+    LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4ull * 65536 * L.hist_copies, s));
+    LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * kSmallWords, s));
+    LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
+    if ((st = prof.end())) return st;
+
+    // ---------------------------------------------------------------- K-a
+    if ((st = prof.begin("K-a tile sort"))) return st;
+    LEY_CUDA("K-a tile sort", launch_ka_tile_sort(in, n, tiles, At, Ai, cnt, lo, hist16, L.hist_copies, (int)o.ka_stream,
+                                                  key, s));
+    ++launches;
+    if ((st = prof.end())) return st;
+
+    // ---------------------------------------------------------------- K-b
+    if ((st = prof.begin("K-b scan"))) return st;
+    LEY_CUDA("K-b scan", launch_hist_reduce(hist16, L.hist_copies, s));
+    LEY_CUDA("K-b scan", launch_scan_excl(cnt, off, L.m, scan_status, tickets + 0, off + L.m, s));
+    LEY_CUDA("K-b scan", launch_scan_excl(hist16, B16, 65536, scan_status + L.scan_status_words, tickets + 1,
+                                          B16 + 65536, s));
+    LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
+    launches += 4;
+    if ((st = prof.end())) return st;
+
+    // ---------------------------------------------------------------- K-c (byte 1)
+    // Fused form (option kc_fuse, off by default: measured slower): the split runs inside the
+    // level-1 K-d+K-e kernel of the tier the average 16-bit bucket falls in (kc_chunk.cuh), meant for the idle
+    // issue slots of its DRAM-bound record gather; the tier is a guess (n / 65536), any choice gives the same
+    // bytes. Not for tiers of small buckets (warp /
+    // 128-thread kernels) unless forced (kc_fuse = 2..5: the 2048 / 8192 / 10240 / 16384 tier; tests), nor in
+    // perm-only mode.
+    int fused_tier = -1;
+    if (o.kc_fuse >= 2 && out) {
+      fused_tier = kListMed2 + (int)(o.kc_fuse - 2);
+    } else if (o.kc_fuse && out) {
+      const uint64_t avg = n / 65536;
+      const int t = avg <= tu.warp_tier_max ? kListWarp : avg > tu.smem_tier_max ? kNumKdLists
+                  : avg <= 512 ? kListMed1 : avg <= 2048 ? kListMed2 : avg <= 8192 ? kListMed3 : avg <= 10240 ? kListMed4
+                                                                                                     : kListMed5;
+      if (t >= kListMed2 && t < kNumKdLists) fused_tier = t;
+    }
+    const uint32_t* order_used = nullptr;
+    if ((st = prof.begin(fused_tier >= 0 ? "K-c plan" : "K-c split"))) return st;
+    LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
+                                                 reinterpret_cast<uint4*>(base + L.off_plan_a),
+                                                 reinterpret_cast<uint2*>(base + L.off_plan_b),
+                                                 reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
+                                                 tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, fused_tier < 0,
+                                                 &order_used));
+    launches += fused_tier < 0 ? 2 : 1;
+    if ((st = prof.end())) return st;
+
+    // ---------------------------------------------------------------- classify level 1, K-d
+    if ((st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
+    LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
+    ++launches;
+    KcArgs kc;
+    if (fused_tier >= 0) {
+      kc.k1_in = At;
+      kc.w_in = Ai;
+      kc.tiles = tiles;
+      kc.off = off;
+      kc.lo = lo;
+      kc.cstart = cstart;
+      kc.plan_a = reinterpret_cast<const uint4*>(base + L.off_plan_a);
+      kc.plan_b = reinterpret_cast<const uint2*>(base + L.off_plan_b);
+      kc.order = order_used;
+      kc.cursor = cursor;
+      kc.ticket = tickets + 2;
+      kc.done = small + 64;
+      kc.kd_ticket = small + 320;
+      kc.tail_out = Bt;
+      kc.idx_out = Bi;
+      kc.hist16 = hist16;
+      kc.B16 = B16;
+    }
+    LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, n, out, digest, s,
+                                               &launches, fused_tier >= 0 ? &kc : nullptr, fused_tier));
+    LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
+    return LEY_OK;
+  };
+  // (not while profiling: elapsed times between event-record nodes of a graph are refused, measured)
+  const bool graphs = o.graphs && !prof.on && !getenv("LEY_DEBUG_SYNC");
+  if (!graphs) {
+    if ((st = level1(s))) return st;
+  } else {
+    const GraphKey gk{{(uint64_t)in, (uint64_t)out, (uint64_t)perm_out, (uint64_t)digest, (uint64_t)work,
+                       (uint64_t)ctx.lists.ptr, (uint64_t)ctx.big[0].ptr, (uint64_t)ctx.host_pinned, n,
+                       ((uint64_t)key.off << 32) | key.len, options_fingerprint(o), (uint64_t)ctx.sms}};
+    if ((st = graph_run(ctx, gk, s, [&](cudaStream_t cs) { return level1(cs); }, prof))) return st;
   }
-  LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, n, out, digest, s,
-                                             &launches, fused_tier >= 0 ? &kc : nullptr, fused_tier));
-  LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
   LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
   uint32_t nbig = host_cnt[0];
   if ((st = prof.end())) return st;

@@ -54,6 +54,7 @@ const OptDesc kOpts[] = {
     {"ka_ring", &Options::ka_ring, 1, 11},
     {"gather_l2_64", &Options::gather_l2_64, 0, 1},
     {"kc_fuse", &Options::kc_fuse, 0, 5},
+    {"graphs", &Options::graphs, 0, 1},
 };
 }  // namespace
 
@@ -306,6 +307,87 @@ ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaSt
   return LEY_OK;
 }
 
+uint64_t options_fingerprint(const Options& o) {
+  uint64_t h = 1469598103934665603ull;
+  for (const OptDesc& d : kOpts) h = (h ^ (uint64_t)(o.*(d.field))) * 1099511628211ull;
+  return h;
+}
+
+void graphs_release(DeviceContext& c) {
+  for (auto& g : c.graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c.graphs.clear();
+}
+
+ley_status graph_run(DeviceContext& ctx, const GraphKey& key, cudaStream_t s,
+                     const std::function<ley_status(cudaStream_t)>& fn, Profiler& prof) {
+  if (!ctx.graph_stream) {
+    LEY_CUDA("graph", cudaStreamCreateWithFlags(&ctx.graph_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx.graph_ev) LEY_CUDA("graph", cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  uint64_t k[13];
+  memcpy(k, key.w, sizeof(key.w));
+  k[12] = ((uint64_t)(prof.on ? 1 : 0) << 32) | (uint32_t)prof.next_event;  // (event indices are baked in)
+  DeviceContext::Graph* g = nullptr;
+  for (auto& e : ctx.graphs)
+    if (memcmp(e.key, k, sizeof(k)) == 0) g = &e;
+  const cudaStream_t prof_stream = prof.stream;
+  if (!g) {
+    const int launches0 = prof.launches, event0 = prof.next_event;
+    const size_t names0 = prof.names.size(), b0 = prof.ev_begin.size(), e0 = prof.ev_end.size();
+    cudaGraph_t graph = nullptr;
+    LEY_CUDA("graph capture", cudaStreamBeginCapture(ctx.graph_stream, cudaStreamCaptureModeThreadLocal));
+    prof.stream = ctx.graph_stream;
+    const ley_status st = fn(ctx.graph_stream);
+    prof.stream = prof_stream;
+    const cudaError_t ce = cudaStreamEndCapture(ctx.graph_stream, &graph);
+    cudaGraphExec_t exec = nullptr;
+    DeviceContext::Graph ng;
+    ng.names.assign(prof.names.begin() + names0, prof.names.end());
+    ng.ev_begin.assign(prof.ev_begin.begin() + b0, prof.ev_begin.end());
+    ng.ev_end.assign(prof.ev_end.begin() + e0, prof.ev_end.end());
+    ng.events = prof.next_event - event0;
+    ng.launches = prof.launches - launches0;
+    prof.names.resize(names0);  // (the replay below adds them back)
+    prof.ev_begin.resize(b0);
+    prof.ev_end.resize(e0);
+    prof.next_event = event0;
+    prof.launches = launches0;
+    const cudaError_t ie = (st || ce != cudaSuccess || !graph) ? cudaErrorUnknown : cudaGraphInstantiate(&exec, graph, 0);
+    if (ie != cudaSuccess) {
+      if (getenv("LEY_DEBUG_GRAPH"))
+        fprintf(stderr, "[ley] graph capture failed: fn %d (%s), end %s, instantiate %s\n", (int)st, last_error(),
+                cudaGetErrorString(ce), cudaGetErrorString(ie));
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      return fn(s);  // (capture is an optimisation: run the sequence directly)
+    }
+    cudaGraphDestroy(graph);
+    if (ctx.graphs.size() >= 8) {  // evict the least recently used
+      auto lru = std::min_element(ctx.graphs.begin(), ctx.graphs.end(),
+                                  [](const auto& x, const auto& y) { return x.used < y.used; });
+      cudaGraphExecDestroy(lru->exec);
+      ctx.graphs.erase(lru);
+    }
+    memcpy(ng.key, k, sizeof(k));
+    ng.exec = exec;
+    ctx.graphs.push_back(std::move(ng));
+    g = &ctx.graphs.back();
+  }
+  g->used = ++ctx.graph_clock;
+  LEY_CUDA("graph", cudaEventRecord(ctx.graph_ev[0], s));
+  LEY_CUDA("graph", cudaStreamWaitEvent(ctx.graph_stream, ctx.graph_ev[0], 0));
+  LEY_CUDA("graph", cudaGraphLaunch(g->exec, ctx.graph_stream));
+  LEY_CUDA("graph", cudaEventRecord(ctx.graph_ev[1], ctx.graph_stream));
+  LEY_CUDA("graph", cudaStreamWaitEvent(s, ctx.graph_ev[1], 0));
+  prof.launches += g->launches;
+  prof.names.insert(prof.names.end(), g->names.begin(), g->names.end());
+  prof.ev_begin.insert(prof.ev_begin.end(), g->ev_begin.begin(), g->ev_begin.end());
+  prof.ev_end.insert(prof.ev_end.end(), g->ev_end.begin(), g->ev_end.end());
+  prof.next_event += g->events;
+  return LEY_OK;
+}
+
 void release_device(int device) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
   for (int d = 0; d < 64; ++d) {
@@ -314,6 +396,7 @@ void release_device(int device) {
     DeviceContext& c = *g_ctx[d];
     pipe_release(c);  // stops the streaming worker first (it takes c.mu for its sorts)
     std::lock_guard<std::mutex> g2(c.mu);
+    graphs_release(c);  // (they hold this context's buffer and pinned-counter addresses)
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(d);
@@ -395,7 +478,10 @@ void Profiler::finish() {
   // stages that recur (one per MSD recursion level) are summed under their name, in first-use order
   for (size_t i = 0; i < names.size() && i < ev_end.size(); ++i) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, ctx->events[ev_begin[i]], ctx->events[ev_end[i]]);
+    if (cudaEventElapsedTime(&ms, ctx->events[ev_begin[i]], ctx->events[ev_end[i]]) != cudaSuccess) {
+      cudaGetLastError();  // (a stage without a valid pair of events reports 0 rather than poisoning the next call)
+      ms = 0.f;
+    }
     size_t k = 0;
     while (k < g_stages.names.size() && strcmp(g_stages.names[k], names[i]) != 0) ++k;
     if (k == g_stages.names.size()) {

@@ -7,6 +7,7 @@
 
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -59,6 +60,7 @@ struct Options {
   int64_t tma_l2_promo = 64;  // L2 promotion of the record tensor maps (0 = none, 64, 128, 256)
   int64_t ws_gather_tma = 0;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
   int64_t gather_l2_64 = 1;   // K-d CTA-tier gathers with cp.async .L2::64B (1) or without the hint (0)
+  int64_t graphs = 1;   // replay level 1 of the internal sort from a cached CUDA graph (0: launch directly)
   int64_t kc_fuse = 0;  // level-1 split fused into a K-d+K-e tier (0 off, 1 auto, 2..5 force tier 2048..16384):
                         // measured slower (C2 K-c+K-de 7.49 vs 6.40 ms, C4 54.5 vs 38.8 ms)
   int64_t ka_ring = 6;        // K-a key-row form: ring slots (4, 6, 8 or 11 pieces in flight)
@@ -116,6 +118,21 @@ struct DeviceContext {
   static constexpr int kExtEvents = 8;
   cudaEvent_t ev[kExtEvents] = {};
   std::vector<cudaEvent_t> events;
+  // cached CUDA graphs of the internal sort's level 1 (internal.cu), replayed on their own stream
+  struct Graph {
+    uint64_t key[13] = {};
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+    uint64_t used = 0;
+    // profiler ranges recorded inside the graph (event record nodes): names and event indices
+    std::vector<const char*> names;
+    std::vector<int> ev_begin, ev_end;
+    int events = 0;
+  };
+  std::vector<Graph> graphs;
+  uint64_t graph_clock = 0;
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t graph_ev[2] = {nullptr, nullptr};
   // streaming host sort (ley_sort_submit): two device staging slots (in | out), three streams and a
   // worker thread, so the H2D of call k+1, the sort of call k and the D2H of call k-1 all overlap
   struct Pipe {
@@ -160,6 +177,19 @@ struct DeviceContext {
 };
 DeviceContext& device_context(int device);
 ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaStream_t s);
+// Runs fn (a fixed sequence of stream work) as a CUDA graph cached under key: on the first call fn is
+// captured on the context's graph stream (falling back to running fn(s) directly if capture fails), then
+// the graph is launched on the graph stream ordered after s, and s after it. prof's launch count grows by
+// the kernel launches fn made while captured, and the profiler ranges fn opened (their events are record
+// nodes of the graph, so stage times stay live) are replayed into prof.
+struct GraphKey {
+  uint64_t w[12];
+};
+uint64_t options_fingerprint(const Options& o);
+struct Profiler;
+ley_status graph_run(DeviceContext& ctx, const GraphKey& key, cudaStream_t s,
+                     const std::function<ley_status(cudaStream_t)>& fn, Profiler& prof);
+void graphs_release(DeviceContext& ctx);
 // library device-memory accounting (ensure_buffer and the few direct allocations report here)
 void track_device_bytes(int64_t delta);
 void device_bytes(uint64_t* current, uint64_t* peak, bool reset_peak);

@@ -62,7 +62,16 @@ for v in variants:
         for k, val in ley.ley_stage_times()[0]:
             acc.setdefault(k, []).append(val)
     ley.ley_set_option("profile", 0)
-    print(f"{name:14s} {dist} n={n} {'CHECK-OK' if ok else 'CHECK-FAILED'} total {statistics.median(tot):.3f} ms",
+    plain = []
+    for _ in range(5):  # without stage events (level 1 from its CUDA graph)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ley.ley_sort(x, out, n)
+        e1.record()
+        torch.cuda.synchronize()
+        plain.append(e0.elapsed_time(e1))
+    print(f"{name:14s} {dist} n={n} {'CHECK-OK' if ok else 'CHECK-FAILED'} plain {statistics.median(plain):.3f} ms "
+          f"profiled {statistics.median(tot):.3f} ms",
           {k: round(statistics.mean(vv), 3) for k, vv in acc.items()}, flush=True)
     for k, val in defaults.items():
         ley.ley_set_option(k, val)
