@@ -227,11 +227,11 @@ __global__ void __launch_bounds__(256) mbt_gv(const __grid_constant__ CUtensorMa
     const uint32_t mb = sa(&bars[w * STAGES + st]);
     const uint32_t p = perm[g * 32 + lane];
     const uint32_t dst = sa(stage0 + (st * 32 + lane) * 128);
-    const uint8_t* src = in + (((uint64_t)p * 100) & ~15ull);
-    if (mode <= 1) {
-      if (lane == 0) mbar_expect(mb, 32 * 112);
+    const uint8_t* src = mode == 7 ? in + (uint64_t)p * 128 : in + (((uint64_t)p * 100) & ~15ull);  // 7: line-aligned
+    if (mode <= 1 || mode >= 4) {
+      if (lane == 0) mbar_expect(mb, 32 * 112);  // (mode 7 copies 112 B of a 128-B-aligned slot)
       __syncwarp();
-      if (mode == 0) bulk_g2s(dst, src, 112, mb);
+      if (mode == 0 || mode >= 4) bulk_g2s(dst, src, 112, mb);
       else asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                         ::"r"(dst), "l"((uint64_t)&gm), "r"(0), "r"((int)((100u * (p & 3u)) >> 4)), "r"((int)(p >> 2)), "r"(mb) : "memory");
     } else {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) mbt_gv(const __grid_constant__ CUtensorMa
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(mb) : "memory");
     }
   };
-  if (mode >= 2 && lane < STAGES) {  // cp.async completion: 32 arrivals (one per lane) per phase
+  if ((mode == 2 || mode == 3) && lane < STAGES) {  // cp.async completion: 32 arrivals (one per lane) per phase
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&bars[w * STAGES + lane])), "r"(32) : "memory");
   }
   __syncwarp();
@@ -271,6 +271,13 @@ __global__ void __launch_bounds__(256) mbt_gv(const __grid_constant__ CUtensorMa
       __syncwarp();
       const uint64_t gn = g + (uint64_t)STAGES * nw;
       if (gn < ngroups) { issue(gn, st); pr[st] = perm[gn * 32 + lane]; }
+      if (mode >= 4) {  // L2 prefetch of the window PF groups beyond the next issue (no shared memory used)
+        const uint64_t pf = gn + (uint64_t)(mode == 4 ? 2 : mode == 5 ? 4 : 8) * nw;
+        if (pf < ngroups) {
+          const uint32_t q = perm[pf * 32 + lane];
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], 112;" ::"l"(in + (((uint64_t)q * 100) & ~15ull)) : "memory");
+        }
+      }
     }
     phase ^= 1;
   }
