@@ -141,6 +141,41 @@ def test_repeat_bit_identical():
     assert_parity(recs, a, pa)
 
 
+def test_graph_replay_matches_direct():
+    """Level 1 is captured into a CUDA graph on the first call and replayed after (option graphs): replays,
+    a direct launch, a changed option (new graph key), a different caller stream, the profiled form and a
+    released cache (graphs dropped with the buffers they point into) all give the oracle's bytes."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    n = 150_001
+    recs = gen.records(n, seed=41, dist="skewed")
+    exp, _ = oracle.sort(recs)
+    x = to_device(recs)
+    out = torch.empty_like(x)
+
+    def run(**opts):
+        out.zero_()
+        with Options(**opts):
+            ley.ley_sort(x, out, n)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), exp)
+
+    for _ in range(3):
+        run(graphs=1)
+    run(graphs=0)
+    run(graphs=1, kd_ws=0)
+    run(graphs=1, profile=1)
+    side = torch.cuda.Stream()
+    out.zero_()
+    ley.ley_sort(x, out, n, stream=side)
+    side.synchronize()
+    assert np.array_equal(out.cpu().numpy(), exp)
+    ley.ley_release_cache(-1)
+    run(graphs=1)
+
+
 def test_pinned_host_path():
     """Pinned host pointers take the staged path (H2D, internal sort, D2H)."""
     import paper_1909_08006_b200 as ley

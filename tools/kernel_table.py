@@ -1,12 +1,14 @@
 """Per-kernel DRAM table from the committed ncu launch lists (SURVEY §8d "ncu evidence"): for the second
 ley_sort call of each config, every kernel's summed duration, DRAM bytes, bytes per record, achieved GB/s
 and its fraction of the measured copy peak (MEASURED_PEAKS.json) and of the 8 TB/s nominal HBM3e peak.
-usage: python tools/kernel_table.py > profiles/r01_kernel_table.md"""
+usage: python tools/kernel_table.py [round] > profiles/rNN_kernel_table.md"""
 import csv
 import json
 import os
 import re
+import sys
 
+ROUND = sys.argv[1] if len(sys.argv) > 1 else "r02"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CFG = {"c1": 1e6, "c2": 1e8, "c3": 2e8, "c4": 6e8}
 peak = 6456.8
@@ -23,7 +25,7 @@ def short(name):
 
 print(f"# Per-kernel DRAM traffic and rate (ncu, 2nd ley_sort call; peak {peak} GB/s measured, 8000 nominal)\n")
 for c, n in CFG.items():
-    f = os.path.join(ROOT, "profiles", f"r01_launches_{c}.csv")
+    f = os.path.join(ROOT, "profiles", f"{ROUND}_launches_{c}.csv")
     if not os.path.exists(f):
         continue
     rows = list(csv.reader(open(f)))
