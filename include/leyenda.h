@@ -235,6 +235,12 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *   "ws_gather_tma"  warp-specialised K-d+K-e tier: 0 (default) = record windows by plain bulk copies,
  *                    1 = by tensor copies with 64-B L2 fetches (fewer DRAM bytes, measured slower)
  *   "gather_l2_64"   alternating K-d+K-e tiers: 1 (default) = cp.async with .L2::64B, 0 = without the hint
+ *   "ext_keyptr"     external path form: 0 (default) = runs of whole records; 1 = the paper's key-pointer
+ *                    pattern: runs of 16-byte (key, ordinal) tuples (host
+ *                    scratch 16 instead of 100 B/record), every output record gathered from the pinned
+ *                    input by its ordinal over the host link (the input must be mapped pinned memory:
+ *                    cudaHostAlloc, or cudaHostRegister with cudaHostRegisterMapped; else
+ *                    LEY_ERR_UNSUPPORTED). Same bytes; slower on PCIe (random reads over the link)
  *   "graphs"         1 (default) = level 1 of the internal sort (init .. K-e, ~16 launches) is captured once
  *                    per (buffers, n, options) into a CUDA graph and replayed on a library stream joined to
  *                    the caller's by events (C1 1e6 records: 0.225 -> 0.187 ms); not while "profile" is on

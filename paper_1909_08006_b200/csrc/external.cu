@@ -175,6 +175,149 @@ __global__ void ext_gather(const uint32_t* __restrict__ slice, const uint64_t* _
   }
 }
 
+// ------------------------------------------------------------------ key-pointer form (option ext_keyptr)
+// SURVEY §8f NEXT 3, the paper's own §3.2 pattern ("radix sort ... on key-pointer tuples only";
+// P:104-106 the records are then scattered given the sorted tuples): runs hold 16-byte (key, ordinal)
+// tuples instead of 100-byte records, and the merge gathers every output record from the caller's pinned
+// input by its ordinal. Tuple: x,y = key bytes 0..7 big-endian (y = high word), z = key bytes 8..9
+// big-endian (bytes [kb, 10) zeroed), w = global ordinal.
+__device__ __forceinline__ void key_masks(uint32_t kb, uint64_t& mhi, uint32_t& m89) {
+  mhi = kb >= 8 ? ~0ull : ~(~0ull >> (8 * kb));
+  m89 = kb >= 10 ? 0xFFFFu : (kb == 9 ? 0xFF00u : 0u);
+}
+
+// tuples of a sorted run: t[j] = (key of run record perm[j], base + perm[j])
+__global__ void ext_make_tuples(const uint8_t* __restrict__ recs, const uint32_t* __restrict__ perm, uint64_t len,
+                                uint32_t base, uint32_t kb, uint4* __restrict__ t) {
+  uint64_t mhi;
+  uint32_t m89;
+  key_masks(kb, mhi, m89);
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[j];
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(recs + (uint64_t)p * kRecordBytes);
+    const uint32_t a = w[0], b = w[1], c = w[2];
+    const uint64_t hi = (((uint64_t)bswap32(a) << 32) | bswap32(b)) & mhi;
+    t[j] = make_uint4((uint32_t)hi, (uint32_t)(hi >> 32), ((((c & 0xFFu) << 8) | ((c >> 8) & 0xFFu)) & m89), base + p);
+  }
+}
+
+// samples[base + s] = a 100-byte pseudo-record carrying the key of tuple s * S (the sample sort orders by
+// key, then sample index = (run, pos) order)
+__global__ void ext_take_tuple_samples(const uint4* __restrict__ t, uint64_t run_len, uint32_t S,
+                                       uint8_t* __restrict__ samples, uint64_t base) {
+  const uint64_t nsamp = (run_len + S - 1) / S;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsamp; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = t[s * S];
+    uint32_t* r = reinterpret_cast<uint32_t*>(samples + (base + s) * kRecordBytes);
+    r[0] = bswap32(v.y);
+    r[1] = bswap32(v.x);
+    r[2] = ((v.z >> 8) & 0xFFu) | ((v.z & 0xFFu) << 8);
+  }
+}
+
+// ext_locate over tuple runs (16-byte stride in the zero-copy scratch)
+__global__ void ext_locate_tuples(const uint4* __restrict__ scratch_dev, const uint64_t* __restrict__ run_off,
+                                  const uint64_t* __restrict__ run_len, uint32_t R, const Splitter* __restrict__ spl,
+                                  uint32_t nspl, uint32_t kb, uint64_t* __restrict__ split) {
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (uint64_t)nspl * R) return;
+  const uint32_t p = (uint32_t)(id / R), r = (uint32_t)(id % R);
+  const Splitter sp = spl[p];
+  const uint4* base = scratch_dev + run_off[r];
+  uint64_t lo = 0, hi = run_len[r];
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    const uint4 v = base[mid];
+    uint8_t k[10];
+    const uint64_t h = ((uint64_t)v.y << 32) | v.x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) k[i] = (uint8_t)(h >> (56 - 8 * i));
+    k[8] = (uint8_t)(v.z >> 8);
+    k[9] = (uint8_t)v.z;
+    const int c = cmp_key(k, sp.key, kb);
+    const bool before = c < 0 || (c == 0 && (r < sp.run || (r == sp.run && mid < sp.pos)));
+    if (before) lo = mid + 1; else hi = mid;
+  }
+  split[id] = lo;
+}
+
+// merge composites of a concatenated tuple slice: (key bytes 0..7, bytes 8..9 << 48 | position)
+__global__ void ext_make_comp_tuples(const uint4* __restrict__ t, uint64_t m, uint64_t* __restrict__ hi,
+                                     uint64_t* __restrict__ lo) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = t[i];
+    hi[i] = ((uint64_t)v.y << 32) | v.x;
+    lo[i] = (uint64_t)v.z << 48 | i;
+  }
+}
+
+// out[j] = in[ordinal of the merged tuple j], read from the caller's pinned input through its device
+// mapping (zero-copy over the host link). Random 100-byte reads over PCIe need few, large requests: one TMA
+// bulk copy of the record's 16-byte-aligned 112-byte window per record (16-byte pieces were 2-3x slower),
+// two groups of 32 records in flight per warp (mbarrier completion); a window that would pass the input's
+// end (the last record or two) is read with exact 4-byte loads instead.
+__device__ __forceinline__ void xg_mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}"
+               ::"r"(a), "r"(parity) : "memory");
+}
+__global__ void __launch_bounds__(128) ext_gather_host(const uint8_t* __restrict__ in, uint64_t in_bytes,
+                                                       const uint4* __restrict__ t, const uint64_t* __restrict__ lo,
+                                                       uint64_t m, uint8_t* __restrict__ out, uint32_t* __restrict__ pout) {
+  constexpr int kWin = 112, kSlot = 128;
+  __shared__ __align__(128) uint8_t stage[4][2][32 * kSlot];  // 4 warps per CTA
+  __shared__ uint32_t s_p[4][2][32];
+  __shared__ __align__(8) uint64_t s_mb[4][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&s_mb[w][0]);
+  if (lane < 2) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8 * lane) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const uint64_t ngroups = (m + 31) / 32, nw = (uint64_t)gridDim.x * 4;
+  auto issue = [&](uint64_t g, int st) {
+    const uint64_t j0 = g * 32;
+    const uint32_t cnt = (uint32_t)min((uint64_t)32, m - j0);
+    const uint32_t p = lane < (int)cnt ? t[lo[j0 + lane] & 0xFFFFFFFFFFFFull].w : 0u;
+    s_p[w][st][lane] = p;
+    if (pout && lane < (int)cnt) pout[j0 + lane] = p;
+    const uint64_t a = ((uint64_t)p * kRecordBytes) & ~uint64_t(15);
+    const bool bulk = lane < (int)cnt && a + kWin <= in_bytes;
+    const uint32_t nbulk = __popc(__ballot_sync(0xffffffffu, bulk));
+    const uint32_t mb = mb0 + 8 * st;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(nbulk * kWin) : "memory");
+    __syncwarp();
+    uint8_t* slot = stage[w][st] + lane * kSlot;
+    if (bulk) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"((uint32_t)__cvta_generic_to_shared(slot)), "l"(in + a), "r"(kWin), "r"(mb) : "memory");
+    } else if (lane < (int)cnt) {  // the input's last record(s): exact loads
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(in + (uint64_t)p * kRecordBytes);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(slot + ((p * 4u) & 15u));
+      for (int o = 0; o < (int)kRecordWords; ++o) dst[o] = src[o];
+    }
+  };
+  const uint64_t g_first = (uint64_t)blockIdx.x * 4 + w;
+  if (g_first < ngroups) issue(g_first, 0);
+  uint32_t phases = 0;
+  int st = 0;
+  for (uint64_t g = g_first; g < ngroups; g += nw) {
+    if (g + nw < ngroups) issue(g + nw, st ^ 1);
+    xg_mbar_wait(mb0 + 8 * st, (phases >> st) & 1u);
+    phases ^= 1u << st;
+    __syncwarp();
+    const uint64_t j0 = g * 32;
+    const uint32_t cnt = (uint32_t)min((uint64_t)32, m - j0);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + j0 * kRecordBytes);
+    for (uint32_t x = lane; x < cnt * kRecordWords; x += 32) {
+      const uint32_t r = x / kRecordWords, o = x - r * kRecordWords;
+      dst[x] = *reinterpret_cast<const uint32_t*>(stage[w][st] + r * kSlot + ((s_p[w][st][r] * 4u) & 15u) + 4 * o);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    st ^= 1;
+  }
+}
+
 // LEY_TRACE_EXT=1: events around every copy / sort of the external path; per-category busy time and
 // span printed to stderr at the end (diagnostics only; never on by default).
 struct ExtTrace {
@@ -248,6 +391,9 @@ struct RunSet {
   uint8_t* h_runs = nullptr;
   uint8_t* h_runs_dev = nullptr;
   uint32_t* h_perm = nullptr;  // global ordinals of the run records (perm requested)
+  bool kp = false;             // key-pointer form: runs of 16-byte tuples (option ext_keyptr)
+  const uint8_t* in_dev = nullptr;  // kp: the caller's pinned input through its device mapping
+  uint64_t in_bytes = 0;
   std::vector<uint64_t> off, len, S, samp_base;
   uint64_t nsamp = 0;
 };
@@ -338,6 +484,27 @@ ley_status ext_generate(DeviceContext& ctx, const uint8_t* in, uint64_t n, uint6
     LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_in[sl], 0));
     if (r >= 2) LEY_CUDA("ext runs", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_out[sl] copied out
     const size_t t_s = tr.begin("run sort", s);
+    if (rs.kp) {  // key-pointer form: perm-only sort (no gather), then the run's sorted (key, ordinal) tuples
+      st = sort_internal_device(ctx, b.d_in[sl], nullptr, b.d_run_perm[sl], len, s, quiet, b.d_work, b.work_bytes,
+                                key_bytes);
+      if (st) return st;
+      ext_make_tuples<<<grid_for(len, sms), 256, 0, s>>>(b.d_in[sl], b.d_run_perm[sl], len, (uint32_t)rs.off[k],
+                                                         key_bytes, reinterpret_cast<uint4*>(b.d_out[sl]));
+      LEY_CUDA("ext tuples", cudaGetLastError());
+      ext_take_tuple_samples<<<grid_for((len + S - 1) / S, sms), 256, 0, s>>>(
+          reinterpret_cast<const uint4*>(b.d_out[sl]), len, (uint32_t)S, b.d_samp, rs.samp_base[k]);
+      LEY_CUDA("ext samples", cudaGetLastError());
+      prof.launches += quiet.launches + 2;
+      quiet.launches = 0;
+      tr.end(t_s, s);
+      LEY_CUDA("ext runs", cudaEventRecord(ev_sorted[sl], s));
+      LEY_CUDA("ext runs", cudaStreamWaitEvent(d2h, ev_sorted[sl], 0));
+      const size_t t_d = tr.begin("run D2H", d2h);
+      LEY_CUDA("ext D2H", cudaMemcpyAsync(rs.h_runs + rs.off[k] * 16, b.d_out[sl], len * 16, cudaMemcpyDeviceToHost, d2h));
+      tr.end(t_d, d2h);
+      LEY_CUDA("ext runs", cudaEventRecord(ev_out[sl], d2h));
+      continue;
+    }
     st = sort_internal_device(ctx, b.d_in[sl], b.d_out[sl], want_perm ? b.d_run_perm[sl] : nullptr, len, s, quiet,
                               b.d_work, b.work_bytes, key_bytes);
     if (st) return st;
@@ -411,8 +578,13 @@ ley_status ext_partition(DeviceContext& ctx, const RunSet& rs, const Phase1& b, 
     LEY_CUDA("ext locate", cudaMemcpyAsync(d_runoff, rs.off.data(), 8 * R, cudaMemcpyHostToDevice, s));
     LEY_CUDA("ext locate", cudaMemcpyAsync(d_runlen, rs.len.data(), 8 * R, cudaMemcpyHostToDevice, s));
     const uint64_t nthreads = (uint64_t)(P - 1) * R;
-    ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(rs.h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
-                                                                  key_bytes, d_split);
+    if (rs.kp)
+      ext_locate_tuples<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(reinterpret_cast<const uint4*>(rs.h_runs_dev),
+                                                                           d_runoff, d_runlen, R, d_spl, P - 1, key_bytes,
+                                                                           d_split);
+    else
+      ext_locate<<<(unsigned)((nthreads + 127) / 128), 128, 0, s>>>(rs.h_runs_dev, d_runoff, d_runlen, R, d_spl, P - 1,
+                                                                    key_bytes, d_split);
     LEY_CUDA("ext locate", cudaGetLastError());
     prof.launches += 1;
     LEY_CUDA("ext locate", cudaMemcpyAsync(split.data() + R, d_split, 8 * nthreads, cudaMemcpyDeviceToHost, s));
@@ -450,7 +622,9 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
     m_max = std::max(m_max, part_off[p + 1] - part_off[p]);
     if (part_off[p + 1] > part_off[p]) parts.push_back(p);
   }
-  const size_t sz_slice = a256(m_max * kRecordBytes);
+  const size_t elem = rs.kp ? 16 : kRecordBytes;  // a run element: a tuple or a record
+  const size_t sz_slice = a256(m_max * elem);
+  const size_t sz_mout = a256(m_max * kRecordBytes);
   const size_t sz_comp = a256(m_max * 8);
   const size_t sz_p = perm_out ? a256(m_max * 4) : 0;
   // merge-tree boundaries of every level of every partition, computed once on the host and copied to the
@@ -480,14 +654,14 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
       cur.swap(nxt);
     }
   }
-  const size_t phase2 = 4 * sz_slice + 4 * sz_comp + 4 * sz_p + a256(8 * hb.size());
+  const size_t phase2 = 2 * sz_slice + 2 * sz_mout + 4 * sz_comp + 4 * sz_p + a256(8 * hb.size());
   if (phase2 > ctx.ext.cap) {
     if ((st = ensure_buffer(ctx.ext, phase2, "external merge buffers", s))) return st;
   }
   uint8_t* eb = static_cast<uint8_t*>(ctx.ext.ptr);
   uint8_t* d_slice[2] = {eb, eb + sz_slice};
-  uint8_t* d_mout[2] = {eb + 2 * sz_slice, eb + 3 * sz_slice};
-  uint8_t* cb = eb + 4 * sz_slice;
+  uint8_t* d_mout[2] = {eb + 2 * sz_slice, eb + 2 * sz_slice + sz_mout};
+  uint8_t* cb = eb + 2 * sz_slice + 2 * sz_mout;
   uint64_t* c_h[2] = {reinterpret_cast<uint64_t*>(cb), reinterpret_cast<uint64_t*>(cb + 2 * sz_comp)};
   uint64_t* c_l[2] = {reinterpret_cast<uint64_t*>(cb + sz_comp), reinterpret_cast<uint64_t*>(cb + 3 * sz_comp)};
   uint8_t* pb = cb + 4 * sz_comp;
@@ -513,10 +687,9 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
       const uint64_t lo = split[(size_t)p * R + r], hi = split[(size_t)(p + 1) * R + r];
       const uint64_t at = off0[r];
       if (hi > lo) {
-        LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice[sl] + at * kRecordBytes,
-                                                  rs.h_runs + (rs.off[r] + lo) * kRecordBytes, (hi - lo) * kRecordBytes,
-                                                  cudaMemcpyHostToDevice, h2d));
-        if (perm_out)
+        LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_slice[sl] + at * elem, rs.h_runs + (rs.off[r] + lo) * elem,
+                                                  (hi - lo) * elem, cudaMemcpyHostToDevice, h2d));
+        if (perm_out && !rs.kp)
           LEY_CUDA("ext merge H2D", cudaMemcpyAsync(d_pslice[sl] + at, rs.h_perm + rs.off[r] + lo, (hi - lo) * 4,
                                                     cudaMemcpyHostToDevice, h2d));
       }
@@ -538,7 +711,10 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
     LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_in[sl], 0));
     if (i >= 2) LEY_CUDA("ext merge", cudaStreamWaitEvent(s, ev_out[sl], 0));  // d_mout[sl] copied out
     const size_t t_mm = tr.begin("merge K-m", s);
-    ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice[sl], m, key_bytes, c_h[0], c_l[0]);
+    if (rs.kp)
+      ext_make_comp_tuples<<<grid_for(m, sms), 256, 0, s>>>(reinterpret_cast<const uint4*>(d_slice[sl]), m, c_h[0], c_l[0]);
+    else
+      ext_make_comp<<<grid_for(m, sms), 256, 0, s>>>(d_slice[sl], m, key_bytes, c_h[0], c_l[0]);
     LEY_CUDA("K-m merge", cudaGetLastError());
     prof.launches += 1;
     // merge tree over the R run slices: one launch per level, boundaries already on the device
@@ -551,9 +727,14 @@ ley_status ext_merge(DeviceContext& ctx, const RunSet& rs, const std::vector<uin
       prof.launches += 1;
       src ^= 1;
     }
-    ext_gather<<<grid_for(m * kRecordWords, sms), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(d_slice[sl]), c_l[src],
-                                                               m, reinterpret_cast<uint32_t*>(d_mout[sl]), d_pslice[sl],
-                                                               d_pout[sl]);
+    if (rs.kp)  // the records come from the caller's pinned input, by the merged tuples' ordinals
+      ext_gather_host<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m + 127) / 128, (uint64_t)sms * 6)), 128, 0,
+                        s>>>(rs.in_dev, rs.in_bytes, reinterpret_cast<const uint4*>(d_slice[sl]), c_l[src], m, d_mout[sl],
+                             d_pout[sl]);
+    else
+      ext_gather<<<grid_for(m * kRecordWords, sms), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(d_slice[sl]), c_l[src],
+                                                                 m, reinterpret_cast<uint32_t*>(d_mout[sl]), d_pslice[sl],
+                                                                 d_pout[sl]);
     LEY_CUDA("K-e gather", cudaGetLastError());
     prof.launches += 1;
     LEY_CUDA("ext merge", cudaEventRecord(ev_sorted[sl], s));
@@ -617,10 +798,22 @@ ley_status sort_external_host(DeviceContext& ctx, const uint8_t* in, uint8_t* ou
   if ((st = ensure_buffer(ctx.ext, phase1_bytes(C, nsamp_cap), "external buffers", s))) return st;
   const Phase1 b = phase1_layout(static_cast<uint8_t*>(ctx.ext.ptr), C, nsamp_cap);
   // pinned host run scratch (records, and global ordinals when perm is requested)
-  if ((st = ensure_host_scratch(ctx, (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0)))) return st;
   RunSet rs;
+  rs.kp = options_snapshot().ext_keyptr != 0;
+  if (rs.kp) {  // key-pointer form: the records are gathered from the input itself, through its device mapping
+    if (cudaHostGetDevicePointer((void**)&rs.in_dev, const_cast<uint8_t*>(in), 0) != cudaSuccess || !rs.in_dev) {
+      cudaGetLastError();
+      set_error("external (ext_keyptr): the input is not mapped pinned memory (cudaHostGetDevicePointer failed)");
+      return LEY_ERR_UNSUPPORTED;
+    }
+    rs.in_bytes = n * kRecordBytes;
+  }
+  // pinned host run scratch: records (+ global ordinals when perm is requested), or 16-byte tuples
+  if ((st = ensure_host_scratch(ctx, rs.kp ? (size_t)n * 16
+                                           : (size_t)n * kRecordBytes + (perm_out ? (size_t)n * 4 : 0))))
+    return st;
   rs.h_runs = static_cast<uint8_t*>(ctx.host_scratch);
-  rs.h_perm = perm_out ? reinterpret_cast<uint32_t*>(rs.h_runs + (size_t)n * kRecordBytes) : nullptr;
+  rs.h_perm = perm_out && !rs.kp ? reinterpret_cast<uint32_t*>(rs.h_runs + (size_t)n * kRecordBytes) : nullptr;
   LEY_CUDA("external scratch", cudaHostGetDevicePointer((void**)&rs.h_runs_dev, rs.h_runs, 0));
   if ((st = ensure_copy_streams(ctx))) return st;
   ExtTrace tr;

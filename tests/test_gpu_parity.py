@@ -520,6 +520,38 @@ def test_external_matches_oracle(dist, n, budget):
     assert_parity(recs, out.numpy(), perm.numpy().view(np.uint32))
 
 
+@pytest.mark.parametrize("dist,n,budget", [
+    ("uniform", 1_000_003, 24 << 20),
+    ("skewed", 600_001, 12 << 20),
+    ("all_equal", 300_000, 8 << 20),
+    ("three_keys", 250_003, 8 << 20),
+])
+def test_external_keyptr_matches_oracle(dist, n, budget):
+    """SURVEY §8f NEXT 3, the paper's key-pointer pattern on the external path (option
+    ext_keyptr): runs of 16-byte (key, ordinal) tuples instead of records, the merge gathering every output
+    record from the pinned input by its ordinal. Same bytes and permutation as the oracle (ties across runs
+    and partitions included), the device high-water mark within the budget, and equal to the record form."""
+    import paper_1909_08006_b200 as ley
+
+    recs = gen.records(n, seed=45, dist=dist)
+    x, out = _pinned(recs)
+    perm = torch.empty(n, dtype=torch.int32).pin_memory()
+    with Options(ext_keyptr=1):
+        ley.ley_release_cache(-1)
+        ley.ley_device_bytes(reset_peak=True)
+        ley.ley_sort_perm(x, out, perm, n, device_budget_bytes=budget)
+        _, peak = ley.ley_device_bytes()
+    assert peak <= budget, f"library held {peak} bytes under a {budget}-byte budget"
+    assert_parity(recs, out.numpy(), perm.numpy().view(np.uint32))
+    out2 = torch.empty_like(x).pin_memory()
+    ley.ley_sort(x, out2, n, device_budget_bytes=budget)
+    assert np.array_equal(out2.numpy(), out.numpy())
+    with Options(ext_keyptr=1):  # short keys on the key-pointer form too (P:164)
+        ley.ley_sort(x, out2, n, key_bytes=3, device_budget_bytes=budget)
+    exp3, _ = oracle.sort(recs, key_bytes=3)
+    assert np.array_equal(out2.numpy(), exp3)
+
+
 def test_external_equals_internal_and_single_run():
     import paper_1909_08006_b200 as ley
 

@@ -6,7 +6,9 @@ sorted digest of `in` (oracle/oracle.cpp oracle_sorted_digest: the tuple sort of
 Host memory: in 60 GB + out 60 GB + the library's run scratch 60 GB (pinned) = 180 GB of the box's 196 GB;
 the scratch is released (ley_release_cache) before the oracle's 12 GB of tuples are built.
 
-usage: python tools/c5_full.py [n] [steps]      -> one JSON line (profiles/r02_c5_full.json)
+usage: python tools/c5_full.py [n] [steps] [--keyptr]   -> one JSON line (profiles/r02_c5_full*.json)
+--keyptr: the key-pointer form of the external path (option ext_keyptr): runs of 16-byte
+tuples (9.6 GB of host scratch instead of 60 GB), records gathered from the pinned input by ordinal.
 """
 import json
 import os
@@ -21,8 +23,10 @@ import gen
 import oracle
 import paper_1909_08006_b200 as ley
 
-n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 600_000_000
-steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+keyptr = "--keyptr" in sys.argv
+n = int(float(args[0])) if len(args) > 0 else 600_000_000
+steps = int(args[1]) if len(args) > 1 else 2
 budget = 4 << 30
 seed = 4
 
@@ -41,7 +45,7 @@ def pinned(nbytes):
     """Page-locked host buffer of exactly nbytes (numpy + cudaHostRegister; torch's pinned allocator would
     round 60 GB up to a power of two)."""
     a = np.empty(nbytes, dtype=np.uint8)
-    rc = torch.cuda.cudart().cudaHostRegister(a.ctypes.data, nbytes, 0)
+    rc = torch.cuda.cudart().cudaHostRegister(a.ctypes.data, nbytes, 2)  # cudaHostRegisterMapped
     assert int(rc) == 0, f"cudaHostRegister failed: {rc}"
     return a, torch.from_numpy(a)
 
@@ -57,6 +61,9 @@ for at in range(0, n, 50_000_000):
 del stage
 torch.cuda.empty_cache()
 res["setup_s"] = round(time.time() - t0, 1)
+if keyptr:
+    ley.ley_set_option("ext_keyptr", 1)
+    res["config"] += " (key-pointer external form)"
 ley.ley_sort(x, out, n, device_budget_bytes=budget, stream=s)  # warm: run scratch, streams
 res["free_gb_after_warm"] = free_gb()
 ley.ley_set_option("profile", 1)
