@@ -218,7 +218,7 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
       st = sort_internal_device(ctx, din, dout, perm, n_records, s, prof, nullptr, 0, key_bytes);
       if (st) return st;
       if ((st = prof.begin("D2H"))) return st;
-      LEY_CUDA("D2H", cudaMemcpyAsync(out8, dout, bytes, cudaMemcpyDeviceToHost, s));
+      if ((st = copy_split(ctx, out8, dout, bytes, cudaMemcpyDeviceToHost, s, DeviceContext::kSplitParts))) return st;
       if ((st = prof.end())) return st;
     } else if (info.host_path == 2) {
       st = sort_resident_host(ctx, in8, out8, perm, n_records, key_bytes, s, prof);

@@ -201,6 +201,31 @@ ley_status ensure_copy_streams(DeviceContext& ctx) {
   return LEY_OK;
 }
 
+ley_status copy_split(DeviceContext& ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                      cudaStream_t s, int parts) {
+  parts = std::max(1, std::min(parts, DeviceContext::kSplitParts));
+  if (parts == 1 || bytes < ((size_t)256 << 20)) {
+    LEY_CUDA("copy", cudaMemcpyAsync(dst, src, bytes, kind, s));
+    return LEY_OK;
+  }
+  if (!ctx.split_stream[0]) {
+    for (auto& st : ctx.split_stream) LEY_CUDA("copy streams", cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : ctx.split_ev) LEY_CUDA("copy streams", cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  LEY_CUDA("copy", cudaEventRecord(ctx.split_ev[0], s));
+  const size_t piece = ((bytes / parts) + 255) & ~size_t(255);
+  for (int i = 0; i < parts; ++i) {
+    const size_t a = std::min(bytes, (size_t)i * piece), b = i == parts - 1 ? bytes : std::min(bytes, a + piece);
+    LEY_CUDA("copy", cudaStreamWaitEvent(ctx.split_stream[i], ctx.split_ev[0], 0));
+    if (b > a)
+      LEY_CUDA("copy", cudaMemcpyAsync(static_cast<uint8_t*>(dst) + a, static_cast<const uint8_t*>(src) + a, b - a, kind,
+                                       ctx.split_stream[i]));
+    LEY_CUDA("copy", cudaEventRecord(ctx.split_ev[i + 1], ctx.split_stream[i]));
+    LEY_CUDA("copy", cudaStreamWaitEvent(s, ctx.split_ev[i + 1], 0));
+  }
+  return LEY_OK;
+}
+
 uint64_t resident_chunk_records(uint64_t n) {
   const int64_t o = options_snapshot().resident_chunk_records;
   const uint64_t c = o > 0 ? (uint64_t)o : (uint64_t)1 << 21;  // 210 MB windows: full-speed D2H copies

@@ -134,6 +134,10 @@ struct DeviceContext {
   uint64_t graph_clock = 0;
   cudaStream_t graph_stream = nullptr;
   cudaEvent_t graph_ev[2] = {nullptr, nullptr};
+  // one large host-link copy split into pieces on their own streams (copy_split)
+  static constexpr int kSplitParts = 4;
+  cudaStream_t split_stream[kSplitParts] = {};
+  cudaEvent_t split_ev[kSplitParts + 1] = {};
   // streaming host sort (ley_sort_submit): two device staging slots (in | out), three streams and a
   // worker thread, so the H2D of call k+1, the sort of call k and the D2H of call k-1 all overlap
   struct Pipe {
@@ -229,6 +233,10 @@ uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm);
 ley_status sort_resident_host(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                               uint32_t key_bytes, cudaStream_t s, Profiler& prof);
 ley_status ensure_copy_streams(DeviceContext& ctx);  // ctx.copy_stream[2] + ctx.ev (external / resident)
+// cudaMemcpyAsync of `bytes` as `parts` pieces on the context's split streams, ordered after s and joined
+// back into s (a single D2H copy engine stream reaches ~52 GB/s on this link, four ~55: profiles/r02_*)
+ley_status copy_split(DeviceContext& ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                      cudaStream_t s, int parts);
 ley_status ensure_host_scratch(DeviceContext& ctx, size_t bytes);  // ctx.host_scratch (external.cu)
 
 // Multi-GPU external sort (external.cu): the plan every rank derives alike from the ranks'
