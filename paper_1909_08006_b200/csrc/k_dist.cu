@@ -60,6 +60,14 @@ __device__ __forceinline__ uint32_t dest_of(uint32_t hi, uint32_t mid, uint32_t 
 // ------------------------------------------------------------------------------------------ K-s0
 // Also keeps every record's 16-bit prefix (2 B/record, coalesced) so that K-s1 finds the boundary-bin
 // records from the prefixes instead of reading every record's key line again (~100 B/record).
+// (the 4 key bytes of a record sit in one 64-byte block: .L2::64B fetches that block instead of the whole
+// 128-byte line a plain miss brings, 64 instead of 100 DRAM bytes per record; profiles/r02_fetch_granularity.txt)
+__device__ __forceinline__ uint32_t ld_key_word(const uint8_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __global__ void __launch_bounds__(256) ks_hist16(const uint8_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ hist,
                                                  uint16_t* __restrict__ pref, uint32_t mask_hi) {
   const uint32_t lt = lanemask_lt();
@@ -67,7 +75,7 @@ __global__ void __launch_bounds__(256) ks_hist16(const uint8_t* __restrict__ in,
     const uint64_t i = base + threadIdx.x;
     const bool valid = i < n;
     uint32_t hi = 0;
-    if (valid) hi = bswap32(__ldg(reinterpret_cast<const uint32_t*>(in + i * kRecordBytes))) & mask_hi;
+    if (valid) hi = bswap32(ld_key_word(in + i * kRecordBytes)) & mask_hi;
     const uint32_t p16 = hi >> 16;
     if (valid) pref[i] = (uint16_t)p16;
     const uint32_t peers = warp_peers8(p16 & 0xFFu, valid) & warp_peers8(p16 >> 8, valid);
