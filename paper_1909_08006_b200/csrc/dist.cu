@@ -478,11 +478,15 @@ ley_status comm_sync(ley_comm* c, cudaStream_t s, const char* stage) {
     ncclResult_t a = ncclSuccess;
     if (ncclCommGetAsyncError(c->nccl, &a) == ncclSuccess && a != ncclSuccess && a != ncclInProgress)
       return comm_fail(c, s, stage, std::string("NCCL asynchronous error: ") + ncclGetErrorString(a));
-    if (spin >= 64 && elapsed_ms(t0) > to)
+    const int64_t ms = elapsed_ms(t0);
+    if (ms > to)
       return comm_fail(c, s, stage, "collective not complete after " + std::to_string(to) +
                                         " ms (a peer failed before it or died)");
-    if (spin < 64) std::this_thread::yield();
+    // poll tightly for the first millisecond (the usual wait: a sync must not add sleep latency to every
+    // phase of a 2-ms sort), then back off
+    if (ms < 1) std::this_thread::yield();
     else std::this_thread::sleep_for(std::chrono::microseconds(20));
+    (void)spin;
   }
 }
 
