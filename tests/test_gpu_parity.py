@@ -11,7 +11,7 @@ import torch
 
 import gen
 import oracle
-from gpu_util import Options, assert_parity, device_records, gpu_sort
+from gpu_util import Options, assert_parity, device_records, gpu_sort, to_device
 
 pytestmark = pytest.mark.gpu
 
