@@ -57,39 +57,52 @@ __device__ __forceinline__ uint64_t prefix_digest(const uint32_t* w) {
   return ((uint64_t)w[1] << 32 | w[0]) ^ ((uint64_t)(w[2] & 0xFFFFu) * 0x9E3779B97F4A7C15ull);
 }
 
+// One group of cnt <= 32 records in[perm[g0 + r]] by one warp: group_issue starts the 16-byte cp.async
+// copies of every record's window into `stage` (kStageBytes, 16-byte aligned); after cp_async_wait_all,
+// group_store re-aligns the group and writes it as a coalesced word stream to dst (and, with dg, the
+// records' prefix digests).
+__device__ __forceinline__ void group_issue(const uint32_t* perm, uint32_t g0, uint32_t cnt, const uint8_t* __restrict__ in,
+                                            uint64_t in_bytes, uint32_t stage_s, bool l2_64) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t p = lane < (int)cnt ? perm[g0 + lane] : 0u;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const int cidx = q * 32 + lane;
+    const int r = cidx / 7, c = cidx - r * 7;
+    const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
+    const uint64_t a = (((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16;
+    if (r < (int)cnt && a < in_bytes)  // (chunks past the input's end hold no record byte)
+      cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u, l2_64);
+  }
+}
+__device__ __forceinline__ void group_store(const uint32_t* perm, uint32_t g0, uint32_t cnt, const uint8_t* stage,
+                                            uint32_t* __restrict__ dst, uint64_t* __restrict__ dg) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t words = cnt * kRecordWords;
+  for (uint32_t w = lane; w < words; w += 32) {
+    const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
+    const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
+    stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
+  }
+  if (dg && lane < (int)cnt)
+    dg[lane] = prefix_digest(reinterpret_cast<const uint32_t*>(stage + lane * kWindow + ((perm[g0 + lane] * 4u) & 15u)));
+}
+
 // Records in[perm[i]] -> out_base[i] for i in [0, s) by one warp, groups g0 = first, first + stride, ...
-// of 32 records, through `stage` (kStageBytes, 16-byte aligned). perm lives in shared memory. With
-// dg_base, also dg_base[i] = prefix_digest(record).
+// of 32 records, through `stage`. perm lives in shared memory. With dg_base, also dg_base[i] =
+// prefix_digest(record).
 __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
                                             const uint8_t* __restrict__ in, uint64_t in_bytes,
                                             uint8_t* __restrict__ out_base, uint8_t* stage,
                                             uint64_t* __restrict__ dg_base, bool l2_64 = true) {
-  const int lane = threadIdx.x & 31;
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
   for (uint32_t g0 = first; g0 < s; g0 += stride) {
     const uint32_t cnt = min((uint32_t)kGroup, s - g0);
-    const uint32_t p = lane < (int)cnt ? perm[g0 + lane] : 0u;
-#pragma unroll
-    for (int q = 0; q < 7; ++q) {
-      const int cidx = q * 32 + lane;
-      const int r = cidx / 7, c = cidx - r * 7;
-      const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
-      const uint64_t a = (((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16;
-      if (r < (int)cnt && a < in_bytes)  // (chunks past the input's end hold no record byte)
-        cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u, l2_64);
-    }
+    group_issue(perm, g0, cnt, in, in_bytes, stage_s, l2_64);
     cp_async_wait_all();
     __syncwarp();
-    uint32_t* dst = reinterpret_cast<uint32_t*>(out_base + (uint64_t)g0 * kRecordBytes);
-    const uint32_t words = cnt * kRecordWords;
-    for (uint32_t w = lane; w < words; w += 32) {
-      const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
-      const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
-      stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
-    }
-    if (dg_base && lane < (int)cnt)
-      dg_base[g0 + lane] =
-          prefix_digest(reinterpret_cast<const uint32_t*>(stage + lane * kWindow + ((p * 4u) & 15u)));
+    group_store(perm, g0, cnt, stage, reinterpret_cast<uint32_t*>(out_base + (uint64_t)g0 * kRecordBytes),
+                dg_base ? dg_base + g0 : nullptr);
     __syncwarp();
   }
 }
@@ -102,55 +115,6 @@ __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const ui
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers exactly 65536 buckets
   const Seg s{B16[p], hist16[p], 2u, 1u};
   classify_block(s, true, tu, kd, big_out, big_count, s_cnt);
-}
-
-// ---------------------------------------------------------------------------- warp tier (len <= 32)
-// (DG: write prefix digests too — a separate instantiation, so the plain form keeps its 46 registers)
-template <bool DG>
-__global__ void __launch_bounds__(256)
-    kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
-                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
-                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint64_t in_bytes,
-                 uint8_t* __restrict__ out, uint64_t* __restrict__ dg) {
-  __shared__ __align__(16) uint8_t s_stage[8][kStageBytes];
-  __shared__ uint32_t s_perm[8][32];
-  const uint32_t nitems = *count;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + wib; it < nitems; it += nwarps) {
-    const Seg sg = list[it];
-    const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
-    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
-    uint64_t t = ~0ull;
-    uint32_t x = ~0u;
-    if ((uint32_t)lane < sg.len) {
-      t = tp[lane];
-      x = ip[lane];
-    }
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        uint64_t ot = __shfl_xor_sync(0xffffffffu, t, j);
-        uint32_t ox = __shfl_xor_sync(0xffffffffu, x, j);
-        bool up = (lane & k) == 0;
-        bool lower = (lane & j) == 0;
-        bool take = (lower == up) ? pair_less(ot, ox, t, x) : pair_less(t, x, ot, ox);
-        if (take) {
-          t = ot;
-          x = ox;
-        }
-      }
-    }
-    if ((uint32_t)lane < sg.len) {
-      if (perm) perm[sg.start + lane] = x;
-      s_perm[wib][lane] = x;
-    }
-    __syncwarp();
-    if (out)  // (perm-only mode: the resident host path gathers later, chunk by chunk)
-      warp_gather(s_perm[wib], sg.len, 0, kGroup, in, in_bytes, out + (uint64_t)sg.start * kRecordBytes,
-                  s_stage[wib], DG ? dg + sg.start : nullptr);
-  }
 }
 
 // ---------------------------------------------------------------------------- CTA tier
@@ -530,6 +494,172 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 constexpr int kWsSlot = 128;                     // tensor-copy destinations 128-byte aligned
 constexpr int kWsStageBytes = kGroup * kWsSlot;  // 4096 B per gathering warp and stage
 
+// ---------------------------------------------------------------------------- warp tier (len <= 32)
+// One warp per bucket, software-pipelined: the next bucket's list entry and pairs are loaded and sorted in
+// registers while the current bucket's record copies are in flight. The kernel is issue-bound at small n
+// (C1: 56 M warp instructions for 1e6 records, ncu), so every step is cut to few instructions:
+//  * the network sorts one 64-bit composite (tail >> 5, lane) per lane — 7 instructions per exchange
+//    instead of ~25 for the (tail, ordinal) pair — then fetches each position's pair from its source lane.
+//    It equals the (tail, ordinal) order unless two tails agree in their top 59 bits; that case (detected
+//    on adjacent sorted tails) re-sorts the pairs with the full comparison;
+//  * each record is one bulk copy of its 16-byte-aligned 112-byte window (the last n mod 4 records, whose
+//    window may pass the input's end, by exact word loads), completion counted on the warp's mbarrier;
+//  * the bucket's output is written in 16-byte stores (4-byte head and tail words at its unaligned ends).
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  return (uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src) << 32 | __shfl_sync(0xffffffffu, (uint32_t)v, src);
+}
+
+__device__ __forceinline__ void warp_sort_pairs(uint64_t& t, uint32_t& x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      uint64_t ot = __shfl_xor_sync(0xffffffffu, t, j);
+      uint32_t ox = __shfl_xor_sync(0xffffffffu, x, j);
+      bool up = (lane & k) == 0;
+      bool lower = (lane & j) == 0;
+      bool take = (lower == up) ? pair_less(ot, ox, t, x) : pair_less(t, x, ot, ox);
+      if (take) {
+        t = ot;
+        x = ox;
+      }
+    }
+  }
+}
+
+// (t, x) of lane i < len -> lane i holds the i-th smallest pair; lanes >= len hold (~0, ~0) padding.
+// Bitonic network over the composites of lanes [0, KMAX) (KMAX = 16: the lower half-warp ends ascending).
+template <int KMAX>
+__device__ __forceinline__ uint64_t warp_sort_composite(uint64_t c) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= KMAX; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t oc = shfl_u64(c, lane ^ j);
+      const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+      c = ((oc < c) == keep_min) ? oc : c;  // (composites are distinct: their low 5 bits are the lanes)
+    }
+  }
+  return c;
+}
+
+__device__ __forceinline__ void warp_sort_bucket(uint32_t len, uint64_t& t, uint32_t& x) {
+  const int lane = threadIdx.x & 31;
+  uint64_t c = (t & ~uint64_t(31)) | (uint64_t)lane;
+  c = len <= 16 ? warp_sort_composite<16>(c) : warp_sort_composite<32>(c);  // (10 or 15 exchange steps)
+  const int src = (int)(c & 31u);
+  const uint64_t st = shfl_u64(t, src);
+  const uint32_t sx = __shfl_sync(0xffffffffu, x, src);
+  const uint64_t prev = shfl_u64(st >> 5, (lane + 31) & 31);
+  if (__any_sync(0xffffffffu, lane > 0 && (uint32_t)lane < len && prev == (st >> 5))) {
+    warp_sort_pairs(t, x);  // tails equal in their top 59 bits: the full (tail, ordinal) network
+    return;
+  }
+  t = st;
+  x = sx;
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+
+template <bool DG>
+__global__ void __launch_bounds__(256)
+    kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
+                 const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
+                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                 uint64_t* __restrict__ dg) {
+  __shared__ __align__(128) uint8_t s_stage[8][kStageBytes];
+  const uint32_t nitems = *count;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(s_stage[wib]);
+  uint32_t it = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (it >= nitems) return;
+  uint64_t pol = 0;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto load = [&](const Seg& sg, uint64_t& t, uint32_t& x) {
+    const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
+    const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
+    t = ~0ull;
+    x = ~0u;
+    if ((uint32_t)lane < sg.len) {
+      t = tp[lane];
+      x = ip[lane];
+    }
+  };
+  Seg sg = list[it];
+  uint64_t t;
+  uint32_t x;
+  load(sg, t, x);
+  warp_sort_bucket(sg.len, t, x);
+  while (true) {
+    const uint32_t len = sg.len;
+    if (perm && (uint32_t)lane < len) perm[sg.start + lane] = x;
+    const uint64_t obyte = (uint64_t)sg.start * kRecordBytes;
+    const uint32_t a = (uint32_t)(obyte & 15u);  // stage byte a + i holds bucket output byte i (same phase mod 16)
+    const uint32_t words = len * kRecordWords;
+    if (out) {  // (perm-only mode: the resident host path gathers later, chunk by chunk)
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous store read the stage
+      __syncwarp();
+      // 8 lanes per record, 4 records per round: lane j of a record copies its words j, j+8, j+16 (and
+      // j = 0 word 24), so each copy instruction reads 32 contiguous bytes of each of its 4 records
+      const uint32_t j = lane & 7;
+      for (uint32_t r0 = 0; r0 < len; r0 += 4) {
+        const uint32_t r = r0 + (lane >> 3);
+        const uint32_t p = __shfl_sync(0xffffffffu, x, r & 31);
+        if (r < len) {
+          const uint8_t* src = in + (uint64_t)p * kRecordBytes + 4 * j;
+          const uint32_t dst = stage_s + a + r * kRecordBytes + 4 * j;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (j + 8 * i < (uint32_t)kRecordWords) cp_async4(dst + 32 * i, src + 32 * i);
+        }
+      }
+    }
+    const uint32_t nit = it + nwarps;
+    Seg ns{};
+    uint64_t nt = 0;
+    uint32_t nx = 0;
+    if (nit < nitems) {  // overlaps the copies in flight
+      ns = list[nit];
+      load(ns, nt, nx);
+      warp_sort_bucket(ns.len, nt, nx);
+    }
+    if (out) {
+      cp_async_wait_all();
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the copies, before the bulk store reads them
+      __syncwarp();
+      const uint32_t bytes = words * 4u;
+      const uint32_t i0 = (16u - a) & 15u;                                // first 16-byte-aligned output byte
+      const uint32_t mid = bytes > i0 ? (bytes - i0) & ~15u : 0u;         // aligned middle, one bulk store
+      const uint32_t i1 = i0 + mid;
+      uint32_t* o32 = reinterpret_cast<uint32_t*>(out + obyte);
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s_stage[wib] + a);
+      if (lane == 0 && mid) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(out + obyte + i0),
+                     "r"(stage_s + a + i0), "r"(mid), "l"(pol)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      const uint32_t hw = (i0 < bytes ? i0 : bytes) >> 2, tw = (bytes - (i0 < bytes ? i1 : bytes)) >> 2;
+      if ((uint32_t)lane < hw) stg_cs_u32(o32 + lane, s32[lane]);
+      else if ((uint32_t)lane >= 4 && (uint32_t)lane < 4 + tw) stg_cs_u32(o32 + (i1 >> 2) + lane - 4, s32[(i1 >> 2) + lane - 4]);
+      if (DG && (uint32_t)lane < len) dg[sg.start + lane] = prefix_digest(s32 + lane * kRecordWords);
+    }
+    __syncwarp();
+    if (nit >= nitems) break;
+    it = nit;
+    sg = ns;
+    t = nt;
+    x = nx;
+  }
+  if (out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------- warp-specialised tier
 // The fused kernel above alternates: all warps sort a bucket, then all warps gather it, so a CTA issues no
 // record reads while it sorts. Here a CTA splits into a sort group (ST threads) and a gather group (GW
@@ -884,7 +1014,7 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
     switch (t) {
       case kListWarp:
         kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1,
-                                                          perm, in, in_bytes, out, dg);
+                                                          perm, in, out, dg);
         return cudaGetLastError();
       // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
       // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)

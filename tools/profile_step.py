@@ -17,7 +17,11 @@ ap.add_argument("--dist", default="uniform")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--l2", type=int, default=0)
+ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (repeatable)")
 a = ap.parse_args()
+for kv in a.opt:
+    k, v = kv.split("=")
+    ley.ley_set_option(k, int(v))
 n = int(a.n)
 if a.l2:
     ley.ley_set_option("l2_fetch_bytes", a.l2)
