@@ -101,9 +101,9 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 
     // ---------------------------------------------------------------- zero counters / look-back state
     if ((st = prof.begin("init"))) return st;
-    LEY_CUDA("init", cudaMemsetAsync(hist16, 0, 4ull * 65536 * L.hist_copies, s));
-    LEY_CUDA("init", cudaMemsetAsync(small, 0, 4 * kSmallWords, s));
-    LEY_CUDA("init", cudaMemsetAsync(scan_status, 0, 8 * 2 * L.scan_status_words, s));
+    LEY_CUDA("init", launch_zero3(hist16, 4ull * 65536 * L.hist_copies, small, 4 * kSmallWords, scan_status,
+                                  8 * 2 * L.scan_status_words, sms, s));
+    ++launches;
     if ((st = prof.end())) return st;
 
     // ---------------------------------------------------------------- K-a
@@ -116,11 +116,10 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     // ---------------------------------------------------------------- K-b
     if ((st = prof.begin("K-b scan"))) return st;
     LEY_CUDA("K-b scan", launch_hist_reduce(hist16, L.hist_copies, s));
-    LEY_CUDA("K-b scan", launch_scan_excl(cnt, off, L.m, scan_status, tickets + 0, off + L.m, s));
-    LEY_CUDA("K-b scan", launch_scan_excl(hist16, B16, 65536, scan_status + L.scan_status_words, tickets + 1,
-                                          B16 + 65536, s));
+    LEY_CUDA("K-b scan", launch_scan_excl2(cnt, off, L.m, scan_status, off + L.m, hist16, B16, 65536,
+                                           scan_status + L.scan_status_words, B16 + 65536, tickets + 0, s));
     LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
-    launches += 4;
+    launches += 3;
     if ((st = prof.end())) return st;
 
     // ---------------------------------------------------------------- K-c (byte 1)

@@ -55,29 +55,68 @@ __device__ __forceinline__ uint64_t search_le_g(const uint32_t* a, uint64_t lo, 
   return lo;
 }
 
+// Largest t in [lo, hi) with a[t] <= v (a non-decreasing, a[lo] <= v), galloping out from the guess g: a
+// good guess (the tiles are equal-sized, so a byte-0 run's start grows about linearly in t) costs 2-4
+// dependent loads instead of log2(hi - lo).
+__device__ __forceinline__ uint64_t search_le_guess(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t v, uint64_t g) {
+  g = g < lo ? lo : (g >= hi ? hi - 1 : g);
+  uint64_t l, h;  // invariant target: a[l] <= v, (h == hi or a[h] > v)
+  if (a[g] <= v) {
+    l = g;
+    uint64_t step = 1;
+    h = l + step;
+    while (h < hi && a[h] <= v) {
+      l = h;
+      step <<= 1;
+      h = l + step;
+    }
+    if (h > hi) h = hi;
+  } else {
+    h = g;
+    uint64_t step = 1;
+    l = h > lo + step ? h - step : lo;
+    while (l > lo && a[l] > v) {
+      h = l;
+      step <<= 1;
+      l = h > lo + step ? h - step : lo;
+    }
+  }
+  return search_le_g(a, l, h, v);
+}
+
 // Per-chunk decomposition of level 1, one thread per chunk: segment b, virtual range [v0, v0+cnt), the
-// tile range [t0, t1] whose byte-0 runs cover it, and the segment's first chunk k0. Parallel binary
-// searches here keep them off the K-c critical path.
+// tile range [t0, t1] whose byte-0 runs cover it, and the segment's first chunk k0. Parallel searches
+// here keep them off the K-c critical path. The same launch also initialises the split's write cursors
+// (cursor = B16) with its spare threads.
 __global__ void kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles, const uint32_t* __restrict__ B16,
                                uint64_t n, const uint32_t* __restrict__ cstart, uint32_t grid_ub,
-                               uint4* __restrict__ plan_a, uint2* __restrict__ plan_b) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cstart[256] || k >= grid_ub) return;
-  uint32_t b = 0, hi = 256;
-  while (hi - b > 1) {
-    uint32_t mid = (b + hi) >> 1;
-    if (cstart[mid] <= k) b = mid; else hi = mid;
+                               uint4* __restrict__ plan_a, uint2* __restrict__ plan_b, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t s_cst[257];
+  for (uint32_t i = threadIdx.x; i < 257; i += blockDim.x) s_cst[i] = cstart[i];
+  const uint32_t nth = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 65536 / 4; i += nth)
+    reinterpret_cast<uint4*>(cursor)[i] = reinterpret_cast<const uint4*>(B16)[i];
+  __syncthreads();
+  const uint32_t kend = min(s_cst[256], grid_ub);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += nth) {
+    uint32_t b = 0, hi = 256;
+    while (hi - b > 1) {
+      uint32_t mid = (b + hi) >> 1;
+      if (s_cst[mid] <= k) b = mid; else hi = mid;
+    }
+    const uint32_t c = k - s_cst[b];
+    const uint32_t seg_beg = B16[b * 256];
+    const uint64_t seg_end = (b < 255) ? B16[(b + 1) * 256] : n;
+    const uint32_t v0 = seg_beg + c * kChunk;
+    const uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
+    const uint32_t* off_b = off + (uint64_t)b * tiles;
+    const uint64_t len = seg_end - seg_beg;
+    const uint32_t t0 = (uint32_t)search_le_guess(off_b, 0, tiles, v0, (uint64_t)(v0 - seg_beg) * tiles / len);
+    const uint32_t t1 =
+        (uint32_t)search_le_guess(off_b, t0, tiles, v0 + cnt - 1, (uint64_t)(v0 + cnt - 1 - seg_beg) * tiles / len);
+    plan_a[k] = make_uint4(b, v0, cnt, k - c);
+    plan_b[k] = make_uint2(t0, t1);
   }
-  const uint32_t c = k - cstart[b];
-  const uint32_t seg_beg = B16[b * 256];
-  const uint64_t seg_end = (b < 255) ? B16[(b + 1) * 256] : n;
-  const uint32_t v0 = seg_beg + c * kChunk;
-  const uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
-  const uint32_t* off_b = off + (uint64_t)b * tiles;
-  const uint32_t t0 = (uint32_t)search_le_g(off_b, 0, tiles, v0);
-  const uint32_t t1 = (uint32_t)search_le_g(off_b, t0, tiles, v0 + cnt - 1);
-  plan_a[k] = make_uint4(b, v0, cnt, k - c);
-  plan_b[k] = make_uint2(t0, t1);
 }
 
 // Processing order of the level-1 chunks: bucket-major, but the chunks of 4 neighbouring byte-0 buckets
@@ -482,7 +521,8 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
                                    bool run_split, const uint32_t** order_used) {
-  kc_plan_level1<<<(grid_ub + 255) / 256, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b);
+  const uint32_t pblocks = std::max<uint32_t>((grid_ub + 255) / 256, 16);  // (>= 16: the cursor copy)
+  kc_plan_level1<<<pblocks, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b, cursor);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // the interleaved order pays only once K-a's output is many times the L2 (C4: 30.6 -> ~18 B/pair of
@@ -493,8 +533,6 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
     kc_order_chunks<<<1, kRadix / kOrderGroup, 0, s>>>(cstart, order);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  e = cudaMemcpyAsync(cursor, B16, 4 * 65536, cudaMemcpyDeviceToDevice, s);
-  if (e != cudaSuccess) return e;
   if (order_used) *order_used = order;
   if (!run_split) return cudaSuccess;  // (the fused K-d+K-e kernel runs the chunks: kc_chunk.cuh)
   size_t smem = SplitSmem::kBytes;

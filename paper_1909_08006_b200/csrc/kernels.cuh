@@ -28,10 +28,16 @@ cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, u
                                 KeySpec key, cudaStream_t s);
 
 // K-b (k_scan.cu)
+// (two independent exclusive scans in one launch; one ticket word)
+cudaError_t launch_scan_excl2(const uint32_t* in_a, uint32_t* out_a, uint64_t m_a, uint64_t* status_a,
+                              uint32_t* total_a, const uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
+                              uint64_t* status_b, uint32_t* total_b, uint32_t* ticket, cudaStream_t s);
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
                              uint32_t* total_out, cudaStream_t s);
 uint64_t scan_status_words(uint64_t m);
 cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s);
+cudaError_t launch_zero3(void* a, uint64_t a_bytes, void* b, uint64_t b_bytes, void* c, uint64_t c_bytes, int sms,
+                         cudaStream_t s);
 cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, cudaStream_t s);
 cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
                                   cudaStream_t s);

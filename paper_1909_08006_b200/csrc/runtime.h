@@ -74,6 +74,7 @@ ley_status option_get(const char* name, int64_t* value);
 // small counters of one sort (zeroed per call): [0, 16) tickets, [16, 16 + kNumKdLists) K-d list counts,
 // [32] big-bucket count, [64, 320) done chunks per byte-0 bucket (fused split), [320] fused K-d ticket
 constexpr uint32_t kSmallWords = 64 + 256 + 16;
+static_assert(kSmallWords % 4 == 0, "zeroed in 16-byte words (launch_zero3)");
 struct InternalLayout {
   uint64_t n = 0, tiles = 0, m = 0;  // m = 256 * tiles
   uint64_t split_chunks_ub = 0;      // level-1 chunk upper bound
