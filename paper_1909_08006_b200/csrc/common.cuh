@@ -44,7 +44,31 @@ struct Tunables {
   int kd_ws = 1;  // warp-specialised sort/gather tiers (kd_ws_sort) instead of the alternating kd_cta_sort
   int ws_tma = 0;  // kd_ws_sort: record windows by TMA tensor copies (64-B L2 fetches) or plain bulk copies
   int gather_l2_64 = 1;  // kd_cta_sort gathers: cp.async with .L2::64B (1) or without the hint (0)
+  int pdl = 1;           // K-d/K-e tier kernels launched with programmatic dependent launch (launch_k);
+                         // per launch: 1 wait, then let the next tier launch; 2 let it launch at once and
+                         // wait only before exiting (independent tiers overlap); 0 plain stream order
 };
+
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization attribute
+// may become resident while its predecessor in the stream still runs; it lets its own successor launch
+// at once (pdl_trigger) and waits for the predecessor's completion and memory (pdl_wait) before touching
+// anything the predecessor wrote. Without the attribute both are no-ops. The launch latency and empty
+// grids of a chain of tier kernels then overlap the running one.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Kernel entry of a tier kernel under Tunables::pdl mode m; the returned guard waits at every exit in mode
+// 2, so a tier never completes before its predecessor (stream order of completions is kept).
+struct PdlExitWait {
+  bool on;
+  __device__ __forceinline__ ~PdlExitWait() {
+    if (on) pdl_wait();
+  }
+};
+__device__ __forceinline__ PdlExitWait pdl_enter(int m) {
+  if (m != 2) pdl_wait();
+  pdl_trigger();
+  return PdlExitWait{m == 2};
+}
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }

@@ -59,7 +59,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   uint32_t* small = reinterpret_cast<uint32_t*>(base + L.off_small);
   uint32_t* tickets = small;          // [0..15]
   uint32_t* kd_counts = small + 16;   // [kNumKdLists]
-  uint32_t* big_count = small + 32;   // [1]
+  uint32_t* big_count = small + 32;   // [1]; small[33]: classify's CTA-done counter
   volatile uint32_t* host_cnt = static_cast<volatile uint32_t*>(ctx.host_pinned);
   uint32_t* host_cnt_dev = nullptr;  // its device alias: counters are published by a kernel store
   LEY_CUDA("setup", cudaHostGetDevicePointer((void**)&host_cnt_dev, ctx.host_pinned, 0));
@@ -73,6 +73,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   tu.kd_ws = (int)o.kd_ws;
   tu.ws_tma = (int)o.ws_gather_tma;
   tu.gather_l2_64 = (int)o.gather_l2_64;
+  tu.pdl = (int)o.pdl;
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;
@@ -115,11 +116,11 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 
     // ---------------------------------------------------------------- K-b
     if ((st = prof.begin("K-b scan"))) return st;
-    LEY_CUDA("K-b scan", launch_hist_reduce(hist16, L.hist_copies, s));
+    // (the hist16 copies are summed by the scan itself, which writes the sum back over copy 0)
     LEY_CUDA("K-b scan", launch_scan_excl2(cnt, off, L.m, scan_status, off + L.m, hist16, B16, 65536,
-                                           scan_status + L.scan_status_words, B16 + 65536, tickets + 0, s));
-    LEY_CUDA("K-b scan", launch_kc_plan_chunks(B16, n, kChunk, cstart, s));
-    launches += 3;
+                                           scan_status + L.scan_status_words, B16 + 65536, L.hist_copies, 65536,
+                                           tickets + 0, s));
+    ++launches;
     if ((st = prof.end())) return st;
 
     // ---------------------------------------------------------------- K-c (byte 1)
@@ -152,7 +153,8 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
 
     // ---------------------------------------------------------------- classify level 1, K-d
     if ((st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
-    LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count, s));
+    LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count,
+                                                   small + 33, host_cnt_dev, s));
     ++launches;
     KcArgs kc;
     if (fused_tier >= 0) {
@@ -176,7 +178,6 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     }
     LEY_CUDA("K-de sort+gather", launch_kd_all(kd, At, Ai, Bt, Bi, perm_out ? perm : nullptr, tu, sms, in, n, out, digest, s,
                                                &launches, fused_tier >= 0 ? &kc : nullptr, fused_tier));
-    LEY_CUDA("K-de sort+gather", launch_publish_u32(big_count, host_cnt_dev, s));
     return LEY_OK;
   };
   // (not while profiling: elapsed times between event-record nodes of a graph are refused, measured)

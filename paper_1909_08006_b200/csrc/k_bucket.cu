@@ -109,12 +109,22 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
 
 constexpr int kGatherStages = 1;  // groups in flight per gathering warp
 
+// (the last CTA to finish also publishes the big-bucket count to the host-mapped word: the host reads it
+// after the level's final synchronisation, so no separate publish launch)
 __global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
-                                   Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count) {
+                                   Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count,
+                                   uint32_t* __restrict__ done, volatile uint32_t* host_mapped_dev) {
   __shared__ uint32_t s_cnt[16];
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers exactly 65536 buckets
   const Seg s{B16[p], hist16[p], 2u, 1u};
   classify_block(s, true, tu, kd, big_out, big_count, s_cnt);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      *host_mapped_dev = *reinterpret_cast<volatile uint32_t*>(big_count);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------- CTA tier
@@ -221,6 +231,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
   uint32_t* s_nbig = s_tmp + 32;
   uint8_t* s_stage = smem + L::kStage;                               // gather staging (reuses the sort area)
 
+  const PdlExitWait pdl_exit = pdl_enter(tu.pdl);
   const uint32_t nitems = FUSED ? 0u : *count;
   const int warp = threadIdx.x >> 5;
   constexpr int KC_ITEMS = (kChunk + THREADS - 1) / THREADS;
@@ -456,8 +467,9 @@ cudaError_t launch_cta_sort(const Seg* list, const uint32_t* count, const uint64
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, THREADS, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, in, in_bytes, out, dg,
-                                           kc ? *kc : KcArgs{}, tier);
+  e = launch_k(kern, sms * per_sm, THREADS, smem, s, tu.pdl != 0, list, count, t0, i0, t1, i1, perm, tu, in, in_bytes, out, dg,
+               kc ? *kc : KcArgs{}, tier);
+  if (e != cudaSuccess) return e;
   if (getenv("LEY_DEBUG_SYNC")) {
     fprintf(stderr, "[ley] kd_cta_sort<%u,%d> grid %d smem %zu\n", CAP, THREADS, sms * per_sm, smem);
     cudaError_t e2 = cudaStreamSynchronize(s);
@@ -570,8 +582,9 @@ __global__ void __launch_bounds__(256)
     kd_warp_sort(const Seg* __restrict__ list, const uint32_t* __restrict__ count, const uint64_t* __restrict__ t0,
                  const uint32_t* __restrict__ i0, const uint64_t* __restrict__ t1, const uint32_t* __restrict__ i1,
                  uint32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                 uint64_t* __restrict__ dg) {
+                 uint64_t* __restrict__ dg, int pdl) {
   __shared__ __align__(128) uint8_t s_stage[8][kStageBytes];
+  const PdlExitWait pdl_exit = pdl_enter(pdl);
   const uint32_t nitems = *count;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
@@ -745,6 +758,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
   uint32_t* s_nbig = s_tmp + 32;
   uint32_t* s_ring = reinterpret_cast<uint32_t*>(smem + L::kRing);
   uint2* s_desc = reinterpret_cast<uint2*>(smem + L::kDesc);
+  const PdlExitWait pdl_exit = pdl_enter(tu.pdl);
   const uint32_t nitems = FUSED ? 0u : *count;
   const int tid = threadIdx.x;
   static_assert(!FUSED || kKcSmem <= L::kTmp, "the split's staging reuses the sort area");
@@ -984,16 +998,16 @@ cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST + 32 * GW, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  kern<<<sms * per_sm, ST + 32 * GW, smem, s>>>(list, count, t0, i0, t1, i1, perm, tu, map, in, n_in & ~uint64_t(3), out, dg,
-                                               kc ? *kc : KcArgs{});
-  return cudaGetLastError();
+  return launch_k(kern, sms * per_sm, ST + 32 * GW, smem, s, tu.pdl != 0, list, count, t0, i0, t1, i1, perm, tu, map, in,
+                  n_in & ~uint64_t(3), out, dg, kc ? *kc : KcArgs{});
 }
 
 }  // namespace
 
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
-                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s) {
-  kd_classify_level1<<<256, 256, 0, s>>>(hist16, B16, tu, kd, big_out, big_count);
+                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, uint32_t* done,
+                                      uint32_t* host_mapped_dev, cudaStream_t s) {
+  kd_classify_level1<<<256, 256, 0, s>>>(hist16, B16, tu, kd, big_out, big_count, done, host_mapped_dev);
   return cudaGetLastError();
 }
 
@@ -1001,7 +1015,7 @@ namespace {
 // All K-d/K-e tiers for the lists of one level (counts are read on the device; no host sync).
 template <bool DG>
 cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, const uint64_t* t1, const uint32_t* i1,
-                   uint32_t* perm, const Tunables& tu, int sms, const uint8_t* in, uint64_t n_in, uint8_t* out,
+                   uint32_t* perm, const Tunables& tu0, int sms, const uint8_t* in, uint64_t n_in, uint8_t* out,
                    uint64_t* dg, cudaStream_t s, int* launches, const KcArgs* kc, int fused_tier) {
   const uint64_t in_bytes = n_in * kRecordBytes;
   static int warp_per_sm = 0;  // resident CTAs per SM (registers bound it: 5 at 46 registers)
@@ -1010,12 +1024,16 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
     warp_per_sm = 4;
   // tier t's kernel; with split != nullptr the fused form (it also runs the level-1 split, and claims its
   // buckets itself instead of reading list t)
+  // PDL modes (common.cuh): the first tier waits for the split/classification, later ones overlap it (their
+  // lists, pairs and output ranges are disjoint) — except around a fused tier, whose split the others need.
+  int nlaunched = 0;
   auto tier_launch = [&](int t, const KcArgs* split) -> cudaError_t {
+    Tunables tu = tu0;
+    tu.pdl = !tu0.pdl ? 0 : (nlaunched++ == 0 || kc) ? 1 : 2;
     switch (t) {
       case kListWarp:
-        kd_warp_sort<DG><<<sms * warp_per_sm, 256, 0, s>>>(kd.items[kListWarp], kd.counts + kListWarp, t0, i0, t1, i1,
-                                                          perm, in, out, dg);
-        return cudaGetLastError();
+        return launch_k(kd_warp_sort<DG>, sms * warp_per_sm, 256, 0, s, tu.pdl != 0, kd.items[kListWarp],
+                        kd.counts + kListWarp, t0, i0, t1, i1, perm, in, out, dg, tu.pdl);
       // (the warp-specialised form loses on small buckets: a ~100-record bucket keeps only 3 of its gather
       // warps busy and the ring hand-off dominates — measured C3 level 3: 17.0 vs 12.3 ms)
       case kListMed1:

@@ -24,6 +24,9 @@ struct ScanJob {
   uint64_t m;
   uint64_t* status;
   uint32_t* total_out;
+  uint32_t copies = 1;     // in = `copies` arrays `stride` words apart: the scan is over their sum ...
+  uint64_t stride = 0;
+  uint32_t* sum_out = nullptr;  // ... written back here (copy 0; level-1 hist16), if given
 };
 
 // Exclusive prefix of block blk's predecessors by warp 0: a window of 32 predecessor status words per
@@ -57,12 +60,21 @@ __device__ __forceinline__ void scan_block(const ScanJob& jb, uint32_t blk, uint
   static_assert(kScanItems % 4 == 0, "vector loads");
   uint32_t v[kScanItems];
   uint32_t sum = 0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
+                     reinterpret_cast<uintptr_t>(jb.sum_out) | (jb.stride * 4)) & 15) == 0 &&
                    base + kScanItems <= m;
   if (vec) {
 #pragma unroll
     for (int q = 0; q < kScanItems / 4; ++q) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(in + base) + q);
+      uint4 x = __ldg(reinterpret_cast<const uint4*>(in + base) + q);
+      for (uint32_t c = 1; c < jb.copies; ++c) {
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(in + c * jb.stride + base) + q);
+        x.x += y.x;
+        x.y += y.y;
+        x.z += y.z;
+        x.w += y.w;
+      }
+      if (jb.sum_out) reinterpret_cast<uint4*>(jb.sum_out + base)[q] = x;
       v[4 * q] = x.x;
       v[4 * q + 1] = x.y;
       v[4 * q + 2] = x.z;
@@ -70,7 +82,13 @@ __device__ __forceinline__ void scan_block(const ScanJob& jb, uint32_t blk, uint
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < m) ? in[base + i] : 0u;
+    for (int i = 0; i < kScanItems; ++i) {
+      v[i] = 0;
+      if (base + i < m) {
+        for (uint32_t c = 0; c < jb.copies; ++c) v[i] += in[c * jb.stride + base + i];
+        if (jb.sum_out) jb.sum_out[base + i] = v[i];
+      }
+    }
   }
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) sum += v[i];
@@ -130,30 +148,6 @@ __global__ void __launch_bounds__(kScanThreads)
   else scan_block(jb, t - blocks_a, s_tmp, &s_prefix);
 }
 
-// Level-1 decomposition (K-c): byte-0 segment b = [B16[256 b], B16[256 (b+1)]) of the byte-0-ordered
-// sequence; it is cut into ceil(len / chunk) chunks; cstart = exclusive scan of the chunk counts.
-__global__ void kc_plan_chunks(const uint32_t* __restrict__ B16, uint64_t n, uint32_t chunk,
-                               uint32_t* __restrict__ cstart) {
-  __shared__ uint32_t s_tmp[32];
-  const int b = threadIdx.x;  // 256 threads
-  uint64_t beg = B16[b * 256];
-  uint64_t end = (b < 255) ? B16[(b + 1) * 256] : n;
-  uint32_t nch = (uint32_t)((end - beg + chunk - 1) / chunk);
-  uint32_t total;
-  uint32_t ex = block_excl_scan<256>(nch, s_tmp, &total);
-  cstart[b] = ex;
-  if (b == 0) cstart[256] = total;
-}
-
-// hist16[b] = sum of the kHistCopies copies (copy 0 is overwritten in place).
-__global__ void kb_hist_reduce(uint32_t* __restrict__ hist, uint32_t copies) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= 65536) return;
-  uint32_t s = 0;
-  for (uint32_t c = 0; c < copies; ++c) s += hist[(size_t)c * 65536 + b];
-  hist[b] = s;
-}
-
 // Copy one device counter into mapped pinned host memory with a store from the SM: the host reads a
 // recursion level's big-bucket count without a copy-engine transfer, which would queue behind a large
 // D2H on the copy engine (the streaming and external paths overlap sorts with such copies).
@@ -188,11 +182,6 @@ cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s) {
-  if (copies <= 1) return cudaSuccess;
-  kb_hist_reduce<<<256, 256, 0, s>>>(hist, copies);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
                              uint32_t* total_out, cudaStream_t s) {
@@ -204,21 +193,18 @@ cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint
 }
 
 cudaError_t launch_scan_excl2(const uint32_t* in_a, uint32_t* out_a, uint64_t m_a, uint64_t* status_a,
-                              uint32_t* total_a, const uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
-                              uint64_t* status_b, uint32_t* total_b, uint32_t* ticket, cudaStream_t s) {
+                              uint32_t* total_a, uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
+                              uint64_t* status_b, uint32_t* total_b, uint32_t copies_b, uint64_t stride_b,
+                              uint32_t* ticket, cudaStream_t s) {
   const uint64_t ba = (m_a + kScanTile - 1) / kScanTile, bb = (m_b + kScanTile - 1) / kScanTile;
   if (ba + bb == 0) return cudaSuccess;
+  ScanJob jb{in_b, out_b, m_b, status_b, total_b, copies_b, stride_b, copies_b > 1 ? in_b : nullptr};
   kb_scan_excl<<<(unsigned)(ba + bb), kScanThreads, 0, s>>>(ScanJob{in_a, out_a, m_a, status_a, total_a}, (uint32_t)ba,
-                                                            ScanJob{in_b, out_b, m_b, status_b, total_b}, ticket);
+                                                            jb, ticket);
   return cudaGetLastError();
 }
 
 uint64_t scan_status_words(uint64_t m) { return (m + kScanTile - 1) / kScanTile; }
 
-cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
-                                  cudaStream_t s) {
-  kc_plan_chunks<<<1, 256, 0, s>>>(B16, n, chunk, cstart);
-  return cudaGetLastError();
-}
 
 }  // namespace ley

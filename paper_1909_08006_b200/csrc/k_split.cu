@@ -86,13 +86,29 @@ __device__ __forceinline__ uint64_t search_le_guess(const uint32_t* a, uint64_t 
 
 // Per-chunk decomposition of level 1, one thread per chunk: segment b, virtual range [v0, v0+cnt), the
 // tile range [t0, t1] whose byte-0 runs cover it, and the segment's first chunk k0. Parallel searches
-// here keep them off the K-c critical path. The same launch also initialises the split's write cursors
-// (cursor = B16) with its spare threads.
-__global__ void kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles, const uint32_t* __restrict__ B16,
-                               uint64_t n, const uint32_t* __restrict__ cstart, uint32_t grid_ub,
-                               uint4* __restrict__ plan_a, uint2* __restrict__ plan_b, uint32_t* __restrict__ cursor) {
+// here keep them off the K-c critical path. Every CTA first derives the chunk starts itself (byte-0
+// segment b = [B16[256 b], B16[256 (b+1)]) is cut into ceil(len / kChunk) chunks; cstart = exclusive
+// scan of the chunk counts; CTA 0 publishes them), and the launch also initialises the split's write
+// cursors (cursor = B16) with its spare threads. 256 threads per CTA.
+__global__ void __launch_bounds__(256)
+    kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles, const uint32_t* __restrict__ B16, uint64_t n,
+                   uint32_t* __restrict__ cstart, uint32_t grid_ub, uint4* __restrict__ plan_a,
+                   uint2* __restrict__ plan_b, uint32_t* __restrict__ cursor) {
   __shared__ uint32_t s_cst[257];
-  for (uint32_t i = threadIdx.x; i < 257; i += blockDim.x) s_cst[i] = cstart[i];
+  __shared__ uint32_t s_tmp[32];
+  {
+    const uint32_t b = threadIdx.x;
+    const uint64_t beg = B16[b * 256], end = (b < 255) ? B16[(b + 1) * 256] : n;
+    const uint32_t nch = (uint32_t)((end - beg + kChunk - 1) / kChunk);
+    uint32_t total;
+    const uint32_t ex = block_excl_scan<256>(nch, s_tmp, &total);
+    s_cst[b] = ex;
+    if (b == 0) s_cst[256] = total;
+    if (blockIdx.x == 0) {
+      cstart[b] = ex;
+      if (b == 0) cstart[256] = total;
+    }
+  }
   const uint32_t nth = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 65536 / 4; i += nth)
     reinterpret_cast<uint4*>(cursor)[i] = reinterpret_cast<const uint4*>(B16)[i];
@@ -111,9 +127,10 @@ __global__ void kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles,
     const uint32_t cnt = (uint32_t)(seg_end - v0 < kChunk ? seg_end - v0 : kChunk);
     const uint32_t* off_b = off + (uint64_t)b * tiles;
     const uint64_t len = seg_end - seg_beg;
+    // (two independent searches, so their load chains overlap)
     const uint32_t t0 = (uint32_t)search_le_guess(off_b, 0, tiles, v0, (uint64_t)(v0 - seg_beg) * tiles / len);
     const uint32_t t1 =
-        (uint32_t)search_le_guess(off_b, t0, tiles, v0 + cnt - 1, (uint64_t)(v0 + cnt - 1 - seg_beg) * tiles / len);
+        (uint32_t)search_le_guess(off_b, 0, tiles, v0 + cnt - 1, (uint64_t)(v0 + cnt - 1 - seg_beg) * tiles / len);
     plan_a[k] = make_uint4(b, v0, cnt, k - c);
     plan_b[k] = make_uint2(t0, t1);
   }
@@ -290,11 +307,9 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
 
     uint32_t pos[kItems], total_d, excl_d;
         block_rank_atomic<kThreads, kItems, true>(dig, cnt, pos, s_wh, s_misc, total_d, excl_d);
-    if (threadIdx.x < kRadix) {
-      const int d = threadIdx.x;
-      const uint32_t base = total_d ? atomicAdd(&cursor[b * 256 + d], total_d) : 0u;
-      s_dst[d] = base - excl_d;
-    }
+    // each digit's slice of its 16-bit bucket: the atomic's round trip overlaps the staging scatter below
+    static_assert(kThreads == kRadix, "one digit per thread");
+    const uint32_t dbase = total_d ? atomicAdd(&cursor[b * 256 + threadIdx.x], total_d) : 0u;
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       uint32_t e = warp * (32 * kItems) + j * 32 + lane;
@@ -305,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
         s_dig[p] = (uint8_t)dig[j];
       }
     }
+    s_dst[threadIdx.x] = dbase - excl_d;
     __syncthreads();
     // the next chunk's plan is in s_misc[40..46]: prefetch this thread's run-table entry while writing
     pf = false;
@@ -517,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
 size_t split_smem_bytes() { return SplitSmem::kBytes; }
 
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
-                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
+                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
                                    bool run_split, const uint32_t** order_used) {

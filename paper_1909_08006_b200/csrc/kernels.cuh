@@ -1,6 +1,7 @@
 // kernels.cuh — launch wrappers of the sm_100a kernels (K-a .. K-e) used by the host drivers.
 #pragma once
 #include <cuda.h>
+#include <utility>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -8,6 +9,24 @@
 #include "common.cuh"
 
 namespace ley {
+
+// kern<<<grid, block, smem, s>>>(args...), with the programmatic-serialization attribute when pdl (the
+// kernel must call pdl_wait() before reading its predecessor's output; common.cuh).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // The 10-byte key window one sort pass orders by: record bytes [off, off + len), off a multiple of 10,
 // 1 <= len <= 10 (len < 10: bytes [len, 10) of the window carry the ordinal; k_tile.cu)
@@ -29,23 +48,23 @@ cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, u
 
 // K-b (k_scan.cu)
 // (two independent exclusive scans in one launch; one ticket word)
+// (job b's input may be `copies_b` histogram copies `stride_b` words apart: it scans their sum and writes
+// the sum back over copy 0)
 cudaError_t launch_scan_excl2(const uint32_t* in_a, uint32_t* out_a, uint64_t m_a, uint64_t* status_a,
-                              uint32_t* total_a, const uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
-                              uint64_t* status_b, uint32_t* total_b, uint32_t* ticket, cudaStream_t s);
+                              uint32_t* total_a, uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
+                              uint64_t* status_b, uint32_t* total_b, uint32_t copies_b, uint64_t stride_b,
+                              uint32_t* ticket, cudaStream_t s);
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
                              uint32_t* total_out, cudaStream_t s);
 uint64_t scan_status_words(uint64_t m);
-cudaError_t launch_hist_reduce(uint32_t* hist, uint32_t copies, cudaStream_t s);
 cudaError_t launch_zero3(void* a, uint64_t a_bytes, void* b, uint64_t b_bytes, void* c, uint64_t c_bytes, int sms,
                          cudaStream_t s);
 cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, cudaStream_t s);
-cudaError_t launch_kc_plan_chunks(const uint32_t* B16, uint64_t n, uint32_t chunk, uint32_t* cstart,
-                                  cudaStream_t s);
 
 // K-c / K-c' (k_split.cu)
 size_t split_smem_bytes();
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
-                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, const uint32_t* cstart,
+                                   const uint32_t* lo, const uint32_t* B16, uint64_t n, uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
                                    bool run_split = true, const uint32_t** order_used = nullptr);
@@ -63,7 +82,8 @@ cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* csta
 
 // K-d (k_bucket.cu)
 cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
-                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, cudaStream_t s);
+                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, uint32_t* done,
+                                      uint32_t* host_mapped_dev, cudaStream_t s);
 // K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
 // out == nullptr: perm-only, no gather; dg non-null: dg[j] = digest of output record j's 10-byte prefix).
 // in holds n_in records; no gather reads outside them. Level 1 only: with kc and a fused_tier in

@@ -55,6 +55,7 @@ const OptDesc kOpts[] = {
     {"gather_l2_64", &Options::gather_l2_64, 0, 1},
     {"kc_fuse", &Options::kc_fuse, 0, 5},
     {"graphs", &Options::graphs, 0, 1},
+    {"pdl", &Options::pdl, 0, 1},
     {"ext_keyptr", &Options::ext_keyptr, 0, 1},
 };
 }  // namespace
@@ -349,7 +350,6 @@ ley_status graph_run(DeviceContext& ctx, const GraphKey& key, cudaStream_t s,
                      const std::function<ley_status(cudaStream_t)>& fn, Profiler& prof) {
   if (!ctx.graph_stream) {
     LEY_CUDA("graph", cudaStreamCreateWithFlags(&ctx.graph_stream, cudaStreamNonBlocking));
-    for (auto& e : ctx.graph_ev) LEY_CUDA("graph", cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   uint64_t k[13];
   memcpy(k, key.w, sizeof(key.w));
@@ -401,11 +401,7 @@ ley_status graph_run(DeviceContext& ctx, const GraphKey& key, cudaStream_t s,
     g = &ctx.graphs.back();
   }
   g->used = ++ctx.graph_clock;
-  LEY_CUDA("graph", cudaEventRecord(ctx.graph_ev[0], s));
-  LEY_CUDA("graph", cudaStreamWaitEvent(ctx.graph_stream, ctx.graph_ev[0], 0));
-  LEY_CUDA("graph", cudaGraphLaunch(g->exec, ctx.graph_stream));
-  LEY_CUDA("graph", cudaEventRecord(ctx.graph_ev[1], ctx.graph_stream));
-  LEY_CUDA("graph", cudaStreamWaitEvent(s, ctx.graph_ev[1], 0));
+  LEY_CUDA("graph", cudaGraphLaunch(g->exec, s));  // (captured on graph_stream; replayed in the caller's stream order)
   prof.launches += g->launches;
   prof.names.insert(prof.names.end(), g->names.begin(), g->names.end());
   prof.ev_begin.insert(prof.ev_begin.end(), g->ev_begin.begin(), g->ev_begin.end());
