@@ -241,9 +241,15 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    input by its ordinal over the host link (the input must be mapped pinned memory:
  *                    cudaHostAlloc, or cudaHostRegister with cudaHostRegisterMapped; else
  *                    LEY_ERR_UNSUPPORTED). Same bytes; slower on PCIe (random reads over the link)
- *   "graphs"         1 (default) = level 1 of the internal sort (init .. K-e, ~16 launches) is captured once
- *                    per (buffers, n, options) into a CUDA graph and replayed on a library stream joined to
- *                    the caller's by events (C1 1e6 records: 0.225 -> 0.187 ms); not while "profile" is on
+ *   "graphs"         1 (default) = level 1 of the internal sort (init .. K-e, 12 launches) is captured once
+ *                    per (buffers, n, options) into a CUDA graph and replayed in the caller's stream (C1 1e6
+ *                    records: 0.225 -> 0.187 ms when introduced); not while "profile" is on
+ *   "pdl"            programmatic dependent launch of the K-d+K-e tier kernels: 0 = plain stream order,
+ *                    1 = each tier waits for its predecessor, then lets the next launch, 2 = the first tier
+ *                    waits, the later (independent) tiers launch at once and wait only before exiting,
+ *                    3 (default) = 2 below 1e7 records, else 0 (measured: pays at C1, costs at C2/C4)
+ *   "kd_claim"       K-d+K-e tier CTAs take buckets from their list by atomic ticket, one bucket ahead
+ *                    (1, default), or by a static stride (0)
  *   "kc_fuse"        level-1 K-c split inside the K-d+K-e kernel of one tier: 0 (default) = its own kernel,
  *                    1 = the tier of the average 16-bit bucket, 2..5 = the 2048 / 8192 / 10240 / 16384
  *                    tier (tests); same bytes, measured slower

@@ -31,9 +31,11 @@ static_assert(kNumKdLists == kNumKdListsHost, "host planning mirrors the K-d lis
 
 struct ListSet {
   Seg* items[kNumKdLists];
-  uint32_t* counts;  // [kNumKdLists] device counters
+  uint32_t* counts;  // [kNumKdLists] device counters; counts[kTierTicket + l]: list l's claim ticket
   uint32_t cap;      // capacity of each list
 };
+constexpr int kTierTicket = 8;  // (counts and tickets are zeroed together: 2 * kTierTicket words)
+static_assert(kNumKdLists <= kTierTicket, "tickets follow the counts");
 
 // Runtime tunables (ley_set_option); copied by value into kernels that need them.
 struct Tunables {
@@ -44,9 +46,10 @@ struct Tunables {
   int kd_ws = 1;  // warp-specialised sort/gather tiers (kd_ws_sort) instead of the alternating kd_cta_sort
   int ws_tma = 0;  // kd_ws_sort: record windows by TMA tensor copies (64-B L2 fetches) or plain bulk copies
   int gather_l2_64 = 1;  // kd_cta_sort gathers: cp.async with .L2::64B (1) or without the hint (0)
-  int pdl = 1;           // K-d/K-e tier kernels launched with programmatic dependent launch (launch_k);
-                         // per launch: 1 wait, then let the next tier launch; 2 let it launch at once and
-                         // wait only before exiting (independent tiers overlap); 0 plain stream order
+  int kd_claim = 1;      // tier CTAs claim buckets by atomic ticket (1) or stride the list statically (0)
+  int pdl = 0;           // K-d/K-e tier kernels launched with programmatic dependent launch (launch_k): 0
+                         // plain stream order; 1 every tier waits, then lets the next launch; 2 the first
+                         // tier waits, later ones launch at once and wait only before exiting (overlap)
 };
 
 // Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization attribute

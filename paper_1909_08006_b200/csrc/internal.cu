@@ -21,6 +21,7 @@ namespace ley {
 
 namespace {
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr uint64_t kPdlMaxRecords = 10000000;  // (option pdl = 3: tier overlap below this size)
 }  // namespace
 
 namespace {
@@ -58,7 +59,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   uint32_t* cursor = reinterpret_cast<uint32_t*>(base + L.off_cursor);
   uint32_t* small = reinterpret_cast<uint32_t*>(base + L.off_small);
   uint32_t* tickets = small;          // [0..15]
-  uint32_t* kd_counts = small + 16;   // [kNumKdLists]
+  uint32_t* kd_counts = small + 16;   // [kNumKdLists] counts, [kTierTicket + l] claim tickets
   uint32_t* big_count = small + 32;   // [1]; small[33]: classify's CTA-done counter
   volatile uint32_t* host_cnt = static_cast<volatile uint32_t*>(ctx.host_pinned);
   uint32_t* host_cnt_dev = nullptr;  // its device alias: counters are published by a kernel store
@@ -73,7 +74,11 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
   tu.kd_ws = (int)o.kd_ws;
   tu.ws_tma = (int)o.ws_gather_tma;
   tu.gather_l2_64 = (int)o.gather_l2_64;
-  tu.pdl = (int)o.pdl;
+  // PDL of the tier kernels (k_bucket.cu kd_all): overlapping the tiers pays for small sorts, where their
+  // launch latency and empty grids are a visible share (C1 0.148 -> 0.141 ms), and costs at large ones (C4
+  // +2.3 ms, C2 +0.1 ms: measured, tools/ab_opts.py); option 3 (default) picks by n
+  tu.pdl = o.pdl == 3 ? (n < kPdlMaxRecords ? 2 : 0) : (int)o.pdl;
+  tu.kd_claim = (int)o.kd_claim;
   const uint32_t tiles = (uint32_t)L.tiles;
   const int sms = ctx.sms;
   int& launches = prof.launches;
@@ -231,7 +236,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(seg_hist, 0, 4ull * nbig * kRadix, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rscan, 0, 8 * scan_words, s));
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(rtick, 0, 256, s));
-    LEY_CUDA("K-c' recursion", cudaMemsetAsync(kd_counts, 0, 4 * kNumKdLists, s));
+    LEY_CUDA("K-c' recursion", cudaMemsetAsync(kd_counts, 0, 4 * 2 * kTierTicket, s));  // counts + tickets
     LEY_CUDA("K-c' recursion", cudaMemsetAsync(big_count, 0, 4, s));
     LEY_CUDA("K-c' recursion", launch_kr_nchunks(segs, nbig, nch, s));
     LEY_CUDA("K-c' recursion", launch_scan_excl(nch, cst, nbig, rscan, rtick + 0, cst + nbig, s));

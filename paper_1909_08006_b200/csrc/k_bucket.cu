@@ -248,7 +248,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     __syncthreads();
     return c;
   };
-  uint32_t it = blockIdx.x;
+  uint32_t* const ticket = const_cast<uint32_t*>(count) + kTierTicket;
+  uint32_t it = 0, nxt = tu.kd_claim ? 0u : blockIdx.x;
+  if (!FUSED && tu.kd_claim && threadIdx.x == 0) s_claim[3] = atomicAdd(ticket, 1u);
   while (true) {
     Seg sg;
     if constexpr (FUSED) {
@@ -269,10 +271,19 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
         else __nanosleep(1000);  // the remaining chunks are being split by running CTAs
       }
       sg = Seg{kc.B16[p], kc.hist16[p], 2u, 1u};
-    } else {
+    } else {  // buckets claimed dynamically (ticket kTierTicket words past the count), one bucket ahead so
+              // the claim's round trip overlaps the current bucket: a CTA that becomes resident late (PDL
+              // overlap with the previous tier) just takes fewer
+      if (tu.kd_claim) {
+        __syncthreads();
+        it = s_claim[3];
+        if (threadIdx.x == 0 && it < nitems) nxt = atomicAdd(ticket, 1u);
+      } else {
+        it = nxt;  // static: blockIdx.x, + gridDim.x, ...
+        nxt = it + gridDim.x;
+      }
       if (it >= nitems) break;
       sg = list[it];
-      it += gridDim.x;
     }
     for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;  // was gather staging
     __syncthreads();
@@ -446,6 +457,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in, in_bytes,
                   out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
                   DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
+    if (!FUSED && tu.kd_claim && threadIdx.x == 0) s_claim[3] = nxt;  // (every thread read this claim long ago)
     __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
   if constexpr (FUSED)  // the split's remaining chunks: the other tiers' buckets (later kernels) need them
@@ -781,7 +793,9 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       return c;
     };
     uint32_t k = 0;
-    uint32_t it = blockIdx.x;
+    uint32_t* const ticket = const_cast<uint32_t*>(count) + kTierTicket;
+    uint32_t it = 0, nxt = tu.kd_claim ? 0u : blockIdx.x;
+    if (!FUSED && tu.kd_claim && tid == 0) s_claim[3] = atomicAdd(ticket, 1u);
     for (;; ++k) {
       Seg sg;
       if constexpr (FUSED) {
@@ -803,10 +817,17 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
           else __nanosleep(1000);  // the remaining chunks are being split by running CTAs
         }
         sg = Seg{kc.B16[p], kc.hist16[p], 2u, 1u};
-      } else {
+      } else {  // (dynamic claims one bucket ahead, or static, as in kd_cta_sort)
+        if (tu.kd_claim) {
+          nbar_sync(kBarSort, ST);
+          it = s_claim[3];
+          if (tid == 0 && it < nitems) nxt = atomicAdd(ticket, 1u);
+        } else {
+          it = nxt;
+          nxt = it + gridDim.x;
+        }
         if (it >= nitems) break;
         sg = list[it];
-        it += gridDim.x;
       }
       const int q = k & 1;
       uint32_t* s_perm = s_ring + q * CAP;
@@ -896,6 +917,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
         warp_bitonic_smem(s_tail, s_idx, b, e);
         for (uint32_t i = b + (tid & 31); i < e; i += 32) s_perm[i] = s_idx[i];
       }
+      if (!FUSED && tu.kd_claim && tid == 0) s_claim[3] = nxt;
       nbar_sync(kBarSort, ST);
       if (perm)
         for (uint32_t i = tid; i < s; i += ST) perm[sg.start + i] = s_perm[i];
@@ -1029,7 +1051,7 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
   int nlaunched = 0;
   auto tier_launch = [&](int t, const KcArgs* split) -> cudaError_t {
     Tunables tu = tu0;
-    tu.pdl = !tu0.pdl ? 0 : (nlaunched++ == 0 || kc) ? 1 : 2;
+    tu.pdl = !tu0.pdl ? 0 : (nlaunched++ == 0 || kc || tu0.pdl == 1) ? 1 : 2;
     switch (t) {
       case kListWarp:
         return launch_k(kd_warp_sort<DG>, sms * warp_per_sm, 256, 0, s, tu.pdl != 0, kd.items[kListWarp],

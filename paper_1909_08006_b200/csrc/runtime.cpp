@@ -55,7 +55,8 @@ const OptDesc kOpts[] = {
     {"gather_l2_64", &Options::gather_l2_64, 0, 1},
     {"kc_fuse", &Options::kc_fuse, 0, 5},
     {"graphs", &Options::graphs, 0, 1},
-    {"pdl", &Options::pdl, 0, 1},
+    {"pdl", &Options::pdl, 0, 3},
+    {"kd_claim", &Options::kd_claim, 0, 1},
     {"ext_keyptr", &Options::ext_keyptr, 0, 1},
 };
 }  // namespace

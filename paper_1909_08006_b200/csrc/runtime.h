@@ -61,7 +61,8 @@ struct Options {
   int64_t ws_gather_tma = 0;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
   int64_t gather_l2_64 = 1;   // K-d CTA-tier gathers with cp.async .L2::64B (1) or without the hint (0)
   int64_t ext_keyptr = 0;  // external path: runs of (key, ordinal) tuples, records gathered from the input
-  int64_t pdl = 1;      // programmatic dependent launch of the K-d/K-e tier kernels (0: plain stream order)
+  int64_t kd_claim = 1;  // K-d/K-e tier CTAs claim buckets dynamically (1) or stride their list (0)
+  int64_t pdl = 3;      // PDL of the K-d/K-e tier kernels: 0 off, 1 wait-first, 2 overlap, 3 overlap below 1e7 records
   int64_t graphs = 1;   // replay level 1 of the internal sort from a cached CUDA graph (0: launch directly)
   int64_t kc_fuse = 0;  // level-1 split fused into a K-d+K-e tier (0 off, 1 auto, 2..5 force tier 2048..16384):
                         // measured slower (C2 K-c+K-de 7.49 vs 6.40 ms, C4 54.5 vs 38.8 ms)

@@ -122,6 +122,11 @@ def test_zero_records():
     dict(kc_fuse=2, kd_ws=0),                        # ... into the alternating 2048 tier (256 threads)
     dict(kc_fuse=3), dict(kc_fuse=4), dict(kc_fuse=5),  # ... into the 8192 / 10240 / 16384 tiers
     dict(kc_fuse=4, smem_tier_max=600),              # fused tier empty, big buckets recurse after it
+    dict(pdl=0), dict(pdl=1), dict(pdl=2),           # tier kernels: stream order / PDL wait-first / overlap
+    dict(pdl=2, smem_tier_max=600),                  # ... overlapping tiers at the recursion levels too
+    dict(pdl=2, kd_ws=0), dict(pdl=2, kc_fuse=3),    # ... with the alternating tiers / a fused tier
+    dict(kd_claim=0), dict(kd_claim=0, kd_ws=0),     # tier CTAs stride their list instead of claiming
+    dict(kd_claim=0, pdl=2, smem_tier_max=600),
 ])
 @pytest.mark.parametrize("dist", ["uniform", "skewed", "tiny_alphabet", "byte9"])
 def test_forced_thresholds(opts, dist):

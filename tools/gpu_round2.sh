@@ -20,3 +20,5 @@ timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"kd
   -o $O/full_kde_c4 python tools/profile_step.py --n 6e8 --seed 3 --steps 1 --warmup 1 > $O/ncu_full_c4.log 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"kd_ws_sort|ka_tile_keys|kc_split_level1" -s 3 -c 3 \
   -o $O/full_c2 python tools/profile_step.py --n 1e8 --seed 1 --steps 1 --warmup 1 > $O/ncu_full_c2.log 2>&1
+timeout 300 python tools/timeline.py 1e6 > $O/timeline_c1.txt 2>&1
+timeout 300 python tools/timeline.py 1e6 uniform pdl=0 > $O/timeline_c1_pdl0.txt 2>&1
