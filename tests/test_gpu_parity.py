@@ -138,6 +138,32 @@ def test_forced_thresholds(opts, dist):
     assert_parity(recs, out, perm)
 
 
+@pytest.mark.parametrize("pdl", [0, 2])
+def test_warp_tier_near_ties(pdl):
+    """The warp tier sorts one 64-bit composite per lane (the tail with its low 5 bits replaced by the lane)
+    and falls back to the full (tail, ordinal) network when two sorted tails agree in their top 59 bits.
+    Buckets of 2..32 records whose keys differ only in the low 5 bits of key byte 9, or not at all
+    (duplicates, ordered by ordinal), must still come out in the oracle's order; so must buckets next to
+    them that take the fast path."""
+    rng = np.random.default_rng(5)
+    base = gen.records(40_000, seed=5, dist="uniform").reshape(-1, 100).copy()
+    groups = []
+    for g in range(300):
+        size = int(rng.integers(2, 33))
+        proto = base[rng.integers(0, len(base))].copy()
+        proto[0], proto[1] = g >> 8 | 0x40, g & 0xFF  # its own 16-bit bucket
+        grp = np.repeat(proto[None, :], size, axis=0)
+        if g % 3:  # near ties: only the low 5 bits of byte 9 differ (some exact duplicates among them)
+            grp[:, 9] = (proto[9] & 0xE0) | rng.integers(0, 8, size=size).astype(np.uint8)
+        grp[:, 10:] = rng.integers(0, 256, size=(size, 90), dtype=np.uint8)  # payload tells records apart
+        groups.append(grp)
+    recs = np.concatenate([base] + groups)
+    recs = np.ascontiguousarray(recs[rng.permutation(len(recs))].reshape(-1))
+    with Options(pdl=pdl):
+        out, perm = gpu_sort(recs)
+    assert_parity(recs, out, perm)
+
+
 def test_repeat_bit_identical():
     recs = gen.records(200_003, seed=21, dist="skewed")
     a, pa = gpu_sort(recs)
