@@ -624,7 +624,8 @@ __global__ void __launch_bounds__(256)
     const uint32_t len = sg.len;
     if (perm && (uint32_t)lane < len) perm[sg.start + lane] = x;
     const uint64_t obyte = (uint64_t)sg.start * kRecordBytes;
-    const uint32_t a = (uint32_t)(obyte & 15u);  // stage byte a + i holds bucket output byte i (same phase mod 16)
+    // stage byte a + i holds bucket output byte i: the same phase mod 16 as its global address
+    const uint32_t a = (uint32_t)(reinterpret_cast<uintptr_t>(out + obyte) & 15u);
     const uint32_t words = len * kRecordWords;
     if (out) {  // (perm-only mode: the resident host path gathers later, chunk by chunk)
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous store read the stage
