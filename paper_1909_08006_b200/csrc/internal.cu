@@ -153,7 +153,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
                                                  reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
                                                  tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, fused_tier < 0,
                                                  &order_used));
-    launches += fused_tier < 0 ? 2 : 1;
+    launches += (fused_tier < 0 ? 2 : 1) + (order_used ? 1 : 0);  // plan (+ chunk order) (+ split)
     if ((st = prof.end())) return st;
 
     // ---------------------------------------------------------------- classify level 1, K-d
