@@ -263,25 +263,48 @@ def measure(args, cfg_name, world, rank, local, comm, with_cpu=True):
         if world > 1:
             dist.barrier()
 
+    ley.ley_set_option("async", 0 if comm is not None or external else 1)  # (as in the value pass below)
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
+    ley.ley_set_option("async", 0)
 
     # ---------------------------------------------------------------- timed region (device events)
     # (1) the step as a user runs it (no per-stage events: level 1 replays its cached CUDA graph) -> value;
     # (2) the same K steps again with per-stage CUDA events (the library's "profile" option, which launches
     #     level 1 directly) -> stages_ms and the dominant kernel's roofline, from its own timed region.
+    # Inputs below 1e7 records (C1: 100 MB) fit the 126 MB L2: every timed step then gets its own event
+    # pair, with a 256 MB write between steps (outside the timed intervals) flushing the L2.
+    # (then a 256 MB read: the write leaves the L2 full of dirty lines, whose write-back would otherwise
+    # land inside the next timed step; after the read the L2 is cold and clean)
+    flush_buf = (torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+                 if n_total < 10**7 and comm is None and not external else None)
+    flush_rd = torch.ones(64 << 20, dtype=torch.int32, device="cuda") if flush_buf is not None else None
+
     def timed_steps(profile):
         ley.ley_set_option("profile", profile)
+        # the value pass uses the stream-ordered API (option async: a device sort without recursion returns
+        # once enqueued, so back-to-back steps keep the GPU busy); every step's work is inside the timed
+        # region, which ends with an event after the last step and a synchronize
+        ley.ley_set_option("async", 0 if profile or comm is not None or external else 1)
         stage_ms: dict[str, list[float]] = {}
         launches = 0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        per_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)] if flush_buf is not None else None
         barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
             e0.record(stream)
-            for _ in range(args.steps):
+            for i in range(args.steps):
+                if per_step is not None:
+                    with torch.cuda.stream(stream):
+                        flush_buf.fill_(i & 0xFF)
+                        flush_rd.sum(dtype=torch.int64)
+                    per_step[i][0].record(stream)
                 step()
+                if per_step is not None:
+                    per_step[i][1].record(stream)
                 if profile:  # (the stage read-back is host work: kept out of the value pass)
                     st, nl = ley.ley_stage_times()
                     launches += nl
@@ -293,7 +316,14 @@ def measure(args, cfg_name, world, rank, local, comm, with_cpu=True):
             launches = ley.ley_stage_times()[1] * args.steps
         barrier()
         ley.ley_set_option("profile", 0)
-        ms_ = e0.elapsed_time(e1) / args.steps
+        ley.ley_set_option("async", 0)
+        if per_step is not None:
+            ts = [a.elapsed_time(b) for a, b in per_step]
+            if os.environ.get("LEY_BENCH_STEPS"):
+                print("per-step ms:", " ".join(f"{t:.4f}" for t in ts), file=sys.stderr)
+            ms_ = sum(ts) / args.steps
+        else:
+            ms_ = e0.elapsed_time(e1) / args.steps
         if world > 1:
             t = torch.tensor([ms_], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -431,7 +461,10 @@ def measure(args, cfg_name, world, rank, local, comm, with_cpu=True):
                    "seed": cfg["seed"], "distribution": cfg["dist"],
                    "device_budget_bytes": budget,
                    "l2": "inputs (>= 10 GB) larger than the 126 MB L2; no flush needed" if n_total >= 10**7
-                   else "100 MB input: L2 flushed by the next step's 100 MB output + 29 MB scratch",
+                   else "input fits the L2: a 256 MB write, then a 256 MB read, between timed steps flushes it "
+                        "(per-step event pairs, the flush outside them)",
+                   "api": "ley_sort on device buffers, stream-ordered (option async)" if comm is None and not external
+                   else "ley_sort_dist" if comm is not None else "ley_sort on pinned host buffers",
                    "parallelism": (f"key-range dist x{world} (NCCL, " +
                                    ("all-to-all-v" if args.alltoall else "fused partition+exchange") +
                                    (", exchange at G=1" if args.exchange else "") + ")")

@@ -73,7 +73,11 @@ typedef enum {
  *   device_budget_bytes : cap on device memory the LIBRARY allocates for this call (caller buffers
  *                   excluded); 0 = no cap (P:19's memory limit; BJ configs[4] "4 GB per GPU").
  *   stream        : a cudaStream_t (0 = legacy default stream). Work is ordered after prior work on
- *                   `stream`; v1 returns when `out` is complete (host-synchronous). */
+ *                   `stream`; returns when `out` is complete (host-synchronous) — unless option "async"
+ *                   is 1, the pointers are device pointers, key_bytes <= 10 and no bucket needs the
+ *                   byte-2 recursion: then it returns once the sort is enqueued and `out` (and perm) are
+ *                   complete when `stream` gets there (stream-ordered, like cudaMemcpyAsync). Later
+ *                   library calls on the same device order themselves after it. */
 ley_status ley_sort(const void* in, void* out, uint64_t n_records, uint32_t record_bytes,
                     uint32_t key_bytes, uint64_t device_budget_bytes, void* stream);
 
@@ -248,6 +252,9 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *                    1 = each tier waits for its predecessor, then lets the next launch, 2 = the first tier
  *                    waits, the later (independent) tiers launch at once and wait only before exiting,
  *                    3 (default) = 2 below 1e7 records, else 0 (measured: pays at C1, costs at C2/C4)
+ *   "async"          0 (default) = ley_sort / ley_sort_perm return when the output is complete; 1 = device
+ *                    sorts that need no recursion return once enqueued (the host waits only for the
+ *                    level-1 classification's big-bucket count; see ley_sort "stream")
  *   "kd_claim"       K-d+K-e tier CTAs take buckets from their list by atomic ticket, one bucket ahead
  *                    (1, default), or by a static stride (0)
  *   "kc_fuse"        level-1 K-c split inside the K-d+K-e kernel of one tier: 0 (default) = its own kernel,

@@ -176,6 +176,7 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
     if (sms > 0) ctx.sms = sms;
   }
   const Options opts = options_snapshot();
+  if ((st = async_join(ctx, s))) return st;  // (a previous stream-ordered sort may still use the buffers)
   if (opts.l2_fetch_bytes) LEY_CUDA("setup", cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)opts.l2_fetch_bytes));
   Profiler prof;
   prof.on = opts.profile != 0;
@@ -192,7 +193,7 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
                 std::to_string(device_budget_bytes));
       return LEY_ERR_BUDGET;
     }
-    st = sort_internal_device(ctx, in8, out8, perm, n_records, s, prof, nullptr, 0, key_bytes);
+    st = sort_internal_device(ctx, in8, out8, perm, n_records, s, prof, nullptr, 0, key_bytes, opts.async != 0);
   } else {
     ley_plan_info info;
     plan_query(n_records, device_budget_bytes, &info);
@@ -227,6 +228,10 @@ ley_status ley_sort_perm(const void* in, void* out, uint32_t* perm, uint64_t n_r
     }
   }
   if (st) return st;
+  if (ctx.async_pending) {  // stream-ordered: out is complete when the stream gets there
+    record_launches(prof.launches);
+    return LEY_OK;
+  }
   LEY_CUDA("complete", cudaStreamSynchronize(s));
   LEY_CUDA("complete", cudaGetLastError());
   prof.finish();

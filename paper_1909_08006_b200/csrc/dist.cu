@@ -671,6 +671,7 @@ ley_status dist_sort_device(ley_comm* comm, const void* in_local, uint64_t n_loc
   LEY_CUDA("dist", cudaSetDevice(comm->device));
   DeviceContext& ctx = device_context(comm->device);
   std::lock_guard<std::mutex> guard(ctx.mu);
+  if (ley_status ast = async_drain(ctx)) return ast;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
   if (sms > 0) ctx.sms = sms;
@@ -930,6 +931,7 @@ ley_status dist_sort_external(ley_comm* comm, const uint8_t* in, uint64_t n_loca
   }
   DeviceContext& ctx = device_context(comm->device);
   std::lock_guard<std::mutex> guard(ctx.mu);
+  if (ley_status ast = async_drain(ctx)) return ast;
   if (!ctx.host_pinned) LEY_CUDA("dist", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
   // slice sizes -> the plan every rank derives alike
   std::vector<uint64_t> nl(G);
@@ -1063,6 +1065,7 @@ ley_status dist_sort(ley_comm* comm, const void* in_local, uint64_t n_local, voi
   {
     DeviceContext& ctx = device_context(comm->device);
     std::lock_guard<std::mutex> guard(ctx.mu);
+    if (ley_status ast = async_drain(ctx)) return ast;
     uint64_t* flag = reinterpret_cast<uint64_t*>(comm->state.d_status);
     if (!flag) {  // first call on this comm: scratch for the agreement
       if (ley_status st = rank_alloc(comm->state)) return st;
@@ -1110,6 +1113,7 @@ ley_status dist_external_loopback(int G, const void* const* in, const uint64_t* 
   LEY_CUDA("loopback", cudaGetDevice(&dev));
   DeviceContext& ctx = device_context(dev);
   std::lock_guard<std::mutex> guard(ctx.mu);
+  if (ley_status ast = async_drain(ctx)) return ast;
   if (!ctx.host_pinned) LEY_CUDA("loopback", cudaHostAlloc(&ctx.host_pinned, 4096, cudaHostAllocMapped));
   const ExtDistPlan P = ext_dist_plan(std::vector<uint64_t>(n_local, n_local + G), budget);
   if (budget && ext_dist_device_bytes(P) > budget) {
@@ -1157,6 +1161,7 @@ ley_status dist_sort_loopback(int G, const void* const* in, const uint64_t* n_lo
   LEY_CUDA("loopback", cudaGetDevice(&dev));
   DeviceContext& ctx = device_context(dev);
   std::lock_guard<std::mutex> guard(ctx.mu);
+  if (ley_status ast = async_drain(ctx)) return ast;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms > 0) ctx.sms = sms;

@@ -28,7 +28,7 @@ namespace {
 // One pass of the internal sort (K-a .. K-e) ordered by the key window `key`.
 ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                      cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, KeySpec key,
-                     uint64_t* digest = nullptr) {
+                     uint64_t* digest = nullptr, bool allow_async = false) {
   const InternalLayout L = plan_internal(n);
   ley_status st;
   if (!out && !perm_out) {  // out == nullptr is the perm-only mode (K-d without the fused gather)
@@ -185,6 +185,21 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
                                                &launches, fused_tier >= 0 ? &kc : nullptr, fused_tier));
     return LEY_OK;
   };
+  auto copy_perm = [&]() -> ley_status {  // the workspace permutation to the caller's (stream-ordered)
+    if (perm_out) {
+      cudaPointerAttributes pa{};
+      LEY_CUDA("perm", cudaPointerGetAttributes(&pa, perm_out));
+      cudaMemcpyKind kind = pa.type == cudaMemoryTypeDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      LEY_CUDA("perm", cudaMemcpyAsync(perm_out, perm, 4 * n, kind, s));
+    }
+    return LEY_OK;
+  };
+  // Stream-ordered mode (option async, device pointers, keys <= 10 bytes): the host waits only for the
+  // classification's big-bucket count, published from the SM into mapped memory over a sentinel it wrote
+  // before the launch; with no big buckets it returns while the tier kernels still run.
+  constexpr uint32_t kPending = 0xFFFFFFFFu;
+  const bool async_ok = allow_async && !prof.on;
+  if (async_ok) host_cnt[0] = kPending;
   // (not while profiling: elapsed times between event-record nodes of a graph are refused, measured)
   const bool graphs = o.graphs && !prof.on && !getenv("LEY_DEBUG_SYNC");
   if (!graphs) {
@@ -195,8 +210,29 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
                        ((uint64_t)key.off << 32) | key.len, options_fingerprint(o), (uint64_t)ctx.sms}};
     if ((st = graph_run(ctx, gk, s, [&](cudaStream_t cs) { return level1(cs); }, prof))) return st;
   }
+  uint32_t nbig;
+  if (async_ok) {
+    for (uint32_t spin = 1; (nbig = host_cnt[0]) == kPending; ++spin) {
+      if (spin % 1024) continue;
+      const cudaError_t q = cudaStreamQuery(s);  // (a failed launch never publishes)
+      if (q == cudaSuccess && (nbig = host_cnt[0]) == kPending) {
+        set_error("internal: level 1 completed without publishing its big-bucket count");
+        return LEY_ERR_CUDA;
+      }
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) LEY_CUDA("K-de sort+gather", q);
+    }
+    if (!nbig) {  // done once the stream gets there
+      if ((st = copy_perm())) return st;
+      if (!ctx.async_ev) LEY_CUDA("async", cudaEventCreateWithFlags(&ctx.async_ev, cudaEventDisableTiming));
+      LEY_CUDA("async", cudaEventRecord(ctx.async_ev, s));
+      ctx.async_pending = true;
+      ctx.async_stream = s;
+      return LEY_OK;
+    }
+  }
   LEY_CUDA("K-de sort+gather", cudaStreamSynchronize(s));
-  uint32_t nbig = host_cnt[0];
+  nbig = host_cnt[0];
   if ((st = prof.end())) return st;
 
   // ---------------------------------------------------------------- recursion on big buckets
@@ -258,13 +294,7 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     if ((st = prof.end())) return st;
   }
 
-  if (perm_out) {
-    cudaPointerAttributes pa{};
-    LEY_CUDA("perm", cudaPointerGetAttributes(&pa, perm_out));
-    cudaMemcpyKind kind = pa.type == cudaMemoryTypeDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    LEY_CUDA("perm", cudaMemcpyAsync(perm_out, perm, 4 * n, kind, s));
-  }
-  return LEY_OK;
+  return copy_perm();
 }
 
 }  // namespace
@@ -308,12 +338,14 @@ ley_status window_passes(DeviceContext& ctx, uint8_t* data, uint8_t* tmp, uint64
 // are in (window 0, window 1, ..., original index) order. Passes alternate between out and a scratch
 // buffer so the last one lands in out; with perm, the passes' permutations are composed on the device.
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
-                                cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, uint32_t key_bytes) {
+                                cudaStream_t s, Profiler& prof, void* work, size_t work_bytes, uint32_t key_bytes,
+                                bool allow_async) {
   if (key_bytes < 1 || key_bytes > kRecordBytes) {
     set_error("internal: key_bytes must be in [1, 100]");
     return LEY_ERR_UNSUPPORTED;
   }
-  if (key_bytes <= kKeyBytes) return sort_pass(ctx, in, out, perm_out, n, s, prof, work, work_bytes, KeySpec{0, key_bytes});
+  if (key_bytes <= kKeyBytes)
+    return sort_pass(ctx, in, out, perm_out, n, s, prof, work, work_bytes, KeySpec{0, key_bytes}, nullptr, allow_async);
   if (!out) {
     set_error("internal: keys longer than 10 bytes need an output buffer (multi-pass)");
     return LEY_ERR_UNSUPPORTED;

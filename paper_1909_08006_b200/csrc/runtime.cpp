@@ -57,6 +57,7 @@ const OptDesc kOpts[] = {
     {"graphs", &Options::graphs, 0, 1},
     {"pdl", &Options::pdl, 0, 3},
     {"kd_claim", &Options::kd_claim, 0, 1},
+    {"async", &Options::async, 0, 1},
     {"ext_keyptr", &Options::ext_keyptr, 0, 1},
 };
 }  // namespace
@@ -337,8 +338,24 @@ ley_status ensure_buffer(DeviceBuffer& b, size_t bytes, const char* what, cudaSt
 
 uint64_t options_fingerprint(const Options& o) {
   uint64_t h = 1469598103934665603ull;
-  for (const OptDesc& d : kOpts) h = (h ^ (uint64_t)(o.*(d.field))) * 1099511628211ull;
+  for (const OptDesc& d : kOpts)
+    if (d.field != &Options::async)  // (host-side only: the captured level-1 sequence does not depend on it)
+      h = (h ^ (uint64_t)(o.*(d.field))) * 1099511628211ull;
   return h;
+}
+
+ley_status async_join(DeviceContext& c, cudaStream_t s) {
+  if (!c.async_pending) return LEY_OK;
+  c.async_pending = false;
+  if (s != c.async_stream) LEY_CUDA("async join", cudaStreamWaitEvent(s, c.async_ev, 0));
+  return LEY_OK;
+}
+
+ley_status async_drain(DeviceContext& c) {
+  if (!c.async_pending) return LEY_OK;
+  c.async_pending = false;
+  LEY_CUDA("async drain", cudaEventSynchronize(c.async_ev));
+  return LEY_OK;
 }
 
 void graphs_release(DeviceContext& c) {
@@ -419,6 +436,7 @@ void release_device(int device) {
     DeviceContext& c = *g_ctx[d];
     pipe_release(c);  // stops the streaming worker first (it takes c.mu for its sorts)
     std::lock_guard<std::mutex> g2(c.mu);
+    async_drain(c);     // (a stream-ordered sort may still use the buffers)
     graphs_release(c);  // (they hold this context's buffer and pinned-counter addresses)
     int prev = 0;
     cudaGetDevice(&prev);

@@ -61,6 +61,7 @@ struct Options {
   int64_t ws_gather_tma = 0;  // kd_ws_sort gathers by tensor copies (1) or by plain bulk copies (0)
   int64_t gather_l2_64 = 1;   // K-d CTA-tier gathers with cp.async .L2::64B (1) or without the hint (0)
   int64_t ext_keyptr = 0;  // external path: runs of (key, ordinal) tuples, records gathered from the input
+  int64_t async = 0;     // ley_sort on device pointers returns once enqueued (stream-ordered), see leyenda.h
   int64_t kd_claim = 1;  // K-d/K-e tier CTAs claim buckets dynamically (1) or stride their list (0)
   int64_t pdl = 3;      // PDL of the K-d/K-e tier kernels: 0 off, 1 wait-first, 2 overlap, 3 overlap below 1e7 records
   int64_t graphs = 1;   // replay level 1 of the internal sort from a cached CUDA graph (0: launch directly)
@@ -116,6 +117,11 @@ struct DeviceContext {
   DeviceBuffer ext;       // external path device buffers
   DeviceBuffer keypass;   // keys > 10 bytes: the other record buffer of the LSD window passes (+ perms)
   void* host_pinned = nullptr;  // small pinned host scratch (counters)
+  // a stream-ordered ley_sort (option async) may still run on async_stream when its call returns: the next
+  // user of this context's buffers orders itself after async_ev (async_join / async_drain)
+  bool async_pending = false;
+  cudaStream_t async_stream = nullptr;
+  cudaEvent_t async_ev = nullptr;
   void* host_scratch = nullptr;  // external path: pinned (mapped) host run scratch
   size_t host_scratch_cap = 0;
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // external path: H2D / D2H copy streams
@@ -225,9 +231,15 @@ int stage_times(const char** names, float* ms, int max, int* launches);
 // `work` (optional) is a caller-provided workspace of >= plan_internal(n).bytes; else ctx.work is used.
 // key_bytes (1..100): the key is record bytes [0, key_bytes) (> 10: LSD passes over 10-byte windows,
 // scratch keypass_bytes from ctx.keypass; perm-only mode (out == nullptr) needs key_bytes <= 10).
+// allow_async: with no big buckets after level 1, return without waiting for the tier kernels and set
+// ctx.async_pending (the ABI's stream-ordered mode; the caller records ctx.async_ev).
 ley_status sort_internal_device(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32_t* perm_out, uint64_t n,
                                 cudaStream_t s, Profiler& prof, void* work = nullptr, size_t work_bytes = 0,
-                                uint32_t key_bytes = 10);
+                                uint32_t key_bytes = 10, bool allow_async = false);
+// Order work on this context after a stream-ordered sort still in flight: stream s waits for it
+// (async_join) or the host does (async_drain). Call with ctx.mu held.
+ley_status async_join(DeviceContext& ctx, cudaStream_t s);
+ley_status async_drain(DeviceContext& ctx);
 uint64_t keypass_bytes(uint64_t n, uint32_t key_bytes, bool perm);
 // Streaming staged-internal sort of pinned host records (ley_sort_submit / ley_sort_drain).
 // Host path 2 (resident.cu): input staged whole on the device, sorted in perm-only mode, output gathered

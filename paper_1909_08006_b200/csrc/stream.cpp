@@ -87,7 +87,12 @@ void worker_main(DeviceContext* ctx) {
         st = LEY_ERR_CUDA;
         msg = std::string(what) + ": " + cudaGetErrorString(e);
       };
-      cudaError_t e = cudaStreamWaitEvent(P.comp, P.copied_in[s], 0);
+      cudaError_t e = cudaSuccess;
+      if (ctx->async_pending) {  // (a stream-ordered ley_sort may still use the workspace: async_join)
+        ctx->async_pending = false;
+        if (P.comp != ctx->async_stream) e = cudaStreamWaitEvent(P.comp, ctx->async_ev, 0);
+      }
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(P.comp, P.copied_in[s], 0);
       if (e == cudaSuccess && job.k >= 2) e = cudaStreamWaitEvent(P.comp, P.copied_out[s], 0);
       if (e != cudaSuccess) fail("submit sort", e);
       g_trace.mark((uint64_t)(6 * job.k + 2), P.comp);

@@ -164,6 +164,37 @@ def test_warp_tier_near_ties(pdl):
     assert_parity(recs, out, perm)
 
 
+def test_async_stream_ordered():
+    """Option async: device sorts without recursion return once enqueued. Back-to-back sorts on one stream,
+    a sort on a second stream right after (same library workspace), one that needs the byte-2 recursion
+    (falls back to waiting), a host-pointer sort and a perm sort all give the oracle's bytes."""
+    import torch
+
+    import paper_1909_08006_b200 as ley
+
+    cases = [(gen.records(n, seed=60 + i, dist=d), n) for i, (n, d) in
+             enumerate([(200_003, "uniform"), (150_001, "skewed"), (70_001, "prefix2"), (300_007, "uniform")])]
+    xs = [to_device(r) for r, _ in cases]
+    outs = [torch.empty_like(x) for x in xs]
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    with Options(**{"async": 1}):
+        for x, o, (_, n) in zip(xs[:3], outs[:3], cases[:3]):
+            ley.ley_sort(x, o, n, stream=a)
+        ley.ley_sort(xs[3], outs[3], cases[3][1], stream=b)  # other stream, same workspace
+        perm = torch.empty(cases[0][1], dtype=torch.int32, device="cuda")
+        pout = torch.empty_like(xs[0])
+        ley.ley_sort_perm(xs[0], pout, perm, cases[0][1], stream=a)
+        hin = torch.from_numpy(cases[1][0]).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        ley.ley_sort(hin, hout, cases[1][1])  # host pointers: synchronous, after the device sorts
+    torch.cuda.synchronize()
+    for (recs, _), o in zip(cases, outs):
+        exp, _ = oracle.sort(recs)
+        assert np.array_equal(o.cpu().numpy(), exp)
+    assert_parity(cases[0][0], pout.cpu().numpy(), perm.cpu().numpy().view(np.uint32))
+    assert np.array_equal(hout.numpy(), oracle.sort(cases[1][0])[0])
+
+
 def test_repeat_bit_identical():
     recs = gen.records(200_003, seed=21, dist="skewed")
     a, pa = gpu_sort(recs)
