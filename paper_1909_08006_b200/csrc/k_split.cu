@@ -40,13 +40,6 @@ struct SplitSmem {
 };
 
 // largest i in [lo, hi) with a[i] <= v (a non-decreasing, a[lo] <= v)
-__device__ __forceinline__ uint32_t search_le(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t v) {
-  while (hi - lo > 1) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] <= v) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 __device__ __forceinline__ uint64_t search_le_g(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t v) {
   while (hi - lo > 1) {
     uint64_t mid = (lo + hi) >> 1;

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(THREADS, 2) ka_tile_sort(const uint8_t* __rest
                                                          uint32_t* __restrict__ hist16, uint32_t copies, KeySpec key) {
   constexpr int T = THREADS * ITEMS;
   constexpr int WARPS = THREADS / 32;
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* s_k1 = reinterpret_cast<uint64_t*>(smem);                   // [T]
   uint32_t* s_w = reinterpret_cast<uint32_t*>(s_k1 + T);                // [T]
   uint32_t* s_wh = s_w + T;                                             // [WARPS][256]
