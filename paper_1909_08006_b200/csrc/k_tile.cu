@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* s_tmp = s_wh + WARPS * kRadix;                                      // [32]
   __shared__ __align__(8) uint64_t s_full[kRing];
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
   uint32_t* hist_copy = hist16 + (size_t)(blockIdx.x % copies) * 65536;
   uint64_t pol_ef, pol_el;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
