@@ -195,6 +195,18 @@ def test_async_stream_ordered():
     assert np.array_equal(hout.numpy(), oracle.sort(cases[1][0])[0])
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 4097, 65537])
+def test_async_small_sizes(n):
+    """Stream-ordered calls at tiny and ragged sizes (one tile, partial tiles, a single record)."""
+    import torch
+
+    recs = gen.records(n, seed=n + 3, dist="uniform")
+    with Options(**{"async": 1}):
+        out, perm = gpu_sort(recs)
+    torch.cuda.synchronize()
+    assert_parity(recs, out, perm)
+
+
 def test_repeat_bit_identical():
     recs = gen.records(200_003, seed=21, dist="skewed")
     a, pa = gpu_sort(recs)
