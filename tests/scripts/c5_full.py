@@ -6,7 +6,7 @@ sorted digest of `in` (oracle/oracle.cpp oracle_sorted_digest: the tuple sort of
 Host memory: in 60 GB + out 60 GB + the library's run scratch 60 GB (pinned) = 180 GB of the box's 196 GB;
 the scratch is released (ley_release_cache) before the oracle's 12 GB of tuples are built.
 
-usage: python tools/c5_full.py [n] [steps] [--keyptr]   -> one JSON line (profiles/r02_c5_full*.json)
+usage: python tests/scripts/c5_full.py [n] [steps] [--keyptr]   -> one JSON line (profiles/r02_c5_full*.json)
 --keyptr: the key-pointer form of the external path (option ext_keyptr): runs of 16-byte
 tuples (9.6 GB of host scratch instead of 60 GB), records gathered from the pinned input by ordinal.
 """
@@ -16,7 +16,7 @@ import subprocess
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 
 import gen

@@ -1,7 +1,7 @@
 """A/B of the streaming host sort's copy layout (option pipe_split): C2-sized pinned host in/out, 16 calls
 through ley_sort_submit, CUDA-event time per call. usage: e2e_ab.py [n] [calls]"""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import gen
 import oracle

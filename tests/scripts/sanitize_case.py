@@ -1,7 +1,7 @@
 """Small sorts covering every kernel tier, recursion, the external path, the streaming path and the dist
 loopback, each checked against the oracle — the workload for compute-sanitizer runs (one tool per run)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import gen, oracle
 import paper_1909_08006_b200 as ley

@@ -2,12 +2,12 @@
 with the CPU oracle byte for byte (records and permutation). For races the fixed test cases might miss
 (tier overlap under PDL, dynamic bucket claims, stream-ordered calls back to back).
 
-usage: python tools/stress.py [iterations] [seed]
+usage: python tests/scripts/stress.py [iterations] [seed]
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 
