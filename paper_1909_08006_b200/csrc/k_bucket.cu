@@ -167,15 +167,20 @@ __device__ void warp_bitonic_smem(uint64_t* st, uint32_t* si, uint32_t b, uint32
   }
 }
 
-template <uint32_t CAP>
+// Counting bins of a tier: 2^13 for the register-form tiers of >= 8192 records (C4's 10240 tier: 13-bit
+// digits leave sub-buckets of ~1 record instead of ~2, K-d+K-e 34.5 -> see DESIGN.md §9), 2^12 otherwise.
+template <uint32_t CAP, int THREADS>
 __host__ __device__ constexpr uint32_t kd_bins() {
-  return CAP >= 4096 ? 4096u : CAP;  // <= 2^12 counting bins
+  return (CAP / THREADS <= 16 && CAP >= 8192) ? 8192u : CAP >= 4096 ? 4096u : CAP;
 }
 template <uint32_t CAP, int THREADS>
 struct KdLayout {
-  static constexpr uint32_t BINS = kd_bins<CAP>();
+  static constexpr uint32_t BINS = kd_bins<CAP, THREADS>();
   static constexpr int WARPS = THREADS / 32;
   static constexpr bool REGS = CAP / THREADS <= 16;  // bucket held in registers (else re-read from L2)
+  // s_bigl: the sub-buckets of >= 2 records left for the warp network (<= CAP / 2 of them) in the register
+  // form; the large-CAP form also uses it as a second per-bin counter array
+  static constexpr uint32_t BIGL = REGS ? (BINS < CAP / 2 ? BINS : CAP / 2) : BINS;
   static_assert(!REGS || CAP % THREADS == 0, "the register form holds exactly CAP / THREADS items per thread");
   // [s_idx CAP x 4][s_perm CAP x 4 (REGS only)][reusable: s_tail CAP x 8 | s_cnt | s_bigl | s_tmp][stage]
   static constexpr size_t kIdx = 0;
@@ -183,7 +188,7 @@ struct KdLayout {
   static constexpr size_t kTail = kPerm + (REGS ? (size_t)CAP * 4 : 0);
   static constexpr size_t kCnt = kTail + (size_t)CAP * 8;
   static constexpr size_t kBigl = kCnt + (size_t)(BINS + 1) * 4;
-  static constexpr size_t kTmp = kBigl + (size_t)BINS * 4;
+  static constexpr size_t kTmp = kBigl + (size_t)BIGL * 4;
   static constexpr size_t kReuseEnd = kTmp + 64 * 4;
   // gather staging: every warp gets kGatherStages groups, overlapping the sort area (free once the bucket
   // is sorted) and extending past it where the sort area is smaller
