@@ -5,7 +5,7 @@
 // are finished by one worker each — SingleThreadRadixSort on the next radix, then ComparisonSort for
 // buckets under tinyBucketThreshold ("size is small enough for comparison-based sort to perform
 // more efficient than Radix Sort"). On the GPU a "worker" is a warp (tiny buckets, register bitonic
-// network over the composite (tail, ordinal)) or a CTA (shared-memory counting pass on the next 1..12
+// network over the composite (tail, ordinal)) or a CTA (shared-memory counting pass on the next 1..13
 // unconsumed bits of the composite key, then an exact rank inside every tiny sub-bucket, or a warp
 // bitonic network for larger ones). SURVEY.md §8a row a5.
 //
@@ -168,7 +168,7 @@ __device__ void warp_bitonic_smem(uint64_t* st, uint32_t* si, uint32_t b, uint32
 }
 
 // Counting bins of a tier: 2^13 for the register-form tiers of >= 8192 records (C4's 10240 tier: 13-bit
-// digits leave sub-buckets of ~1 record instead of ~2, K-d+K-e 34.5 -> see DESIGN.md §9), 2^12 otherwise.
+// digits leave sub-buckets of ~1 record instead of ~2: C4 K-d+K-e -1 ms), 2^12 otherwise.
 template <uint32_t CAP, int THREADS>
 __host__ __device__ constexpr uint32_t kd_bins() {
   return (CAP / THREADS <= 16 && CAP >= 8192) ? 8192u : CAP >= 4096 ? 4096u : CAP;
