@@ -200,8 +200,8 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *   "smem_tier_max"  K-d: buckets up to this size are sorted in shared memory; larger ones recurse
  *                    on the next key byte (Alg. 1 bigBucketThreshold) (0..16384, default 16384)
  *   "kd_digit_bits"  K-d: max width of the in-CTA counting digit; 0 = pure comparison sort of each
- *                    bucket (Alg. 1 ComparisonSort); 13 applies to the 8192/10240 tiers, the
- *                    others use at most 12                                          (0..13, default 13)
+ *                    bucket (Alg. 1 ComparisonSort); 13-14 apply to the 8192/10240 tiers, the
+ *                    others use at most 12                                          (0..14, default 14)
  *   "kd_insert_max"  K-d: sub-buckets up to this size use per-thread insertion sort, larger ones a
  *                    warp bitonic network (tinyBucketThreshold)       (1..64, default 16)
  *   "kd_ws"          1 = warp-specialised K-d+K-e for 513..2048-record buckets (sort warps feed gather

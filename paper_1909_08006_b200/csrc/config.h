@@ -47,7 +47,7 @@ constexpr uint32_t kScanTile = kScanThreads * kScanItems;
 // K-d tiers (Algorithm 1: bigBucketThreshold / tinyBucketThreshold).
 constexpr uint32_t kWarpTierMax = 32;
 constexpr uint32_t kSmemTierMax = 16384;
-constexpr int kKdMaxBits = 13;
+constexpr int kKdMaxBits = 14;
 constexpr int kNumKdListsHost = 6;  // = kNumKdLists (common.cuh): K-d work-list tiers, for host planning
 
 // multi-GPU: at most 8 ranks (one 8 x B200 box; BASELINE.json configs)

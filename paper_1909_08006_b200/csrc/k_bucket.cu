@@ -167,11 +167,12 @@ __device__ void warp_bitonic_smem(uint64_t* st, uint32_t* si, uint32_t b, uint32
   }
 }
 
-// Counting bins of a tier: 2^13 for the register-form tiers of >= 8192 records (C4's 10240 tier: 13-bit
-// digits leave sub-buckets of ~1 record instead of ~2: C4 K-d+K-e -1 ms), 2^12 otherwise.
+// Counting bins of a tier: 2^14 for the register-form tiers of >= 8192 records, as two 16-bit counters
+// per shared-memory word (C4's 10240 tier: sub-buckets of ~0.6 records; 13 bits gave C4 K-d+K-e -1 ms
+// over 12), 2^12 otherwise.
 template <uint32_t CAP, int THREADS>
 __host__ __device__ constexpr uint32_t kd_bins() {
-  return (CAP / THREADS <= 16 && CAP >= 8192) ? 8192u : CAP >= 4096 ? 4096u : CAP;
+  return (CAP / THREADS <= 16 && CAP >= 8192) ? 16384u : CAP >= 4096 ? 4096u : CAP;
 }
 template <uint32_t CAP, int THREADS>
 struct KdLayout {
@@ -181,13 +182,17 @@ struct KdLayout {
   // s_bigl: the sub-buckets of >= 2 records left for the warp network (<= CAP / 2 of them) in the register
   // form; the large-CAP form also uses it as a second per-bin counter array
   static constexpr uint32_t BIGL = REGS ? (BINS < CAP / 2 ? BINS : CAP / 2) : BINS;
+  // counters packed two per 32-bit word (16 bits hold any count or start of a bucket of <= CAP < 2^16)
+  static constexpr bool PACKED = REGS && BINS > 8192;
+  static_assert(!PACKED || CAP < 65536, "16-bit counters");
+  static constexpr uint32_t CNT_WORDS = PACKED ? BINS / 2 + 1 : BINS + 1;
   static_assert(!REGS || CAP % THREADS == 0, "the register form holds exactly CAP / THREADS items per thread");
   // [s_idx CAP x 4][s_perm CAP x 4 (REGS only)][reusable: s_tail CAP x 8 | s_cnt | s_bigl | s_tmp][stage]
   static constexpr size_t kIdx = 0;
   static constexpr size_t kPerm = kIdx + (size_t)CAP * 4;
   static constexpr size_t kTail = kPerm + (REGS ? (size_t)CAP * 4 : 0);
   static constexpr size_t kCnt = kTail + (size_t)CAP * 8;
-  static constexpr size_t kBigl = kCnt + (size_t)(BINS + 1) * 4;
+  static constexpr size_t kBigl = kCnt + (size_t)CNT_WORDS * 4;
   static constexpr size_t kTmp = kBigl + (size_t)BIGL * 4;
   static constexpr size_t kReuseEnd = kTmp + 64 * 4;
   // gather staging: every warp gets kGatherStages groups, overlapping the sort area (free once the bucket
@@ -225,12 +230,17 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
   constexpr int WARPS = L::WARPS;
   constexpr int ITEMS = CAP / THREADS;
   constexpr bool REGS = L::REGS;
+  constexpr bool PACKED = L::PACKED;
   constexpr int RITEMS = REGS ? ITEMS : 1;
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem + L::kIdx);
   uint32_t* s_perm = REGS ? reinterpret_cast<uint32_t*>(smem + L::kPerm) : s_idx;  // sorted ordinals
   uint64_t* s_tail = reinterpret_cast<uint64_t*>(smem + L::kTail);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L::kCnt);    // [BINS + 1]: counts, then starts
+  auto cnt_get = [&](uint32_t g) -> uint32_t {                       // (PACKED: 16-bit halves)
+    if constexpr (PACKED) return (s_cnt[g >> 1] >> (16u * (g & 1u))) & 0xFFFFu;
+    else return s_cnt[g];
+  };
   uint32_t* s_bigl = reinterpret_cast<uint32_t*>(smem + L::kBigl);  // [BINS]: sub-buckets for the network
   uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem + L::kTmp);    // [32] scan tmp, [32] = #big
   uint32_t* s_nbig = s_tmp + 32;
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       if (it >= nitems) break;
       sg = list[it];
     }
-    for (uint32_t g = threadIdx.x; g <= BINS; g += THREADS) s_cnt[g] = 0;  // was gather staging
+    for (uint32_t g = threadIdx.x; g < L::CNT_WORDS; g += THREADS) s_cnt[g] = 0;  // was gather staging
     __syncthreads();
     const uint32_t s = sg.len;
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
@@ -324,7 +334,15 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
+        if (i < s) {
+          const uint32_t d = digit2(tr[j], xr[j]);
+          if constexpr (PACKED) {
+            const uint32_t sh = 16u * (d & 1u);
+            rr[j] = (atomicAdd(&s_cnt[d >> 1], 1u << sh) >> sh) & 0xFFFFu;
+          } else {
+            rr[j] = atomicAdd(&s_cnt[d], 1u);
+          }
+        }
       }
     } else {
       // batches of 8 independent loads per thread keep the bucket read latency-tolerant
@@ -345,7 +363,26 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     if (threadIdx.x == 0) *s_nbig = 0;
     __syncthreads();
     // exclusive scan of the nb counters in place (contiguous slice per thread)
-    {
+    if constexpr (PACKED) {  // slices of whole words (two counters each; an odd nb leaves a zero high half)
+      const uint32_t nw = (nb + 1) >> 1;
+      const uint32_t per = (nw + THREADS - 1) / THREADS;
+      const uint32_t w0 = threadIdx.x * per;
+      const uint32_t w1 = min(nw, w0 + per);
+      uint32_t sum = 0;
+      for (uint32_t w = w0; w < w1; ++w) sum += (s_cnt[w] & 0xFFFFu) + (s_cnt[w] >> 16);
+      uint32_t run = block_excl_scan<THREADS>(sum, s_tmp, nullptr);
+      for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t c = s_cnt[w];
+        const uint32_t lo = run;
+        run += c & 0xFFFFu;
+        s_cnt[w] = lo | (run << 16);
+        run += c >> 16;
+      }
+      if (threadIdx.x == 0) {  // the sentinel start of bin nb (word nb/2 is no thread's slice unless nb = 1)
+        const uint32_t w = nb >> 1, sh = 16u * (nb & 1u);
+        s_cnt[w] = (s_cnt[w] & ~(0xFFFFu << sh)) | (s << sh);
+      }
+    } else {
       const uint32_t per = (nb + THREADS - 1) / THREADS;
       const uint32_t g0 = threadIdx.x * per;
       const uint32_t g1 = min(nb, g0 + per);
@@ -367,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       for (int j = 0; j < RITEMS; ++j) {
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
-          const uint32_t b = s_cnt[digit2(tr[j], xr[j])];
+          const uint32_t b = cnt_get(digit2(tr[j], xr[j]));
           s_tail[b + rr[j]] = tr[j];
           s_idx[b + rr[j]] = xr[j];
         }
@@ -378,7 +415,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
         uint32_t i = j * THREADS + threadIdx.x;
         if (i < s) {
           const uint32_t d = digit2(tr[j], xr[j]);
-          const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
+          const uint32_t b = cnt_get(d), sz = cnt_get(d + 1) - b;
           if (sz == 1) {
             s_perm[b] = xr[j];
           } else if (sz <= (uint32_t)tu.kd_insert_max) {
@@ -396,7 +433,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       const uint32_t nbig = *s_nbig;
       for (uint32_t q = warp; q < nbig; q += WARPS) {
         const uint32_t g = s_bigl[q];
-        const uint32_t b = s_cnt[g], e = s_cnt[g + 1];
+        const uint32_t b = cnt_get(g), e = cnt_get(g + 1);
         warp_bitonic_smem(s_tail, s_idx, b, e);
         for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) s_perm[i] = s_idx[i];
       }

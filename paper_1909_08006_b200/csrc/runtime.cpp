@@ -34,7 +34,7 @@ struct OptDesc {
 const OptDesc kOpts[] = {
     {"warp_tier_max", &Options::warp_tier_max, 1, 32},
     {"smem_tier_max", &Options::smem_tier_max, 0, 16384},
-    {"kd_digit_bits", &Options::kd_digit_bits, 0, 13},
+    {"kd_digit_bits", &Options::kd_digit_bits, 0, 14},
     {"kd_insert_max", &Options::kd_insert_max, 1, 64},
     {"kd_ws", &Options::kd_ws, 0, 1},
     {"ka_stream", &Options::ka_stream, 0, 2},

@@ -42,7 +42,7 @@ struct Status {
 struct Options {
   int64_t warp_tier_max = 32;
   int64_t smem_tier_max = 16384;
-  int64_t kd_digit_bits = 13;
+  int64_t kd_digit_bits = 14;
   int64_t kd_insert_max = 16;
   int64_t kd_ws = 1;
   int64_t ka_stream = 1;
