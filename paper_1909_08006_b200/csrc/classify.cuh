@@ -47,4 +47,32 @@ __device__ __forceinline__ void classify_block(const Seg& s, bool valid, const T
   }
 }
 
+// Level-1 classification (run by extra CTAs of the K-c plan launch, k_split.cu): bucket p = key bytes
+// 0..1 is Seg{B16[p], hist16[p], depth 2, buffer B}; 256 CTAs x 256 buckets. The last CTA to finish
+// publishes the big-bucket count into mapped host memory (the host polls it; no separate publish launch).
+struct ClassifyJob {
+  Tunables tu;
+  ListSet kd;
+  const uint32_t* hist16;
+  const uint32_t* B16;
+  Seg* big_out;
+  uint32_t* big_count;
+  uint32_t* done;         // CTA-done counter (zeroed with the level-1 counters)
+  uint32_t* host_mapped;  // device alias of the mapped pinned word the host polls
+};
+constexpr uint32_t kClassifyBlocks = 256;  // x 256 threads = 65536 buckets
+
+__device__ __forceinline__ void classify_level1_block(const ClassifyJob& cj, uint32_t blk, uint32_t* s_cnt) {
+  const uint32_t p = blk * 256 + threadIdx.x;
+  const Seg s{cj.B16[p], cj.hist16[p], 2u, 1u};
+  classify_block(s, true, cj.tu, cj.kd, cj.big_out, cj.big_count, s_cnt);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(cj.done, 1u) == kClassifyBlocks - 1) {
+      __threadfence();
+      *reinterpret_cast<volatile uint32_t*>(cj.host_mapped) = *reinterpret_cast<volatile uint32_t*>(cj.big_count);
+    }
+  }
+}
+
 }  // namespace ley

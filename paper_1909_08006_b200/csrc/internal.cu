@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "classify.cuh"
 #include "kc_chunk.cuh"
 #include "kernels.cuh"
 #include "runtime.h"
@@ -122,9 +123,10 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     // ---------------------------------------------------------------- K-b
     if ((st = prof.begin("K-b scan"))) return st;
     // (the hist16 copies are summed by the scan itself, which writes the sum back over copy 0)
+    // (the hist16 blocks also write the split's fill cursors = B16)
     LEY_CUDA("K-b scan", launch_scan_excl2(cnt, off, L.m, scan_status, off + L.m, hist16, B16, 65536,
                                            scan_status + L.scan_status_words, B16 + 65536, L.hist_copies, 65536,
-                                           tickets + 0, s));
+                                           tickets + 0, s, cursor));
     ++launches;
     if ((st = prof.end())) return st;
 
@@ -145,22 +147,29 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
                                                                                                      : kListMed5;
       if (t >= kListMed2 && t < kNumKdLists) fused_tier = t;
     }
+    // (the plan launch also classifies the level-1 buckets: Alg. 1's queues, classify.cuh)
+    ClassifyJob cj{};
+    cj.tu = tu;
+    cj.kd = kd;
+    cj.hist16 = hist16;
+    cj.B16 = B16;
+    cj.big_out = static_cast<Seg*>(ctx.big[0].ptr);
+    cj.big_count = big_count;
+    cj.done = small + 33;
+    cj.host_mapped = host_cnt_dev;
     const uint32_t* order_used = nullptr;
     if ((st = prof.begin(fused_tier >= 0 ? "K-c plan" : "K-c split"))) return st;
     LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
                                                  reinterpret_cast<uint4*>(base + L.off_plan_a),
                                                  reinterpret_cast<uint2*>(base + L.off_plan_b),
                                                  reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
-                                                 tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, fused_tier < 0,
-                                                 &order_used));
-    launches += (fused_tier < 0 ? 2 : 1) + (order_used ? 1 : 0);  // plan (+ chunk order) (+ split)
+                                                 tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, cj,
+                                                 fused_tier < 0, &order_used));
+    launches += fused_tier < 0 ? 2 : 1;  // plan (+ split)
     if ((st = prof.end())) return st;
 
     // ---------------------------------------------------------------- classify level 1, K-d
     if ((st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
-    LEY_CUDA("classify", launch_kd_classify_level1(hist16, B16, tu, kd, static_cast<Seg*>(ctx.big[0].ptr), big_count,
-                                                   small + 33, host_cnt_dev, s));
-    ++launches;
     KcArgs kc;
     if (fused_tier >= 0) {
       kc.k1_in = At;

@@ -109,24 +109,6 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
 
 constexpr int kGatherStages = 1;  // groups in flight per gathering warp
 
-// (the last CTA to finish also publishes the big-bucket count to the host-mapped word: the host reads it
-// after the level's final synchronisation, so no separate publish launch)
-__global__ void kd_classify_level1(const uint32_t* __restrict__ hist16, const uint32_t* __restrict__ B16,
-                                   Tunables tu, ListSet kd, Seg* __restrict__ big_out, uint32_t* __restrict__ big_count,
-                                   uint32_t* __restrict__ done, volatile uint32_t* host_mapped_dev) {
-  __shared__ uint32_t s_cnt[16];
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers exactly 65536 buckets
-  const Seg s{B16[p], hist16[p], 2u, 1u};
-  classify_block(s, true, tu, kd, big_out, big_count, s_cnt);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(done, 1u) == gridDim.x - 1) {
-      __threadfence();
-      *host_mapped_dev = *reinterpret_cast<volatile uint32_t*>(big_count);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------- CTA tier
 // In-smem all-ascending bitonic network over [b, e) by one warp; virtual +inf padding beyond e never
 // moves, so compare-exchanges touching it are skipped.
@@ -1068,13 +1050,6 @@ cudaError_t launch_ws_sort(const Seg* list, const uint32_t* count, const uint64_
 }
 
 }  // namespace
-
-cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
-                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, uint32_t* done,
-                                      uint32_t* host_mapped_dev, cudaStream_t s) {
-  kd_classify_level1<<<256, 256, 0, s>>>(hist16, B16, tu, kd, big_out, big_count, done, host_mapped_dev);
-  return cudaGetLastError();
-}
 
 namespace {
 // All K-d/K-e tiers for the lists of one level (counts are read on the device; no host sync).

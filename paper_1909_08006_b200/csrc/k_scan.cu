@@ -27,6 +27,7 @@ struct ScanJob {
   uint32_t copies = 1;     // in = `copies` arrays `stride` words apart: the scan is over their sum ...
   uint64_t stride = 0;
   uint32_t* sum_out = nullptr;  // ... written back here (copy 0; level-1 hist16), if given
+  uint32_t* out2 = nullptr;     // a second copy of the exclusive prefix (level 1: the split's fill cursors)
 };
 
 // Exclusive prefix of block blk's predecessors by warp 0: a window of 32 predecessor status words per
@@ -132,6 +133,22 @@ __device__ __forceinline__ void scan_block(const ScanJob& jb, uint32_t blk, uint
       run += v[i];
     }
   }
+  if (jb.out2) {  // (same layout and alignment as out: 65536 words)
+    uint32_t r = *s_prefix + texcl;
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      uint4 x;
+      x.x = r;
+      r += v[4 * q];
+      x.y = r;
+      r += v[4 * q + 1];
+      x.z = r;
+      r += v[4 * q + 2];
+      x.w = r;
+      r += v[4 * q + 3];
+      reinterpret_cast<uint4*>(jb.out2 + base)[q] = x;
+    }
+  }
 }
 
 // Two independent scans in one launch: tickets [0, blocks_a) scan job a, the rest job b (claimed in
@@ -195,10 +212,10 @@ cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint
 cudaError_t launch_scan_excl2(const uint32_t* in_a, uint32_t* out_a, uint64_t m_a, uint64_t* status_a,
                               uint32_t* total_a, uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
                               uint64_t* status_b, uint32_t* total_b, uint32_t copies_b, uint64_t stride_b,
-                              uint32_t* ticket, cudaStream_t s) {
+                              uint32_t* ticket, cudaStream_t s, uint32_t* out2_b) {
   const uint64_t ba = (m_a + kScanTile - 1) / kScanTile, bb = (m_b + kScanTile - 1) / kScanTile;
   if (ba + bb == 0) return cudaSuccess;
-  ScanJob jb{in_b, out_b, m_b, status_b, total_b, copies_b, stride_b, copies_b > 1 ? in_b : nullptr};
+  ScanJob jb{in_b, out_b, m_b, status_b, total_b, copies_b, stride_b, copies_b > 1 ? in_b : nullptr, out2_b};
   kb_scan_excl<<<(unsigned)(ba + bb), kScanThreads, 0, s>>>(ScanJob{in_a, out_a, m_a, status_a, total_a}, (uint32_t)ba,
                                                             jb, ticket);
   return cudaGetLastError();

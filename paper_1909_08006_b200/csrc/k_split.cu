@@ -81,14 +81,20 @@ __device__ __forceinline__ uint64_t search_le_guess(const uint32_t* a, uint64_t 
 // tile range [t0, t1] whose byte-0 runs cover it, and the segment's first chunk k0. Parallel searches
 // here keep them off the K-c critical path. Every CTA first derives the chunk starts itself (byte-0
 // segment b = [B16[256 b], B16[256 (b+1)]) is cut into ceil(len / kChunk) chunks; cstart = exclusive
-// scan of the chunk counts; CTA 0 publishes them), and the launch also initialises the split's write
-// cursors (cursor = B16) with its spare threads. 256 threads per CTA.
+// scan of the chunk counts; CTA 0 publishes them). With `order` non-null it also writes the chunks'
+// processing order (kOrderGroup, below). (The split's fill cursors = B16 are written by the K-b scan.)
+// 256 threads per CTA.
+constexpr int kOrderGroup = 4;
 __global__ void __launch_bounds__(256)
     kc_plan_level1(const uint32_t* __restrict__ off, uint32_t tiles, const uint32_t* __restrict__ B16, uint64_t n,
                    uint32_t* __restrict__ cstart, uint32_t grid_ub, uint4* __restrict__ plan_a,
-                   uint2* __restrict__ plan_b, uint32_t* __restrict__ cursor) {
+                   uint2* __restrict__ plan_b, uint32_t* __restrict__ order, const ClassifyJob cj, uint32_t pblocks) {
   __shared__ uint32_t s_cst[257];
   __shared__ uint32_t s_tmp[32];
+  if (blockIdx.x >= pblocks) {  // the classification CTAs (they run beside the planning ones)
+    classify_level1_block(cj, blockIdx.x - pblocks, s_tmp);
+    return;
+  }
   {
     const uint32_t b = threadIdx.x;
     const uint64_t beg = B16[b * 256], end = (b < 255) ? B16[(b + 1) * 256] : n;
@@ -102,9 +108,7 @@ __global__ void __launch_bounds__(256)
       if (b == 0) cstart[256] = total;
     }
   }
-  const uint32_t nth = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 65536 / 4; i += nth)
-    reinterpret_cast<uint4*>(cursor)[i] = reinterpret_cast<const uint4*>(B16)[i];
+  const uint32_t nth = pblocks * blockDim.x;
   __syncthreads();
   const uint32_t kend = min(s_cst[256], grid_ub);
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += nth) {
@@ -126,31 +130,26 @@ __global__ void __launch_bounds__(256)
         (uint32_t)search_le_guess(off_b, 0, tiles, v0 + cnt - 1, (uint64_t)(v0 + cnt - 1 - seg_beg) * tiles / len);
     plan_a[k] = make_uint4(b, v0, cnt, k - c);
     plan_b[k] = make_uint2(t0, t1);
+    if (order) {  // position of chunk c of bucket j of its group in the interleaved order
+      const uint32_t g0 = b & ~(uint32_t)(kOrderGroup - 1), j = b - g0;
+      uint32_t pos = s_cst[g0];
+#pragma unroll
+      for (uint32_t q = 0; q < (uint32_t)kOrderGroup; ++q) {
+        const uint32_t nq = s_cst[g0 + q + 1] - s_cst[g0 + q];
+        pos += min(c, nq) + (q < j && nq > c ? 1u : 0u);
+      }
+      order[pos] = k;
+    }
   }
 }
 
-// Processing order of the level-1 chunks: bucket-major, but the chunks of 4 neighbouring byte-0 buckets
-// interleaved (chunk c of buckets 4g..4g+3, then chunk c+1, ...). A tile's runs of neighbouring buckets
-// share their boundary lines; interleaving reads both sides of most boundaries while the line is still in
-// L2 once K-a's output outgrows the L2 (C4: a boundary line would otherwise be fetched twice, ~1/256 of
-// the pass apart), and keeps the writes to 1024 active 16-bit buckets. One thread per group of 4.
-constexpr int kOrderGroup = 4;
+// Processing order of the level-1 chunks (written by kc_plan_level1): bucket-major, but the chunks of
+// kOrderGroup = 4 neighbouring byte-0 buckets interleaved (chunk c of buckets 4g..4g+3, then chunk c+1,
+// ...). A tile's runs of neighbouring buckets share their boundary lines; interleaving reads both sides of
+// most boundaries while the line is still in L2 once K-a's output outgrows the L2 (C4: a boundary line
+// would otherwise be fetched twice, ~1/256 of the pass apart), and keeps the writes to 1024 active 16-bit
+// buckets.
 constexpr uint64_t kInterleaveMinRecords = 300000000;
-__global__ void kc_order_chunks(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ order) {
-  const uint32_t g = threadIdx.x;  // 64 threads
-  const uint32_t b0 = g * kOrderGroup;
-  uint32_t nc[kOrderGroup], mx = 0;
-#pragma unroll
-  for (int j = 0; j < kOrderGroup; ++j) {
-    nc[j] = cstart[b0 + j + 1] - cstart[b0 + j];
-    mx = max(mx, nc[j]);
-  }
-  uint32_t pos = cstart[b0];
-  for (uint32_t c = 0; c < mx; ++c)
-#pragma unroll
-    for (int j = 0; j < kOrderGroup; ++j)
-      if (c < nc[j]) order[pos++] = cstart[b0 + j] + c;
-}
 
 constexpr uint32_t kMaxRuns = (uint32_t)((kChunk * 13 + 16) / 8);  // run table fits the staging region
 
@@ -529,19 +528,15 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
-                                   bool run_split, const uint32_t** order_used) {
-  const uint32_t pblocks = std::max<uint32_t>((grid_ub + 255) / 256, 16);  // (>= 16: the cursor copy)
-  kc_plan_level1<<<pblocks, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b, cursor);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+                                   const ClassifyJob& cls, bool run_split, const uint32_t** order_used) {
   // the interleaved order pays only once K-a's output is many times the L2 (C4: 30.6 -> ~18 B/pair of
   // reads, K-c 6.7 -> 6.1 ms); below that the plain bucket-major order is as fast or faster (C3 skew)
-  if (n < kInterleaveMinRecords) {
-    order = nullptr;
-  } else {
-    kc_order_chunks<<<1, kRadix / kOrderGroup, 0, s>>>(cstart, order);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
+  if (n < kInterleaveMinRecords) order = nullptr;
+  const uint32_t pblocks = std::max<uint32_t>((grid_ub + 255) / 256, 1);
+  kc_plan_level1<<<pblocks + kClassifyBlocks, 256, 0, s>>>(off, tiles, B16, n, cstart, grid_ub, plan_a, plan_b, order,
+                                                            cls, pblocks);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   if (order_used) *order_used = order;
   if (!run_split) return cudaSuccess;  // (the fused K-d+K-e kernel runs the chunks: kc_chunk.cuh)
   size_t smem = SplitSmem::kBytes;

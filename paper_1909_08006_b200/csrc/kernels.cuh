@@ -49,11 +49,11 @@ cudaError_t launch_ka_tile_sort(const uint8_t* in, uint64_t n, uint32_t tiles, u
 // K-b (k_scan.cu)
 // (two independent exclusive scans in one launch; one ticket word)
 // (job b's input may be `copies_b` histogram copies `stride_b` words apart: it scans their sum and writes
-// the sum back over copy 0)
+// the sum back over copy 0; out2_b: a second copy of its prefix)
 cudaError_t launch_scan_excl2(const uint32_t* in_a, uint32_t* out_a, uint64_t m_a, uint64_t* status_a,
                               uint32_t* total_a, uint32_t* in_b, uint32_t* out_b, uint64_t m_b,
                               uint64_t* status_b, uint32_t* total_b, uint32_t copies_b, uint64_t stride_b,
-                              uint32_t* ticket, cudaStream_t s);
+                              uint32_t* ticket, cudaStream_t s, uint32_t* out2_b = nullptr);
 cudaError_t launch_scan_excl(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* status, uint32_t* ticket,
                              uint32_t* total_out, cudaStream_t s);
 uint64_t scan_status_words(uint64_t m);
@@ -61,13 +61,15 @@ cudaError_t launch_zero3(void* a, uint64_t a_bytes, void* b, uint64_t b_bytes, v
                          cudaStream_t s);
 cudaError_t launch_publish_u32(const uint32_t* src, uint32_t* host_mapped_dev, cudaStream_t s);
 
-// K-c / K-c' (k_split.cu)
+// K-c / K-c' (k_split.cu). The level-1 plan launch also classifies the level-1 buckets (classify.cuh).
+struct ClassifyJob;
 size_t split_smem_bytes();
 cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, uint32_t tiles, const uint32_t* off,
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
-                                   bool run_split = true, const uint32_t** order_used = nullptr);
+                                   const ClassifyJob& cls, bool run_split = true,
+                                   const uint32_t** order_used = nullptr);
 cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
 cudaError_t launch_kr_chunk_map(const uint32_t* cstart, uint32_t nseg, uint32_t ub, uint2* map, cudaStream_t s);
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,
@@ -81,9 +83,6 @@ cudaError_t launch_kr_split(const Seg* segs, uint32_t nseg, const uint32_t* csta
                             uint32_t* idx1, uint32_t* ticket, const uint2* map, uint32_t grid_ub, cudaStream_t s);
 
 // K-d (k_bucket.cu)
-cudaError_t launch_kd_classify_level1(const uint32_t* hist16, const uint32_t* B16, const Tunables& tu,
-                                      const ListSet& kd, Seg* big_out, uint32_t* big_count, uint32_t* done,
-                                      uint32_t* host_mapped_dev, cudaStream_t s);
 // K-d + K-e fused: sorts every listed bucket and gathers its records into out (perm written if non-null;
 // out == nullptr: perm-only, no gather; dg non-null: dg[j] = digest of output record j's 10-byte prefix).
 // in holds n_in records; no gather reads outside them. Level 1 only: with kc and a fused_tier in
