@@ -261,6 +261,10 @@ ley_status ley_plan_query(uint64_t n_records, uint64_t device_budget_bytes, ley_
  *   "kc_fuse"        level-1 K-c split inside the K-d+K-e kernel of one tier: 0 (default) = its own kernel,
  *                    1 = the tier of the average 16-bit bucket, 2..5 = the 2048 / 8192 / 10240 / 16384
  *                    tier (tests); same bytes, measured slower
+ *   "kc_corun"       level-1 K-c kernel narrowed to this many CTAs per SM (1..3) with the warp-specialised
+ *                    2048 tier launched beside it (PDL), each bucket sorted once its byte-0 bucket is split;
+ *                    applies when the average 16-bit bucket falls in that tier (C2) and kc_fuse is 0, or
+ *                    whenever kc_fuse is 2 (tests); 0 = off
  * Returns LEY_ERR_INVALID_ARGUMENT for an unknown name or out-of-range value. */
 ley_status ley_set_option(const char* name, int64_t value);
 ley_status ley_get_option(const char* name, int64_t* value);

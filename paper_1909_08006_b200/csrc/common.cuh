@@ -47,6 +47,7 @@ struct Tunables {
   int ws_tma = 0;  // kd_ws_sort: record windows by TMA tensor copies (64-B L2 fetches) or plain bulk copies
   int gather_l2_64 = 1;  // kd_cta_sort gathers: cp.async with .L2::64B (1) or without the hint (0)
   int kd_claim = 1;      // tier CTAs claim buckets by atomic ticket (1) or stride the list statically (0)
+  int kc_corun = 0;      // the fused tier runs beside the level-1 K-c kernel (PDL, no entry wait; internal.cu)
   int pdl = 0;           // K-d/K-e tier kernels launched with programmatic dependent launch (launch_k): 0
                          // plain stream order; 1 every tier waits, then lets the next launch; 2 the first
                          // tier waits, later ones launch at once and wait only before exiting (overlap)

@@ -147,6 +147,20 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
                                                                                                      : kListMed5;
       if (t >= kListMed2 && t < kNumKdLists) fused_tier = t;
     }
+    // Co-run form (option kc_corun = K-c CTAs per SM): the split keeps its own persistent kernel, narrowed to
+    // leave room on every SM for a warp-specialised 2048-tier CTA, and that tier (the fused form: buckets
+    // claimed in ascending order, each sorted once done[] shows its byte-0 bucket split) is PDL-launched
+    // beside it, so the issue-bound split overlaps the DRAM-bound gather. Only where the average bucket
+    // falls in that tier (whose CTAs fit beside a split CTA; C2), or with kc_fuse = 2 (forced: tests).
+    bool corun = false;
+    if (o.kc_corun && (!o.kc_fuse || o.kc_fuse == 2) && out && tu.kd_ws) {
+      const uint64_t avg = n / 65536;
+      if (o.kc_fuse == 2 || (avg > 512 && avg <= 2048 && avg > tu.warp_tier_max && 2048 <= tu.smem_tier_max)) {
+        fused_tier = kListMed2;
+        corun = true;
+        tu.kc_corun = 1;
+      }
+    }
     // (the plan launch also classifies the level-1 buckets: Alg. 1's queues, classify.cuh)
     ClassifyJob cj{};
     cj.tu = tu;
@@ -158,18 +172,20 @@ ley_status sort_pass(DeviceContext& ctx, const uint8_t* in, uint8_t* out, uint32
     cj.done = small + 33;
     cj.host_mapped = host_cnt_dev;
     const uint32_t* order_used = nullptr;
-    if ((st = prof.begin(fused_tier >= 0 ? "K-c plan" : "K-c split"))) return st;
+    if ((st = prof.begin(corun ? "K-c+K-de co-run" : fused_tier >= 0 ? "K-c plan" : "K-c split"))) return st;
     LEY_CUDA("K-c split", launch_kc_split_level1(At, Ai, tiles, off, lo, B16, n, cstart,
                                                  reinterpret_cast<uint4*>(base + L.off_plan_a),
                                                  reinterpret_cast<uint2*>(base + L.off_plan_b),
                                                  reinterpret_cast<uint32_t*>(base + L.off_order), cursor,
                                                  tickets + 2, Bt, Bi, (uint32_t)L.split_chunks_ub, s, cj,
-                                                 fused_tier < 0, &order_used));
-    launches += fused_tier < 0 ? 2 : 1;  // plan (+ split)
-    if ((st = prof.end())) return st;
+                                                 fused_tier < 0 || corun, &order_used, corun ? small + 64 : nullptr,
+                                                 corun ? (int)o.kc_corun : 0));
+    launches += fused_tier < 0 || corun ? 2 : 1;  // plan (+ split)
+    // (co-run: no stage boundary between the split and the tier kernel, whose launch must follow it directly)
+    if (!corun && (st = prof.end())) return st;
 
     // ---------------------------------------------------------------- classify level 1, K-d
-    if ((st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
+    if (!corun && (st = prof.begin(fused_tier >= 0 ? "K-c+K-de fused" : "K-de sort+gather"))) return st;
     KcArgs kc;
     if (fused_tier >= 0) {
       kc.k1_in = At;

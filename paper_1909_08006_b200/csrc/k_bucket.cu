@@ -837,9 +837,9 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
           const bool ready = s_claim[1] != 0;
           nbar_sync(kBarSort, ST);
           if (ready) break;
-          const uint32_t c = claim_chunk();
+          const uint32_t c = tu.kc_corun ? ~0u : claim_chunk();  // (co-run: the split kernel runs them all)
           if (c != ~0u) kc_chunk<ST, (kChunk + ST - 1) / ST, Group>(kc, c, smem);
-          else __nanosleep(1000);  // the remaining chunks are being split by running CTAs
+          else __nanosleep(tu.kc_corun ? 256 : 1000);  // the remaining chunks are being split by running CTAs
         }
         sg = Seg{kc.B16[p], kc.hist16[p], 2u, 1u};
       } else {  // (dynamic claims one bucket ahead, or static, as in kd_cta_sort)
@@ -951,7 +951,8 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       nbar_arrive(kBarFull + q, NT);  // bucket k is in slot q
     }
     if constexpr (FUSED) {  // the split's remaining chunks: the other tiers' buckets (later kernels) need them
-      for (uint32_t c = claim_chunk(); c != ~0u; c = claim_chunk()) kc_chunk<ST, (kChunk + ST - 1) / ST, Group>(kc, c, smem);
+      if (!tu.kc_corun)
+        for (uint32_t c = claim_chunk(); c != ~0u; c = claim_chunk()) kc_chunk<ST, (kChunk + ST - 1) / ST, Group>(kc, c, smem);
     }
     // end marker for the gather group, then consume its last releases so no barrier keeps pending arrivals
     {
@@ -1070,6 +1071,10 @@ cudaError_t kd_all(const ListSet& kd, const uint64_t* t0, const uint32_t* i0, co
   auto tier_launch = [&](int t, const KcArgs* split) -> cudaError_t {
     Tunables tu = tu0;
     tu.pdl = !tu0.pdl ? 0 : (nlaunched++ == 0 || kc || tu0.pdl == 1) ? 1 : 2;
+    // co-run: the fused tier becomes resident beside the running split kernel (launched with PDL, no entry
+    // wait: its bucket waits on done[] order it after the split; it waits for the split's completion only
+    // at exit, so the tiers after it still find the split complete)
+    if (split && tu0.kc_corun) tu.pdl = 2;
     switch (t) {
       case kListWarp:
         return launch_k(kd_warp_sort<DG>, sms * warp_per_sm, 256, 0, s, tu.pdl != 0, kd.items[kListWarp],

@@ -159,8 +159,11 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
                     const uint32_t* __restrict__ B16, const uint32_t* __restrict__ cstart,
                     const uint4* __restrict__ plan_a, const uint2* __restrict__ plan_b,
                     const uint32_t* __restrict__ order, uint32_t* __restrict__ cursor, uint32_t* __restrict__ ticket,
-                    uint64_t* __restrict__ tail_out, uint32_t* __restrict__ idx_out) {
+                    uint64_t* __restrict__ tail_out, uint32_t* __restrict__ idx_out, uint32_t* __restrict__ done) {
   extern __shared__ __align__(16) uint8_t smem[];
+  // co-run form (done != null, internal.cu): every CTA is resident before the fused K-d+K-e tier launches
+  // beside it (PDL); each finished chunk is published in done[b] for that kernel's bucket waits
+  if (done) pdl_trigger();
   uint8_t* region = smem;
   uint32_t* s_wh = reinterpret_cast<uint32_t*>(smem + SplitSmem::kRegion);
   uint32_t* s_dst = s_wh + kWarps * kRadix;
@@ -333,7 +336,11 @@ __global__ void __launch_bounds__(kThreads, kSplitMinBlocks)
       idx_out[g] = s_idx[i];
     }
     for (int q = threadIdx.x; q < kRadix; q += kThreads) s_wh[q] = 0;  // the next chunk's rank histogram
-    __syncthreads();  // staging reused by the next chunk
+    __syncthreads();  // staging reused by the next chunk; every store of this chunk issued
+    if (done && threadIdx.x == 0) {
+      __threadfence();  // cumulative over the CTA's stores ordered by the barrier above
+      atomicAdd(&done[b], 1u);
+    }
   }
 }
 
@@ -528,7 +535,8 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
                                    const uint32_t* lo, const uint32_t* B16, uint64_t n, uint32_t* cstart,
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
-                                   const ClassifyJob& cls, bool run_split, const uint32_t** order_used) {
+                                   const ClassifyJob& cls, bool run_split, const uint32_t** order_used,
+                                   uint32_t* done, int corun_per_sm) {
   // the interleaved order pays only once K-a's output is many times the L2 (C4: 30.6 -> ~18 B/pair of
   // reads, K-c 6.7 -> 6.1 ms); below that the plain bucket-major order is as fast or faster (C3 skew)
   if (n < kInterleaveMinRecords) order = nullptr;
@@ -547,10 +555,18 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc_split_level1, kThreads, smem);
   if (e != cudaSuccess) return e;
+  // (co-run: corun_per_sm CTAs per SM leave room for a K-d+K-e tier CTA beside them; the SMs must be
+  // configured for the largest shared-memory carveout while the split runs, else the tier's CTAs cannot
+  // join them until they drain)
+  const bool corun = done && corun_per_sm > 0;
+  if (corun && corun_per_sm < per_sm) per_sm = corun_per_sm;
+  e = cudaFuncSetAttribute(kc_split_level1, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           corun ? (int)cudaSharedmemCarveoutMaxShared : (int)cudaSharedmemCarveoutDefault);
+  if (e != cudaSuccess) return e;
   uint32_t grid = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
   if (grid > grid_ub) grid = grid_ub;
   kc_split_level1<<<grid, kThreads, smem, s>>>(k1_in, w_in, tiles, off, lo, B16, cstart, plan_a, plan_b, order,
-                                               cursor, ticket, tail_out, idx_out);
+                                               cursor, ticket, tail_out, idx_out, done);
   return cudaGetLastError();
 }
 

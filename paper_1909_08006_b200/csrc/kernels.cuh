@@ -69,7 +69,8 @@ cudaError_t launch_kc_split_level1(const uint64_t* k1_in, const uint32_t* w_in, 
                                    uint4* plan_a, uint2* plan_b, uint32_t* order, uint32_t* cursor, uint32_t* ticket,
                                    uint64_t* tail_out, uint32_t* idx_out, uint32_t grid_ub, cudaStream_t s,
                                    const ClassifyJob& cls, bool run_split = true,
-                                   const uint32_t** order_used = nullptr);
+                                   const uint32_t** order_used = nullptr, uint32_t* done = nullptr,
+                                   int corun_per_sm = 0);
 cudaError_t launch_kr_nchunks(const Seg* segs, uint32_t nseg, uint32_t* nch, cudaStream_t s);
 cudaError_t launch_kr_chunk_map(const uint32_t* cstart, uint32_t nseg, uint32_t ub, uint2* map, cudaStream_t s);
 cudaError_t launch_kr_hist(const Seg* segs, uint32_t nseg, const uint32_t* cstart, uint32_t grid,

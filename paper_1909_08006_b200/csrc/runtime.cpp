@@ -54,6 +54,7 @@ const OptDesc kOpts[] = {
     {"ka_ring", &Options::ka_ring, 1, 11},
     {"gather_l2_64", &Options::gather_l2_64, 0, 1},
     {"kc_fuse", &Options::kc_fuse, 0, 5},
+    {"kc_corun", &Options::kc_corun, 0, 3},
     {"graphs", &Options::graphs, 0, 1},
     {"pdl", &Options::pdl, 0, 3},
     {"kd_claim", &Options::kd_claim, 0, 1},

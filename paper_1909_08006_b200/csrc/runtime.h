@@ -65,6 +65,7 @@ struct Options {
   int64_t kd_claim = 1;  // K-d/K-e tier CTAs claim buckets dynamically (1) or stride their list (0)
   int64_t pdl = 3;      // PDL of the K-d/K-e tier kernels: 0 off, 1 wait-first, 2 overlap, 3 overlap below 1e7 records
   int64_t graphs = 1;   // replay level 1 of the internal sort from a cached CUDA graph (0: launch directly)
+  int64_t kc_corun = 0;  // level-1 K-c kernel co-resident with the fused 2048 tier: K-c CTAs per SM (0 off)
   int64_t kc_fuse = 0;  // level-1 split fused into a K-d+K-e tier (0 off, 1 auto, 2..5 force tier 2048..16384):
                         // measured slower (C2 K-c+K-de 7.49 vs 6.40 ms, C4 54.5 vs 38.8 ms)
   int64_t ka_ring = 6;        // K-a key-row form: ring slots (4, 6, 8 or 11 pieces in flight)

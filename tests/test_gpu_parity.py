@@ -84,19 +84,22 @@ def test_medium_buckets_both_kd_forms(ws):
 
 @pytest.mark.parametrize("size", [32, 33, 512, 513, 2048, 2049, 8192, 8193, 10240, 10241, 16384, 16385])
 @pytest.mark.parametrize("ws", [1, 0])
-@pytest.mark.parametrize("fuse", [0, 1], ids=["split", "fused"])
+@pytest.mark.parametrize("fuse", [0, 1, 2], ids=["split", "fused", "corun"])
 def test_kd_tier_boundaries(size, ws, fuse):
     """One level-1 bucket of exactly `size` records (a constant 2-byte prefix, prefix2) among a few
     thousand others, at every K-d tier boundary (warp 32, 512/128, 2048 warp-specialised or not,
     8192/1024, 10240/1024, 16384/768, and 16385 -> the byte-2 recursion): byte-exact with the oracle.
     fused: the level-1 split runs inside the K-d+K-e kernel of the big bucket's tier (kc_fuse 2..5; the
-    2048 tier for sizes below it, which then has no bucket of its own)."""
+    2048 tier for sizes below it, which then has no bucket of its own); corun: the split's own kernel with
+    that tier PDL-launched beside it (kc_corun)."""
+    if fuse == 2 and (size > 2048 or not ws):
+        pytest.skip("co-run applies to the warp-specialised 2048 tier only")
     big = gen.records(size, seed=size, dist="prefix2").reshape(size, 100)
     rest = gen.records(3001, seed=size + 1, dist="uniform").reshape(3001, 100)
     rest[rest[:, 0] == 0xAB, 0] = 0xAC  # keep the big bucket exactly `size` records
     recs = np.ascontiguousarray(np.concatenate([rest[:1500], big, rest[1500:]]).reshape(-1))
     tier_force = 2 if size <= 2048 else 3 if size <= 8192 else 4 if size <= 10240 else 5
-    with Options(kd_ws=ws, kc_fuse=tier_force if fuse else 0):
+    with Options(kd_ws=ws, kc_fuse=tier_force if fuse else 0, kc_corun=1 if fuse == 2 else 0):
         out, perm = gpu_sort(recs)
     assert_parity(recs, out, perm)
 
@@ -120,6 +123,8 @@ def test_zero_records():
     dict(kc_fuse=0),                                 # level-1 split as its own kernel
     dict(kc_fuse=2),                                 # split fused into the warp-specialised 2048 tier
     dict(kc_fuse=2, kd_ws=0),                        # ... into the alternating 2048 tier (256 threads)
+    dict(kc_fuse=2, kc_corun=1), dict(kc_fuse=2, kc_corun=2),  # split kernel beside the 2048 tier (co-run)
+    dict(kc_fuse=2, kc_corun=1, pdl=2), dict(kc_fuse=2, kc_corun=1, smem_tier_max=600),
     dict(kc_fuse=3), dict(kc_fuse=4), dict(kc_fuse=5),  # ... into the 8192 / 10240 / 16384 tiers
     dict(kc_fuse=4, smem_tier_max=600),              # fused tier empty, big buckets recurse after it
     dict(pdl=0), dict(pdl=1), dict(pdl=2),           # tier kernels: stream order / PDL wait-first / overlap
