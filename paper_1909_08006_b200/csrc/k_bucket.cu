@@ -107,7 +107,46 @@ __device__ __forceinline__ void warp_gather(const uint32_t* perm, uint32_t s, ui
   }
 }
 
-constexpr int kGatherStages = 1;  // groups in flight per gathering warp
+// Two groups in flight per warp (cp.async commit groups): group g's copies land while group g - stride is
+// stored. stage0 / stage1: two kStageBytes slots (16-byte aligned, anywhere in shared memory).
+__device__ __forceinline__ void warp_gather2(const uint32_t* perm, uint32_t s, uint32_t first, uint32_t stride,
+                                             const uint8_t* __restrict__ in, uint64_t in_bytes,
+                                             uint8_t* __restrict__ out_base, uint8_t* stage0, uint8_t* stage1,
+                                             uint64_t* __restrict__ dg_base, bool l2_64) {
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage0), s1 = (uint32_t)__cvta_generic_to_shared(stage1);
+  uint32_t ga = first, gb = first + stride;  // (two named slots, not an indexed pair: no local memory)
+  auto issue = [&](uint32_t g, uint32_t ss) {
+    if (g < s) group_issue(perm, g, min((uint32_t)kGroup, s - g), in, in_bytes, ss, l2_64);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto drain = [&](uint32_t g, const uint8_t* st) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // group g landed (the newer one may be in flight)
+    __syncwarp();
+    group_store(perm, g, min((uint32_t)kGroup, s - g), st, reinterpret_cast<uint32_t*>(out_base + (uint64_t)g * kRecordBytes),
+                dg_base ? dg_base + g : nullptr);
+    __syncwarp();
+  };
+  issue(ga, s0);
+  issue(gb, s1);
+  while (ga < s) {
+    drain(ga, stage0);
+    ga += 2 * stride;
+    issue(ga, s0);
+    if (gb >= s) break;
+    drain(gb, stage1);
+    gb += 2 * stride;
+    issue(gb, s1);
+  }
+  cp_async_wait_all();
+}
+
+// LEY_KD_STAGES = 2 (build flag): the 1024-thread register tiers gather with warp_gather2 — measured slower
+// (C4 K-d+K-e 40.8 vs 35.4 ms, C3 11.89 vs 11.65: 26 warps with two groups each lose to 32 with one;
+// DESIGN.md §9)
+#ifndef LEY_KD_STAGES
+#define LEY_KD_STAGES 1
+#endif
+constexpr int kGatherStages = 1;  // groups in flight per gathering warp (one-stage tiers)
 
 // ---------------------------------------------------------------------------- CTA tier
 // In-smem all-ascending bitonic network over [b, e) by one warp; virtual +inf padding beyond e never
@@ -184,8 +223,20 @@ struct KdLayout {
   static constexpr int GWARPS_FIT = (int)((kSmemMax - kTail) / kWarpStage);
   static constexpr int GWARPS = GWARPS_FIT < WARPS ? GWARPS_FIT : WARPS;
   static constexpr size_t kStage = kTail;
-  static constexpr size_t kStageEnd = kStage + (size_t)GWARPS * kWarpStage;
+  // Two-stage form (the one-CTA-per-SM register tiers, LEY_KD_STAGES = 2): slots in the dead s_idx area
+  // [0, kPerm) and from kTail on; GW2 warps hold two slots each (C4's 10240 tier: 52 groups in flight per SM
+  // instead of 32)
+  static constexpr int SLOTS_A = REGS ? (int)(kPerm / kStageBytes) : 0;
+  static constexpr int SLOTS_B = (int)((kSmemMax - kTail) / kStageBytes);
+  static constexpr int GW2_FIT = (SLOTS_A + SLOTS_B) / 2;
+  static constexpr int GW2 = GW2_FIT < WARPS ? GW2_FIT : WARPS;
+  static constexpr bool TWO = LEY_KD_STAGES == 2 && REGS && THREADS >= 1024 && 2 * GW2 > GWARPS;
+  static constexpr int SLOTS_B_USED = TWO ? (2 * GW2 - SLOTS_A > 0 ? 2 * GW2 - SLOTS_A : 0) : GWARPS;
+  static constexpr size_t kStageEnd = kStage + (size_t)SLOTS_B_USED * kWarpStage;
   static constexpr size_t kBytes = kStageEnd > kReuseEnd ? kStageEnd : kReuseEnd;
+  __host__ __device__ static constexpr size_t slot(int j) {
+    return j < SLOTS_A ? (size_t)j * kStageBytes : kStage + (size_t)(j - SLOTS_A) * kStageBytes;
+  }
   static_assert(kStage % 16 == 0, "gather staging must be 16-byte aligned");
   static_assert(GWARPS >= 1 && kBytes <= kSmemMax, "K-de tier does not fit shared memory");
 };
@@ -477,10 +528,17 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     __syncthreads();  // sorted ordinals complete; the sort area is free for the gather staging
     if (perm)
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
-    if (out && warp < L::GWARPS)
-      warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in, in_bytes,
-                  out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
-                  DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
+    if constexpr (L::TWO) {
+      if (out && warp < L::GW2)
+        warp_gather2(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GW2 * kGroup, in, in_bytes,
+                     out + (uint64_t)sg.start * kRecordBytes, smem + L::slot(2 * warp), smem + L::slot(2 * warp + 1),
+                     DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
+    } else {
+      if (out && warp < L::GWARPS)
+        warp_gather(s_perm, s, (uint32_t)warp * kGroup, (uint32_t)L::GWARPS * kGroup, in, in_bytes,
+                    out + (uint64_t)sg.start * kRecordBytes, s_stage + (size_t)warp * kStageBytes,
+                    DG ? dg + sg.start : nullptr, tu.gather_l2_64 != 0);
+    }
     if (!FUSED && tu.kd_claim && threadIdx.x == 0) s_claim[3] = nxt;  // (every thread read this claim long ago)
     __syncthreads();  // staging (and s_perm) reused by the next bucket
   }
