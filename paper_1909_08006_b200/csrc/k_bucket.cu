@@ -78,11 +78,26 @@ __device__ __forceinline__ void group_issue(const uint32_t* perm, uint32_t g0, u
 __device__ __forceinline__ void group_store(const uint32_t* perm, uint32_t g0, uint32_t cnt, const uint8_t* stage,
                                             uint32_t* __restrict__ dst, uint64_t* __restrict__ dg) {
   const int lane = threadIdx.x & 31;
-  const uint32_t words = cnt * kRecordWords;
-  for (uint32_t w = lane; w < words; w += 32) {
-    const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
-    const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
-    stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
+  if (cnt == kGroup) {
+    // a full group, unrolled: output word w = lane + 32 i of record r = w / 25 sits at stage byte
+    // r * 112 + off_r + 4 (w - 25 r) = 4 w + X[r], X[r] = 12 r + off_r held by lane r (one shuffle per word
+    // instead of a shared-memory load of perm[r] and the address arithmetic; the stores take immediate offsets)
+    const uint32_t xl = 12u * lane + ((perm[g0 + lane] * 4u) & 15u);
+    const uint8_t* sb = stage + 4 * lane;
+    uint32_t* db = dst + lane;
+#pragma unroll
+    for (int i = 0; i < kRecordWords; ++i) {
+      const uint32_t r = ((lane + 32u * i) * 1311u) >> 15;  // == (lane + 32 i) / 25 for all w < 800
+      const uint32_t x = __shfl_sync(0xffffffffu, xl, r);
+      stg_cs_u32(db + 32 * i, *reinterpret_cast<const uint32_t*>(sb + 128 * i + x));
+    }
+  } else {
+    const uint32_t words = cnt * kRecordWords;
+    for (uint32_t w = lane; w < words; w += 32) {
+      const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
+      const uint32_t off = (perm[g0 + r] * 4u) & 15u;  // 100 p mod 16 == 4 p mod 16
+      stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(stage + r * kWindow + off + 4 * o));
+    }
   }
   if (dg && lane < (int)cnt)
     dg[lane] = prefix_digest(reinterpret_cast<const uint32_t*>(stage + lane * kWindow + ((perm[g0 + lane] * 4u) & 15u)));
