@@ -1085,11 +1085,23 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
         const uint32_t cnt = min((uint32_t)kGroup, len - g0);
         const uint8_t* sb = stage + st * kWsStageBytes;
         uint32_t* dst = reinterpret_cast<uint32_t*>(ob + (uint64_t)g0 * kRecordBytes);
-        const uint32_t words = cnt * kRecordWords;
-        for (uint32_t w = lane; w < words; w += 32) {
-          const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
-          const uint32_t off = (pr[g0 + r] * 4u) & 15u;
-          stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWsSlot + off + 4 * o));
+        if (cnt == (uint32_t)kGroup) {  // unrolled, as group_store: word w of record r at 4 w + 28 r + off_r
+          const uint32_t xl = (uint32_t)(kWsSlot - kRecordBytes) * lane + ((pr[g0 + lane] * 4u) & 15u);
+          const uint8_t* sbl = sb + 4 * lane;
+          uint32_t* dl = dst + lane;
+#pragma unroll
+          for (int i = 0; i < kRecordWords; ++i) {
+            const uint32_t r = ((lane + 32u * i) * 1311u) >> 15;  // == (lane + 32 i) / 25 for all w < 800
+            const uint32_t x = __shfl_sync(0xffffffffu, xl, r);
+            stg_cs_u32(dl + 32 * i, *reinterpret_cast<const uint32_t*>(sbl + 128 * i + x));
+          }
+        } else {
+          const uint32_t words = cnt * kRecordWords;
+          for (uint32_t w = lane; w < words; w += 32) {
+            const uint32_t r = w / kRecordWords, o = w - r * kRecordWords;
+            const uint32_t off = (pr[g0 + r] * 4u) & 15u;
+            stg_cs_u32(dst + w, *reinterpret_cast<const uint32_t*>(sb + r * kWsSlot + off + 4 * o));
+          }
         }
         if (DG && lane < (int)cnt)
           dg[d.x + g0 + lane] =
