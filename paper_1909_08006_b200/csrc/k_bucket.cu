@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     for (uint32_t g = threadIdx.x; g < L::CNT_WORDS; g += THREADS) s_cnt[g] = 0;  // was gather staging
     __syncthreads();
     const uint32_t s = sg.len;
+    // item j of this thread (index j THREADS + tid) exists iff j < nv: one register instead of the index
+    // (which the compiler would otherwise rematerialise from %tid.x in every per-item loop)
+    const uint32_t nv = s > threadIdx.x ? (s - threadIdx.x + THREADS - 1) / THREADS : 0u;
     const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
     const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
     // unconsumed bits of the composite key (tail = key bytes 2..9, then the 32-bit ordinal): key bits
@@ -381,8 +384,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       }
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
-        uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) {
+        if (j < nv) {
           const uint32_t d = digit2(tr[j], xr[j]);
           if constexpr (PACKED) {
             const uint32_t sh = 16u * (d & 1u);
@@ -450,8 +452,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       // smaller composites there
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
-        uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) {
+        if (j < nv) {
           const uint32_t b = cnt_get(digit2(tr[j], xr[j]));
           s_tail[b + rr[j]] = tr[j];
           s_idx[b + rr[j]] = xr[j];
@@ -460,8 +461,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < RITEMS; ++j) {
-        uint32_t i = j * THREADS + threadIdx.x;
-        if (i < s) {
+        if (j < nv) {
           const uint32_t d = digit2(tr[j], xr[j]);
           const uint32_t b = cnt_get(d), sz = cnt_get(d + 1) - b;
           if (sz == 1) {
@@ -934,6 +934,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       if (tid == 0) *s_nbig = 0;
       nbar_sync(kBarSort, ST);
       const uint32_t s = sg.len;
+      const uint32_t nv = s > (uint32_t)tid ? (s - tid + ST - 1) / ST : 0u;  // (item j exists iff j < nv)
       const uint64_t* tp = (sg.parity ? t1 : t0) + sg.start;
       const uint32_t* ip = (sg.parity ? i1 : i0) + sg.start;
       const bool on_idx = sg.depth >= kKeyBytes;
@@ -960,8 +961,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       }
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t i = j * ST + tid;
-        if (i < s) rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
+        if (j < nv) rr[j] = atomicAdd(&s_cnt[digit2(tr[j], xr[j])], 1u);
       }
       nbar_sync(kBarSort, ST);
       {
@@ -980,8 +980,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       nbar_sync(kBarSort, ST);
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t i = j * ST + tid;
-        if (i < s) {
+        if (j < nv) {
           const uint32_t b = s_cnt[digit2(tr[j], xr[j])];
           s_tail[b + rr[j]] = tr[j];
           s_idx[b + rr[j]] = xr[j];
@@ -990,8 +989,7 @@ __global__ void __launch_bounds__(ST + 32 * GW, 2)
       nbar_sync(kBarSort, ST);
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t i = j * ST + tid;
-        if (i < s) {
+        if (j < nv) {
           const uint32_t d = digit2(tr[j], xr[j]);
           const uint32_t b = s_cnt[d], sz = s_cnt[d + 1] - b;
           if (sz == 1) {
