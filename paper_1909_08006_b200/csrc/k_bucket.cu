@@ -65,6 +65,7 @@ __device__ __forceinline__ void group_issue(const uint32_t* perm, uint32_t g0, u
                                             uint64_t in_bytes, uint32_t stage_s, bool l2_64) {
   const int lane = threadIdx.x & 31;
   const uint32_t p = lane < (int)cnt ? perm[g0 + lane] : 0u;
+  const uint32_t sl = stage_s + 16u * lane;  // chunk cidx -> stage byte r * 112 + c * 16 = 16 cidx
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
     const int cidx = q * 32 + lane;
@@ -72,7 +73,7 @@ __device__ __forceinline__ void group_issue(const uint32_t* perm, uint32_t g0, u
     const uint32_t pr = __shfl_sync(0xffffffffu, p, r);
     const uint64_t a = (((uint64_t)pr * kRecordBytes) & ~uint64_t(15)) + (uint64_t)c * 16;
     if (r < (int)cnt && a < in_bytes)  // (chunks past the input's end hold no record byte)
-      cp_async16(stage_s + r * kWindow + c * 16, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u, l2_64);
+      cp_async16(sl + 512u * q, in + a, in_bytes - a < 16 ? (uint32_t)(in_bytes - a) : 16u, l2_64);
   }
 }
 __device__ __forceinline__ void group_store(const uint32_t* perm, uint32_t g0, uint32_t cnt, const uint8_t* stage,
