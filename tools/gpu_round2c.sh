@@ -1,6 +1,6 @@
 # Round-2 final refresh (r02c): as gpu_round2.sh without the host-path lines (C5/C7 unchanged since r02b).
 # ncu launch list of bench.py itself, DRAM launch lists for C1/C3 (profiles/ncu_traffic.json), and
-# --set full captures of the dominant kernels at C4 and C2. Everything lands in gpurun_out/r2/.
+# --set full captures of the dominant kernels at C4 and C2. Everything lands in gpurun_out/r2c/.
 O=gpurun_out/r2c; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw --format=csv > $O/smi.log
 timeout 1500 python -m pytest tests -m gpu -q > $O/tests.log 2>&1; echo "tests exit $?" >> $O/tests.log
@@ -10,7 +10,7 @@ python bench.py --no-e2e --no-cpu --steps 2 --warmup 3 --secondary none > $O/nb_
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $O/launches_bench_c4.csv python bench.py --no-e2e --no-cpu --steps 2 --warmup 3 --secondary none > $O/nb_ncu.log 2>&1
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
-for spec in "c1 1e6 uniform 0" "c3 2e8 skewed 2"; do
+for spec in "c1 1e6 uniform 0" "c2 1e8 uniform 1" "c3 2e8 skewed 2" "c4 6e8 uniform 3"; do
   set -- $spec
   timeout 1200 ncu --metrics $M --clock-control none --csv --log-file $O/launches_$1.csv \
     python tools/profile_step.py --n $2 --dist $3 --seed $4 --steps 1 --warmup 1 > $O/ncu_$1.log 2>&1
