@@ -75,6 +75,19 @@ __device__ __forceinline__ PdlExitWait pdl_enter(int m) {
 }
 
 // ------------------------------------------------------------------ device helpers
+// Bulk L2 prefetch of [p, p + bytes) (widened to 16-byte bounds) with an evict-last policy: a K-d tier CTA
+// fetches its next bucket's pairs while it gathers the current one, so the pair loads that start the next
+// sort hit L2 instead of waiting on DRAM behind the gather traffic (C4 K-d+K-e 33.3 -> 32.7 ms).
+__device__ __forceinline__ void prefetch_l2_last(const void* p, uint64_t bytes) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~uint64_t(15);
+  const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~uint64_t(15);
+  if (e <= a) return;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"((uint32_t)(e - a)), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

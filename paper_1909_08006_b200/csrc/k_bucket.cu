@@ -542,6 +542,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
       }
     }
     __syncthreads();  // sorted ordinals complete; the sort area is free for the gather staging
+    if (!FUSED && threadIdx.x == 0 && nxt < nitems) {  // the next bucket's pairs, while this one is gathered
+      const Seg ns = list[nxt];
+      prefetch_l2_last((ns.parity ? t1 : t0) + ns.start, (uint64_t)ns.len * 8);
+      prefetch_l2_last((ns.parity ? i1 : i0) + ns.start, (uint64_t)ns.len * 4);
+    }
     if (perm)
       for (uint32_t i = threadIdx.x; i < s; i += THREADS) perm[sg.start + i] = s_perm[i];
     if constexpr (L::TWO) {
