@@ -314,6 +314,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
   };
   uint32_t* const ticket = const_cast<uint32_t*>(count) + kTierTicket;
   uint32_t it = 0, nxt = tu.kd_claim ? 0u : blockIdx.x;
+  __shared__ Seg s_next;  // the next bucket's descriptor, read early by the prefetch (s_next_it: its index)
+  __shared__ uint32_t s_next_it;
+  if (threadIdx.x == 0) s_next_it = ~0u;
   if (!FUSED && tu.kd_claim && threadIdx.x == 0) s_claim[3] = atomicAdd(ticket, 1u);
   while (true) {
     Seg sg;
@@ -347,7 +350,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
         nxt = it + gridDim.x;
       }
       if (it >= nitems) break;
-      sg = list[it];
+      // (claimed mode: the descriptor was read by the prefetch below during the last bucket, and the
+      // barrier above orders that store before this read)
+      sg = tu.kd_claim && s_next_it == it ? s_next : list[it];
     }
     for (uint32_t g = threadIdx.x; g < L::CNT_WORDS; g += THREADS) s_cnt[g] = 0;  // was gather staging
     __syncthreads();
@@ -544,6 +549,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 1024 || (CAP / THREADS) >
     __syncthreads();  // sorted ordinals complete; the sort area is free for the gather staging
     if (!FUSED && threadIdx.x == 0 && nxt < nitems) {  // the next bucket's pairs, while this one is gathered
       const Seg ns = list[nxt];
+      if (tu.kd_claim) {  // (published by the barriers that end this bucket)
+        s_next = ns;
+        s_next_it = nxt;
+      }
       prefetch_l2_last((ns.parity ? t1 : t0) + ns.start, (uint64_t)ns.len * 8);
       prefetch_l2_last((ns.parity ? i1 : i0) + ns.start, (uint64_t)ns.len * 4);
     }
